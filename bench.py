@@ -1,0 +1,453 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 3DGEER render path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE config 2): 1M-Gaussian synthetic scene (synth.random_scene,
+seed 0, SH degree 3, scales (0.06k, 0.25k), k = (1e4/N)^1/2), one 1920x1080
+BEAP camera with 180 x 101.25 deg FoV.  A step is one full forward frame
+(prep -> dup -> sort -> render) of one view.  Under torchrun each rank renders
+its own view (rank r: the C2 camera rotated by 2 pi r / N about the scene's y
+axis; the scene is replicated, views are independent: weak scaling, no
+collective on the data path).
+
+``value`` = frames/s of the whole job with the scene resident in HBM; ``e2e``
+= the same metric through the reference-facing drop-in ``renderer.render``
+(host float64 arrays in, host float64 arrays out, copies inside the timed
+region).  Extra keys: fwd+bwd ms per view (config 3), stage times, per-stage
+roofline, the 64-view training step (config 4: fwd -> L1 grad -> bwd per view,
+NCCL allreduce of the gradients, Adam), and the CPU baseline (the fp64 C port
+of the reference path, oracle/, timed on this host).
+
+``--impl reference`` times that CPU port of the reference path on the same
+config (rank 0 only) and prints the same JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rendered FPS (Mrays/s) at 1080p fisheye, 1M Gaussians; fwd+bwd ms/view"
+WORKLOAD = "C2: 1M Gaussians, 1920x1080 BEAP fisheye 180x101.25 deg, forward render"
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # derived: SMs x FP32 lanes x 2 x max clock
+SURVEY_K5_FLOPS_PER_PAIR = 46  # K5 algorithmic cost per evaluated pair
+SURVEY_K6_FLOPS_PER_PAIR = 128  # K6
+SURVEY_K1_BYTES_PER_GAUSSIAN = 340  # K1
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                maxes.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sms)) if sms else None, "sm_max_mhz": max(maxes) if maxes else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def rank_camera(base, rank, world):
+    """C2 camera for rank 0; rank r sees the scene from the C2 pose rotated by 2 pi r / N about y."""
+    from paper_2505_24053_b200 import synth
+    from paper_2505_24053_b200.scene import Camera
+
+    if rank == 0:
+        return base
+    ang = 2.0 * math.pi * rank / world
+    pos = np.array([-2.0 * math.sin(ang), 0.0, -2.0 * math.cos(ang)])
+    rot, t = synth.look_at(pos)
+    return Camera(width=base.width, height=base.height, model="beap", rotation=rot, translation=t,
+                  fov_x=base.fov_x, fov_y=base.fov_y)
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        dist.init_process_group(backend=backend)
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return rank, world, local
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ----------------------------------------------------------------------------- CPU (reference port) timing
+
+def cpu_frame_seconds(scene, cam, threads=None):
+    """One full C2 frame of the fp64 C port of the reference path (graph + render)."""
+    from oracle import oracle as O
+
+    t0 = time.perf_counter()
+    g = O.build_render_graph(scene, cam)
+    O.render(scene, cam, None, threads=threads, graph=g)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    rank, world, _ = dist_setup(args)
+    if rank != 0:
+        barrier(world)
+        return
+    from oracle import oracle as O
+    from paper_2505_24053_b200 import synth
+
+    scene = synth.config_scene("C2")
+    cam = synth.config_camera("C2")
+    cores = O.num_threads()
+    for _ in range(args.warmup):
+        cpu_frame_seconds(scene, cam)
+    times = [cpu_frame_seconds(scene, cam) for _ in range(args.steps)]
+    total = sum(times)
+    fps = args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "FPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth.random_scene seed 0)",
+        "config": {"workload": WORKLOAD, "gaussians": len(scene), "width": 1920, "height": 1080},
+        "mrays_per_s": fps * 1920 * 1080 / 1e6,
+        "cpu_baseline": {"value": fps, "unit": "FPS", "cores": cores, "kind": "port",
+                         "sample": "full C2 frame per step (association + raster), fp64 C port of the reference "
+                                   "path (oracle/geer_oracle.c), OpenMP over tiles"},
+        "e2e": {"value": fps, "unit": "FPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    barrier(world)
+
+
+# ----------------------------------------------------------------------------- GPU
+
+def count_launches_per_step(fn):
+    """Kernels launched by one call of fn, counted with the CUDA profiler (CUPTI)."""
+    import torch
+
+    try:
+        from torch.profiler import ProfilerActivity, profile
+
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA" and not e.name.startswith("Memcpy")
+                 and not e.name.startswith("Memset") and "memcpy" not in e.name.lower() and "memset" not in e.name.lower()]
+        return len(names), sorted(set(names))
+    except Exception as exc:  # profiler unavailable
+        return None, [f"profiler unavailable: {exc}"]
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_setup(args)
+    from paper_2505_24053_b200 import renderer, synth
+    from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene
+
+    t_setup = time.perf_counter()
+    scene = synth.config_scene("C2", n=args.gaussians)
+    base_cam = synth.config_camera("C2")
+    cam = rank_camera(base_cam, rank, world)
+    cfg = renderer.RenderConfig()
+    dscene = DeviceScene.from_scene(scene, device=f"cuda:{local}")
+    r = DeviceRenderer(local)
+    h, w = cam.height, cam.width
+    out = (torch.empty((h, w, 3), dtype=torch.float32, device="cuda"),
+           torch.empty((h, w), dtype=torch.float32, device="cuda"),
+           torch.empty((h, w), dtype=torch.int32, device="cuda"))
+    stream = torch.cuda.current_stream()
+
+    def step():
+        r.forward(dscene, cam, cfg, out=out)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K forward frames
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = sampler.stop()
+    ms_local = ev0.elapsed_time(ev1)
+    ms_total = allreduce_max(ms_local, world)
+    ms_per_step = ms_total / args.steps
+    value = world * args.steps / (ms_total / 1e3)
+
+    extra = {}
+    # ---- stage times + frame statistics (separate pass; events inside the library)
+    r.set_timing(True)
+    stage_samples = []
+    for _ in range(5):
+        step()
+        stage_samples.append(r.stats())
+    r.set_timing(False)
+    st = {k: float(np.median([s[k] for s in stage_samples])) for k in stage_samples[0]}
+    n_px = w * h
+    pairs = st["evaluated_pairs"]
+    peaks = load_peaks()
+    stages = {
+        "prep": {"ms": st["ms_prep"], "bound": "hbm", "unit": "GB/s",
+                 "achieved": len(scene) * SURVEY_K1_BYTES_PER_GAUSSIAN / (st["ms_prep"] * 1e-3) / 1e9},
+        "dup": {"ms": st["ms_dup"], "bound": "hbm", "unit": "GB/s",
+                "achieved": (len(scene) * (4 * 16 + 24) + st["n_entries"] * 8) / (st["ms_dup"] * 1e-3) / 1e9},
+        "sort": {"ms": st["ms_sort"], "bound": "hbm", "unit": "GB/s",
+                 "achieved": st["n_entries"] * 32 / (st["ms_sort"] * 1e-3) / 1e9},
+        "render": {"ms": st["ms_render"], "bound": "fp32", "unit": "TFLOP/s",
+                   "achieved": pairs * SURVEY_K5_FLOPS_PER_PAIR / (st["ms_render"] * 1e-3) / 1e12},
+    }
+    for k, v in stages.items():
+        peak = peaks["hbm_gbs"] if v["bound"] == "hbm" else FP32_PEAK_TFLOPS
+        v["peak"] = peak
+        v["frac"] = v["achieved"] / peak
+    dominant = max(stages, key=lambda k: stages[k]["ms"])
+    dv = stages[dominant]
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(dominant)
+    except Exception:
+        pass
+    roofline = {"bound": dv["bound"], "kernel": dominant, "achieved": dv["achieved"], "peak": dv["peak"],
+                "unit": dv["unit"], "frac": dv["frac"], "traffic": traffic,
+                "peak_source": (f"{peaks['source']} MEASURED_PEAKS.json hbm_gbs" if dv["bound"] == "hbm" else
+                                "derived FP32 peak 148 SM x 128 lanes x 2 x 1.965 GHz (not in MEASURED_PEAKS)"),
+                "work": (f"{pairs:.0f} evaluated pairs x {SURVEY_K5_FLOPS_PER_PAIR} flops (SURVEY 8d)"
+                         if dominant == "render" else "algorithmic bytes per SURVEY 8d / DESIGN.md")}
+    extra["stages"] = stages
+    extra["frame"] = {"entries": int(st["n_entries"]), "tiles": int(st["n_tiles"]),
+                      "work_items": int(st["n_work_items"]), "evaluated_pairs": int(pairs),
+                      "pairs_per_pixel": pairs / n_px, "kappa_rechecks": int(st["kappa_rechecks"]),
+                      "clamped": int(st["clamped"])}
+
+    # ---- fwd + bwd ms per view (config 3)
+    dl = torch.randn((h, w, 3), device="cuda", generator=torch.Generator(device="cuda").manual_seed(1)) / (h * w)
+    grads = dscene.zeros_like_grads()
+
+    def fb():
+        r.forward(dscene, cam, cfg, out=out)
+        r.backward(dl, grads=grads)
+
+    for _ in range(3):
+        fb()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    kfb = max(3, min(args.steps, 20))
+    e0.record(stream)
+    for _ in range(kfb):
+        fb()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    fb_ms = allreduce_max(e0.elapsed_time(e1), world) / kfb
+    r.set_timing(True)
+    fb()
+    bst = r.stats()
+    r.set_timing(False)
+    extra["fwd_bwd_ms_per_view"] = fb_ms
+    extra["backward_ms"] = bst["ms_backward"]
+    stages["backward"] = {"ms": bst["ms_backward"], "bound": "fp32", "unit": "TFLOP/s",
+                          "achieved": pairs * SURVEY_K6_FLOPS_PER_PAIR / (bst["ms_backward"] * 1e-3) / 1e12,
+                          "peak": FP32_PEAK_TFLOPS}
+    stages["backward"]["frac"] = stages["backward"]["achieved"] / FP32_PEAK_TFLOPS
+
+    # ---- kernel launches per step
+    n_launch, names = count_launches_per_step(step)
+    gpu_launches = n_launch * args.steps if n_launch is not None else None
+    extra["launches_per_step"] = n_launch
+    extra["kernels"] = names
+
+    # ---- e2e through the reference-facing host API (host f64 in/out, copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: _pinned_copy(a)
+        hscene = type(scene)(pin(scene.means), pin(scene.log_scales), pin(scene.quats), pin(scene.opacity_logits),
+                             pin(scene.sh))
+        renderer.render(hscene, cam, cfg, device=local)
+        ke = max(3, min(args.steps, 10))
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            renderer.render(hscene, cam, cfg, device=local)
+        dt = allreduce_max(time.perf_counter() - t0, world)
+        h2d = sum(a.nbytes for a in (hscene.means, hscene.log_scales, hscene.quats, hscene.opacity_logits, hscene.sh))
+        d2h = n_px * (3 * 8 + 8 + 8)
+        e2e = {"value": world * ke / dt, "unit": "FPS", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * dt / ke, "api": "paper_2505_24053_b200.renderer.render (geer_render_host)",
+               "host_memory": "pinned float64 scene arrays"}
+
+    # ---- 64-view training step (config 4)
+    if not args.no_train:
+        try:
+            from paper_2505_24053_b200.train import MultiViewTrainer
+
+            trainer = MultiViewTrainer.for_config4(scene, n_views=args.train_views, rank=rank, world=world,
+                                                   device=local)
+            trainer.step()
+            torch.cuda.synchronize()
+            kt = max(2, min(args.steps, 5))
+            barrier(world)
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record()
+            for _ in range(kt):
+                trainer.step()
+            t1.record()
+            torch.cuda.synchronize()
+            tms = allreduce_max(t0.elapsed_time(t1), world) / kt
+            extra["train_step"] = {"views": args.train_views, "ms_per_step": tms,
+                                   "views_per_s": args.train_views / (tms / 1e3),
+                                   "allreduce_bytes": trainer.grad_numel * 4, "loss": trainer.last_loss}
+        except Exception as exc:
+            extra["train_step"] = {"error": repr(exc)}
+
+    # ---- CPU baseline (rank 0, N=1 only): the fp64 C port of the reference path on this host
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            from oracle import oracle as O
+
+            cpu_s = cpu_frame_seconds(scene, base_cam)
+            cpu = {"value": 1.0 / cpu_s, "unit": "FPS", "cores": O.num_threads(), "kind": "port",
+                   "sample": "one full C2 frame (association + raster) of the fp64 C port oracle/geer_oracle.c",
+                   "seconds": cpu_s}
+        except Exception as exc:
+            cpu = {"value": None, "unit": "FPS", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "FPS", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 raster / f64 association",
+            "data": "synthetic (synth.random_scene seed 0, fp32-rounded)",
+            "config": {"workload": WORKLOAD, "gaussians": len(scene), "width": w, "height": h,
+                       "views": "one per rank (rank r: C2 pose rotated 2*pi*r/N about y)",
+                       "l2": "inputs exceed L2 (scene SoA 236 MB fp32 > 126 MB L2); no explicit flush"},
+            "mrays_per_s": value * w * h / 1e6,
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": gpu_launches,
+            "setup_s": time.perf_counter() - t_setup,
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    barrier(world)
+
+
+def _pinned_copy(a):
+    import torch
+
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+    t.numpy()[...] = a
+    return t.numpy()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--gaussians", type=int, default=1_000_000)
+    ap.add_argument("--train-views", type=int, default=64)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+/*
+ * geer.h — C ABI of the B200-native 3DGEER rendering hot path (libgeer_b200.so).
+ *
+ * The reference (raygauss 0.1.0, pure Python) exposes this path as three
+ * functions; each host-level entry point below replaces one of them 1:1 and
+ * takes the same data the Python call receives, as plain pointers + sizes:
+ *
+ *   geer_render_host           <- raygauss.renderer.render
+ *                                 (pkg/src/raygauss/renderer.py:123-176)
+ *   geer_render_backward_host  <- raygauss.renderer.render_backward
+ *                                 (pkg/src/raygauss/renderer.py:234-333)
+ *   geer_build_graph_host      <- raygauss.association.build_render_graph
+ *   + geer_graph_info/export      (pkg/src/raygauss/association.py:391-476,
+ *                                  RenderGraph :353-370, CSFGrid :272-298)
+ *
+ * Host-level calls take HOST float64 arrays in the reference's layouts
+ * (GaussianScene scene.py:35-51, dl_dimage (H,W,3), FrameOutput
+ * renderer.py:39-44, SceneGrads renderer.py:179-201) and do the
+ * host<->device copies themselves.  The device-level calls (geer_forward /
+ * geer_backward) take DEVICE fp32 pointers and a cudaStream_t and never copy
+ * to the host except the 12-byte frame header (entry count + error flag).
+ *
+ * Errors: every call returns a geer_status; geer_last_error() gives the
+ * thread-local message.  GEER_ERR_NOT_PD / GEER_ERR_NOT_SYMMETRIC carry the
+ * reference's ValueError messages (association.py:155-160) verbatim.
+ * Camera validation (camera.py:54-69) is done by the caller-side wrapper
+ * before the call; geer_* re-checks only what would crash a kernel.
+ */
+#ifndef GEER_H_
+#define GEER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GEER_ABI_VERSION 1
+
+typedef enum geer_status {
+    GEER_OK = 0,
+    GEER_ERR_INVALID = 1,        /* bad argument (ValueError in the wrapper) */
+    GEER_ERR_NOT_SYMMETRIC = 2,  /* "view covariance must be symmetric" */
+    GEER_ERR_NOT_PD = 3,         /* "view covariance must be positive definite" */
+    GEER_ERR_CUDA = 4,           /* CUDA runtime error */
+    GEER_ERR_NOMEM = 5,          /* device allocation failed */
+    GEER_ERR_STATE = 6           /* backward without a matching forward */
+} geer_status;
+
+typedef enum geer_model { GEER_PINHOLE = 0, GEER_KB = 1, GEER_BEAP = 2 } geer_model;
+
+/* raygauss.camera.Camera (camera.py:25-48); unused intrinsics may be NaN. */
+typedef struct geer_camera {
+    int32_t width, height, model, pad_;
+    double rotation[9];    /* R_c row-major: x_c = R_c x + t_c */
+    double translation[3]; /* t_c */
+    double fov_x, fov_y;   /* radians (beap) */
+    double fx, fy, cx, cy; /* pinhole / kb */
+    double k[4];           /* kb distortion */
+} geer_camera;
+
+/* raygauss.renderer.RenderConfig (renderer.py:24-37); threads is ignored. */
+typedef struct geer_config {
+    double lam;
+    double background[3];
+    int32_t tile_px;
+    int32_t support_cutoff;
+    int32_t threads;
+    int32_t pad_;
+} geer_config;
+
+/* Device scene: fp32 SoA in the reference's stored spaces (scene.py:35-51). */
+typedef struct geer_scene {
+    int64_t n;
+    int32_t n_bands; /* 1, 4, 9 or 16 */
+    int32_t pad_;
+    const float *means;          /* (n,3) */
+    const float *log_scales;     /* (n,3) */
+    const float *quats;          /* (n,4) raw (r,i,j,k) */
+    const float *opacity_logits; /* (n,) */
+    const float *sh;             /* (n,n_bands,3) */
+} geer_scene;
+
+/* Device gradients in the same SoA layout (renderer.py:179-201 conventions:
+ * dopacities w.r.t. LINEAR opacity, dquats with the normalisation Jacobian). */
+typedef struct geer_grads {
+    float *dmeans, *dlog_scales, *dquats, *dopacities, *dsh;
+} geer_grads;
+
+/* Host scene: float64 arrays exactly as GaussianScene holds them. */
+typedef struct geer_host_scene {
+    int64_t n;
+    int32_t n_bands;
+    int32_t pad_;
+    const double *means, *log_scales, *quats, *opacity_logits, *sh;
+} geer_host_scene;
+
+typedef struct geer_host_grads {
+    double *dmeans, *dlog_scales, *dquats, *dopacities, *dsh;
+} geer_host_grads;
+
+/* Per-frame statistics of the last forward (filled by geer_frame_stats). */
+typedef struct geer_stats {
+    int64_t n_gaussians;
+    int64_t n_entries;        /* |RenderGraph.order| */
+    int64_t n_tiles;
+    int64_t n_work_items;     /* raster CTAs launched with work */
+    int64_t evaluated_pairs;  /* sum over pixels of alive entries (n_eval) */
+    int64_t kappa_rechecks;   /* fp64 re-evaluations of the kappa cutoff */
+    int64_t clamped;          /* clamped & kept particles */
+    float ms_prep, ms_dup, ms_sort, ms_render, ms_total; /* CUDA-event stage times (if timing on) */
+    float ms_backward;
+} geer_stats;
+
+typedef struct geer_ctx geer_ctx;
+
+int geer_abi_version(void);
+const char *geer_last_error(void);
+
+/* One context per (device, stream) user; owns grow-only device workspaces and the
+ * state of its last forward (used by the next geer_backward). Not thread-safe. */
+geer_ctx *geer_create(int device);
+void geer_destroy(geer_ctx *ctx);
+int geer_set_timing(geer_ctx *ctx, int enable);
+
+/* ---- device level (fast path) -------------------------------------------------
+ * color (H,W,3) f32, remaining (H,W) f32, count (H,W) i32: device buffers.
+ * The scene buffers must stay valid until the matching geer_backward. */
+int geer_forward(geer_ctx *ctx, const geer_scene *scene, const geer_camera *camera, const geer_config *config,
+                 float *color, float *remaining, int32_t *count, void *stream);
+
+/* dl_dimage (H,W,3) f32 device.  flags: GEER_ACCUMULATE adds into grads (multi-view);
+ * GEER_OPACITY_LOGIT returns dopacities w.r.t. the stored logit (trainer.py:208-217)
+ * instead of the reference's linear-opacity convention. */
+#define GEER_ACCUMULATE 1
+#define GEER_OPACITY_LOGIT 2
+int geer_backward(geer_ctx *ctx, const float *dl_dimage, const geer_grads *grads, int flags, void *stream);
+
+int geer_frame_stats(geer_ctx *ctx, geer_stats *out);
+
+/* ---- association export (parity with RenderGraph) ------------------------------ */
+int geer_graph_info(geer_ctx *ctx, int64_t *n_entries, int32_t *n_x, int32_t *n_y);
+/* host pointers; any may be NULL.  order/entry_tile (n_entries), ranges (n_tiles+1),
+ * mu_c (n,3), depth (n), keep/clamped (n), pixel_tile (H,W), medges_x (n_x+1), medges_y (n_y+1) */
+int geer_graph_export(geer_ctx *ctx, int64_t *order, int64_t *entry_tile, int64_t *ranges, double *mu_c,
+                      double *depth, uint8_t *keep, uint8_t *clamped, int64_t *pixel_tile, double *medges_x,
+                      double *medges_y);
+
+/* ---- host level (drop-in replacements of the reference's Python calls) -------- */
+int geer_build_graph_host(geer_ctx *ctx, const geer_host_scene *scene, const geer_camera *camera, double lam,
+                          int32_t tile_px);
+int geer_render_host(geer_ctx *ctx, const geer_host_scene *scene, const geer_camera *camera,
+                     const geer_config *config, double *color, double *remaining, int64_t *count);
+int geer_render_backward_host(geer_ctx *ctx, const geer_host_scene *scene, const geer_camera *camera,
+                              const double *dl_dimage, const geer_config *config, const geer_host_grads *grads);
+
+/* ---- multi-view training glue (BASELINE config 4) ----------------------------- */
+/* g = sign(color - target) * scale per element, 0 where mask == 0 (trainer.py:129-132 L1 term). */
+int geer_l1_grad(const float *color, const float *target, const uint8_t *mask, float *dl_dimage, int64_t n_pixels,
+                 float scale, void *stream);
+/* Adam step over a flat fp32 buffer (trainer.py:181-197), per-element lr. */
+int geer_adam(float *param, const float *grad, float *m, float *v, const float *lr, int64_t n, float beta1,
+              float beta2, float eps, int32_t step, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GEER_H_ */

@@ -188,7 +188,8 @@ def _scene_arrays(scene):
     log_scales = _f64(scene.log_scales).reshape(n, 3)
     quats = _f64(scene.quats).reshape(n, 4)
     logits = _f64(scene.opacity_logits).reshape(n)
-    sh = _f64(scene.sh).reshape(n, -1, 3) if n else _f64(scene.sh).reshape(0, -1, 3)
+    sh = _f64(scene.sh)
+    sh = sh.reshape(n, -1, 3) if n else sh.reshape(0, sh.shape[1] if sh.ndim == 3 else 1, 3)
     return means, log_scales, quats, logits, np.ascontiguousarray(sh)
 
 

@@ -1,0 +1,214 @@
+"""ctypes binding of libgeer_b200.so (the C ABI declared in include/geer.h).
+
+The library is built in-tree (``python -m paper_2505_24053_b200.build``) and
+loaded from this package directory.  There is no fallback: if the shared
+object is missing or a CUDA device is unavailable, calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libgeer_b200.so")
+
+GEER_OK = 0
+GEER_ERR_INVALID = 1
+GEER_ERR_NOT_SYMMETRIC = 2
+GEER_ERR_NOT_PD = 3
+GEER_ERR_CUDA = 4
+GEER_ERR_NOMEM = 5
+GEER_ERR_STATE = 6
+
+MODEL_IDS = {"pinhole": 0, "kb": 1, "beap": 2}
+
+# every symbol include/geer.h declares (checked by tests/test_abi.py)
+EXPORTED = (
+    "geer_abi_version", "geer_last_error", "geer_create", "geer_destroy", "geer_set_timing", "geer_forward",
+    "geer_backward", "geer_frame_stats", "geer_graph_info", "geer_graph_export", "geer_build_graph_host",
+    "geer_render_host", "geer_render_backward_host", "geer_l1_grad", "geer_adam",
+)
+
+
+class GeerCamera(ctypes.Structure):
+    _fields_ = [
+        ("width", ctypes.c_int32), ("height", ctypes.c_int32), ("model", ctypes.c_int32), ("pad_", ctypes.c_int32),
+        ("rotation", ctypes.c_double * 9), ("translation", ctypes.c_double * 3),
+        ("fov_x", ctypes.c_double), ("fov_y", ctypes.c_double),
+        ("fx", ctypes.c_double), ("fy", ctypes.c_double), ("cx", ctypes.c_double), ("cy", ctypes.c_double),
+        ("k", ctypes.c_double * 4),
+    ]
+
+
+class GeerConfig(ctypes.Structure):
+    _fields_ = [
+        ("lam", ctypes.c_double), ("background", ctypes.c_double * 3), ("tile_px", ctypes.c_int32),
+        ("support_cutoff", ctypes.c_int32), ("threads", ctypes.c_int32), ("pad_", ctypes.c_int32),
+    ]
+
+
+class GeerScene(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64), ("n_bands", ctypes.c_int32), ("pad_", ctypes.c_int32),
+        ("means", ctypes.c_void_p), ("log_scales", ctypes.c_void_p), ("quats", ctypes.c_void_p),
+        ("opacity_logits", ctypes.c_void_p), ("sh", ctypes.c_void_p),
+    ]
+
+
+class GeerGrads(ctypes.Structure):
+    _fields_ = [("dmeans", ctypes.c_void_p), ("dlog_scales", ctypes.c_void_p), ("dquats", ctypes.c_void_p),
+                ("dopacities", ctypes.c_void_p), ("dsh", ctypes.c_void_p)]
+
+
+GeerHostScene = GeerScene  # same layout, double pointers
+GeerHostGrads = GeerGrads
+
+
+class GeerStats(ctypes.Structure):
+    _fields_ = [
+        ("n_gaussians", ctypes.c_int64), ("n_entries", ctypes.c_int64), ("n_tiles", ctypes.c_int64),
+        ("n_work_items", ctypes.c_int64), ("evaluated_pairs", ctypes.c_int64), ("kappa_rechecks", ctypes.c_int64),
+        ("clamped", ctypes.c_int64),
+        ("ms_prep", ctypes.c_float), ("ms_dup", ctypes.c_float), ("ms_sort", ctypes.c_float),
+        ("ms_render", ctypes.c_float), ("ms_total", ctypes.c_float), ("ms_backward", ctypes.c_float),
+    ]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class GeerError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load libgeer_b200.so; raises ImportError (never falls back) if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_2505_24053_b200.build` "
+                              "(there is no CPU fallback for the render path)")
+        lib = ctypes.CDLL(LIB_PATH)
+        P, I, I64, F, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float, ctypes.c_double
+        sig = {
+            "geer_abi_version": ([], I),
+            "geer_last_error": ([], ctypes.c_char_p),
+            "geer_create": ([I], P),
+            "geer_destroy": ([P], None),
+            "geer_set_timing": ([P, I], I),
+            "geer_forward": ([P, P, P, P, P, P, P, P], I),
+            "geer_backward": ([P, P, P, I, P], I),
+            "geer_frame_stats": ([P, P], I),
+            "geer_graph_info": ([P, P, P, P], I),
+            "geer_graph_export": ([P, P, P, P, P, P, P, P, P, P, P], I),
+            "geer_build_graph_host": ([P, P, P, D, ctypes.c_int32], I),
+            "geer_render_host": ([P, P, P, P, P, P, P], I),
+            "geer_render_backward_host": ([P, P, P, P, P, P], I),
+            "geer_l1_grad": ([P, P, P, P, I64, F, P], I),
+            "geer_adam": ([P, P, P, P, P, I64, F, F, F, ctypes.c_int32, P], I),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    msg = load().geer_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(code: int) -> None:
+    """Map a geer_status to the reference's exception types (association.py:155-160)."""
+    if code == GEER_OK:
+        return
+    msg = last_error()
+    if code in (GEER_ERR_INVALID, GEER_ERR_NOT_PD, GEER_ERR_NOT_SYMMETRIC):
+        raise ValueError(msg)
+    if code == GEER_ERR_NOMEM:
+        raise MemoryError(msg)
+    raise GeerError(code, msg)
+
+
+def camera_struct(camera) -> GeerCamera:
+    c = GeerCamera()
+    c.width = int(camera.width)
+    c.height = int(camera.height)
+    c.model = MODEL_IDS[camera.model]
+    c.rotation[:] = [float(v) for v in np.asarray(camera.rotation, dtype=np.float64).ravel()]
+    c.translation[:] = [float(v) for v in np.asarray(camera.translation, dtype=np.float64).ravel()]
+    nan = float("nan")
+    opt = lambda v: float(v) if v is not None else nan
+    c.fov_x, c.fov_y = opt(camera.fov_x), opt(camera.fov_y)
+    c.fx, c.fy, c.cx, c.cy = opt(camera.fx), opt(camera.fy), opt(camera.cx), opt(camera.cy)
+    c.k[:] = [float(v) for v in np.asarray(getattr(camera, "k", np.zeros(4)), dtype=np.float64).ravel()]
+    return c
+
+
+def config_struct(config) -> GeerConfig:
+    g = GeerConfig()
+    g.lam = float(config.lam)
+    g.background[:] = [float(v) for v in np.asarray(config.background, dtype=np.float64).reshape(3)]
+    g.tile_px = int(config.tile_px)
+    g.support_cutoff = 1 if config.support_cutoff else 0
+    g.threads = int(getattr(config, "threads", 1) or 0)
+    return g
+
+
+class Context:
+    """Owns one geer_ctx (device workspaces + the state of its last forward)."""
+
+    def __init__(self, device: int = 0):
+        lib = load()
+        self._lib = lib
+        self.device = device
+        self.ptr = lib.geer_create(device)
+        if not self.ptr:
+            raise GeerError(GEER_ERR_CUDA, last_error() or "geer_create failed (no CUDA device?)")
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            self._lib.geer_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_timing(self, on: bool):
+        check(self._lib.geer_set_timing(self.ptr, 1 if on else 0))
+
+    def stats(self) -> dict:
+        s = GeerStats()
+        check(self._lib.geer_frame_stats(self.ptr, ctypes.byref(s)))
+        return s.as_dict()
+
+
+_default: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    """Per-device context used by the reference-compatible host API."""
+    ctx = _default.get(device)
+    if ctx is None:
+        ctx = Context(device)
+        _default[device] = ctx
+    return ctx

@@ -1,0 +1,716 @@
+// geer_api.cu — the extern "C" boundary (include/geer.h) and the per-frame driver.
+//
+// Frame pipeline on one stream (stage names follow SPEC.md:575,602):
+//   prep : K0 camera setup + K1 per-Gaussian preprocess
+//   dup  : depth-order sort of Gaussians, count scan, one 12-byte D2H
+//          (entry total + error flag), load-balanced emit
+//   sort : tile radix sort + per-tile ranges
+//   render: K5 raster
+// The backward (K6 + K7) reuses the forward's graph, payload and per-pixel
+// (n_eval, remaining) state held in the context.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <cmath>
+#include <string>
+
+#include "geer_common.cuh"
+#include "geer_kernels.h"
+
+using namespace geer;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define GEER_CUDA(call)                                                                          \
+    do {                                                                                         \
+        cudaError_t e_ = (call);                                                                 \
+        if (e_ != cudaSuccess)                                                                   \
+            return fail(GEER_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));          \
+    } while (0)
+
+struct Buf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+
+}  // namespace
+
+struct geer_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    bool timing = false;
+    cudaEvent_t ev[6] = {};
+    // frame state
+    FrameConst fc{};
+    geer_scene scene{};
+    bool have_frame = false;
+    bool have_raster = false;
+    int64_t n_entries = 0;
+    int max_items = 0;
+    const float *fwd_remaining = nullptr;  // remaining written by the last forward (backward input)
+    float ms[6] = {};
+    unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs
+    int *d_err = nullptr;
+    int64_t *h_hdr = nullptr;  // pinned: [0] total entries, [1] error code
+    // camera buffers
+    Buf col_sc, row_sc, medges_x, medges_y, edges_x, edges_y, dir64, theta, phi, minmax, pixel_tile, pixel_tile_sorted,
+        pix_iota, pix_list, tile_count, tile_off, item_count, item_off, items, n_items;
+    // per-Gaussian buffers
+    Buf payload, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, cnt_sorted, offs, ranges_ax, flags, mu_c,
+        depth;
+    // per-entry buffers
+    Buf tile_keys, tile_keys_sorted, gids, order, tile_ranges;
+    // per-pixel buffers
+    Buf color, remaining, count_px, n_eval, dl32;
+    // backward
+    Buf accum;
+    // temp
+    Buf temp;
+    // host-path staging
+    Buf h64_means, h64_log, h64_quats, h64_op, h64_sh, s32_means, s32_log, s32_quats, s32_op, s32_sh, out64, g64;
+};
+
+namespace {
+
+template <typename T>
+T *ensure(Buf &b, size_t count, int *rc) {
+    size_t bytes = count * sizeof(T);
+    if (bytes == 0) bytes = 16;
+    if (bytes > b.cap) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+        size_t want = bytes + bytes / 4;
+        if (cudaMalloc(&b.p, want) != cudaSuccess) {
+            cudaGetLastError();
+            if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+                cudaGetLastError();
+                *rc = fail(GEER_ERR_NOMEM, "cudaMalloc of %zu bytes failed", bytes);
+                return nullptr;
+            }
+            want = bytes;
+        }
+        b.cap = want;
+    }
+    return reinterpret_cast<T *>(b.p);
+}
+
+#define ENSURE(T, buf, n)                       \
+    ensure<T>((buf), (size_t)(n), &rc);         \
+    if (rc) return rc
+
+void free_buf(Buf &b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+}
+
+int make_frame_const(const geer_camera *cam, const geer_config *cfg, int n_bands, FrameConst *fc) {
+    if (!cam || !cfg) return fail(GEER_ERR_INVALID, "camera and config are required");
+    if (cam->width <= 0 || cam->height <= 0) return fail(GEER_ERR_INVALID, "image size must be positive");
+    if (cam->model < 0 || cam->model > 2) return fail(GEER_ERR_INVALID, "unknown camera model %d", cam->model);
+    if (cfg->tile_px <= 0) return fail(GEER_ERR_INVALID, "tile_px must be positive");
+    if ((int64_t)cam->width * cam->height >= (int64_t)1 << 31) return fail(GEER_ERR_INVALID, "image too large");
+    memset(fc, 0, sizeof(*fc));
+    fc->width = cam->width;
+    fc->height = cam->height;
+    fc->model = cam->model;
+    fc->tile_px = cfg->tile_px;
+    fc->n_x = (cam->width + cfg->tile_px - 1) / cfg->tile_px;   // association.py:308
+    fc->n_y = (cam->height + cfg->tile_px - 1) / cfg->tile_px;  // association.py:309
+    if (fc->n_x < 1) fc->n_x = 1;
+    if (fc->n_y < 1) fc->n_y = 1;
+    if (fc->n_x >= 65535 || fc->n_y >= 65535) return fail(GEER_ERR_INVALID, "too many tiles per axis");
+    fc->n_tiles = fc->n_x * fc->n_y;
+    fc->n_bands = n_bands;
+    fc->cutoff = cfg->support_cutoff ? 1 : 0;
+    for (int i = 0; i < 9; ++i) fc->R[i] = cam->rotation[i];
+    for (int i = 0; i < 3; ++i) fc->t[i] = cam->translation[i];
+    // camera.py:71-74: o = -R^T t
+    for (int j = 0; j < 3; ++j)
+        fc->origin[j] = -std::fma(cam->rotation[2 * 3 + j], cam->translation[2],
+                                  std::fma(cam->rotation[1 * 3 + j], cam->translation[1],
+                                           cam->rotation[0 * 3 + j] * cam->translation[0]));  // numpy matmul rounding
+    fc->fov_x = cam->fov_x;
+    fc->fov_y = cam->fov_y;
+    fc->fx = cam->fx;
+    fc->fy = cam->fy;
+    fc->cx = cam->cx;
+    fc->cy = cam->cy;
+    for (int i = 0; i < 4; ++i) fc->k[i] = cam->k[i];
+    fc->lam = cfg->lam;
+    fc->lam2 = cfg->lam * cfg->lam;
+    fc->lam2f = (float)fc->lam2;
+    for (int i = 0; i < 3; ++i) fc->bg[i] = (float)cfg->background[i];
+    return GEER_OK;
+}
+
+// K0: camera setup into ctx buffers (tile CSR + work items).
+int camera_setup(geer_ctx *c, bool want_pixel_tile, cudaStream_t st) {
+    int rc = 0;
+    FrameConst &fc = c->fc;
+    const int64_t npx = (int64_t)fc.width * fc.height;
+    int32_t *tile_off = ENSURE(int32_t, c->tile_off, fc.n_tiles + 1);
+    int32_t *pix_list = ENSURE(int32_t, c->pix_list, npx);
+    double *mex = ENSURE(double, c->medges_x, fc.n_x + 1);
+    double *mey = ENSURE(double, c->medges_y, fc.n_y + 1);
+    if (fc.model == GEER_BEAP) {
+        double2 *col = ENSURE(double2, c->col_sc, fc.width);
+        double2 *row = ENSURE(double2, c->row_sc, fc.height);
+        int32_t *pt = nullptr;
+        if (want_pixel_tile) {
+            pt = ENSURE(int32_t, c->pixel_tile, npx);
+        }
+        launch_beap_setup(fc, col, row, mex, mey, tile_off, pix_list, pt, st);
+    } else {
+        double *dir = ENSURE(double, c->dir64, npx * 3);
+        double *th = ENSURE(double, c->theta, npx);
+        double *ph = ENSURE(double, c->phi, npx);
+        long long *mm = ENSURE(long long, c->minmax, 4);
+        double *ex = ENSURE(double, c->edges_x, fc.n_x + 1);
+        double *ey = ENSURE(double, c->edges_y, fc.n_y + 1);
+        int32_t *pt = ENSURE(int32_t, c->pixel_tile, npx);
+        int32_t *pts = ENSURE(int32_t, c->pixel_tile_sorted, npx);
+        int32_t *iota = ENSURE(int32_t, c->pix_iota, npx);
+        int32_t *tcnt = ENSURE(int32_t, c->tile_count, fc.n_tiles + 1);
+        const long long init[4] = {0x7FFFFFFFFFFFFFFFLL, (long long)0x8000000000000000ULL, 0x7FFFFFFFFFFFFFFFLL,
+                                   (long long)0x8000000000000000ULL};
+        GEER_CUDA(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, st));
+        GEER_CUDA(cudaMemsetAsync(tcnt, 0, sizeof(int32_t) * (fc.n_tiles + 1), st));
+        launch_cam_pixels(fc, dir, th, ph, mm, st);
+        launch_cam_edges(fc, mm, ex, ey, mex, mey, st);
+        launch_cam_bin(fc, th, ph, ex, ey, pt, tcnt, st);
+        launch_iota(iota, npx, st);
+        int bits = ceil_log2(fc.n_tiles);
+        size_t tb = sort_pixels_temp_bytes(npx, bits);
+        size_t sb = scan_i32_temp_bytes(fc.n_tiles + 1);
+        void *tmp = ENSURE(char, c->temp, tb > sb ? tb : sb);
+        sort_pixels(tmp, tb, pt, pts, iota, pix_list, npx, bits, st);
+        exclusive_scan_i32(tmp, sb, tcnt, tile_off, fc.n_tiles + 1, st);
+    }
+    int32_t *icnt = ENSURE(int32_t, c->item_count, fc.n_tiles);
+    int32_t *ioff = ENSURE(int32_t, c->item_off, fc.n_tiles);
+    c->max_items = (int)(fc.n_tiles + (npx + kRasterThreads - 1) / kRasterThreads);
+    int4 *items = ENSURE(int4, c->items, c->max_items);
+    int32_t *nit = ENSURE(int32_t, c->n_items, 1);
+    launch_items(fc.n_tiles, tile_off, icnt, st);
+    size_t sb = scan_i32_temp_bytes(fc.n_tiles);
+    void *tmp = ENSURE(char, c->temp, sb);
+    exclusive_scan_i32(tmp, sb, icnt, ioff, fc.n_tiles, st);
+    launch_item_fill(fc.n_tiles, tile_off, ioff, items, nit, st);
+    return GEER_OK;
+}
+
+// Full association (+ raster when color != null) for the scene in c->scene.
+int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, bool want_export, cudaStream_t st) {
+    int rc = 0;
+    FrameConst &fc = c->fc;
+    const geer_scene &sc = c->scene;
+    const int64_t n = sc.n;
+    const int64_t npx = (int64_t)fc.width * fc.height;
+    c->have_frame = false;
+    c->have_raster = false;
+    if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
+    GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 2 * sizeof(unsigned long long), st));
+    GEER_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
+    rc = camera_setup(c, want_export, st);
+    if (rc) return rc;
+
+    // ---- K1 preprocess
+    Payload *payload = ENSURE(Payload, c->payload, n);
+    uint32_t *dkey = ENSURE(uint32_t, c->depth_key, n);
+    uint32_t *dkey_s = ENSURE(uint32_t, c->depth_key_sorted, n);
+    int32_t *giota = ENSURE(int32_t, c->gid_iota, n);
+    int32_t *gsorted = ENSURE(int32_t, c->gid_sorted, n);
+    int64_t *cnt = ENSURE(int64_t, c->count, n);
+    int64_t *cnts = ENSURE(int64_t, c->cnt_sorted, n);
+    int64_t *offs = ENSURE(int64_t, c->offs, n + 1);
+    AxisRanges *ar = ENSURE(AxisRanges, c->ranges_ax, n);
+    uint8_t *flags = ENSURE(uint8_t, c->flags, n);
+    double *mu = nullptr, *dep = nullptr;
+    if (want_export) {
+        mu = ENSURE(double, c->mu_c, n * 3);
+        dep = ENSURE(double, c->depth, n);
+    }
+    int32_t *ranges = ENSURE(int32_t, c->tile_ranges, fc.n_tiles + 1);
+    launch_preprocess(fc, sc, (const double *)c->medges_x.p, (const double *)c->medges_y.p, payload, dkey, cnt, ar,
+                      flags, mu, dep, c->d_err, st);
+    if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[1], st));
+
+    // ---- dup: depth order, scan, header D2H, emit
+    int64_t total = 0;
+    if (n > 0) {
+        launch_iota(giota, n, st);
+        size_t b1 = sort_depth_temp_bytes(n), b2 = scan_temp_bytes(n);
+        void *tmp = ENSURE(char, c->temp, b1 > b2 ? b1 : b2);
+        sort_depth(tmp, b1, dkey, dkey_s, giota, gsorted, n, st);
+        gather_counts(gsorted, cnt, cnts, n, st);
+        GEER_CUDA(cudaMemsetAsync(offs, 0, sizeof(int64_t), st));
+        inclusive_scan_i64(tmp, b2, cnts, offs + 1, n, st);
+        GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[0], offs + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    } else {
+        c->h_hdr[0] = 0;
+    }
+    GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[1], c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GEER_CUDA(cudaStreamSynchronize(st));
+    int err = (int)(c->h_hdr[1] & 0xFFFFFFFF);
+    if (err == GEER_ERR_NOT_PD) return fail(GEER_ERR_NOT_PD, "view covariance must be positive definite");
+    if (err == GEER_ERR_NOT_SYMMETRIC) return fail(GEER_ERR_NOT_SYMMETRIC, "view covariance must be symmetric");
+    if (err) return fail(GEER_ERR_INVALID, "preprocess error %d", err);
+    total = c->h_hdr[0];
+    if (total >= ((int64_t)1 << 31) - 1)
+        return fail(GEER_ERR_NOMEM, "render graph has %lld entries (limit 2^31)", (long long)total);
+    c->n_entries = total;
+    uint32_t *tk = ENSURE(uint32_t, c->tile_keys, total);
+    uint32_t *tks = ENSURE(uint32_t, c->tile_keys_sorted, total);
+    uint32_t *gids = ENSURE(uint32_t, c->gids, total);
+    uint32_t *order = ENSURE(uint32_t, c->order, total);
+    emit_entries(offs, gsorted, ar, fc.n_x, total, n, tk, gids, st);
+    if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[2], st));
+
+    // ---- sort: stable tile sort + ranges
+    if (total > 0) {
+        int bits = ceil_log2(fc.n_tiles);
+        size_t b = sort_tiles_temp_bytes(total, bits);
+        void *tmp = ENSURE(char, c->temp, b);
+        sort_tiles(tmp, b, tk, tks, gids, order, total, bits, st);
+    }
+    tile_ranges(tks, total, fc.n_tiles, ranges, st);
+    if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[3], st));
+    c->have_frame = true;
+
+    // ---- render
+    if (color) {
+        int32_t *ne = ENSURE(int32_t, c->n_eval, npx);
+        launch_forward(fc, sc, c->max_items, (const int4 *)c->items.p, (const int32_t *)c->n_items.p,
+                       (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
+                       (const double *)c->dir64.p, ranges, order, payload, color, remaining, count, ne,
+                       c->d_counters, st);
+        c->fwd_remaining = remaining;
+        c->have_raster = true;
+    }
+    if (c->timing) {
+        GEER_CUDA(cudaEventRecord(c->ev[4], st));
+        GEER_CUDA(cudaEventSynchronize(c->ev[4]));
+        cudaEventElapsedTime(&c->ms[0], c->ev[0], c->ev[1]);
+        cudaEventElapsedTime(&c->ms[1], c->ev[1], c->ev[2]);
+        cudaEventElapsedTime(&c->ms[2], c->ev[2], c->ev[3]);
+        cudaEventElapsedTime(&c->ms[3], c->ev[3], c->ev[4]);
+        cudaEventElapsedTime(&c->ms[4], c->ev[0], c->ev[4]);
+    }
+    GEER_CUDA(cudaGetLastError());
+    return GEER_OK;
+}
+
+int run_backward(geer_ctx *c, const float *dl_dimage, bool f64_out, void *const *gout, int accumulate, cudaStream_t st) {
+    int rc = 0;
+    if (!c->have_raster) return fail(GEER_ERR_STATE, "geer_backward needs a preceding geer_forward with a raster");
+    FrameConst &fc = c->fc;
+    const geer_scene &sc = c->scene;
+    if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
+    float4 *accum = ENSURE(float4, c->accum, sc.n * 4);
+    if (sc.n > 0) GEER_CUDA(cudaMemsetAsync(accum, 0, sizeof(float4) * 4 * sc.n, st));
+    launch_backward(fc, sc, c->max_items, (const int4 *)c->items.p, (const int32_t *)c->n_items.p,
+                    (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
+                    (const double *)c->dir64.p, (const int32_t *)c->tile_ranges.p, (const uint32_t *)c->order.p,
+                    (const Payload *)c->payload.p, c->fwd_remaining, (const int32_t *)c->n_eval.p,
+                    dl_dimage, accum, st);
+    if (f64_out)
+        launch_finalize<double>(fc, sc, accum, (const uint8_t *)c->flags.p, (double *)gout[0], (double *)gout[1],
+                                (double *)gout[2], (double *)gout[3], (double *)gout[4], accumulate, st);
+    else
+        launch_finalize<float>(fc, sc, accum, (const uint8_t *)c->flags.p, (float *)gout[0], (float *)gout[1],
+                               (float *)gout[2], (float *)gout[3], (float *)gout[4], accumulate, st);
+    if (c->timing) {
+        GEER_CUDA(cudaEventRecord(c->ev[1], st));
+        GEER_CUDA(cudaEventSynchronize(c->ev[1]));
+        cudaEventElapsedTime(&c->ms[5], c->ev[0], c->ev[1]);
+    }
+    GEER_CUDA(cudaGetLastError());
+    return GEER_OK;
+}
+
+int check_scene_dev(const geer_scene *s) {
+    if (!s) return fail(GEER_ERR_INVALID, "scene is required");
+    if (s->n < 0) return fail(GEER_ERR_INVALID, "negative Gaussian count");
+    if (s->n >= ((int64_t)1 << 31)) return fail(GEER_ERR_INVALID, "too many Gaussians");
+    // renderer.py:66-68 uses sh_basis(d)[:n_bands]: any 1..16 bands evaluate, more cannot
+    if (s->n_bands < 1 || s->n_bands > 16)
+        return fail(GEER_ERR_INVALID, "unsupported SH band count %d; at most 16 bands (degree 3)", s->n_bands);
+    if (s->n > 0 && (!s->means || !s->log_scales || !s->quats || !s->opacity_logits || !s->sh))
+        return fail(GEER_ERR_INVALID, "scene pointers must be non-null");
+    return GEER_OK;
+}
+
+// Copy a host f64 scene into device fp32 buffers held by the context.
+int upload_host_scene(geer_ctx *c, const geer_host_scene *hs, cudaStream_t st) {
+    int rc = 0;
+    if (!hs) return fail(GEER_ERR_INVALID, "scene is required");
+    const int64_t n = hs->n;
+    if (n < 0 || n >= ((int64_t)1 << 31)) return fail(GEER_ERR_INVALID, "bad Gaussian count");
+    const int64_t nsh = n * hs->n_bands * 3;
+    double *dm = ENSURE(double, c->h64_means, n * 3);
+    double *dl = ENSURE(double, c->h64_log, n * 3);
+    double *dq = ENSURE(double, c->h64_quats, n * 4);
+    double *dop = ENSURE(double, c->h64_op, n);
+    double *dsh = ENSURE(double, c->h64_sh, nsh);
+    float *m = ENSURE(float, c->s32_means, n * 3);
+    float *l = ENSURE(float, c->s32_log, n * 3);
+    float *q = ENSURE(float, c->s32_quats, n * 4);
+    float *op = ENSURE(float, c->s32_op, n);
+    float *sh = ENSURE(float, c->s32_sh, nsh);
+    if (n > 0) {
+        GEER_CUDA(cudaMemcpyAsync(dm, hs->means, sizeof(double) * n * 3, cudaMemcpyHostToDevice, st));
+        GEER_CUDA(cudaMemcpyAsync(dl, hs->log_scales, sizeof(double) * n * 3, cudaMemcpyHostToDevice, st));
+        GEER_CUDA(cudaMemcpyAsync(dq, hs->quats, sizeof(double) * n * 4, cudaMemcpyHostToDevice, st));
+        GEER_CUDA(cudaMemcpyAsync(dop, hs->opacity_logits, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        GEER_CUDA(cudaMemcpyAsync(dsh, hs->sh, sizeof(double) * nsh, cudaMemcpyHostToDevice, st));
+        launch_convert_f64_f32(dm, m, n * 3, st);
+        launch_convert_f64_f32(dl, l, n * 3, st);
+        launch_convert_f64_f32(dq, q, n * 4, st);
+        launch_convert_f64_f32(dop, op, n, st);
+        launch_convert_f64_f32(dsh, sh, nsh, st);
+    }
+    geer_scene s;
+    s.n = n;
+    s.n_bands = hs->n_bands;
+    s.pad_ = 0;
+    s.means = m;
+    s.log_scales = l;
+    s.quats = q;
+    s.opacity_logits = op;
+    s.sh = sh;
+    rc = check_scene_dev(&s);
+    if (rc) return rc;
+    c->scene = s;
+    return GEER_OK;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+
+extern "C" {
+
+int geer_abi_version(void) { return GEER_ABI_VERSION; }
+
+const char *geer_last_error(void) { return g_last_error.c_str(); }
+
+geer_ctx *geer_create(int device) {
+    if (cudaSetDevice(device) != cudaSuccess) {
+        cudaGetLastError();
+        fail(GEER_ERR_CUDA, "cudaSetDevice(%d) failed", device);
+        return nullptr;
+    }
+    geer_ctx *c = new geer_ctx();
+    c->device = device;
+    bool ok = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) == cudaSuccess;
+    for (int i = 0; i < 6 && ok; ++i) ok = cudaEventCreate(&c->ev[i]) == cudaSuccess;
+    ok = ok && cudaMalloc(&c->d_counters, 2 * sizeof(unsigned long long)) == cudaSuccess;
+    ok = ok && cudaMalloc(&c->d_err, sizeof(int)) == cudaSuccess;
+    ok = ok && cudaMallocHost(&c->h_hdr, 2 * sizeof(int64_t)) == cudaSuccess;
+    if (!ok) {
+        fail(GEER_ERR_CUDA, "context creation failed: %s", cudaGetErrorString(cudaGetLastError()));
+        geer_destroy(c);
+        return nullptr;
+    }
+    return c;
+}
+
+void geer_destroy(geer_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+    Buf *bufs[] = {&c->col_sc, &c->row_sc, &c->medges_x, &c->medges_y, &c->edges_x, &c->edges_y, &c->dir64,
+                   &c->theta, &c->phi, &c->minmax, &c->pixel_tile, &c->pixel_tile_sorted, &c->pix_iota, &c->pix_list,
+                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->payload,
+                   &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted, &c->count, &c->cnt_sorted,
+                   &c->offs, &c->ranges_ax, &c->flags, &c->mu_c, &c->depth, &c->tile_keys, &c->tile_keys_sorted,
+                   &c->gids, &c->order, &c->tile_ranges, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32,
+                   &c->accum, &c->temp, &c->h64_means, &c->h64_log, &c->h64_quats, &c->h64_op, &c->h64_sh,
+                   &c->s32_means, &c->s32_log, &c->s32_quats, &c->s32_op, &c->s32_sh, &c->out64, &c->g64};
+    for (Buf *b : bufs) free_buf(*b);
+    for (int i = 0; i < 6; ++i)
+        if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    if (c->d_counters) cudaFree(c->d_counters);
+    if (c->d_err) cudaFree(c->d_err);
+    if (c->h_hdr) cudaFreeHost(c->h_hdr);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+}
+
+int geer_set_timing(geer_ctx *c, int enable) {
+    if (!c) return fail(GEER_ERR_INVALID, "null context");
+    c->timing = enable != 0;
+    return GEER_OK;
+}
+
+int geer_forward(geer_ctx *c, const geer_scene *scene, const geer_camera *camera, const geer_config *config,
+                 float *color, float *remaining, int32_t *count, void *stream) {
+    if (!c) return fail(GEER_ERR_INVALID, "null context");
+    int rc = check_scene_dev(scene);
+    if (rc) return rc;
+    if (!color || !remaining || !count) return fail(GEER_ERR_INVALID, "output buffers must be non-null");
+    rc = make_frame_const(camera, config, scene->n_bands, &c->fc);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    c->scene = *scene;
+    if (scene->n == 0) {
+        // renderer.py:131-138: empty scene renders the background
+        int32_t *ne = ensure<int32_t>(c->n_eval, (size_t)c->fc.width * c->fc.height, &rc);
+        if (rc) return rc;
+        launch_fill_background(c->fc, color, remaining, count, ne, st);
+        c->have_frame = false;
+        c->have_raster = false;
+        c->n_entries = 0;
+        GEER_CUDA(cudaGetLastError());
+        return GEER_OK;
+    }
+    return run_forward(c, color, remaining, count, false, st);
+}
+
+int geer_backward(geer_ctx *c, const float *dl_dimage, const geer_grads *grads, int accumulate, void *stream) {
+    if (!c) return fail(GEER_ERR_INVALID, "null context");
+    if (!grads || !dl_dimage) return fail(GEER_ERR_INVALID, "dl_dimage and grads are required");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c->scene.n == 0) return GEER_OK;  // renderer.py:248-249
+    void *g[5] = {grads->dmeans, grads->dlog_scales, grads->dquats, grads->dopacities, grads->dsh};
+    for (int i = 0; i < 5; ++i)
+        if (!g[i]) return fail(GEER_ERR_INVALID, "gradient pointers must be non-null");
+    return run_backward(c, dl_dimage, false, g, accumulate & (GEER_ACCUMULATE | GEER_OPACITY_LOGIT), st);
+}
+
+int geer_frame_stats(geer_ctx *c, geer_stats *out) {
+    if (!c || !out) return fail(GEER_ERR_INVALID, "null argument");
+    memset(out, 0, sizeof(*out));
+    out->n_gaussians = c->scene.n;
+    out->n_entries = c->n_entries;
+    out->n_tiles = c->fc.n_tiles;
+    if (c->have_raster) {
+        cudaStream_t st = c->own_stream;
+        GEER_CUDA(cudaDeviceSynchronize());
+        GEER_CUDA(cudaMemsetAsync(c->d_counters + 1, 0, sizeof(unsigned long long), st));
+        launch_sum_i32((const int32_t *)c->n_eval.p, (int64_t)c->fc.width * c->fc.height, c->d_counters + 1, st);
+        unsigned long long h[2];
+        int32_t nit = 0;
+        GEER_CUDA(cudaMemcpyAsync(h, c->d_counters, sizeof(h), cudaMemcpyDeviceToHost, st));
+        GEER_CUDA(cudaMemcpyAsync(&nit, c->n_items.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        GEER_CUDA(cudaStreamSynchronize(st));
+        out->kappa_rechecks = (int64_t)h[0];
+        out->evaluated_pairs = (int64_t)h[1];
+        out->n_work_items = nit;
+    }
+    if (c->have_frame && c->scene.n > 0) {
+        // clamped & kept count from the flags
+        int64_t n = c->scene.n;
+        uint8_t *hf = (uint8_t *)malloc((size_t)n);
+        if (hf) {
+            if (cudaMemcpy(hf, c->flags.p, (size_t)n, cudaMemcpyDeviceToHost) == cudaSuccess) {
+                int64_t k = 0;
+                for (int64_t i = 0; i < n; ++i) k += (hf[i] & 3) == 3;
+                out->clamped = k;
+            }
+            free(hf);
+        }
+    }
+    out->ms_prep = c->ms[0];
+    out->ms_dup = c->ms[1];
+    out->ms_sort = c->ms[2];
+    out->ms_render = c->ms[3];
+    out->ms_total = c->ms[4];
+    out->ms_backward = c->ms[5];
+    return GEER_OK;
+}
+
+int geer_graph_info(geer_ctx *c, int64_t *n_entries, int32_t *n_x, int32_t *n_y) {
+    if (!c) return fail(GEER_ERR_INVALID, "null context");
+    if (n_entries) *n_entries = c->n_entries;
+    if (n_x) *n_x = c->fc.n_x;
+    if (n_y) *n_y = c->fc.n_y;
+    return GEER_OK;
+}
+
+static int d2h_u32_as_i64(const void *dev, int64_t *host, int64_t n) {
+    if (!host || n <= 0) return GEER_OK;
+    uint32_t *tmp = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)n);
+    if (!tmp) return fail(GEER_ERR_NOMEM, "host allocation failed");
+    cudaError_t e = cudaMemcpy(tmp, dev, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+        free(tmp);
+        return fail(GEER_ERR_CUDA, "graph export copy failed: %s", cudaGetErrorString(e));
+    }
+    for (int64_t i = 0; i < n; ++i) host[i] = (int64_t)tmp[i];
+    free(tmp);
+    return GEER_OK;
+}
+
+int geer_graph_export(geer_ctx *c, int64_t *order, int64_t *entry_tile, int64_t *ranges, double *mu_c, double *depth,
+                      uint8_t *keep, uint8_t *clamped, int64_t *pixel_tile, double *medges_x, double *medges_y) {
+    if (!c) return fail(GEER_ERR_INVALID, "null context");
+    if (!c->have_frame) return fail(GEER_ERR_STATE, "no render graph: run a forward or geer_build_graph_host first");
+    GEER_CUDA(cudaDeviceSynchronize());
+    const FrameConst &fc = c->fc;
+    const int64_t n = c->scene.n, E = c->n_entries, npx = (int64_t)fc.width * fc.height;
+    int rc = d2h_u32_as_i64(c->order.p, order, E);
+    if (rc) return rc;
+    rc = d2h_u32_as_i64(c->tile_keys_sorted.p, entry_tile, E);
+    if (rc) return rc;
+    if (ranges) {
+        rc = d2h_u32_as_i64(c->tile_ranges.p, ranges, fc.n_tiles + 1);
+        if (rc) return rc;
+    }
+    if (pixel_tile) {
+        if (!c->pixel_tile.p) return fail(GEER_ERR_STATE, "pixel tiles were not recorded (use the host graph build)");
+        rc = d2h_u32_as_i64(c->pixel_tile.p, pixel_tile, npx);
+        if (rc) return rc;
+    }
+    if (mu_c) {
+        if (!c->mu_c.p) return fail(GEER_ERR_STATE, "camera-frame means were not recorded");
+        GEER_CUDA(cudaMemcpy(mu_c, c->mu_c.p, sizeof(double) * n * 3, cudaMemcpyDeviceToHost));
+    }
+    if (depth) {
+        if (!c->depth.p) return fail(GEER_ERR_STATE, "depths were not recorded");
+        GEER_CUDA(cudaMemcpy(depth, c->depth.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    }
+    if ((keep || clamped) && n > 0) {
+        uint8_t *hf = (uint8_t *)malloc((size_t)n);
+        if (!hf) return fail(GEER_ERR_NOMEM, "host allocation failed");
+        cudaError_t e = cudaMemcpy(hf, c->flags.p, (size_t)n, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) {
+            free(hf);
+            return fail(GEER_ERR_CUDA, "flag export failed: %s", cudaGetErrorString(e));
+        }
+        for (int64_t i = 0; i < n; ++i) {
+            if (keep) keep[i] = hf[i] & 1;
+            if (clamped) clamped[i] = (hf[i] >> 1) & 1;
+        }
+        free(hf);
+    }
+    if (medges_x) GEER_CUDA(cudaMemcpy(medges_x, c->medges_x.p, sizeof(double) * (fc.n_x + 1), cudaMemcpyDeviceToHost));
+    if (medges_y) GEER_CUDA(cudaMemcpy(medges_y, c->medges_y.p, sizeof(double) * (fc.n_y + 1), cudaMemcpyDeviceToHost));
+    return GEER_OK;
+}
+
+int geer_build_graph_host(geer_ctx *c, const geer_host_scene *scene, const geer_camera *camera, double lam,
+                          int32_t tile_px) {
+    if (!c) return fail(GEER_ERR_INVALID, "null context");
+    cudaStream_t st = c->own_stream;
+    int rc = upload_host_scene(c, scene, st);
+    if (rc) return rc;
+    geer_config cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.lam = lam;
+    cfg.tile_px = tile_px;
+    cfg.support_cutoff = 1;
+    rc = make_frame_const(camera, &cfg, scene->n_bands, &c->fc);
+    if (rc) return rc;
+    rc = run_forward(c, nullptr, nullptr, nullptr, true, st);
+    if (rc) return rc;
+    GEER_CUDA(cudaStreamSynchronize(st));
+    return GEER_OK;
+}
+
+// Forward into context-owned fp32 buffers (host paths).
+static int host_forward(geer_ctx *c, const geer_host_scene *scene, const geer_camera *camera,
+                        const geer_config *config, cudaStream_t st) {
+    int rc = upload_host_scene(c, scene, st);
+    if (rc) return rc;
+    rc = make_frame_const(camera, config, scene->n_bands, &c->fc);
+    if (rc) return rc;
+    const int64_t npx = (int64_t)c->fc.width * c->fc.height;
+    float *col = ensure<float>(c->color, (size_t)npx * 3, &rc);
+    if (rc) return rc;
+    float *rem = ensure<float>(c->remaining, (size_t)npx, &rc);
+    if (rc) return rc;
+    int32_t *cnt = ensure<int32_t>(c->count_px, (size_t)npx, &rc);
+    if (rc) return rc;
+    if (scene->n == 0) {
+        int32_t *ne = ensure<int32_t>(c->n_eval, (size_t)npx, &rc);
+        if (rc) return rc;
+        launch_fill_background(c->fc, col, rem, cnt, ne, st);
+        c->have_frame = c->have_raster = false;
+        c->n_entries = 0;
+        GEER_CUDA(cudaGetLastError());
+        return GEER_OK;
+    }
+    return run_forward(c, col, rem, cnt, false, st);
+}
+
+int geer_render_host(geer_ctx *c, const geer_host_scene *scene, const geer_camera *camera, const geer_config *config,
+                     double *color, double *remaining, int64_t *count) {
+    if (!c) return fail(GEER_ERR_INVALID, "null context");
+    if (!color || !remaining || !count) return fail(GEER_ERR_INVALID, "output buffers must be non-null");
+    cudaStream_t st = c->own_stream;
+    int rc = host_forward(c, scene, camera, config, st);
+    if (rc) return rc;
+    const int64_t npx = (int64_t)c->fc.width * c->fc.height;
+    // convert on device, then one D2H per output (renderer.py:39-44 dtypes: f64, f64, i64)
+    char *o = ensure<char>(c->out64, (size_t)npx * (3 * 8 + 8 + 8), &rc);
+    if (rc) return rc;
+    double *c64 = (double *)o;
+    double *r64 = c64 + npx * 3;
+    int64_t *n64 = (int64_t *)(r64 + npx);
+    launch_convert_f32_f64((const float *)c->color.p, c64, npx * 3, st);
+    launch_convert_f32_f64((const float *)c->remaining.p, r64, npx, st);
+    launch_convert_i32_i64((const int32_t *)c->count_px.p, n64, npx, st);
+    GEER_CUDA(cudaMemcpyAsync(color, c64, sizeof(double) * npx * 3, cudaMemcpyDeviceToHost, st));
+    GEER_CUDA(cudaMemcpyAsync(remaining, r64, sizeof(double) * npx, cudaMemcpyDeviceToHost, st));
+    GEER_CUDA(cudaMemcpyAsync(count, n64, sizeof(int64_t) * npx, cudaMemcpyDeviceToHost, st));
+    GEER_CUDA(cudaStreamSynchronize(st));
+    return GEER_OK;
+}
+
+int geer_render_backward_host(geer_ctx *c, const geer_host_scene *scene, const geer_camera *camera,
+                              const double *dl_dimage, const geer_config *config, const geer_host_grads *grads) {
+    if (!c) return fail(GEER_ERR_INVALID, "null context");
+    if (!dl_dimage || !grads) return fail(GEER_ERR_INVALID, "dl_dimage and grads are required");
+    cudaStream_t st = c->own_stream;
+    int rc = host_forward(c, scene, camera, config, st);
+    if (rc) return rc;
+    const int64_t n = scene->n, nb = scene->n_bands, npx = (int64_t)c->fc.width * c->fc.height;
+    const int64_t sizes[5] = {n * 3, n * 3, n * 4, n, n * nb * 3};
+    double *hout[5] = {grads->dmeans, grads->dlog_scales, grads->dquats, grads->dopacities, grads->dsh};
+    if (n == 0) return GEER_OK;
+    for (int i = 0; i < 5; ++i)
+        if (!hout[i]) return fail(GEER_ERR_INVALID, "gradient pointers must be non-null");
+    // dl_dimage f64 host -> f32 device
+    double *dl64 = ensure<double>(c->out64, (size_t)npx * 3, &rc);
+    if (rc) return rc;
+    float *dl32 = ensure<float>(c->dl32, (size_t)npx * 3, &rc);
+    if (rc) return rc;
+    GEER_CUDA(cudaMemcpyAsync(dl64, dl_dimage, sizeof(double) * npx * 3, cudaMemcpyHostToDevice, st));
+    launch_convert_f64_f32(dl64, dl32, npx * 3, st);
+    int64_t tot = 0;
+    for (int i = 0; i < 5; ++i) tot += sizes[i];
+    double *g = ensure<double>(c->g64, (size_t)tot, &rc);
+    if (rc) return rc;
+    void *gp[5];
+    int64_t off = 0;
+    for (int i = 0; i < 5; ++i) {
+        gp[i] = g + off;
+        off += sizes[i];
+    }
+    rc = run_backward(c, dl32, true, gp, 0, st);
+    if (rc) return rc;
+    for (int i = 0; i < 5; ++i)
+        GEER_CUDA(cudaMemcpyAsync(hout[i], gp[i], sizeof(double) * sizes[i], cudaMemcpyDeviceToHost, st));
+    GEER_CUDA(cudaStreamSynchronize(st));
+    return GEER_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,768 @@
+// geer_geometry.cu — fp64 per-camera and per-Gaussian stages.
+//
+//   K0  camera setup: BEAP trig tables / pinhole+KB per-pixel rays, CSF tile
+//       edges in mirror space, pixel -> tile CSR, raster work items
+//       (camera.py:119-190,213-282; association.py:91-105,301-332)
+//   K1  per-Gaussian preprocess: view transform, PD check, PBF roots, mirror
+//       arcs, tile ranges, depth key, fp32 raster payload, SH colour
+//       (scene.py:17-80; association.py:82-88,129-224,343-350,373-451;
+//        renderer.py:57-81)
+//   K7  per-Gaussian backward finalisation (renderer.py:204-231,320-332)
+//
+// This translation unit is compiled with -fmad=false: every fp64 expression
+// rounds exactly like the numpy statement it restates (no contraction), so
+// the association decisions (tile sets, clamps, depth keys) are the
+// reference's bit for bit except at enumerated ulp ties.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "geer_common.cuh"
+#include "geer_kernels.h"
+
+namespace geer {
+
+// ---------------------------------------------------------------- shared math
+
+__device__ __forceinline__ double beap_center_angle(int idx, int n, double fov) {
+    return ((idx + 0.5) - (n + 1) / 2.0) * fov / n;  // camera.py:126-127
+}
+__device__ __forceinline__ double beap_edge_angle(int idx, int n, double fov) {
+    return (idx - (n + 1) / 2.0) * fov / n;  // camera.py:136-137
+}
+__device__ __forceinline__ double mirror_from_angle(double theta) {  // association.py:91-105
+    double denom = cos(theta) + 1.0;
+    if (fabs(denom) < 1e-300) return theta >= 0 ? INFINITY : -INFINITY;
+    return sin(theta) / denom;
+}
+
+// camera.py:213-219 / 249-269: camera-space unit ray of a pinhole or KB pixel
+__device__ void unproject(const FrameConst &fc, int x, int y, double out[3]) {
+    double u = ((double)x - fc.cx) / fc.fx;
+    double v = ((double)y - fc.cy) / fc.fy;
+    if (fc.model == GEER_PINHOLE) {
+        double n = sqrt(u * u + v * v + 1.0 * 1.0);
+        out[0] = u / n;
+        out[1] = v / n;
+        out[2] = 1.0 / n;
+        return;
+    }
+    const double *k = fc.k;
+    double alpha_d = sqrt(u * u + v * v);
+    double alpha = alpha_d;
+    for (int it = 0; it < 20; ++it) {
+        double a2 = alpha * alpha;
+        double f = alpha * (1.0 + a2 * (k[0] + a2 * (k[1] + a2 * (k[2] + a2 * k[3])))) - alpha_d;
+        double df = 1.0 + a2 * (3 * k[0] + a2 * (5 * k[1] + a2 * (7 * k[2] + a2 * 9 * k[3])));
+        alpha = alpha - f / df;
+    }
+    double scale = alpha_d > 1e-12 ? sin(alpha) / fmax(alpha_d, 1e-300) : 1.0;
+    double dx = u * scale, dy = v * scale, dz = cos(alpha);
+    double n = sqrt(dx * dx + dy * dy + dz * dz);
+    out[0] = dx / n;
+    out[1] = dy / n;
+    out[2] = dz / n;
+}
+
+// numpy matmul's length-3 dot product: fma(a2, b2, fma(a1, b1, a0 * b0)) (see oracle/geer_oracle.c mm3)
+__device__ __forceinline__ double mm3(double a0, double b0, double a1, double b1, double a2, double b2) {
+    return __fma_rn(a2, b2, __fma_rn(a1, b1, a0 * b0));
+}
+
+__device__ __forceinline__ long long ordered_bits(double x) {
+    long long i = __double_as_longlong(x);
+    return i >= 0 ? i : i ^ 0x7FFFFFFFFFFFFFFFLL;
+}
+__device__ __forceinline__ double from_ordered_bits(long long i) {
+    return __longlong_as_double(i >= 0 ? i : i ^ 0x7FFFFFFFFFFFFFFFLL);
+}
+
+// ---------------------------------------------------------------- K0: BEAP
+
+// Per-column (sin, cos) of theta and per-row (sin, cos) of phi, plus mirror edges.
+__global__ void k_beap_tables(FrameConst fc, double2 *col_sc, double2 *row_sc, double *medges_x, double *medges_y) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < fc.width) {
+        double th = beap_center_angle(i, fc.width, fc.fov_x);
+        col_sc[i] = make_double2(sin(th), cos(th));
+    }
+    if (i < fc.height) {
+        double ph = beap_center_angle(i, fc.height, fc.fov_y);
+        row_sc[i] = make_double2(sin(ph), cos(ph));
+    }
+    if (i <= fc.n_x) {
+        int idx = min(i * fc.tile_px, fc.width);
+        medges_x[i] = mirror_from_angle(beap_edge_angle(idx, fc.width, fc.fov_x));
+    }
+    if (i <= fc.n_y) {
+        int idx = min(i * fc.tile_px, fc.height);
+        medges_y[i] = mirror_from_angle(beap_edge_angle(idx, fc.height, fc.fov_y));
+    }
+}
+
+// BEAP tiles are tile_px x tile_px pixel blocks (association.py:310-316).  Pixel
+// list of a tile: contiguous block, ordered so that each warp covers an 8x4
+// patch of a 16x16 tile (coherent early stop); other sizes row-major.
+__global__ void k_beap_csr(FrameConst fc, int32_t *tile_off, int32_t *pix_list, int32_t *pixel_tile) {
+    int t = blockIdx.x;
+    int tx = t % fc.n_x, ty = t / fc.n_x;
+    int tp = fc.tile_px;
+    int x0 = tx * tp, y0 = ty * tp;
+    // association.py:314-315: the last tile absorbs nothing extra (n = ceil), so sizes are clipped
+    int w = min(tp, fc.width - x0), h = min(tp, fc.height - y0);
+    int64_t base = (int64_t)y0 * fc.width + (int64_t)h * x0;
+    if (threadIdx.x == 0) {
+        tile_off[t] = (int32_t)base;
+        if (t == fc.n_tiles - 1) tile_off[fc.n_tiles] = fc.width * fc.height;
+    }
+    int cnt = w * h;
+    bool swz = (tp == 16 && w == 16 && h == 16);
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+        int lx, ly;
+        if (swz) {
+            int warp = q >> 5, lane = q & 31;
+            lx = (warp & 1) * 8 + (lane & 7);
+            ly = (warp >> 1) * 4 + (lane >> 3);
+        } else {
+            lx = q % w;
+            ly = q / w;
+        }
+        int p = (y0 + ly) * fc.width + (x0 + lx);
+        pix_list[base + q] = p;
+        if (pixel_tile) pixel_tile[p] = t;
+    }
+}
+
+// ---------------------------------------------------------------- K0: pinhole / KB
+
+// Per-pixel world ray (fp64), principal angles (camera.py:158-172) and their min/max.
+__global__ void k_cam_pixels(FrameConst fc, double *dir64, double *theta, double *phi, long long *minmax) {
+    int64_t npx = (int64_t)fc.width * fc.height;
+    double tmin = INFINITY, tmax = -INFINITY, pmin = INFINITY, pmax = -INFINITY;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npx; p += (int64_t)gridDim.x * blockDim.x) {
+        int x = (int)(p % fc.width), y = (int)(p / fc.width);
+        double dc[3];
+        unproject(fc, x, y, dc);
+        for (int j = 0; j < 3; ++j)
+            dir64[p * 3 + j] = mm3(dc[0], fc.R[0 * 3 + j], dc[1], fc.R[1 * 3 + j], dc[2], fc.R[2 * 3 + j]);
+        double th = atan2(dc[0], dc[2]), ph;
+        if (dc[2] == 0.0)
+            ph = dc[1] == 0.0 ? 0.0 : (dc[1] > 0 ? M_PI / 2 : -M_PI / 2);
+        else if (dc[2] > 0)
+            ph = atan2(dc[1], dc[2]);
+        else
+            ph = atan(dc[1] / dc[2]);
+        theta[p] = th;
+        phi[p] = ph;
+        tmin = fmin(tmin, th);
+        tmax = fmax(tmax, th);
+        pmin = fmin(pmin, ph);
+        pmax = fmax(pmax, ph);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+        tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+        pmin = fmin(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+        pmax = fmax(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&minmax[0], ordered_bits(tmin));
+        atomicMax(&minmax[1], ordered_bits(tmax));
+        atomicMin(&minmax[2], ordered_bits(pmin));
+        atomicMax(&minmax[3], ordered_bits(pmax));
+    }
+}
+
+// numpy.linspace(min - 1e-9, max + 1e-9, n + 1) (association.py:320-322) + mirror edges.
+__global__ void k_cam_edges(FrameConst fc, const long long *minmax, double *edges_x, double *edges_y,
+                            double *medges_x, double *medges_y) {
+    const double pad = 1e-9;
+    for (int axis = 0; axis < 2; ++axis) {
+        double lo = from_ordered_bits(minmax[axis * 2 + 0]) - pad;
+        double hi = from_ordered_bits(minmax[axis * 2 + 1]) + pad;
+        int num = (axis == 0 ? fc.n_x : fc.n_y) + 1;
+        double *e = axis == 0 ? edges_x : edges_y;
+        double *m = axis == 0 ? medges_x : medges_y;
+        int div = num - 1;
+        double delta = hi - lo;
+        double step = delta / div;
+        for (int i = threadIdx.x; i < num; i += blockDim.x) {
+            double y = (double)i;
+            if (step == 0.0) {
+                y = y / div;
+                y = y * delta;
+            } else {
+                y = y * step;
+            }
+            double v = y + lo;
+            if (i == num - 1) v = hi;
+            e[i] = v;
+            m[i] = mirror_from_angle(v);
+        }
+    }
+}
+
+__device__ __forceinline__ int ss_right(const double *a, int n, double v) {  // #(a <= v)
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] <= v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ int ss_left(const double *a, int n, double v) {  // #(a < v)
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// association.py:323-325: pixel -> tile by centre angle
+__global__ void k_cam_bin(FrameConst fc, const double *theta, const double *phi, const double *edges_x,
+                          const double *edges_y, int32_t *pixel_tile, int32_t *tile_count) {
+    int64_t npx = (int64_t)fc.width * fc.height;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npx; p += (int64_t)gridDim.x * blockDim.x) {
+        int c = ss_right(edges_x, fc.n_x + 1, theta[p]) - 1;
+        int r = ss_right(edges_y, fc.n_y + 1, phi[p]) - 1;
+        c = min(max(c, 0), fc.n_x - 1);
+        r = min(max(r, 0), fc.n_y - 1);
+        int t = r * fc.n_x + c;
+        pixel_tile[p] = t;
+        atomicAdd(&tile_count[t], 1);
+    }
+}
+
+__global__ void k_iota(int32_t *v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = (int32_t)i;
+}
+
+// ---------------------------------------------------------------- work items
+
+// items per tile = ceil(pixels / 256) (0 for pixel-less tiles)
+__global__ void k_item_counts(int n_tiles, const int32_t *tile_off, int32_t *item_count) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n_tiles) {
+        int c = tile_off[t + 1] - tile_off[t];
+        item_count[t] = (c + kRasterThreads - 1) / kRasterThreads;
+    }
+}
+__global__ void k_item_fill(int n_tiles, const int32_t *tile_off, const int32_t *item_off, int4 *items,
+                            int32_t *n_items) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n_tiles) {
+        int c = tile_off[t + 1] - tile_off[t];
+        int k0 = item_off[t];
+        for (int k = 0; k * kRasterThreads < c; ++k)
+            items[k0 + k] = make_int4(t, tile_off[t] + k * kRasterThreads, min(kRasterThreads, c - k * kRasterThreads), 0);
+        if (t == n_tiles - 1) *n_items = item_off[t] + (c + kRasterThreads - 1) / kRasterThreads;
+    }
+}
+
+// ---------------------------------------------------------------- K1
+
+__device__ __forceinline__ void quat_rot(const float *q4, double rot[9]) {  // scene.py:17-32
+    double q0 = q4[0], q1 = q4[1], q2 = q4[2], q3 = q4[3];
+    double n = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+    double r = q0 / n, i = q1 / n, j = q2 / n, k = q3 / n;
+    rot[0] = 1 - 2 * (j * j + k * k);
+    rot[1] = 2 * (i * j - r * k);
+    rot[2] = 2 * (i * k + r * j);
+    rot[3] = 2 * (i * j + r * k);
+    rot[4] = 1 - 2 * (i * i + k * k);
+    rot[5] = 2 * (j * k - r * i);
+    rot[6] = 2 * (i * k - r * j);
+    rot[7] = 2 * (j * k + r * i);
+    rot[8] = 1 - 2 * (i * i + j * j);
+}
+
+__device__ __forceinline__ double sigmoid(double x) {  // core.py:58-67
+    if (x >= 0) return 1.0 / (1.0 + exp(-x));
+    double e = exp(x);
+    return e / (1.0 + e);
+}
+
+// core.py:289-313
+__device__ __forceinline__ void sh_basis(double x, double y, double z, double b[16]) {
+    const double C0 = 0.28209479177387814, C1 = 0.4886025119029199;
+    const double C2_0 = 1.0925484305920792, C2_1 = -1.0925484305920792, C2_2 = 0.31539156525252005,
+                 C2_3 = -1.0925484305920792, C2_4 = 0.5462742152960396;
+    const double C3_0 = -0.5900435899266435, C3_1 = 2.890611442640554, C3_2 = -0.4570457994644658,
+                 C3_3 = 0.3731763325901154, C3_4 = -0.4570457994644658, C3_5 = 1.445305721320277,
+                 C3_6 = -0.5900435899266435;
+    double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    b[0] = C0;
+    b[1] = -C1 * y;
+    b[2] = C1 * z;
+    b[3] = -C1 * x;
+    b[4] = C2_0 * xy;
+    b[5] = C2_1 * yz;
+    b[6] = C2_2 * (2.0 * zz - xx - yy);
+    b[7] = C2_3 * xz;
+    b[8] = C2_4 * (xx - yy);
+    b[9] = C3_0 * y * (3.0 * xx - yy);
+    b[10] = C3_1 * xy * z;
+    b[11] = C3_2 * y * (4.0 * zz - xx - yy);
+    b[12] = C3_3 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    b[13] = C3_4 * x * (4.0 * zz - xx - yy);
+    b[14] = C3_5 * z * (xx - yy);
+    b[15] = C3_6 * x * (xx - 3.0 * yy);
+}
+
+// association.py:129-145
+__device__ __forceinline__ bool quadratic_roots(double a, double b_half, double c, double &r0, double &r1) {
+    double disc = b_half * b_half - a * c;
+    if (disc < 0) return false;
+    double sq = sqrt(disc);
+    double q = b_half >= 0 ? b_half + sq : b_half - sq;
+    if (q == 0.0) {
+        if (a == 0.0) return false;
+        double r = fabs(sq / a);
+        r0 = -r;
+        r1 = r;
+        return true;
+    }
+    double x0 = q / a, x1 = c / q;
+    r0 = x1 < x0 ? x1 : x0;
+    r1 = x1 < x0 ? x0 : x1;
+    return true;
+}
+
+// association.py:108-126
+__device__ __forceinline__ void mirror_candidates(double t, double &a, double &b) {
+    double denom = 1.0 + 1.0 * 1.0 * sqrt(1.0 + t * t);
+    double m = t / denom;
+    if (fabs(denom) < 1e-300) m = t >= 0 ? INFINITY : -INFINITY;
+    if (m == 0.0) {
+        a = 0.0;
+        b = INFINITY;
+    } else {
+        a = m;
+        b = -1.0 / m;
+    }
+}
+
+__device__ __forceinline__ void cswap(double &a, double &b) {
+    if (b < a) {
+        double t = a;
+        a = b;
+        b = t;
+    }
+}
+
+// association.py:189-217 + :373-388 + union (:435-446): merged disjoint tile-index ranges of one axis.
+// Returns the tile count; ranges packed lo | hi << 16 (empty slots = 0).
+__device__ int axis_tiles(double t_aa, double t_a2, double t22, double r0, double r1, const double *edges, int n_edges,
+                          uint32_t out[3]) {
+    double c[4];
+    mirror_candidates(r0, c[0], c[1]);
+    mirror_candidates(r1, c[2], c[3]);
+    // sorting network (np.sort; +inf sorts last)
+    cswap(c[0], c[1]);
+    cswap(c[2], c[3]);
+    cswap(c[0], c[2]);
+    cswap(c[1], c[3]);
+    cswap(c[1], c[2]);
+    double lo_mid = isfinite(c[1]) ? c[1] : -1e12;
+    double hi_mid = isfinite(c[2]) ? c[2] : 1e12;
+    double probe = 0.5 * (lo_mid + hi_mid);
+    double q;
+    if (!isfinite(probe) || fabs(1.0 - probe * probe) < 1e-12) {
+        q = t22;
+    } else {
+        double cc = 2.0 * probe / (1.0 - probe * probe);
+        q = t22 * cc * cc - 2.0 * t_a2 * cc + t_aa;
+    }
+    double ilo[3], ihi[3];
+    int ni;
+    if (q >= 0) {
+        ilo[0] = c[1]; ihi[0] = c[2];
+        ilo[1] = c[3]; ihi[1] = INFINITY;
+        ilo[2] = -INFINITY; ihi[2] = c[0];
+        ni = 3;
+    } else {
+        ilo[0] = c[0]; ihi[0] = c[1];
+        ilo[1] = c[2]; ihi[1] = c[3];
+        ni = 2;
+    }
+    const double wlo = edges[0], whi = edges[n_edges - 1];
+    int a0[3], a1[3], na = 0;
+    for (int k = 0; k < ni; ++k) {
+        double lo2 = wlo > ilo[k] ? wlo : ilo[k];
+        double hi2 = whi < ihi[k] ? whi : ihi[k];
+        if (lo2 > hi2) continue;
+        int i0 = max(ss_right(edges, n_edges, lo2) - 1, 0);
+        int i1 = min(ss_left(edges, n_edges, hi2), n_edges - 1);
+        if (i0 >= i1) continue;
+        a0[na] = i0;
+        a1[na] = i1;
+        ++na;
+    }
+    // sort by start, merge overlapping/adjacent
+    for (int i = 1; i < na; ++i)
+        for (int j = i; j > 0 && a0[j] < a0[j - 1]; --j) {
+            int t0 = a0[j]; a0[j] = a0[j - 1]; a0[j - 1] = t0;
+            int t1 = a1[j]; a1[j] = a1[j - 1]; a1[j - 1] = t1;
+        }
+    int nm = 0, cnt = 0;
+    int m0[3], m1[3];
+    for (int i = 0; i < na; ++i) {
+        if (nm > 0 && a0[i] <= m1[nm - 1]) {
+            m1[nm - 1] = max(m1[nm - 1], a1[i]);
+        } else {
+            m0[nm] = a0[i];
+            m1[nm] = a1[i];
+            ++nm;
+        }
+    }
+    for (int i = 0; i < 3; ++i) {
+        if (i < nm) {
+            out[i] = (uint32_t)m0[i] | ((uint32_t)m1[i] << 16);
+            cnt += m1[i] - m0[i];
+        } else {
+            out[i] = 0;
+        }
+    }
+    return cnt;
+}
+
+// Conservative bound on |kappa_fp32 - kappa_exact| near kappa = lam^2 for the raster's fp32
+// evaluation (d_u = W d, m = o_u x d_u, kappa = |m|^2/|d_u|^2 with fp32-rounded W, o_u, d).
+// Rounding analysis (u = 2^-24): |d_u| >= 1/s_max, |dW d| <= 4u ||W||_F, so
+//   d sqrt(kappa) <= u (|o_u| (3 + 4 sqrt3 cond) + 12 sqrt3 cond),  d kappa <= 2 sqrt(kappa) d sqrt(kappa),
+// doubled for safety.  Pairs with |kappa_fp32 - lam^2| <= band are re-decided in fp64.
+__device__ __forceinline__ float kappa_band(double ou_norm, double cond, double lam) {
+    const double u = 5.9604644775390625e-08;
+    double dsk = u * (ou_norm * (3.0 + 6.9282032302755 * cond) + 20.784609690826528 * cond);
+    double band = 2.0 * (2.0 * lam * dsk + 4.0 * u * lam * lam);
+    return (float)band;
+}
+
+__global__ void __launch_bounds__(128) k_preprocess(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x,
+                                                    const double *__restrict__ medges_y, Payload *__restrict__ payload,
+                                                    uint32_t *__restrict__ depth_key, int64_t *__restrict__ count,
+                                                    AxisRanges *__restrict__ ranges, uint8_t *__restrict__ flags,
+                                                    double *__restrict__ mu_out, double *__restrict__ depth_out,
+                                                    int *__restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *sex = reinterpret_cast<double *>(smem_raw);
+    double *sey = sex + (fc.n_x + 1);
+    float *ssh = reinterpret_cast<float *>(sey + (fc.n_y + 1));
+    const int nb3 = sc.n_bands * 3;
+    for (int i = threadIdx.x; i <= fc.n_x; i += blockDim.x) sex[i] = medges_x[i];
+    for (int i = threadIdx.x; i <= fc.n_y; i += blockDim.x) sey[i] = medges_y[i];
+    // stage this block's SH block (contiguous) into smem with coalesced loads
+    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
+    const int cnt_b = (int)min((int64_t)blockDim.x, sc.n - g0);
+    {
+        const float *src = sc.sh + g0 * nb3;
+        const int total = cnt_b * nb3;
+        if ((((uintptr_t)src) & 15) == 0 && (total & 3) == 0) {
+            const float4 *s4 = reinterpret_cast<const float4 *>(src);
+            float4 *d4 = reinterpret_cast<float4 *>(ssh);
+            for (int i = threadIdx.x; i < total / 4; i += blockDim.x) d4[i] = __ldg(s4 + i);
+        } else {
+            for (int i = threadIdx.x; i < total; i += blockDim.x) ssh[i] = __ldg(src + i);
+        }
+    }
+    __syncthreads();
+    const int64_t g = g0 + threadIdx.x;
+    if (g >= sc.n) return;
+
+    const double *R = fc.R;
+    double mean[3] = {sc.means[g * 3 + 0], sc.means[g * 3 + 1], sc.means[g * 3 + 2]};
+    float q4[4] = {sc.quats[g * 4 + 0], sc.quats[g * 4 + 1], sc.quats[g * 4 + 2], sc.quats[g * 4 + 3]};
+    double rot[9], s[3];
+    quat_rot(q4, rot);
+    for (int i = 0; i < 3; ++i) s[i] = exp((double)sc.log_scales[g * 3 + i]);
+    // association.py:84-87
+    double mu[3];
+    for (int i = 0; i < 3; ++i) mu[i] = mm3(mean[0], R[i * 3 + 0], mean[1], R[i * 3 + 1], mean[2], R[i * 3 + 2]) + fc.t[i];
+    double m[9], cov[9], covc[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) m[i * 3 + j] = rot[i * 3 + j] * s[j];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            cov[i * 3 + j] = mm3(m[i * 3 + 0], m[j * 3 + 0], m[i * 3 + 1], m[j * 3 + 1], m[i * 3 + 2], m[j * 3 + 2]);
+    for (int i = 0; i < 3; ++i)
+        for (int l = 0; l < 3; ++l) {
+            double acc = 0.0;
+            for (int j = 0; j < 3; ++j)
+                for (int k = 0; k < 3; ++k) acc += R[i * 3 + j] * cov[j * 3 + k] * R[l * 3 + k];
+            covc[i * 3 + l] = acc;
+        }
+    double depth = sqrt(mu[0] * mu[0] + mu[1] * mu[1] + mu[2] * mu[2]);
+    if (mu_out) {
+        for (int i = 0; i < 3; ++i) mu_out[g * 3 + i] = mu[i];
+        depth_out[g] = depth;
+    }
+
+    // fp32 raster payload (renderer.py:78-80): W = S^-1 R^T, o_u = W (o - mean), rgb, sigma
+    double W[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) W[i * 3 + j] = rot[j * 3 + i] / s[i];
+    double rel[3] = {fc.origin[0] - mean[0], fc.origin[1] - mean[1], fc.origin[2] - mean[2]};
+    double ou[3];
+    for (int i = 0; i < 3; ++i) ou[i] = W[i * 3 + 0] * rel[0] + W[i * 3 + 1] * rel[1] + W[i * 3 + 2] * rel[2];
+    double sigma = sigmoid((double)sc.opacity_logits[g]);
+    // renderer.py:57-70 sh_colors
+    double vd[3] = {mean[0] - fc.origin[0], mean[1] - fc.origin[1], mean[2] - fc.origin[2]};
+    double vn = sqrt(vd[0] * vd[0] + vd[1] * vd[1] + vd[2] * vd[2]);
+    vn = vn > 1e-12 ? vn : 1e-12;
+    double basis[16];
+    sh_basis(vd[0] / vn, vd[1] / vn, vd[2] / vn, basis);
+    const float *shg = ssh + threadIdx.x * nb3;
+    double rgb[3];
+    uint8_t gate = 0;
+    for (int c = 0; c < 3; ++c) {
+        double pre = 0.0;
+        for (int b = 0; b < sc.n_bands; ++b) pre += basis[b] * (double)shg[b * 3 + c];
+        pre += 0.5;
+        if (pre > 0) gate |= (uint8_t)(1u << c);
+        rgb[c] = pre > 0.0 ? pre : 0.0;
+    }
+    double ou_norm = sqrt(ou[0] * ou[0] + ou[1] * ou[1] + ou[2] * ou[2]);
+    double smax = fmax(s[0], fmax(s[1], s[2])), smin = fmin(s[0], fmin(s[1], s[2]));
+    Payload pl;
+    pl.r0 = make_float4((float)W[0], (float)W[1], (float)W[2], (float)ou[0]);
+    pl.r1 = make_float4((float)W[3], (float)W[4], (float)W[5], (float)ou[1]);
+    pl.r2 = make_float4((float)W[6], (float)W[7], (float)W[8], (float)ou[2]);
+    pl.col = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], (float)sigma);
+    pl.ext = make_float4(kappa_band(ou_norm, smax / smin, fc.lam), 0.f, 0.f, 0.f);
+    payload[g] = pl;
+
+    uint8_t fl = (uint8_t)(gate << 3);
+    int64_t n_ent = 0;
+    AxisRanges ar;
+    for (int i = 0; i < 3; ++i) ar.x[i] = ar.y[i] = 0;
+    // association.py:417-419 near cull
+    if (depth >= kNearLimit) {
+        // association.py:154-160 symmetric + positive-definite (Cholesky pivots)
+        double amax = 0.0, dmax = 0.0;
+        for (int i = 0; i < 9; ++i) amax = fmax(amax, fabs(covc[i]));
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) dmax = fmax(dmax, fabs(covc[i * 3 + j] - covc[j * 3 + i]));
+        bool ok = true;
+        if (dmax > 1e-9 * fmax(amax, 1e-300)) {
+            atomicMax(err, (int)GEER_ERR_NOT_SYMMETRIC);
+            ok = false;
+        } else {
+            // np.linalg.cholesky (LAPACK potf2, lower) operation sequence: reciprocal-pivot column
+            // scaling and fma dot products (see oracle/geer_oracle.c)
+            double a00 = covc[0];
+            bool pd = a00 > 0.0;
+            if (pd) {
+                double l00 = sqrt(a00), r0 = 1.0 / l00;
+                double l10 = covc[3] * r0, l20 = covc[6] * r0;
+                double a11 = covc[4] - l10 * l10;
+                pd = a11 > 0.0;
+                if (pd) {
+                    double l11 = sqrt(a11);
+                    double l21 = (covc[7] - l20 * l10) * (1.0 / l11);
+                    double a22 = covc[8] - __fma_rn(l21, l21, l20 * l20);
+                    pd = a22 > 0.0;
+                }
+            }
+            if (!pd) {
+                atomicMax(err, (int)GEER_ERR_NOT_PD);
+                ok = false;
+            }
+        }
+        if (ok) {
+            const double lam2 = fc.lam * fc.lam;
+            double t00 = lam2 * covc[0] - mu[0] * mu[0];
+            double t02 = lam2 * covc[2] - mu[0] * mu[2];
+            double t11 = lam2 * covc[4] - mu[1] * mu[1];
+            double t12 = lam2 * covc[5] - mu[1] * mu[2];
+            double t22 = lam2 * covc[8] - mu[2] * mu[2];
+            double scale = fmax(fmax(fmax(fabs(t00), fabs(t02)), fmax(fabs(t11), fabs(t12))), fmax(fabs(t22), 1e-300));
+            bool clamped = false;
+            double rt0 = 0, rt1 = 0, rp0 = 0, rp1 = 0;
+            if (fabs(t22) < 1e-12 * scale) {
+                clamped = true;
+            } else {
+                bool okt = quadratic_roots(t22, t02, t00, rt0, rt1);
+                bool okp = quadratic_roots(t22, t12, t11, rp0, rp1);
+                clamped = !okt || !okp;
+            }
+            bool keep = !(clamped && sigma < kMinClampedOpacity);  // association.py:343-350
+            if (clamped) fl |= 2;
+            if (keep) {
+                fl |= 1;
+                if (clamped) {  // association.py:430-433: every tile
+                    ar.x[0] = (uint32_t)fc.n_x << 16;
+                    ar.y[0] = (uint32_t)fc.n_y << 16;
+                    n_ent = (int64_t)fc.n_x * fc.n_y;
+                } else {
+                    int cx = axis_tiles(t00, t02, t22, rt0, rt1, sex, fc.n_x + 1, ar.x);
+                    int cy = axis_tiles(t11, t12, t22, rp0, rp1, sey, fc.n_y + 1, ar.y);
+                    n_ent = (int64_t)cx * cy;
+                }
+            }
+        }
+    }
+    count[g] = n_ent;
+    ranges[g] = ar;
+    flags[g] = fl;
+    // association.py:335-340 key bits (depth > 0): f32 bits | 0x80000000; non-emitting last
+    uint32_t kb = __float_as_uint((float)depth) | 0x80000000u;
+    depth_key[g] = n_ent > 0 ? kb : 0xFFFFFFFFu;
+}
+
+// ---------------------------------------------------------------- K7
+
+// accum layout per Gaussian (16 f32): dW_rc (9, row-major), sum dl/do_u (3), sum dsigma, sum dcol (3)
+template <typename T>
+__global__ void __launch_bounds__(128) k_finalize(FrameConst fc, geer_scene sc, const float4 *__restrict__ accum,
+                                                  const uint8_t *__restrict__ flags, T *dmeans, T *dlog_scales,
+                                                  T *dquats, T *dopac, T *dsh, int accumulate) {
+    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= sc.n) return;
+    float a[16];
+    for (int i = 0; i < 4; ++i) {
+        float4 v = accum[g * 4 + i];
+        a[i * 4 + 0] = v.x;
+        a[i * 4 + 1] = v.y;
+        a[i * 4 + 2] = v.z;
+        a[i * 4 + 3] = v.w;
+    }
+    double mean[3] = {sc.means[g * 3 + 0], sc.means[g * 3 + 1], sc.means[g * 3 + 2]};
+    float q4[4] = {sc.quats[g * 4 + 0], sc.quats[g * 4 + 1], sc.quats[g * 4 + 2], sc.quats[g * 4 + 3]};
+    double rot[9], s[3], W[9];
+    quat_rot(q4, rot);
+    for (int i = 0; i < 3; ++i) s[i] = exp((double)sc.log_scales[g * 3 + i]);
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) W[i * 3 + j] = rot[j * 3 + i] / s[i];
+    double rel[3] = {fc.origin[0] - mean[0], fc.origin[1] - mean[1], fc.origin[2] - mean[2]};
+    double dos[3] = {a[9], a[10], a[11]};
+    // renderer.py:304-307: dW = dW_rc + (sum dl/do) (o - mu)^T ; dmu = -W^T sum dl/do
+    double dw[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) dw[i * 3 + j] = (double)a[i * 3 + j] + dos[i] * rel[j];
+    double dmu[3];
+    for (int i = 0; i < 3; ++i) dmu[i] = -(W[0 * 3 + i] * dos[0] + W[1 * 3 + i] * dos[1] + W[2 * 3 + i] * dos[2]);
+    // renderer.py:204-231
+    double dls[3];
+    for (int k = 0; k < 3; ++k) {
+        double acc = dw[k * 3 + 0] * rot[0 * 3 + k] + dw[k * 3 + 1] * rot[1 * 3 + k] + dw[k * 3 + 2] * rot[2 * 3 + k];
+        dls[k] = (-acc / (s[k] * s[k])) * s[k];
+    }
+    double q0 = q4[0], q1 = q4[1], q2 = q4[2], q3 = q4[3];
+    double qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+    double r = q0 / qn, i = q1 / qn, j = q2 / qn, k = q3 / qn;
+    const double D[4][9] = {
+        {0, k, -j, -k, 0, i, j, -i, 0},
+        {0, j, k, j, -2 * i, r, k, -r, -2 * i},
+        {-2 * j, i, -r, i, 0, k, r, k, -2 * j},
+        {-2 * k, r, i, -r, -2 * k, j, i, j, 0},
+    };
+    double dqr[4];
+    for (int mm = 0; mm < 4; ++mm) {
+        double acc = 0.0;
+        for (int aa = 0; aa < 3; ++aa)
+            for (int bb = 0; bb < 3; ++bb) acc += dw[aa * 3 + bb] * (2.0 * D[mm][aa * 3 + bb] * (1.0 / s[aa]));
+        dqr[mm] = acc;
+    }
+    double qh[4] = {q0 / qn, q1 / qn, q2 / qn, q3 / qn};
+    double dot = dqr[0] * qh[0] + dqr[1] * qh[1] + dqr[2] * qh[2] + dqr[3] * qh[3];
+    // renderer.py:332 dsh = basis (x) (dcol * gate), view direction stop-gradient
+    double vd[3] = {mean[0] - fc.origin[0], mean[1] - fc.origin[1], mean[2] - fc.origin[2]};
+    double vn = sqrt(vd[0] * vd[0] + vd[1] * vd[1] + vd[2] * vd[2]);
+    vn = vn > 1e-12 ? vn : 1e-12;
+    double basis[16];
+    sh_basis(vd[0] / vn, vd[1] / vn, vd[2] / vn, basis);
+    uint8_t gate = flags[g] >> 3;
+    double dcol[3];
+    for (int c = 0; c < 3; ++c) dcol[c] = ((gate >> c) & 1) ? (double)a[13 + c] : 0.0;
+
+    const bool acc = accumulate & GEER_ACCUMULATE;
+    auto put = [&](T *p, int64_t idx, double v) { p[idx] = acc ? (T)((double)p[idx] + v) : (T)v; };
+    for (int c = 0; c < 3; ++c) put(dmeans, g * 3 + c, dmu[c]);
+    for (int c = 0; c < 3; ++c) put(dlog_scales, g * 3 + c, dls[c]);
+    for (int mm = 0; mm < 4; ++mm) put(dquats, g * 4 + mm, (dqr[mm] - dot * qh[mm]) / qn);
+    double dsig = (double)a[12];
+    if (accumulate & GEER_OPACITY_LOGIT) {  // trainer.py:208-217 stored_grads: chain through the logit
+        double sg = sigmoid((double)sc.opacity_logits[g]);
+        dsig = dsig * sg * (1.0 - sg);
+    }
+    put(dopac, g, dsig);
+    const int nb = sc.n_bands;
+    for (int b = 0; b < nb; ++b)
+        for (int c = 0; c < 3; ++c) put(dsh, (g * nb + b) * 3 + c, basis[b] * dcol[c]);
+}
+
+// ---------------------------------------------------------------- launchers
+
+void launch_beap_setup(const FrameConst &fc, double2 *col_sc, double2 *row_sc, double *medges_x, double *medges_y,
+                       int32_t *tile_off, int32_t *pix_list, int32_t *pixel_tile, cudaStream_t st) {
+    int n = max(max(fc.width, fc.height), max(fc.n_x, fc.n_y) + 1);
+    k_beap_tables<<<(n + 255) / 256, 256, 0, st>>>(fc, col_sc, row_sc, medges_x, medges_y);
+    k_beap_csr<<<fc.n_tiles, 256, 0, st>>>(fc, tile_off, pix_list, pixel_tile);
+}
+
+void launch_cam_pixels(const FrameConst &fc, double *dir64, double *theta, double *phi, long long *minmax,
+                       cudaStream_t st) {
+    int64_t npx = (int64_t)fc.width * fc.height;
+    int blocks = (int)lmin((npx + 255) / 256, 148 * 16);
+    k_cam_pixels<<<blocks, 256, 0, st>>>(fc, dir64, theta, phi, minmax);
+}
+
+void launch_cam_edges(const FrameConst &fc, const long long *minmax, double *edges_x, double *edges_y,
+                      double *medges_x, double *medges_y, cudaStream_t st) {
+    k_cam_edges<<<1, 256, 0, st>>>(fc, minmax, edges_x, edges_y, medges_x, medges_y);
+}
+
+void launch_cam_bin(const FrameConst &fc, const double *theta, const double *phi, const double *edges_x,
+                    const double *edges_y, int32_t *pixel_tile, int32_t *tile_count, cudaStream_t st) {
+    int64_t npx = (int64_t)fc.width * fc.height;
+    int blocks = (int)lmin((npx + 255) / 256, 148 * 16);
+    k_cam_bin<<<blocks, 256, 0, st>>>(fc, theta, phi, edges_x, edges_y, pixel_tile, tile_count);
+}
+
+void launch_iota(int32_t *v, int64_t n, cudaStream_t st) {
+    int blocks = (int)lmin((n + 255) / 256, 148 * 16);
+    if (blocks > 0) k_iota<<<blocks, 256, 0, st>>>(v, n);
+}
+
+void launch_items(int n_tiles, const int32_t *tile_off, int32_t *item_count, cudaStream_t st) {
+    k_item_counts<<<(n_tiles + 255) / 256, 256, 0, st>>>(n_tiles, tile_off, item_count);
+}
+void launch_item_fill(int n_tiles, const int32_t *tile_off, const int32_t *item_off, int4 *items, int32_t *n_items,
+                      cudaStream_t st) {
+    k_item_fill<<<(n_tiles + 255) / 256, 256, 0, st>>>(n_tiles, tile_off, item_off, items, n_items);
+}
+
+size_t preprocess_smem(const FrameConst &fc) {
+    return sizeof(double) * (fc.n_x + fc.n_y + 2) + sizeof(float) * 128 * fc.n_bands * 3 + 16;
+}
+
+void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
+                       Payload *payload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges, uint8_t *flags,
+                       double *mu_out, double *depth_out, int *err, cudaStream_t st) {
+    if (sc.n == 0) return;
+    size_t smem = preprocess_smem(fc);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_preprocess, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_set = true;
+    }
+    int blocks = (int)((sc.n + 127) / 128);
+    k_preprocess<<<blocks, 128, smem, st>>>(fc, sc, medges_x, medges_y, payload, depth_key, count, ranges, flags,
+                                            mu_out, depth_out, err);
+}
+
+template <typename T>
+void launch_finalize(const FrameConst &fc, const geer_scene &sc, const float4 *accum, const uint8_t *flags, T *dmeans,
+                     T *dlog_scales, T *dquats, T *dopac, T *dsh, int accumulate, cudaStream_t st) {
+    if (sc.n == 0) return;
+    int blocks = (int)((sc.n + 127) / 128);
+    k_finalize<T><<<blocks, 128, 0, st>>>(fc, sc, accum, flags, dmeans, dlog_scales, dquats, dopac, dsh, accumulate);
+}
+template void launch_finalize<float>(const FrameConst &, const geer_scene &, const float4 *, const uint8_t *, float *,
+                                     float *, float *, float *, float *, int, cudaStream_t);
+template void launch_finalize<double>(const FrameConst &, const geer_scene &, const float4 *, const uint8_t *,
+                                      double *, double *, double *, double *, double *, int, cudaStream_t);
+
+}  // namespace geer

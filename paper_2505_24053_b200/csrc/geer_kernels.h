@@ -1,0 +1,73 @@
+// geer_kernels.h — host-side launchers shared between the translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "geer_common.cuh"
+
+namespace geer {
+
+// geer_geometry.cu (fp64, -fmad=false)
+void launch_beap_setup(const FrameConst &fc, double2 *col_sc, double2 *row_sc, double *medges_x, double *medges_y,
+                       int32_t *tile_off, int32_t *pix_list, int32_t *pixel_tile, cudaStream_t st);
+void launch_cam_pixels(const FrameConst &fc, double *dir64, double *theta, double *phi, long long *minmax,
+                       cudaStream_t st);
+void launch_cam_edges(const FrameConst &fc, const long long *minmax, double *edges_x, double *edges_y,
+                      double *medges_x, double *medges_y, cudaStream_t st);
+void launch_cam_bin(const FrameConst &fc, const double *theta, const double *phi, const double *edges_x,
+                    const double *edges_y, int32_t *pixel_tile, int32_t *tile_count, cudaStream_t st);
+void launch_iota(int32_t *v, int64_t n, cudaStream_t st);
+void launch_items(int n_tiles, const int32_t *tile_off, int32_t *item_count, cudaStream_t st);
+void launch_item_fill(int n_tiles, const int32_t *tile_off, const int32_t *item_off, int4 *items, int32_t *n_items,
+                      cudaStream_t st);
+size_t preprocess_smem(const FrameConst &fc);
+void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
+                       Payload *payload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges, uint8_t *flags,
+                       double *mu_out, double *depth_out, int *err, cudaStream_t st);
+template <typename T>
+void launch_finalize(const FrameConst &fc, const geer_scene &sc, const float4 *accum, const uint8_t *flags, T *dmeans,
+                     T *dlog_scales, T *dquats, T *dopac, T *dsh, int accumulate, cudaStream_t st);
+
+// geer_sort.cu (association: depth order, scan, emit, tile sort, ranges)
+struct SortTemp {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+size_t sort_depth_temp_bytes(int64_t n);
+size_t scan_temp_bytes(int64_t n);
+size_t sort_tiles_temp_bytes(int64_t n_entries, int n_bits);
+size_t scan_i32_temp_bytes(int64_t n);
+void sort_depth(void *temp, size_t temp_bytes, const uint32_t *keys_in, uint32_t *keys_out, const int32_t *vals_in,
+                int32_t *vals_out, int64_t n, cudaStream_t st);
+void gather_counts(const int32_t *sorted_gid, const int64_t *count, int64_t *cnt_sorted, int64_t n, cudaStream_t st);
+void inclusive_scan_i64(void *temp, size_t temp_bytes, const int64_t *in, int64_t *out, int64_t n, cudaStream_t st);
+void exclusive_scan_i32(void *temp, size_t temp_bytes, const int32_t *in, int32_t *out, int64_t n, cudaStream_t st);
+void emit_entries(const int64_t *offs, const int32_t *sorted_gid, const AxisRanges *ranges, int n_x,
+                  int64_t n_entries, int64_t n, uint32_t *tile_keys, uint32_t *gids, cudaStream_t st);
+void sort_tiles(void *temp, size_t temp_bytes, const uint32_t *keys_in, uint32_t *keys_out, const uint32_t *vals_in,
+                uint32_t *vals_out, int64_t n, int n_bits, cudaStream_t st);
+void sort_pixels(void *temp, size_t temp_bytes, const int32_t *keys_in, int32_t *keys_out, const int32_t *vals_in,
+                 int32_t *vals_out, int64_t n, int n_bits, cudaStream_t st);
+size_t sort_pixels_temp_bytes(int64_t n, int n_bits);
+void tile_ranges(const uint32_t *sorted_tiles, int64_t n_entries, int n_tiles, int32_t *ranges, cudaStream_t st);
+
+// geer_raster.cu (fp32 raster forward / backward)
+void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
+                    const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
+                    const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
+                    float *color, float *remaining, int32_t *count, int32_t *n_eval,
+                    unsigned long long *rechecks, cudaStream_t st);
+void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
+                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
+                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
+                     const float *remaining, const int32_t *n_eval, const float *dl_dimage, float4 *accum,
+                     cudaStream_t st);
+void launch_sum_i32(const int32_t *v, int64_t n, unsigned long long *out, cudaStream_t st);
+void launch_convert_f64_f32(const double *in, float *out, int64_t n, cudaStream_t st);
+void launch_convert_f32_f64(const float *in, double *out, int64_t n, cudaStream_t st);
+void launch_convert_i32_i64(const int32_t *in, int64_t *out, int64_t n, cudaStream_t st);
+void launch_fill_background(const FrameConst &fc, float *color, float *remaining, int32_t *count, int32_t *n_eval,
+                            cudaStream_t st);
+
+}  // namespace geer

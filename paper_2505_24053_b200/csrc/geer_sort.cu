@@ -1,0 +1,177 @@
+// geer_sort.cu — association back half: depth order, scan, emit, tile sort, ranges.
+//
+// The reference orders entries by (tile, f32 depth bits, gid) (association.py:
+// 453-461: np.unique on (tile, gid) then a stable argsort of
+// key = tile << 32 | depth_sort_bits).  We get the same total order with far
+// less sort traffic:
+//   1. stable radix sort of the N per-Gaussian depth keys (values = gid, so
+//      equal depths stay in gid order);
+//   2. scan of the per-Gaussian entry counts in that depth order;
+//   3. load-balanced emit: one thread per entry writes (tile, gid), entries of
+//      each Gaussian contiguous, Gaussians in (depth, gid) order;
+//   4. stable radix sort on the tile id only (ceil(log2 n_tiles) bits,
+//      2 passes at 8,160 tiles instead of 6 passes over 45-bit keys);
+//   5. per-tile [start, end) ranges (association.py:466).
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "geer_common.cuh"
+#include "geer_kernels.h"
+
+namespace geer {
+
+size_t sort_depth_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, (int)n, 0, 32);
+    return bytes;
+}
+
+size_t scan_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, bytes, (const int64_t *)nullptr, (int64_t *)nullptr, (int)n);
+    return bytes;
+}
+
+size_t scan_i32_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int32_t *)nullptr, (int32_t *)nullptr, (int)n);
+    return bytes;
+}
+
+size_t sort_tiles_temp_bytes(int64_t n_entries, int n_bits) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n_entries, 0,
+                                    n_bits > 0 ? n_bits : 1);
+    return bytes;
+}
+
+size_t sort_pixels_temp_bytes(int64_t n, int n_bits) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t *)nullptr, (int32_t *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, (int)n, 0, n_bits > 0 ? n_bits : 1);
+    return bytes;
+}
+
+void sort_depth(void *temp, size_t temp_bytes, const uint32_t *keys_in, uint32_t *keys_out, const int32_t *vals_in,
+                int32_t *vals_out, int64_t n, cudaStream_t st) {
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n, 0, 32, st);
+}
+
+void sort_tiles(void *temp, size_t temp_bytes, const uint32_t *keys_in, uint32_t *keys_out, const uint32_t *vals_in,
+                uint32_t *vals_out, int64_t n, int n_bits, cudaStream_t st) {
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n, 0,
+                                    n_bits > 0 ? n_bits : 1, st);
+}
+
+void sort_pixels(void *temp, size_t temp_bytes, const int32_t *keys_in, int32_t *keys_out, const int32_t *vals_in,
+                 int32_t *vals_out, int64_t n, int n_bits, cudaStream_t st) {
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n, 0,
+                                    n_bits > 0 ? n_bits : 1, st);
+}
+
+__global__ void k_gather_counts(const int32_t *sorted_gid, const int64_t *count, int64_t *cnt_sorted, int64_t n) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        cnt_sorted[r] = count[sorted_gid[r]];
+}
+
+void gather_counts(const int32_t *sorted_gid, const int64_t *count, int64_t *cnt_sorted, int64_t n, cudaStream_t st) {
+    if (n <= 0) return;
+    int blocks = (int)lmin((n + 255) / 256, 148 * 16);
+    k_gather_counts<<<blocks, 256, 0, st>>>(sorted_gid, count, cnt_sorted, n);
+}
+
+void inclusive_scan_i64(void *temp, size_t temp_bytes, const int64_t *in, int64_t *out, int64_t n, cudaStream_t st) {
+    cub::DeviceScan::InclusiveSum(temp, temp_bytes, in, out, (int)n, st);
+}
+
+void exclusive_scan_i32(void *temp, size_t temp_bytes, const int32_t *in, int32_t *out, int64_t n, cudaStream_t st) {
+    cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, (int)n, st);
+}
+
+// Decode the k-th index of a merged range list (ranges packed lo | hi << 16).
+__device__ __forceinline__ int range_index(const uint32_t r[3], int k) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        int lo = (int)(r[i] & 0xFFFFu), hi = (int)(r[i] >> 16);
+        int len = hi - lo;
+        if (k < len) return lo + k;
+        k -= len;
+    }
+    return -1;
+}
+__device__ __forceinline__ int range_len(const uint32_t r[3]) {
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s += (int)(r[i] >> 16) - (int)(r[i] & 0xFFFFu);
+    return s;
+}
+
+// offs[r] = entries before depth-rank r (offs[0] = 0, offs[n] = total).
+// Each block covers kEmitPerBlock consecutive entries.  Every Gaussian of rank
+// < n_emitting owns >= 1 entry, so a block spans <= kEmitPerBlock + 1 ranks:
+// their offsets are staged in shared memory and each thread binary-searches
+// its entry's rank there (coalesced writes, no per-Gaussian load imbalance).
+constexpr int kEmitPerBlock = 1024;
+__device__ __forceinline__ int64_t upper_rank(const int64_t *offs, int64_t lo, int64_t hi, int64_t e) {
+    // largest r in [lo, hi] with offs[r] <= e
+    while (lo < hi) {
+        int64_t mid = (lo + hi + 1) >> 1;
+        if (offs[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+__global__ void __launch_bounds__(256) k_emit(const int64_t *__restrict__ offs, const int32_t *__restrict__ sorted_gid,
+                                              const AxisRanges *__restrict__ ranges, int n_x, int64_t n_entries,
+                                              int64_t n, uint32_t *__restrict__ tile_keys, uint32_t *__restrict__ gids) {
+    __shared__ int64_t s_off[kEmitPerBlock + 2];
+    __shared__ int64_t s_r0, s_r1;
+    const int64_t e_begin = (int64_t)blockIdx.x * kEmitPerBlock;
+    const int64_t e_last = min(e_begin + kEmitPerBlock, n_entries) - 1;
+    if (threadIdx.x == 0) s_r0 = upper_rank(offs, 0, n, e_begin);
+    if (threadIdx.x == 32) s_r1 = upper_rank(offs, 0, n, e_last);
+    __syncthreads();
+    const int64_t r0 = s_r0, r1 = s_r1;
+    const int span = (int)(r1 - r0 + 1);  // <= kEmitPerBlock + 1
+    for (int i = threadIdx.x; i <= span; i += blockDim.x) s_off[i] = offs[r0 + i];
+    __syncthreads();
+    for (int j = threadIdx.x; j < kEmitPerBlock; j += blockDim.x) {
+        const int64_t e = e_begin + j;
+        if (e > e_last) break;
+        const int rl = (int)upper_rank(s_off, 0, span - 1, e);
+        const int32_t g = sorted_gid[r0 + rl];
+        const AxisRanges ar = ranges[g];
+        const int cx = range_len(ar.x);
+        const int k = (int)(e - s_off[rl]);
+        const int ky = k / cx;
+        const int iy = range_index(ar.y, ky);
+        const int ix = range_index(ar.x, k - ky * cx);
+        tile_keys[e] = (uint32_t)(iy * n_x + ix);
+        gids[e] = (uint32_t)g;
+    }
+}
+
+void emit_entries(const int64_t *offs, const int32_t *sorted_gid, const AxisRanges *ranges, int n_x,
+                  int64_t n_entries, int64_t n, uint32_t *tile_keys, uint32_t *gids, cudaStream_t st) {
+    if (n_entries <= 0) return;
+    int64_t blocks = (n_entries + kEmitPerBlock - 1) / kEmitPerBlock;
+    k_emit<<<(unsigned)blocks, 256, 0, st>>>(offs, sorted_gid, ranges, n_x, n_entries, n, tile_keys, gids);
+}
+
+// ranges[t] = first entry with tile >= t (np.searchsorted(tiles, arange(n_tiles + 1)))
+__global__ void k_ranges(const uint32_t *__restrict__ tiles, int64_t n_entries, int n_tiles, int32_t *__restrict__ ranges) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= n_entries; e += (int64_t)gridDim.x * blockDim.x) {
+        int prev = e == 0 ? -1 : (int)tiles[e - 1];
+        int cur = e == n_entries ? n_tiles : (int)tiles[e];
+        for (int t = prev + 1; t <= cur; ++t) ranges[t] = (int32_t)e;
+    }
+}
+
+void tile_ranges(const uint32_t *sorted_tiles, int64_t n_entries, int n_tiles, int32_t *ranges, cudaStream_t st) {
+    int blocks = (int)lmin((n_entries + 1 + 255) / 256, 148 * 16);
+    k_ranges<<<blocks, 256, 0, st>>>(sorted_tiles, n_entries, n_tiles, ranges);
+}
+
+}  // namespace geer

@@ -1,0 +1,70 @@
+// geer_train.cu — multi-view training glue for BASELINE config 4.
+//
+//   geer_l1_grad : dL/dimage of the masked L1 term (trainer.py:127-132):
+//                  sign(rendered - target) * scale, zero where the mask is off
+//                  (scale = 1 / (n_valid * 3) reproduces the reference mean).
+//   geer_adam    : Adam with bias correction over one flat fp32 buffer
+//                  (trainer.py:181-197), per-element learning rate so all five
+//                  parameter groups update in one launch after the allreduce.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "geer.h"
+
+namespace {
+
+__global__ void k_l1_grad(const float *__restrict__ color, const float *__restrict__ target,
+                          const uint8_t *__restrict__ mask, float *__restrict__ g, int64_t n_pixels, float scale) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pixels * 3;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool on = mask == nullptr || mask[i / 3] != 0;
+        const float d = color[i] - target[i];
+        g[i] = on ? (d > 0.f ? scale : (d < 0.f ? -scale : 0.f)) : 0.f;
+    }
+}
+
+__global__ void k_adam(float *__restrict__ p, const float *__restrict__ g, float *__restrict__ m, float *__restrict__ v,
+                       const float *__restrict__ lr, int64_t n, float b1, float b2, float eps, float bc1, float bc2) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float gi = g[i];
+        const float mi = b1 * m[i] + (1.0f - b1) * gi;
+        const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+        m[i] = mi;
+        v[i] = vi;
+        const float mh = mi / bc1, vh = vi / bc2;
+        p[i] = p[i] - lr[i] * mh / (sqrtf(vh) + eps);
+    }
+}
+
+int grid_for(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    if (b < 1) b = 1;
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int geer_l1_grad(const float *color, const float *target, const uint8_t *mask, float *dl_dimage, int64_t n_pixels,
+                 float scale, void *stream) {
+    if (!color || !target || !dl_dimage || n_pixels < 0) return GEER_ERR_INVALID;
+    if (n_pixels == 0) return GEER_OK;
+    k_l1_grad<<<grid_for(n_pixels * 3), 256, 0, (cudaStream_t)stream>>>(color, target, mask, dl_dimage, n_pixels,
+                                                                          scale);
+    return cudaGetLastError() == cudaSuccess ? GEER_OK : GEER_ERR_CUDA;
+}
+
+int geer_adam(float *param, const float *grad, float *m, float *v, const float *lr, int64_t n, float beta1,
+              float beta2, float eps, int32_t step, void *stream) {
+    if (!param || !grad || !m || !v || !lr || n < 0 || step < 1) return GEER_ERR_INVALID;
+    if (n == 0) return GEER_OK;
+    const float bc1 = (float)(1.0 - pow((double)beta1, (double)step));
+    const float bc2 = (float)(1.0 - pow((double)beta2, (double)step));
+    k_adam<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(param, grad, m, v, lr, n, beta1, beta2, eps, bc1, bc2);
+    return cudaGetLastError() == cudaSuccess ? GEER_OK : GEER_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+"""Tensor-level fast path: device-resident scene, no host copies.
+
+``DeviceRenderer.forward`` / ``backward`` call ``geer_forward`` /
+``geer_backward`` (include/geer.h) on torch's current CUDA stream with the
+data pointers of fp32 CUDA tensors.  PyTorch only provides device memory and
+streams here; all compute is the library's sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+@dataclass
+class DeviceScene:
+    """fp32 CUDA tensors in the reference's stored spaces (scene.py:35-51)."""
+
+    means: torch.Tensor
+    log_scales: torch.Tensor
+    quats: torch.Tensor
+    opacity_logits: torch.Tensor
+    sh: torch.Tensor
+
+    @classmethod
+    def from_scene(cls, scene, device="cuda") -> "DeviceScene":
+        t = lambda a: torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=np.float32))).to(device)
+        n = len(np.asarray(scene.means).reshape(-1, 3))
+        sh = np.asarray(scene.sh, dtype=np.float32)
+        return cls(t(np.asarray(scene.means).reshape(n, 3)), t(np.asarray(scene.log_scales).reshape(n, 3)),
+                   t(np.asarray(scene.quats).reshape(n, 4)), t(np.asarray(scene.opacity_logits).reshape(n)),
+                   t(sh.reshape(n, -1, 3)))
+
+    def __len__(self):
+        return int(self.means.shape[0])
+
+    @property
+    def n_bands(self) -> int:
+        return int(self.sh.shape[1])
+
+    def struct(self) -> _lib.GeerScene:
+        for name in ("means", "log_scales", "quats", "opacity_logits", "sh"):
+            v = getattr(self, name)
+            if v.dtype != torch.float32 or not v.is_cuda or not v.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+        s = _lib.GeerScene()
+        s.n = len(self)
+        s.n_bands = self.n_bands
+        s.means = self.means.data_ptr()
+        s.log_scales = self.log_scales.data_ptr()
+        s.quats = self.quats.data_ptr()
+        s.opacity_logits = self.opacity_logits.data_ptr()
+        s.sh = self.sh.data_ptr()
+        return s
+
+    def zeros_like_grads(self) -> "DeviceScene":
+        return DeviceScene(*(torch.zeros_like(getattr(self, k)) for k in
+                             ("means", "log_scales", "quats", "opacity_logits", "sh")))
+
+
+class DeviceRenderer:
+    """One geer context: forward a view, then (optionally) its backward."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        self.ctx = _lib.Context(device)
+        self._keep = None  # tensors the last forward's state points into
+
+    def set_timing(self, on: bool):
+        self.ctx.set_timing(on)
+
+    def forward(self, scene: DeviceScene, camera, config, out=None):
+        """Returns (color (H,W,3) f32, remaining (H,W) f32, count (H,W) i32) CUDA tensors."""
+        h, w = int(camera.height), int(camera.width)
+        dev = scene.means.device
+        if out is None:
+            out = (torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                   torch.empty((h, w), dtype=torch.float32, device=dev),
+                   torch.empty((h, w), dtype=torch.int32, device=dev))
+        color, remaining, count = out
+        s = scene.struct()
+        cam = _lib.camera_struct(camera)
+        cfg = _lib.config_struct(config)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(self.ctx._lib.geer_forward(self.ctx.ptr, ctypes.byref(s), ctypes.byref(cam), ctypes.byref(cfg),
+                                              color.data_ptr(), remaining.data_ptr(), count.data_ptr(), stream))
+        self._keep = (scene, remaining)
+        return color, remaining, count
+
+    def backward(self, dl_dimage: torch.Tensor, grads: DeviceScene | None = None, accumulate: bool = False,
+                 opacity_logit: bool = False):
+        """Gradients of the last forward's scene (renderer.py:179-201 conventions).
+
+        ``opacity_logit=True`` returns the opacity gradient in the stored logit space
+        (trainer.py:208-217 ``stored_grads``) instead of w.r.t. linear opacity.
+        """
+        if self._keep is None:
+            raise RuntimeError("backward needs a preceding forward")
+        scene = self._keep[0]
+        if grads is None:
+            grads = scene.zeros_like_grads()
+        if dl_dimage.dtype != torch.float32 or not dl_dimage.is_contiguous():
+            raise ValueError("dl_dimage must be a contiguous float32 CUDA tensor")
+        g = _lib.GeerGrads()
+        g.dmeans = grads.means.data_ptr()
+        g.dlog_scales = grads.log_scales.data_ptr()
+        g.dquats = grads.quats.data_ptr()
+        g.dopacities = grads.opacity_logits.data_ptr()
+        g.dsh = grads.sh.data_ptr()
+        stream = torch.cuda.current_stream(dl_dimage.device).cuda_stream
+        _lib.check(self.ctx._lib.geer_backward(self.ctx.ptr, dl_dimage.data_ptr(), ctypes.byref(g),
+                                               (1 if accumulate else 0) | (2 if opacity_logit else 0), stream))
+        return grads
+
+    def stats(self) -> dict:
+        return self.ctx.stats()

@@ -1,0 +1,176 @@
+"""Drop-in ``render`` / ``render_backward`` on the B200 (raygauss/renderer.py mirror).
+
+Same signatures, dataclasses, conventions and errors as the reference:
+
+* :func:`render` (renderer.py:123-176) -> :class:`FrameOutput` with float64
+  colour ``(H, W, 3)``, float64 ``remaining_transmittance`` and int64
+  ``contributor_count`` (renderer.py:39-44).
+* :func:`render_backward` (renderer.py:234-333) -> :class:`SceneGrads` in the
+  stored parameter spaces: ``dopacities`` w.r.t. LINEAR opacity, ``dquats``
+  including the normalisation Jacobian, ``dlog_scales`` in log space, SH view
+  direction stop-gradient (renderer.py:179-201).
+* ``RenderConfig.threads`` is accepted and ignored (the GPU runs every tile).
+
+Both calls go through the host-level C ABI (``geer_render_host`` /
+``geer_render_backward_host``): host float64 arrays in, host float64 arrays
+out, with the copies and the fp32 device compute inside the library.  The
+tensor-level fast path (device tensors, no host copies) is
+:class:`paper_2505_24053_b200.device.DeviceRenderer`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .association import RenderGraph, export_graph
+from .scene import BEAPImage, validate_camera
+
+
+@dataclass
+class RenderConfig:
+    """renderer.py:24-37."""
+
+    lam: float = 3.0
+    tile_px: int = 16
+    background: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    support_cutoff: bool = True
+    threads: int = 1
+
+    def __post_init__(self):
+        self.background = np.asarray(self.background, dtype=np.float64).reshape(3)
+
+
+@dataclass
+class FrameOutput:
+    """renderer.py:39-44."""
+
+    color: BEAPImage
+    remaining_transmittance: np.ndarray
+    contributor_count: np.ndarray
+    graph: RenderGraph | None = None
+
+
+@dataclass
+class SceneGrads:
+    """renderer.py:179-201."""
+
+    dmeans: np.ndarray
+    dlog_scales: np.ndarray
+    dquats: np.ndarray
+    dopacities: np.ndarray
+    dsh: np.ndarray
+
+    @classmethod
+    def zeros_like(cls, scene) -> "SceneGrads":
+        return cls(np.zeros_like(scene.means), np.zeros_like(scene.log_scales), np.zeros_like(scene.quats),
+                   np.zeros_like(scene.opacity_logits), np.zeros_like(scene.sh))
+
+
+def resolve_threads(requested=None) -> int:
+    """renderer.py:47-54 (kept for API compatibility; the GPU path ignores it)."""
+    if requested is not None and requested > 0:
+        return int(requested)
+    env = os.environ.get("GEER_THREADS")
+    if env:
+        return max(1, int(env))
+    return os.cpu_count() or 1
+
+
+class _HostScene:
+    """Contiguous float64 views of a GaussianScene (reference or mirror) + the C struct."""
+
+    def __init__(self, scene):
+        means = np.ascontiguousarray(np.asarray(scene.means, dtype=np.float64).reshape(-1, 3))
+        n = len(means)
+        self.n = n
+        self.means = means
+        self.log_scales = np.ascontiguousarray(np.asarray(scene.log_scales, dtype=np.float64).reshape(n, 3))
+        self.quats = np.ascontiguousarray(np.asarray(scene.quats, dtype=np.float64).reshape(n, 4))
+        self.opacity_logits = np.ascontiguousarray(np.asarray(scene.opacity_logits, dtype=np.float64).reshape(n))
+        sh = np.asarray(scene.sh, dtype=np.float64)
+        self.n_bands = int(sh.shape[1]) if sh.ndim == 3 else (sh.size // (3 * n) if n else 1)
+        self.sh = np.ascontiguousarray(sh.reshape(n, self.n_bands, 3))
+        if self.n_bands > 16:
+            raise ValueError(f"unsupported SH band count {self.n_bands}; degree must be 0..3")
+        s = _lib.GeerHostScene()
+        s.n = n
+        s.n_bands = self.n_bands
+        s.means = self.means.ctypes.data
+        s.log_scales = self.log_scales.ctypes.data
+        s.quats = self.quats.ctypes.data
+        s.opacity_logits = self.opacity_logits.ctypes.data
+        s.sh = self.sh.ctypes.data
+        self.struct = s
+
+
+def _ctx(device: int = 0) -> _lib.Context:
+    return _lib.default_context(device)
+
+
+def render(scene, camera, config: RenderConfig | None = None, *, return_graph: bool = False,
+           device: int = 0) -> FrameOutput:
+    """Render ``scene`` through ``camera`` (renderer.py:123-176) on the GPU.
+
+    ``return_graph=True`` also exports the association (``FrameOutput.graph``),
+    which the reference always builds; it costs a device->host copy of the
+    whole graph, so it is opt-in.
+    """
+    config = config or RenderConfig()
+    validate_camera(camera)
+    h, w = int(camera.height), int(camera.width)
+    hs = _HostScene(scene)
+    color = np.empty((h, w, 3), dtype=np.float64)
+    remaining = np.empty((h, w), dtype=np.float64)
+    count = np.empty((h, w), dtype=np.int64)
+    ctx = _ctx(device)
+    cam = _lib.camera_struct(camera)
+    cfg = _lib.config_struct(config)
+    _lib.check(ctx._lib.geer_render_host(ctx.ptr, ctypes.byref(hs.struct), ctypes.byref(cam), ctypes.byref(cfg),
+                                         color.ctypes.data, remaining.ctypes.data, count.ctypes.data))
+    graph = None
+    if return_graph and hs.n > 0:
+        graph = build_graph_for(scene, camera, config.lam, config.tile_px, device=device)
+    return FrameOutput(color=BEAPImage(color=color, mask=np.ones((h, w), dtype=bool)),
+                       remaining_transmittance=remaining, contributor_count=count, graph=graph)
+
+
+def render_backward(scene, camera, dl_dimage: np.ndarray, config: RenderConfig | None = None, *,
+                    device: int = 0) -> SceneGrads:
+    """dLoss/dparameters from an image gradient (renderer.py:234-333) on the GPU."""
+    config = config or RenderConfig()
+    validate_camera(camera)
+    hs = _HostScene(scene)
+    grads = SceneGrads(np.zeros((hs.n, 3)), np.zeros((hs.n, 3)), np.zeros((hs.n, 4)), np.zeros(hs.n),
+                       np.zeros((hs.n, hs.n_bands, 3)))
+    if hs.n == 0:
+        return grads
+    h, w = int(camera.height), int(camera.width)
+    dl = np.ascontiguousarray(np.asarray(dl_dimage, dtype=np.float64).reshape(h, w, 3))
+    ctx = _ctx(device)
+    cam = _lib.camera_struct(camera)
+    cfg = _lib.config_struct(config)
+    g = _lib.GeerHostGrads()
+    g.dmeans = grads.dmeans.ctypes.data
+    g.dlog_scales = grads.dlog_scales.ctypes.data
+    g.dquats = grads.dquats.ctypes.data
+    g.dopacities = grads.dopacities.ctypes.data
+    g.dsh = grads.dsh.ctypes.data
+    _lib.check(ctx._lib.geer_render_backward_host(ctx.ptr, ctypes.byref(hs.struct), ctypes.byref(cam),
+                                                  dl.ctypes.data, ctypes.byref(cfg), ctypes.byref(g)))
+    return grads
+
+
+def build_graph_for(scene, camera, lam: float = 3.0, tile_px: int = 16, device: int = 0) -> RenderGraph:
+    """association.build_render_graph on the GPU (see association.py)."""
+    validate_camera(camera)
+    hs = _HostScene(scene)
+    ctx = _ctx(device)
+    cam = _lib.camera_struct(camera)
+    _lib.check(ctx._lib.geer_build_graph_host(ctx.ptr, ctypes.byref(hs.struct), ctypes.byref(cam), float(lam),
+                                              int(tile_px)))
+    return export_graph(ctx, hs.n, int(camera.width), int(camera.height))

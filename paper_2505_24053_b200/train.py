@@ -1,0 +1,146 @@
+"""Multi-view training step (BASELINE config 4): views sharded over ranks, one NCCL allreduce.
+
+One step:
+
+1. every rank renders its contiguous share of the views (forward), forms the
+   masked-L1 image gradient against the view's target (``geer_l1_grad``,
+   trainer.py:127-132) and runs the backward, accumulating per-Gaussian
+   gradients for all its views into ONE flat fp32 buffer (opacity chained to
+   the stored logit, trainer.py:208-217);
+2. ``torch.distributed.all_reduce(SUM)`` of that buffer (NCCL over
+   NVLink/NVSwitch; gloo in CPU tests);
+3. every rank applies the identical Adam update (trainer.py:181-197) with one
+   ``geer_adam`` launch over the flat parameter buffer, so replicas stay
+   bit-identical.
+
+Parameters and gradients are flat buffers whose slices are the SoA tensors
+the renderer reads, so the allreduce and Adam touch one contiguous buffer.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib, synth
+from .device import DeviceRenderer, DeviceScene
+from .renderer import RenderConfig
+
+FIELDS = (("means", 3), ("log_scales", 3), ("quats", 4), ("opacity_logits", 1), ("sh", None))
+
+
+def shard(n_items: int, rank: int, world: int) -> range:
+    """Contiguous share of ``n_items`` views for ``rank``."""
+    base, extra = divmod(n_items, world)
+    start = rank * base + min(rank, extra)
+    return range(start, start + base + (1 if rank < extra else 0))
+
+
+class FlatScene:
+    """A DeviceScene whose five tensors are views of one contiguous fp32 buffer."""
+
+    def __init__(self, n: int, n_bands: int, device, buf: torch.Tensor | None = None):
+        self.n, self.n_bands = n, n_bands
+        widths = [w if w is not None else n_bands * 3 for _, w in FIELDS]
+        self.numel = n * sum(widths)
+        self.buf = buf if buf is not None else torch.zeros(self.numel, dtype=torch.float32, device=device)
+        views, off = [], 0
+        for (name, w), width in zip(FIELDS, widths):
+            v = self.buf[off: off + n * width]
+            shape = (n,) if name == "opacity_logits" else ((n, n_bands, 3) if name == "sh" else (n, width))
+            views.append(v.view(shape))
+            off += n * width
+        self.scene = DeviceScene(*views)
+
+    def load(self, scene):
+        src = DeviceScene.from_scene(scene, device=self.buf.device)
+        for name, _ in FIELDS:
+            getattr(self.scene, name).copy_(getattr(src, name))
+
+    def lr_vector(self, lrs: dict) -> torch.Tensor:
+        out = torch.empty_like(self.buf)
+        off = 0
+        for name, _ in FIELDS:
+            k = getattr(self.scene, name).numel()
+            out[off: off + k] = lrs[name]
+            off += k
+        return out
+
+
+class MultiViewTrainer:
+    def __init__(self, init_scene, cameras, targets, rank=0, world=1, device=0, config=None, lrs=None):
+        self.rank, self.world = rank, world
+        self.device = torch.device(f"cuda:{device}")
+        self.config = config or RenderConfig()
+        n = len(init_scene)
+        nb = int(np.asarray(init_scene.sh).shape[1])
+        self.params = FlatScene(n, nb, self.device)
+        self.params.load(init_scene)
+        self.grads = FlatScene(n, nb, self.device)
+        self.m = torch.zeros_like(self.params.buf)
+        self.v = torch.zeros_like(self.params.buf)
+        extent = float(init_scene.extent()) if hasattr(init_scene, "extent") else 1.0
+        lrs = lrs or {"means": 1.6e-4 * extent, "log_scales": 5e-3, "quats": 1e-3, "opacity_logits": 5e-2,
+                      "sh": 2.5e-3}  # trainer.py:160-165,243
+        self.lr = self.params.lr_vector(lrs)
+        self.cameras = cameras
+        self.targets = targets  # list of (H,W,3) fp32 CUDA tensors, one per local view
+        self.renderer = DeviceRenderer(device)
+        self.t = 0
+        self.grad_numel = self.params.numel
+        self.last_loss = None
+        self._bufs = {}
+        self.lib = _lib.load()
+
+    @classmethod
+    def for_config4(cls, target_scene, n_views=64, rank=0, world=1, device=0, width=1920, height=1080):
+        """C4: target = C2 scene, init = perturbed(C2, default_rng(1)), ring of BEAP 180x101.25 views."""
+        cams_all = synth.ring_cameras(n_views, 2.0, width, height, fov_deg=180.0, fov_y_deg=180.0 * height / width)
+        mine = [cams_all[i] for i in shard(n_views, rank, world)]
+        init = synth.to_f32_values(synth.perturbed(target_scene, np.random.default_rng(1)))
+        r = DeviceRenderer(device)
+        tscene = DeviceScene.from_scene(target_scene, device=f"cuda:{device}")
+        cfg = RenderConfig()
+        targets = []
+        for cam in mine:
+            color, _, _ = r.forward(tscene, cam, cfg)
+            targets.append(color.clone())
+        del r, tscene
+        return cls(init, mine, targets, rank, world, device, cfg)
+
+    def _out(self, cam):
+        key = (cam.height, cam.width)
+        if key not in self._bufs:
+            h, w = key
+            self._bufs[key] = (torch.empty((h, w, 3), dtype=torch.float32, device=self.device),
+                               torch.empty((h, w), dtype=torch.float32, device=self.device),
+                               torch.empty((h, w), dtype=torch.int32, device=self.device),
+                               torch.empty((h, w, 3), dtype=torch.float32, device=self.device))
+        return self._bufs[key]
+
+    def step(self, compute_loss=False):
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.grads.buf.zero_()
+        loss = 0.0
+        for cam, target in zip(self.cameras, self.targets):
+            color, rem, cnt, dl = self._out(cam)
+            self.renderer.forward(self.params.scene, cam, self.config, out=(color, rem, cnt))
+            npx = cam.height * cam.width
+            _lib.check(self.lib.geer_l1_grad(color.data_ptr(), target.data_ptr(), None, dl.data_ptr(), npx,
+                                             ctypes.c_float(1.0 / (npx * 3)), stream))
+            self.renderer.backward(dl, grads=self.grads.scene, accumulate=True, opacity_logit=True)
+            if compute_loss:
+                loss += float((color - target).abs().mean())
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(self.grads.buf, op=dist.ReduceOp.SUM)
+        self.t += 1
+        _lib.check(self.lib.geer_adam(self.params.buf.data_ptr(), self.grads.buf.data_ptr(), self.m.data_ptr(),
+                                      self.v.data_ptr(), self.lr.data_ptr(), self.params.numel, ctypes.c_float(0.9),
+                                      ctypes.c_float(0.999), ctypes.c_float(1e-15), self.t, stream))
+        if compute_loss:
+            self.last_loss = loss
+        return loss

@@ -1,0 +1,85 @@
+"""Tensor-level fast path (geer_forward / geer_backward on device tensors) and training glue kernels."""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2505_24053_b200 import _lib, renderer, synth
+from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene
+
+pytestmark = pytest.mark.gpu
+
+
+def _small():
+    scene = synth.config_scene("C2", n=20_000)
+    cam = synth.config_camera("C2", width=320, height=180)
+    return scene, cam
+
+
+def test_device_forward_matches_host_api():
+    scene, cam = _small()
+    cfg = renderer.RenderConfig(background=np.array([0.2, 0.3, 0.4]))
+    host = renderer.render(scene, cam, cfg)
+    r = DeviceRenderer(0)
+    color, rem, cnt = r.forward(DeviceScene.from_scene(scene), cam, cfg)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(color.cpu().numpy().astype(np.float64), host.color.color)
+    np.testing.assert_array_equal(rem.cpu().numpy().astype(np.float64), host.remaining_transmittance)
+    np.testing.assert_array_equal(cnt.cpu().numpy().astype(np.int64), host.contributor_count)
+
+
+def test_device_backward_accumulates_and_matches_host():
+    scene, cam = _small()
+    cfg = renderer.RenderConfig()
+    dl = np.random.default_rng(3).standard_normal((cam.height, cam.width, 3)) / 1e4
+    host = renderer.render_backward(scene, cam, dl, cfg)
+    r = DeviceRenderer(0)
+    ds = DeviceScene.from_scene(scene)
+    r.forward(ds, cam, cfg)
+    dlt = torch.as_tensor(dl.astype(np.float32)).cuda()
+    g = r.backward(dlt)
+    g = r.backward(dlt, grads=g, accumulate=True)
+    torch.cuda.synchronize()
+    for name, ref in (("means", host.dmeans), ("log_scales", host.dlog_scales), ("quats", host.dquats),
+                      ("opacity_logits", host.dopacities), ("sh", host.dsh)):
+        got = getattr(g, name).cpu().numpy().astype(np.float64)
+        scale = np.abs(ref).max()
+        # fp32 atomics: reduction order differs run to run
+        assert np.abs(got - 2 * ref).max() <= 2e-3 * 2 * scale, name
+
+
+def test_backward_without_forward_raises():
+    r = DeviceRenderer(0)
+    with pytest.raises(RuntimeError):
+        r.backward(torch.zeros((4, 4, 3), device="cuda"))
+
+
+def test_l1_grad_and_adam_kernels():
+    lib = _lib.load()
+    n = 1000
+    a = torch.rand(n, 3, device="cuda")
+    b = torch.rand(n, 3, device="cuda")
+    mask = (torch.rand(n, device="cuda") > 0.3).to(torch.uint8)
+    g = torch.empty_like(a)
+    scale = 1.0 / (int(mask.sum()) * 3)
+    _lib.check(lib.geer_l1_grad(a.data_ptr(), b.data_ptr(), mask.data_ptr(), g.data_ptr(), n, scale,
+                                torch.cuda.current_stream().cuda_stream))
+    ref = torch.sign(a - b) * scale * mask[:, None]
+    torch.testing.assert_close(g, ref)
+    # Adam (trainer.py:181-197)
+    p = torch.randn(5000, device="cuda")
+    grad = torch.randn(5000, device="cuda")
+    m = torch.zeros_like(p)
+    v = torch.zeros_like(p)
+    lr = torch.full_like(p, 1e-3)
+    p_ref, m_ref, v_ref = p.clone(), m.clone(), v.clone()
+    for step in (1, 2, 3):
+        _lib.check(lib.geer_adam(p.data_ptr(), grad.data_ptr(), m.data_ptr(), v.data_ptr(), lr.data_ptr(), 5000,
+                                 ctypes.c_float(0.9), ctypes.c_float(0.999), ctypes.c_float(1e-15), step,
+                                 torch.cuda.current_stream().cuda_stream))
+        m_ref = 0.9 * m_ref + 0.1 * grad
+        v_ref = 0.999 * v_ref + 0.001 * grad * grad
+        p_ref = p_ref - 1e-3 * (m_ref / (1 - 0.9 ** step)) / (torch.sqrt(v_ref / (1 - 0.999 ** step)) + 1e-15)
+    torch.testing.assert_close(p, p_ref, rtol=1e-5, atol=1e-6)

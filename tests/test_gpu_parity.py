@@ -1,0 +1,113 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference fixtures and the oracle.
+
+Small fixtures and BASELINE config 1 are compared with the outputs of the
+unmodified reference (tests/golden, made by make_golden.py); bigger scenes up
+to the full 1M-Gaussian 1080p config are compared with the fp64 C oracle,
+which is itself pinned to the reference by tests/test_oracle_golden.py.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2505_24053_b200 import association, renderer, synth
+from tests import golden_cases as G
+from tests import parity as P
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", G.SMALL_CASES)
+def test_fixture_association_forward_backward(name):
+    c = G.case(name)
+    d = c.data
+    if "error" in d:
+        with pytest.raises(ValueError, match=str(d["error"])):
+            renderer.render(c.scene, c.camera, c.config)
+        with pytest.raises(ValueError, match=str(d["error"])):
+            association.build_render_graph(c.scene, c.camera, c.config.lam, c.config.tile_px)
+        return
+    fr = renderer.render(c.scene, c.camera, c.config)
+    assert fr.color.color.dtype == np.float64 and fr.contributor_count.dtype == np.int64
+    if len(c.scene) == 0:
+        np.testing.assert_array_equal(fr.color.color, d["color"])
+        np.testing.assert_array_equal(fr.remaining_transmittance, d["remaining"])
+        np.testing.assert_array_equal(fr.contributor_count, d["count"])
+        return
+    g = association.build_render_graph(c.scene, c.camera, c.config.lam, c.config.tile_px)
+    P.assert_graph_equal(g, d["order"], d["entry_tile"], d["ranges"], d["keep"], d["clamped"])
+    np.testing.assert_array_equal(g.grid.pixel_tile, d["grid_pixel_tile"])
+    np.testing.assert_allclose(g.grid.mirror_edges_x, d["grid_ex"], rtol=1e-14, atol=1e-15)
+    np.testing.assert_allclose(g.grid.mirror_edges_y, d["grid_ey"], rtol=1e-14, atol=1e-15)
+    # contributor_count is not comparable fp32-vs-fp64 without the support cutoff
+    P.assert_image_close(fr.color.color, fr.remaining_transmittance, fr.contributor_count, d["color"],
+                         d["remaining"], d["count"], check_count=bool(c.config.support_cutoff))
+    gr = renderer.render_backward(c.scene, c.camera, d["dl_dimage"], c.config)
+    P.assert_grads_close(gr, d)
+
+
+def test_c1_against_reference():
+    """BASELINE config 1: 10k Gaussians, 256x256 pinhole, vs the reference's own outputs."""
+    d = G.load("C1")
+    scene = synth.config_scene("C1")
+    cam = synth.config_camera("C1")
+    g = association.build_render_graph(scene, cam)
+    P.assert_graph_equal(g, d["order"], None, d["ranges"], d["keep"], d["clamped"])
+    fr = renderer.render(scene, cam, renderer.RenderConfig())
+    P.assert_image_close(fr.color.color, fr.remaining_transmittance, fr.contributor_count, d["color"],
+                         d["remaining"], d["count"])
+    dl = np.random.default_rng(1).standard_normal((256, 256, 3)) / (256 * 256)
+    gr = renderer.render_backward(scene, cam, dl, renderer.RenderConfig())
+    P.assert_grads_close(gr, d, idx=d["grad_sample"])
+
+
+@pytest.mark.parametrize("n,w,h", [(100_000, 480, 270)])
+def test_c2_distribution_reduced_vs_oracle(n, w, h):
+    """C2 scene distribution at reduced size: association, image and gradients vs the oracle."""
+    scene = synth.config_scene("C2", n=n)
+    cam = synth.config_camera("C2", width=w, height=h)
+    og = O.build_render_graph(scene, cam)
+    g = association.build_render_graph(scene, cam)
+    P.assert_graph_equal(g, og.order, og.entry_tile, og.ranges, og.keep, og.clamped)
+    cfg = renderer.RenderConfig(background=np.array([0.1, 0.0, 0.3]))
+    of = O.render(scene, cam, cfg, graph=og)
+    fr = renderer.render(scene, cam, cfg)
+    P.assert_image_close(fr.color.color, fr.remaining_transmittance, fr.contributor_count, of.color, of.remaining,
+                         of.count)
+    dl = np.random.default_rng(1).standard_normal((h, w, 3)) / (h * w)
+    ob = O.render_backward(scene, cam, dl, cfg, graph=og)
+    gr = renderer.render_backward(scene, cam, dl, cfg)
+    P.assert_grads_close(gr, vars(ob))
+
+
+def test_kb_wide_vs_oracle():
+    """Equidistant KB fisheye (C5 camera model, reduced): non-separable grid, empty and oversized tiles."""
+    scene = synth.config_scene("C5", n=60_000)
+    cam = synth.config_camera("C5", width=640, height=360)
+    og = O.build_render_graph(scene, cam)
+    g = association.build_render_graph(scene, cam)
+    np.testing.assert_array_equal(g.grid.pixel_tile, og.grid.pixel_tile)
+    P.assert_graph_equal(g, og.order, og.entry_tile, og.ranges, og.keep, og.clamped)
+    cfg = renderer.RenderConfig()
+    of = O.render(scene, cam, cfg, graph=og)
+    fr = renderer.render(scene, cam, cfg)
+    P.assert_image_close(fr.color.color, fr.remaining_transmittance, fr.contributor_count, of.color, of.remaining,
+                         of.count)
+    dl = np.random.default_rng(2).standard_normal((360, 640, 3)) / (360 * 640)
+    ob = O.render_backward(scene, cam, dl, cfg, graph=og)
+    gr = renderer.render_backward(scene, cam, dl, cfg)
+    P.assert_grads_close(gr, vars(ob))
+
+
+def test_full_c2_association_and_forward_vs_oracle():
+    """BASELINE config 2 at full size (1M Gaussians, 1920x1080 BEAP 180 deg): bit-exact graph, image."""
+    scene = synth.config_scene("C2")
+    cam = synth.config_camera("C2")
+    og = O.build_render_graph(scene, cam)
+    g = association.build_render_graph(scene, cam)
+    P.assert_graph_equal(g, og.order, og.entry_tile, og.ranges, og.keep, og.clamped)
+    of = O.render(scene, cam, None, graph=og)
+    fr = renderer.render(scene, cam, renderer.RenderConfig())
+    rep = P.assert_image_close(fr.color.color, fr.remaining_transmittance, fr.contributor_count, of.color,
+                               of.remaining, of.count)
+    print("C2 image parity", rep, "entries", len(g.order))

@@ -1,0 +1,79 @@
+"""Pin the CPU oracle (oracle/geer_oracle.c) to the reference's own outputs.
+
+tests/golden/*.npz were produced by the unmodified reference
+(tests/golden/make_golden.py).  The oracle must reproduce the association
+exactly and the fp64 images / gradients to rounding noise, otherwise it is not
+fit to judge the GPU path.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2505_24053_b200 import synth
+from tests import golden_cases as G
+
+
+def _grad_close(a, b, rel=1e-9):
+    scale = max(np.abs(b).max(), 1e-30)
+    return np.abs(a - b).max() <= rel * scale
+
+
+@pytest.mark.parametrize("name", G.SMALL_CASES)
+def test_oracle_matches_reference_fixture(name):
+    c = G.case(name)
+    d = c.data
+    if "error" in d:
+        with pytest.raises(ValueError, match=str(d["error"])):
+            O.build_render_graph(c.scene, c.camera, c.config.lam, c.config.tile_px)
+        return
+    if len(c.scene) == 0:
+        fr = O.render(c.scene, c.camera, c.config)
+        np.testing.assert_array_equal(fr.color, d["color"])
+        np.testing.assert_array_equal(fr.remaining, d["remaining"])
+        return
+    g = O.build_render_graph(c.scene, c.camera, c.config.lam, c.config.tile_px)
+    np.testing.assert_array_equal(g.grid.pixel_tile, d["grid_pixel_tile"])
+    np.testing.assert_allclose(g.grid.mirror_edges_x, d["grid_ex"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(g.grid.mirror_edges_y, d["grid_ey"], rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(g.order, d["order"])
+    np.testing.assert_array_equal(g.entry_tile, d["entry_tile"])
+    np.testing.assert_array_equal(g.ranges, d["ranges"])
+    np.testing.assert_array_equal(g.keep, d["keep"])
+    np.testing.assert_array_equal(g.clamped, d["clamped"])
+    fr = O.render(c.scene, c.camera, c.config, graph=g)
+    assert np.abs(fr.color - d["color"]).max() < 1e-12
+    assert np.abs(fr.remaining - d["remaining"]).max() < 1e-12
+    np.testing.assert_array_equal(fr.count, d["count"])
+    gr = O.render_backward(c.scene, c.camera, d["dl_dimage"], c.config, graph=g)
+    for k in ("dmeans", "dlog_scales", "dquats", "dopacities", "dsh"):
+        assert _grad_close(getattr(gr, k), d[k]), k
+
+
+def test_synth_scene_regenerates_c1_fixture():
+    d = G.load("C1")
+    scene = synth.config_scene("C1")
+    h = hashlib.sha256()
+    for a in (scene.means, scene.log_scales, scene.quats, scene.opacity_logits, scene.sh):
+        h.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
+    assert h.hexdigest() == str(d["scene_sha256"])
+
+
+def test_oracle_matches_reference_c1():
+    """BASELINE config 1 (10k Gaussians, 256x256 pinhole): association, image, gradient sample."""
+    d = G.load("C1")
+    scene = synth.config_scene("C1")
+    cam = synth.config_camera("C1")
+    g = O.build_render_graph(scene, cam)
+    np.testing.assert_array_equal(g.order, d["order"].astype(np.int64))
+    np.testing.assert_array_equal(g.ranges, d["ranges"])
+    fr = O.render(scene, cam, None, graph=g)
+    assert np.abs(fr.color - d["color"]).max() < 1e-12
+    np.testing.assert_array_equal(fr.count, d["count"])
+    dl = np.random.default_rng(1).standard_normal((256, 256, 3)) / (256 * 256)
+    gr = O.render_backward(scene, cam, dl, None, graph=g)
+    idx = d["grad_sample"]
+    for k in ("dmeans", "dlog_scales", "dquats", "dopacities", "dsh"):
+        assert _grad_close(getattr(gr, k)[idx], d[k]), k
