@@ -108,6 +108,7 @@ typedef struct geer_stats {
     int64_t n_work_items;     /* raster CTAs launched with work */
     int64_t evaluated_pairs;  /* sum over pixels of alive entries (n_eval) */
     int64_t kappa_rechecks;   /* fp64 re-evaluations of the kappa cutoff */
+    int64_t fixup_pixels;     /* pixels recomposited in fp64 (early stop too close to call in fp32) */
     int64_t clamped;          /* clamped & kept particles */
     float ms_prep, ms_dup, ms_sort, ms_render, ms_total; /* CUDA-event stage times (if timing on) */
     float ms_backward;

@@ -64,19 +64,19 @@ struct geer_ctx {
     int max_items = 0;
     const float *fwd_remaining = nullptr;  // remaining written by the last forward (backward input)
     float ms[6] = {};
-    unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs
+    unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs, [2] fp64 fix-up pixels
     int *d_err = nullptr;
     int64_t *h_hdr = nullptr;  // pinned: [0] total entries, [1] error code
     // camera buffers
     Buf col_sc, row_sc, medges_x, medges_y, edges_x, edges_y, dir64, theta, phi, minmax, pixel_tile, pixel_tile_sorted,
         pix_iota, pix_list, tile_count, tile_off, item_count, item_off, items, n_items;
     // per-Gaussian buffers
-    Buf payload, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, cnt_sorted, offs, ranges_ax, flags, mu_c,
+    Buf payload, gpayload, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, cnt_sorted, offs, ranges_ax, flags, mu_c,
         depth;
     // per-entry buffers
     Buf tile_keys, tile_keys_sorted, gids, order, tile_ranges;
     // per-pixel buffers
-    Buf color, remaining, count_px, n_eval, dl32;
+    Buf color, remaining, count_px, n_eval, dl32, fixup;
     // backward
     Buf accum;
     // temp
@@ -96,14 +96,18 @@ T *ensure(Buf &b, size_t count, int *rc) {
         b.p = nullptr;
         b.cap = 0;
         size_t want = bytes + bytes / 4;
-        if (cudaMalloc(&b.p, want) != cudaSuccess) {
+        cudaError_t e = cudaMalloc(&b.p, want);
+        if (e == cudaErrorMemoryAllocation) {
             cudaGetLastError();
-            if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
-                cudaGetLastError();
-                *rc = fail(GEER_ERR_NOMEM, "cudaMalloc of %zu bytes failed", bytes);
-                return nullptr;
-            }
             want = bytes;
+            e = cudaMalloc(&b.p, want);
+        }
+        if (e != cudaSuccess) {
+            b.p = nullptr;
+            *rc = e == cudaErrorMemoryAllocation
+                      ? fail(GEER_ERR_NOMEM, "cudaMalloc of %zu bytes failed", bytes)
+                      : fail(GEER_ERR_CUDA, "cudaMalloc of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+            return nullptr;
         }
         b.cap = want;
     }
@@ -226,13 +230,14 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     c->have_frame = false;
     c->have_raster = false;
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
-    GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 2 * sizeof(unsigned long long), st));
+    GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 3 * sizeof(unsigned long long), st));
     GEER_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
     rc = camera_setup(c, want_export, st);
     if (rc) return rc;
 
     // ---- K1 preprocess
     Payload *payload = ENSURE(Payload, c->payload, n);
+    GradPayload *gpayload = ENSURE(GradPayload, c->gpayload, n);
     uint32_t *dkey = ENSURE(uint32_t, c->depth_key, n);
     uint32_t *dkey_s = ENSURE(uint32_t, c->depth_key_sorted, n);
     int32_t *giota = ENSURE(int32_t, c->gid_iota, n);
@@ -248,7 +253,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         dep = ENSURE(double, c->depth, n);
     }
     int32_t *ranges = ENSURE(int32_t, c->tile_ranges, fc.n_tiles + 1);
-    launch_preprocess(fc, sc, (const double *)c->medges_x.p, (const double *)c->medges_y.p, payload, dkey, cnt, ar,
+    launch_preprocess(fc, sc, (const double *)c->medges_x.p, (const double *)c->medges_y.p, payload, gpayload, dkey, cnt, ar,
                       flags, mu, dep, c->d_err, st);
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[1], st));
 
@@ -297,10 +302,11 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     // ---- render
     if (color) {
         int32_t *ne = ENSURE(int32_t, c->n_eval, npx);
+        int32_t *fix = ENSURE(int32_t, c->fixup, npx);
         launch_forward(fc, sc, c->max_items, (const int4 *)c->items.p, (const int32_t *)c->n_items.p,
                        (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
                        (const double *)c->dir64.p, ranges, order, payload, color, remaining, count, ne,
-                       c->d_counters, st);
+                       c->d_counters, fix, st);
         c->fwd_remaining = remaining;
         c->have_raster = true;
     }
@@ -323,18 +329,18 @@ int run_backward(geer_ctx *c, const float *dl_dimage, bool f64_out, void *const 
     FrameConst &fc = c->fc;
     const geer_scene &sc = c->scene;
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
-    float4 *accum = ENSURE(float4, c->accum, sc.n * 4);
-    if (sc.n > 0) GEER_CUDA(cudaMemsetAsync(accum, 0, sizeof(float4) * 4 * sc.n, st));
+    float *accum = ENSURE(float, c->accum, sc.n * 16);
+    if (sc.n > 0) GEER_CUDA(cudaMemsetAsync(accum, 0, sizeof(float) * 16 * sc.n, st));
     launch_backward(fc, sc, c->max_items, (const int4 *)c->items.p, (const int32_t *)c->n_items.p,
                     (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
                     (const double *)c->dir64.p, (const int32_t *)c->tile_ranges.p, (const uint32_t *)c->order.p,
-                    (const Payload *)c->payload.p, c->fwd_remaining, (const int32_t *)c->n_eval.p,
+                    (const Payload *)c->payload.p, (const GradPayload *)c->gpayload.p, c->fwd_remaining, (const int32_t *)c->n_eval.p,
                     dl_dimage, accum, st);
     if (f64_out)
-        launch_finalize<double>(fc, sc, accum, (const uint8_t *)c->flags.p, (double *)gout[0], (double *)gout[1],
+        launch_finalize<double>(fc, sc, (const float4 *)accum, (const uint8_t *)c->flags.p, (double *)gout[0], (double *)gout[1],
                                 (double *)gout[2], (double *)gout[3], (double *)gout[4], accumulate, st);
     else
-        launch_finalize<float>(fc, sc, accum, (const uint8_t *)c->flags.p, (float *)gout[0], (float *)gout[1],
+        launch_finalize<float>(fc, sc, (const float4 *)accum, (const uint8_t *)c->flags.p, (float *)gout[0], (float *)gout[1],
                                (float *)gout[2], (float *)gout[3], (float *)gout[4], accumulate, st);
     if (c->timing) {
         GEER_CUDA(cudaEventRecord(c->ev[1], st));
@@ -421,7 +427,7 @@ geer_ctx *geer_create(int device) {
     c->device = device;
     bool ok = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) == cudaSuccess;
     for (int i = 0; i < 6 && ok; ++i) ok = cudaEventCreate(&c->ev[i]) == cudaSuccess;
-    ok = ok && cudaMalloc(&c->d_counters, 2 * sizeof(unsigned long long)) == cudaSuccess;
+    ok = ok && cudaMalloc(&c->d_counters, 3 * sizeof(unsigned long long)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->d_err, sizeof(int)) == cudaSuccess;
     ok = ok && cudaMallocHost(&c->h_hdr, 2 * sizeof(int64_t)) == cudaSuccess;
     if (!ok) {
@@ -438,10 +444,10 @@ void geer_destroy(geer_ctx *c) {
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     Buf *bufs[] = {&c->col_sc, &c->row_sc, &c->medges_x, &c->medges_y, &c->edges_x, &c->edges_y, &c->dir64,
                    &c->theta, &c->phi, &c->minmax, &c->pixel_tile, &c->pixel_tile_sorted, &c->pix_iota, &c->pix_list,
-                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->payload,
+                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->payload, &c->gpayload,
                    &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted, &c->count, &c->cnt_sorted,
                    &c->offs, &c->ranges_ax, &c->flags, &c->mu_c, &c->depth, &c->tile_keys, &c->tile_keys_sorted,
-                   &c->gids, &c->order, &c->tile_ranges, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32,
+                   &c->gids, &c->order, &c->tile_ranges, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,
                    &c->accum, &c->temp, &c->h64_means, &c->h64_log, &c->h64_quats, &c->h64_op, &c->h64_sh,
                    &c->s32_means, &c->s32_log, &c->s32_quats, &c->s32_op, &c->s32_sh, &c->out64, &c->g64};
     for (Buf *b : bufs) free_buf(*b);
@@ -506,13 +512,14 @@ int geer_frame_stats(geer_ctx *c, geer_stats *out) {
         GEER_CUDA(cudaDeviceSynchronize());
         GEER_CUDA(cudaMemsetAsync(c->d_counters + 1, 0, sizeof(unsigned long long), st));
         launch_sum_i32((const int32_t *)c->n_eval.p, (int64_t)c->fc.width * c->fc.height, c->d_counters + 1, st);
-        unsigned long long h[2];
+        unsigned long long h[3];
         int32_t nit = 0;
         GEER_CUDA(cudaMemcpyAsync(h, c->d_counters, sizeof(h), cudaMemcpyDeviceToHost, st));
         GEER_CUDA(cudaMemcpyAsync(&nit, c->n_items.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         GEER_CUDA(cudaStreamSynchronize(st));
         out->kappa_rechecks = (int64_t)h[0];
         out->evaluated_pairs = (int64_t)h[1];
+        out->fixup_pixels = (int64_t)h[2];
         out->n_work_items = nit;
     }
     if (c->have_frame && c->scene.n > 0) {

@@ -35,12 +35,21 @@ struct FrameConst {
     float lam2f;
 };
 
-// fp32 raster payload, one per Gaussian (80 B, 16-B aligned):
-//   r0..r2 = (W_i0, W_i1, W_i2, o_u_i)  rows of W = S^-1 R^T with o_u = W (o - mu)
-//   col    = (r, g, b, sigma)
-//   ext    = (kappa band, 0, 0, 0)   half-width of the fp64 re-check band around lam^2
+// Raster payload, one per Gaussian (128 B, see make_payload in geer_geometry.cu):
+//   q[12]  mode 0: quadratic forms of |d_u|^2 and |m|^2 in the ray d:
+//                  (A00, A11, A22, 2A01, 2A02, 2A12, B00, B11, B22, 2B01, 2B02, 2B12)
+//          mode 1: W (row-major) and o_u for the fp64 cross-product evaluation
+//   col  = (r, g, b, sigma); sigma < 0 flags mode 1
+//   ext  = (absolute kappa error bound of the fp64 evaluation, 0, 0, 0)
 struct __align__(16) Payload {
-    float4 r0, r1, r2, col, ext;
+    double q[12];
+    float4 col;
+    float4 ext;
+};
+
+// fp32 W rows and o_u (w component) for the backward's gradient vectors.
+struct __align__(16) GradPayload {
+    float4 r0, r1, r2;
 };
 
 // Per-axis tile ranges: up to 3 disjoint [lo, hi) pairs packed lo | hi << 16.

@@ -428,28 +428,59 @@ __device__ int axis_tiles(double t_aa, double t_a2, double t22, double r0, doubl
     return cnt;
 }
 
-// Conservative bound on |kappa_fp32 - kappa_exact| near kappa = lam^2 for the raster's fp32
-// evaluation (d_u = W d, m = o_u x d_u, kappa = |m|^2/|d_u|^2 with fp32-rounded W, o_u, d).
-// Rounding analysis (u = 2^-24): |d_u| >= 1/s_max, |dW d| <= 4u ||W||_F, so
-//   d sqrt(kappa) <= u (|o_u| (3 + 4 sqrt3 cond) + 12 sqrt3 cond),  d kappa <= 2 sqrt(kappa) d sqrt(kappa),
-// doubled for safety.  Pairs with |kappa_fp32 - lam^2| <= band are re-decided in fp64.
-__device__ __forceinline__ float kappa_band(double ou_norm, double cond, double lam) {
-    const double u = 5.9604644775390625e-08;
-    double dsk = u * (ou_norm * (3.0 + 6.9282032302755 * cond) + 20.784609690826528 * cond);
-    double band = 2.0 * (2.0 * lam * dsk + 4.0 * u * lam * lam);
-    return (float)band;
+// Raster payload of one Gaussian (renderer.py:78-80 quantities, precomputed per view).
+// kappa = |m|^2 / |d_u|^2 with d_u = W d and m = o_u x d_u = M d, M = [o_u]_x W, so both
+// norms are quadratic forms in the pixel ray d: |d_u|^2 = d^T A d (A = W^T W) and
+// |m|^2 = d^T B d (B = M^T M).  Evaluated in fp64 (12 DFMA per pair) their relative error is
+// ~1e-16 |o_u|^2 cond(W)^2; the absolute kappa error bound is stored in ext.x.  When that bound
+// exceeds 1e-7 (|o_u| cond > ~7e3: tiny, far or very anisotropic Gaussians) the payload
+// instead carries W and o_u (mode 1) and the raster uses the fp64 cross product, the
+// reference's own formulation (core.py:184-199), whose error grows only like |o_u|.
+__device__ void make_payload(const double W[9], const double ou[3], const double rgb[3], double sigma, double cond,
+                             double lam, Payload &pl, GradPayload &gp) {
+    const double u64 = 1.1102230246251565e-16;
+    const double on2 = ou[0] * ou[0] + ou[1] * ou[1] + ou[2] * ou[2];
+    const double band0 = 32.0 * u64 * (on2 * cond * cond + lam * lam + 1.0);
+    const bool mode1 = !(band0 <= 1e-7);
+    if (!mode1) {
+        double A[9], M[9], B[9];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) A[i * 3 + j] = W[0 * 3 + i] * W[0 * 3 + j] + W[1 * 3 + i] * W[1 * 3 + j] + W[2 * 3 + i] * W[2 * 3 + j];
+        // M = [o]_x W : row i of M = (o x column) components
+        for (int j = 0; j < 3; ++j) {
+            M[0 * 3 + j] = ou[1] * W[2 * 3 + j] - ou[2] * W[1 * 3 + j];
+            M[1 * 3 + j] = ou[2] * W[0 * 3 + j] - ou[0] * W[2 * 3 + j];
+            M[2 * 3 + j] = ou[0] * W[1 * 3 + j] - ou[1] * W[0 * 3 + j];
+        }
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) B[i * 3 + j] = M[0 * 3 + i] * M[0 * 3 + j] + M[1 * 3 + i] * M[1 * 3 + j] + M[2 * 3 + i] * M[2 * 3 + j];
+        pl.q[0] = A[0]; pl.q[1] = A[4]; pl.q[2] = A[8];
+        pl.q[3] = 2.0 * A[1]; pl.q[4] = 2.0 * A[2]; pl.q[5] = 2.0 * A[5];
+        pl.q[6] = B[0]; pl.q[7] = B[4]; pl.q[8] = B[8];
+        pl.q[9] = 2.0 * B[1]; pl.q[10] = 2.0 * B[2]; pl.q[11] = 2.0 * B[5];
+    } else {
+        for (int i = 0; i < 9; ++i) pl.q[i] = W[i];
+        for (int i = 0; i < 3; ++i) pl.q[9 + i] = ou[i];
+    }
+    const double band1 = 64.0 * u64 * (sqrt(on2) + 1.0) * (cond + 1.0) * (2.0 * lam + 1.0);
+    pl.col = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], mode1 ? -(float)sigma : (float)sigma);
+    pl.ext = make_float4((float)(mode1 ? band1 : band0), 0.f, 0.f, 0.f);
+    gp.r0 = make_float4((float)W[0], (float)W[1], (float)W[2], (float)ou[0]);
+    gp.r1 = make_float4((float)W[3], (float)W[4], (float)W[5], (float)ou[1]);
+    gp.r2 = make_float4((float)W[6], (float)W[7], (float)W[8], (float)ou[2]);
 }
 
 __global__ void __launch_bounds__(128) k_preprocess(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x,
                                                     const double *__restrict__ medges_y, Payload *__restrict__ payload,
-                                                    uint32_t *__restrict__ depth_key, int64_t *__restrict__ count,
+                                                    GradPayload *__restrict__ gpayload, uint32_t *__restrict__ depth_key, int64_t *__restrict__ count,
                                                     AxisRanges *__restrict__ ranges, uint8_t *__restrict__ flags,
                                                     double *__restrict__ mu_out, double *__restrict__ depth_out,
                                                     int *__restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *sex = reinterpret_cast<double *>(smem_raw);
     double *sey = sex + (fc.n_x + 1);
-    float *ssh = reinterpret_cast<float *>(sey + (fc.n_y + 1));
+    // SH staging area, 16-byte aligned for the float4 copies
+    float *ssh = reinterpret_cast<float *>(smem_raw + ((sizeof(double) * (fc.n_x + fc.n_y + 2) + 15) & ~(size_t)15));
     const int nb3 = sc.n_bands * 3;
     for (int i = threadIdx.x; i <= fc.n_x; i += blockDim.x) sex[i] = medges_x[i];
     for (int i = threadIdx.x; i <= fc.n_y; i += blockDim.x) sey[i] = medges_y[i];
@@ -523,15 +554,12 @@ __global__ void __launch_bounds__(128) k_preprocess(FrameConst fc, geer_scene sc
         if (pre > 0) gate |= (uint8_t)(1u << c);
         rgb[c] = pre > 0.0 ? pre : 0.0;
     }
-    double ou_norm = sqrt(ou[0] * ou[0] + ou[1] * ou[1] + ou[2] * ou[2]);
     double smax = fmax(s[0], fmax(s[1], s[2])), smin = fmin(s[0], fmin(s[1], s[2]));
     Payload pl;
-    pl.r0 = make_float4((float)W[0], (float)W[1], (float)W[2], (float)ou[0]);
-    pl.r1 = make_float4((float)W[3], (float)W[4], (float)W[5], (float)ou[1]);
-    pl.r2 = make_float4((float)W[6], (float)W[7], (float)W[8], (float)ou[2]);
-    pl.col = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], (float)sigma);
-    pl.ext = make_float4(kappa_band(ou_norm, smax / smin, fc.lam), 0.f, 0.f, 0.f);
+    GradPayload gp;
+    make_payload(W, ou, rgb, sigma, smax / smin, fc.lam, pl, gp);
     payload[g] = pl;
+    gpayload[g] = gp;
 
     uint8_t fl = (uint8_t)(gate << 3);
     int64_t n_ent = 0;
@@ -735,11 +763,11 @@ void launch_item_fill(int n_tiles, const int32_t *tile_off, const int32_t *item_
 }
 
 size_t preprocess_smem(const FrameConst &fc) {
-    return sizeof(double) * (fc.n_x + fc.n_y + 2) + sizeof(float) * 128 * fc.n_bands * 3 + 16;
+    return ((sizeof(double) * (fc.n_x + fc.n_y + 2) + 15) & ~(size_t)15) + sizeof(float) * 128 * fc.n_bands * 3;
 }
 
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
-                       Payload *payload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges, uint8_t *flags,
+                       Payload *payload, GradPayload *gpayload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges, uint8_t *flags,
                        double *mu_out, double *depth_out, int *err, cudaStream_t st) {
     if (sc.n == 0) return;
     size_t smem = preprocess_smem(fc);
@@ -749,7 +777,7 @@ void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double 
         attr_set = true;
     }
     int blocks = (int)((sc.n + 127) / 128);
-    k_preprocess<<<blocks, 128, smem, st>>>(fc, sc, medges_x, medges_y, payload, depth_key, count, ranges, flags,
+    k_preprocess<<<blocks, 128, smem, st>>>(fc, sc, medges_x, medges_y, payload, gpayload, depth_key, count, ranges, flags,
                                             mu_out, depth_out, err);
 }
 

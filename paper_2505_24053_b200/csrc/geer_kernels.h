@@ -23,7 +23,7 @@ void launch_item_fill(int n_tiles, const int32_t *tile_off, const int32_t *item_
                       cudaStream_t st);
 size_t preprocess_smem(const FrameConst &fc);
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
-                       Payload *payload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges, uint8_t *flags,
+                       Payload *payload, GradPayload *gpayload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges, uint8_t *flags,
                        double *mu_out, double *depth_out, int *err, cudaStream_t st);
 template <typename T>
 void launch_finalize(const FrameConst &fc, const geer_scene &sc, const float4 *accum, const uint8_t *flags, T *dmeans,
@@ -56,12 +56,12 @@ void tile_ranges(const uint32_t *sorted_tiles, int64_t n_entries, int n_tiles, i
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    float *color, float *remaining, int32_t *count, int32_t *n_eval,
-                    unsigned long long *rechecks, cudaStream_t st);
+                    float *color, float *remaining, int32_t *count, int32_t *n_eval, unsigned long long *counters,
+                    int32_t *fixup_list, cudaStream_t st);
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                      const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                     const float *remaining, const int32_t *n_eval, const float *dl_dimage, float4 *accum,
+                     const GradPayload *gpayload, const float *remaining, const int32_t *n_eval, const float *dl_dimage, float *accum,
                      cudaStream_t st);
 void launch_sum_i32(const int32_t *v, int64_t n, unsigned long long *out, cudaStream_t st);
 void launch_convert_f64_f32(const double *in, float *out, int64_t n, cudaStream_t st);

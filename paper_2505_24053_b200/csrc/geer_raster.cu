@@ -68,8 +68,12 @@ __device__ __forceinline__ void pixel_ray(const FrameConst &fc, int p, const dou
 
 // fp64 kappa of (Gaussian g, ray d) from the stored parameters, in the
 // reference's operation order (renderer.py:78-79,96-101; no contraction).
-__device__ __noinline__ double kappa_fp64(const FrameConst &fc, const geer_scene &sc, int64_t g, const double d[3]) {
-    double q0 = sc.quats[g * 4 + 0], q1 = sc.quats[g * 4 + 1], q2 = sc.quats[g * 4 + 2], q3 = sc.quats[g * 4 + 3];
+__device__ __noinline__ double kappa_fp64(const float *__restrict__ means, const float *__restrict__ log_scales,
+                                          const float *__restrict__ quats, double ox, double oy, double oz, int64_t g,
+                                          double dx, double dy, double dz) {
+    const double origin[3] = {ox, oy, oz};
+    const double d[3] = {dx, dy, dz};
+    double q0 = quats[g * 4 + 0], q1 = quats[g * 4 + 1], q2 = quats[g * 4 + 2], q3 = quats[g * 4 + 3];
     double qn = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(q0, q0), __dmul_rn(q1, q1)), __dmul_rn(q2, q2)),
                                      __dmul_rn(q3, q3)));
     double r = __ddiv_rn(q0, qn), i = __ddiv_rn(q1, qn), j = __ddiv_rn(q2, qn), k = __ddiv_rn(q3, qn);
@@ -84,11 +88,11 @@ __device__ __noinline__ double kappa_fp64(const FrameConst &fc, const geer_scene
     rot[7] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(j, k), __dmul_rn(r, i)));
     rot[8] = __dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(__dmul_rn(i, i), __dmul_rn(j, j))));
     double s[3], W[9];
-    for (int a = 0; a < 3; ++a) s[a] = exp((double)sc.log_scales[g * 3 + a]);
+    for (int a = 0; a < 3; ++a) s[a] = exp((double)log_scales[g * 3 + a]);
     for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b) W[a * 3 + b] = __ddiv_rn(rot[b * 3 + a], s[a]);
     double rel[3];
-    for (int a = 0; a < 3; ++a) rel[a] = __dsub_rn(fc.origin[a], (double)sc.means[g * 3 + a]);
+    for (int a = 0; a < 3; ++a) rel[a] = __dsub_rn(origin[a], (double)means[g * 3 + a]);
     double ou[3], du[3];
     for (int a = 0; a < 3; ++a) {
         ou[a] = __dadd_rn(__dadd_rn(__dmul_rn(W[a * 3 + 0], rel[0]), __dmul_rn(W[a * 3 + 1], rel[1])),
@@ -104,32 +108,63 @@ __device__ __noinline__ double kappa_fp64(const FrameConst &fc, const geer_scene
     return __ddiv_rn(mm, dd);
 }
 
-struct PairEval {
-    float du0, du1, du2, m0, m1, m2, rdd, kap, alpha, u, t;
+// Per-pixel ray in fp64 plus its quadratic monomials (for the mode-0 payload).
+struct Ray64 {
+    double d0, d1, d2;
+    double m00, m11, m22, m01, m02, m12;
 };
 
-// Shared by forward and backward: identical instruction sequence -> identical bits.
-__device__ __forceinline__ void eval_pair(const Payload &P, float dx, float dy, float dz, const FrameConst &fc,
-                                          const geer_scene &sc, uint32_t gid, const double d64[3], PairEval &e,
-                                          int &rechecks) {
-    const float4 r0 = P.r0, r1 = P.r1, r2 = P.r2;
-    e.du0 = __fmaf_rn(r0.z, dz, __fmaf_rn(r0.y, dy, __fmul_rn(r0.x, dx)));
-    e.du1 = __fmaf_rn(r1.z, dz, __fmaf_rn(r1.y, dy, __fmul_rn(r1.x, dx)));
-    e.du2 = __fmaf_rn(r2.z, dz, __fmaf_rn(r2.y, dy, __fmul_rn(r2.x, dx)));
-    const float o0 = r0.w, o1 = r1.w, o2 = r2.w;
-    e.m0 = __fmaf_rn(o1, e.du2, -__fmul_rn(o2, e.du1));
-    e.m1 = __fmaf_rn(o2, e.du0, -__fmul_rn(o0, e.du2));
-    e.m2 = __fmaf_rn(o0, e.du1, -__fmul_rn(o1, e.du0));
-    const float dd = __fmaf_rn(e.du2, e.du2, __fmaf_rn(e.du1, e.du1, __fmul_rn(e.du0, e.du0)));
-    const float mm = __fmaf_rn(e.m2, e.m2, __fmaf_rn(e.m1, e.m1, __fmul_rn(e.m0, e.m0)));
-    e.rdd = rcp_approx(dd);
-    e.kap = __fmul_rn(mm, e.rdd);
+__device__ __forceinline__ Ray64 make_ray(const double d[3]) {
+    Ray64 r;
+    r.d0 = d[0];
+    r.d1 = d[1];
+    r.d2 = d[2];
+    r.m00 = d[0] * d[0];
+    r.m11 = d[1] * d[1];
+    r.m22 = d[2] * d[2];
+    r.m01 = d[0] * d[1];
+    r.m02 = d[0] * d[2];
+    r.m12 = d[1] * d[2];
+    return r;
+}
+
+struct PairT {
+    float kap, alpha, u, t, dd;
+};
+
+// kappa of (payload P, ray R) in fp64, then the blend quantities in fp32:
+//   u = sigma exp(-kappa/2) [kappa <= lam^2], t = min(u, 0.999)   (renderer.py:96-105)
+// Shared verbatim by forward, backward and fix-up, so t is bit-identical in all three.
+__device__ __forceinline__ void eval_t(const Payload &P, const Ray64 &R, const FrameConst &fc, const geer_scene &sc,
+                                       uint32_t gid, PairT &e, int &rechecks) {
+    double dd, mm;
+    const float sw = P.col.w;
+    if (sw >= 0.0f) {  // mode 0: quadratic forms
+        dd = fma(P.q[5], R.m12, fma(P.q[4], R.m02, fma(P.q[3], R.m01, fma(P.q[2], R.m22, fma(P.q[1], R.m11, P.q[0] * R.m00)))));
+        mm = fma(P.q[11], R.m12, fma(P.q[10], R.m02, fma(P.q[9], R.m01, fma(P.q[8], R.m22, fma(P.q[7], R.m11, P.q[6] * R.m00)))));
+    } else {  // mode 1: d_u = W d, m = o_u x d_u (core.py:184-199)
+        const double u0 = fma(P.q[2], R.d2, fma(P.q[1], R.d1, P.q[0] * R.d0));
+        const double u1 = fma(P.q[5], R.d2, fma(P.q[4], R.d1, P.q[3] * R.d0));
+        const double u2 = fma(P.q[8], R.d2, fma(P.q[7], R.d1, P.q[6] * R.d0));
+        const double o0 = P.q[9], o1 = P.q[10], o2 = P.q[11];
+        const double x0 = fma(o1, u2, -(o2 * u1)), x1 = fma(o2, u0, -(o0 * u2)), x2 = fma(o0, u1, -(o1 * u0));
+        dd = fma(u2, u2, fma(u1, u1, u0 * u0));
+        mm = fma(x2, x2, fma(x1, x1, x0 * x0));
+    }
+    const float ddf = (float)dd;
+    e.dd = ddf;
+    e.kap = __fmul_rn((float)mm, rcp_approx(ddf));
     e.alpha = ex2_approx(__fmul_rn(e.kap, -0.72134752044448170f));  // exp(-kappa/2)
-    float u = __fmul_rn(P.col.w, e.alpha);
+    float u = __fmul_rn(fabsf(sw), e.alpha);
     if (fc.cutoff) {
         bool inside = e.kap <= fc.lam2f;
-        if (fabsf(__fsub_rn(e.kap, fc.lam2f)) <= P.ext.x) {
-            inside = kappa_fp64(fc, sc, gid, d64) <= fc.lam2;
+        // kappa_fp32 carries ~3e-7 relative error: re-decide the cutoff in fp64 near lam^2
+        if (fabsf(__fsub_rn(e.kap, fc.lam2f)) <= 1e-6f * fc.lam2f + P.ext.x) {
+            const double k64 = mm / dd;
+            inside = k64 <= fc.lam2;
+            if (fabs(k64 - fc.lam2) <= (double)P.ext.x)  // inside the fp64 error bound: reference formulation
+                inside = kappa_fp64(sc.means, sc.log_scales, sc.quats, fc.origin[0], fc.origin[1], fc.origin[2], gid,
+                                    R.d0, R.d1, R.d2) <= fc.lam2;
             ++rechecks;
         }
         u = inside ? u : 0.0f;
@@ -138,90 +173,333 @@ __device__ __forceinline__ void eval_pair(const Payload &P, float dx, float dy, 
     e.t = fminf(u, kMaxBlendTF);
 }
 
+// Relative bound on |t_fp32 - t_exact| / t for a pair (fp64 kappa rounded to fp32, rcp/ex2 approximations).
+__device__ __forceinline__ float t_rel_bound(float kap) { return 3e-7f * (1.0f + kap); }
+
+// ------------------------------------------------------------------------------ pipeline plumbing
+//
+// Each raster CTA = kConsumerWarps consumer warps (one pixel per lane) + 1
+// producer warp.  The producer streams the tile's entries through a ring of
+// kStages shared-memory stages: it gathers each entry's 80-byte payload with one
+// cp.async.bulk (global -> shared, completion counted on the stage's "full"
+// mbarrier) and the consumer warps release a stage through its "empty" mbarrier.
+// Consumer warps never meet at a CTA barrier: each warp retires as soon as its
+// own 32 pixels are opaque, and the producer stops streaming once every
+// consumer warp is done.
+
+constexpr int kConsumerWarps = kRasterThreads / 32;  // 8
+constexpr int kStages = 4;
+constexpr int kStageEntries = 32;  // one entry per producer lane
+constexpr int kPipeThreads = kRasterThreads + 32;
+
+struct __align__(16) PipeSmem {
+    Payload ring[kStages][kStageEntries];
+    GradPayload gring[kStages][kStageEntries];  // backward only
+    uint32_t gid[kStages][kStageEntries];
+    int count[kStages];  // entries in the stage; 0 = end of stream
+    unsigned long long full[kStages];
+    unsigned long long empty[kStages];
+    int done_warps;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void pipe_init(PipeSmem &S) {
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.empty[s], kConsumerWarps);
+        }
+        S.done_warps = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+}
+
+// Producer warp: stream entries [first, first + n_total) (forward order) or the
+// same range walked from the back (reverse) in stages of kStageEntries.
+template <bool kReverse>
+__device__ __forceinline__ void pipe_produce(PipeSmem &S, const uint32_t *__restrict__ order,
+                                             const Payload *__restrict__ payload,
+                                             const GradPayload *__restrict__ gpayload, int first, int n_total,
+                                             bool stop_when_done) {
+    const unsigned per_entry = (unsigned)(sizeof(Payload) + (gpayload ? sizeof(GradPayload) : 0));
+    const int lane = threadIdx.x & 31;
+    unsigned phase = 0;
+    int s = 0;
+    for (int b = 0;; ++b) {
+        const int done = kStageEntries * b;
+        int n = min(kStageEntries, n_total - done);
+        if (n > 0 && stop_when_done && *((volatile int *)&S.done_warps) == kConsumerWarps) n = 0;
+        mbar_wait(&S.empty[s], phase ^ 1);
+        if (n <= 0) {
+            if (lane == 0) {
+                S.count[s] = 0;
+                mbar_arrive(&S.full[s]);
+            }
+            return;
+        }
+        // reverse: stage b holds entries [first + n_total - done - n, first + n_total - done)
+        const int base = kReverse ? first + n_total - done - n : first + done;
+        uint32_t g = 0;
+        if (lane < n) {
+            g = __ldg(order + base + lane);
+            S.gid[s][lane] = g;
+        }
+        if (lane == 0) {
+            S.count[s] = n;
+            mbar_arrive_expect_tx(&S.full[s], n * per_entry);
+        }
+        __syncwarp();
+        if (lane < n) {
+            bulk_g2s(&S.ring[s][lane], payload + g, sizeof(Payload), &S.full[s]);
+            if (gpayload) bulk_g2s(&S.gring[s][lane], gpayload + g, sizeof(GradPayload), &S.full[s]);
+        }
+        if (++s == kStages) {
+            s = 0;
+            phase ^= 1;
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------ K5
 
+// Forward blend of one pair into the pixel state, with a running bound on
+// |rem_fp32 - rem_fp64| (err).  Returns false when the pixel stops: either
+// surely opaque, or too close to the 1e-4 threshold to decide in fp32
+// (borderline -> the pixel is redone in fp64 by k_fixup).
+struct PixelState {
+    float cr, cg, cb, rem, err;
+    int cnt, ne;
+};
+
+__device__ __forceinline__ int blend_step(PixelState &ps, const PairT &e, const Payload &P) {
+    const float hb = t_rel_bound(e.kap);
+    // alive test of renderer.py:113, decided against the fp64 remaining: rem64 in [rem - err, rem + err]
+    const float lo = ps.rem - ps.err, hi = ps.rem + ps.err;
+    if (!(lo >= 1.00001e-4f)) return hi < 0.99999e-4f ? 0 : 2;  // 0: stop, 2: borderline
+    ++ps.ne;
+    const float w = __fmul_rn(ps.rem, e.t);
+    ps.cr = __fmaf_rn(w, P.col.x, ps.cr);
+    ps.cg = __fmaf_rn(w, P.col.y, ps.cg);
+    ps.cb = __fmaf_rn(w, P.col.z, ps.cb);
+    const float omt = __fsub_rn(1.0f, e.t);
+    // |d rem| <= |d rem| (1 - t) + rem |d t|, |d t| <= t * hb (hb: kappa band / 2 + approx. error)
+    ps.err = __fmaf_rn(ps.err, omt, __fmul_rn(w, hb)) + 1.2e-7f * ps.rem;
+    ps.rem = __fmul_rn(ps.rem, omt);
+    ps.cnt += e.t > 0.0f;
+    return 1;
+}
+
 template <bool kBEAP>
-__global__ void __launch_bounds__(kRasterThreads, 2)
+__global__ void __launch_bounds__(kPipeThreads, 2)
     k_forward(FrameConst fc, geer_scene sc, const int4 *__restrict__ items, const int32_t *__restrict__ n_items,
               const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
               const double2 *__restrict__ row_sc, const double *__restrict__ dir64, const int32_t *__restrict__ ranges,
               const uint32_t *__restrict__ order, const Payload *__restrict__ payload, float *__restrict__ color,
               float *__restrict__ remaining, int32_t *__restrict__ count, int32_t *__restrict__ n_eval,
-              unsigned long long *__restrict__ rechecks_out) {
-    __shared__ Payload sbuf[2][kFwdBatch];
-    __shared__ uint32_t sgid[2][kFwdBatch];
+              unsigned long long *__restrict__ counters, int32_t *__restrict__ fixup_list) {
+    __shared__ PipeSmem S;
     if ((int)blockIdx.x >= *n_items) return;
     const int4 it = items[blockIdx.x];
+    const int e0 = ranges[it.x], e1 = ranges[it.x + 1];
+    pipe_init(S);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == kConsumerWarps) {
+        pipe_produce<false>(S, order, payload, nullptr, e0, e1 - e0, true);
+        return;
+    }
     const int tid = threadIdx.x;
     const bool valid = tid < it.z;
     const int p = valid ? pix_list[it.y + tid] : 0;
     double d64[3] = {0.0, 0.0, 1.0};
     if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
-    const float dx = (float)d64[0], dy = (float)d64[1], dz = (float)d64[2];
-
-    const int e0 = ranges[it.x], e1 = ranges[it.x + 1];
-    float cr = 0.f, cg = 0.f, cb = 0.f, rem = 1.0f;
-    int cnt = 0, ne = 0, rechecks = 0;
-    bool done = !valid;
-
-    auto stage = [&](int buf, int base) {
-        const int n = min(kFwdBatch, e1 - base);
-        for (int i = tid; i < n * 5; i += kRasterThreads) {
-            const int e = i / 5, part = i - e * 5;
-            const uint32_t g = __ldg(order + base + e);
-            cp_async16(reinterpret_cast<float4 *>(&sbuf[buf][e]) + part, reinterpret_cast<const float4 *>(payload + g) + part);
-            if (part == 0) sgid[buf][e] = g;
-        }
-        cp_async_commit();
-    };
-
-    int buf = 0;
-    if (e0 < e1) stage(0, e0);
-    for (int base = e0; base < e1; base += kFwdBatch) {
-        const bool more = base + kFwdBatch < e1;
-        if (more) {
-            stage(buf ^ 1, base + kFwdBatch);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        if (!done) {
-            const int n = min(kFwdBatch, e1 - base);
-            for (int j = 0; j < n; ++j) {
-                if (!(rem >= kMinRemainingF)) {  // renderer.py:113 alive test, before the contribution
-                    done = true;
-                    break;
+    const Ray64 R = make_ray(d64);
+    PixelState ps{0.f, 0.f, 0.f, 1.0f, 0.f, 0, 0};
+    bool live = valid, border = false;
+    int rechecks = 0;
+    bool warp_live = __any_sync(0xffffffffu, live);
+    if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
+    unsigned phase = 0;
+    int s = 0;
+    for (;;) {
+        mbar_wait(&S.full[s], phase);
+        const int n = S.count[s];
+        if (n == 0) break;
+        if (warp_live) {
+            for (int j = 0; j < n; j += 2) {
+                if (!__any_sync(0xffffffffu, live)) break;
+                const Payload &Pa = S.ring[s][j];
+                const bool has_b = j + 1 < n;
+                const Payload &Pb = S.ring[s][has_b ? j + 1 : j];
+                PairT a, b;
+                int rc_dup = 0;
+                eval_t(Pa, R, fc, sc, S.gid[s][j], a, rechecks);
+                eval_t(Pb, R, fc, sc, S.gid[s][has_b ? j + 1 : j], b, has_b ? rechecks : rc_dup);
+                if (live) {
+                    int r = blend_step(ps, a, Pa);
+                    if (r != 1) {
+                        live = false;
+                        border = r == 2;
+                    } else if (has_b) {
+                        r = blend_step(ps, b, Pb);
+                        if (r != 1) {
+                            live = false;
+                            border = r == 2;
+                        }
+                    }
                 }
-                ++ne;
-                const Payload &P = sbuf[buf][j];
-                PairEval e;
-                eval_pair(P, dx, dy, dz, fc, sc, sgid[buf][j], d64, e, rechecks);
-                const float w = __fmul_rn(rem, e.t);
-                cr = __fmaf_rn(w, P.col.x, cr);
-                cg = __fmaf_rn(w, P.col.y, cg);
-                cb = __fmaf_rn(w, P.col.z, cb);
-                rem = __fmul_rn(rem, __fsub_rn(1.0f, e.t));
-                cnt += e.t > 0.0f;
             }
+            warp_live = __any_sync(0xffffffffu, live);
+            if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
         }
-        buf ^= 1;
-        if (!__syncthreads_or(!done)) break;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[s]);
+        if (++s == kStages) {
+            s = 0;
+            phase ^= 1;
+        }
     }
-    cp_async_wait<0>();  // no copy may be in flight when the CTA retires
     if (valid) {
         // renderer.py:118 background with the final remaining transmittance
-        color[(int64_t)p * 3 + 0] = __fmaf_rn(rem, fc.bg[0], cr);
-        color[(int64_t)p * 3 + 1] = __fmaf_rn(rem, fc.bg[1], cg);
-        color[(int64_t)p * 3 + 2] = __fmaf_rn(rem, fc.bg[2], cb);
-        remaining[p] = rem;
+        color[(int64_t)p * 3 + 0] = __fmaf_rn(ps.rem, fc.bg[0], ps.cr);
+        color[(int64_t)p * 3 + 1] = __fmaf_rn(ps.rem, fc.bg[1], ps.cg);
+        color[(int64_t)p * 3 + 2] = __fmaf_rn(ps.rem, fc.bg[2], ps.cb);
+        remaining[p] = ps.rem;
+        count[p] = ps.cnt;
+        n_eval[p] = ps.ne;
+        if (border) {
+            unsigned long long slot = atomicAdd(&counters[2], 1ull);
+            fixup_list[slot] = (int32_t)(((int64_t)blockIdx.x << 8) | tid);  // work item, thread
+        }
+    }
+    rechecks = __reduce_add_sync(0xffffffffu, rechecks);
+    if (lane == 0 && rechecks) atomicAdd(&counters[0], (unsigned long long)rechecks);
+}
+
+// ------------------------------------------------------------------------------ fp64 fix-up of borderline pixels
+
+// One warp per borderline pixel: the pixel is recomposited in fp64 exactly as
+// renderer.py:96-118 (kappa, u, t, remaining in fp64; the 1e-4 early-stop test
+// on the fp64 remaining), so its early-stop decision is the reference's.
+template <bool kBEAP>
+__device__ void fixup_pixel(FrameConst fc, const geer_scene &sc, const int4 *__restrict__ items,
+                            const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
+                            const double2 *__restrict__ row_sc, const double *__restrict__ dir64,
+                            const int32_t *__restrict__ ranges, const uint32_t *__restrict__ order,
+                            const Payload *__restrict__ payload, int code, int lane, float *__restrict__ color,
+                            float *__restrict__ remaining, int32_t *__restrict__ count, int32_t *__restrict__ n_eval) {
+    const int4 it = items[code >> 8];
+    const int p = pix_list[it.y + (code & 255)];
+    double d[3];
+    pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d);
+    const int e0 = ranges[it.x], e1 = ranges[it.x + 1];
+    double cr = 0, cg = 0, cb = 0, rem = 1.0;
+    int cnt = 0, ne = 0;
+    bool alive = true;
+    const Ray64 R = make_ray(d);
+    for (int base = e0; base < e1 && alive; base += 32) {
+        const int e = base + lane;
+        double t = 0.0;
+        uint32_t g = 0;
+        if (e < e1) {
+            // fp64 kappa (payload quadratic forms / cross product), fp64 exp: renderer.py:96-105 in fp64
+            g = order[e];
+            const Payload &P = payload[g];
+            double dd, mm;
+            if (P.col.w >= 0.0f) {
+                dd = fma(P.q[5], R.m12, fma(P.q[4], R.m02, fma(P.q[3], R.m01, fma(P.q[2], R.m22, fma(P.q[1], R.m11, P.q[0] * R.m00)))));
+                mm = fma(P.q[11], R.m12, fma(P.q[10], R.m02, fma(P.q[9], R.m01, fma(P.q[8], R.m22, fma(P.q[7], R.m11, P.q[6] * R.m00)))));
+            } else {
+                const double u0 = fma(P.q[2], R.d2, fma(P.q[1], R.d1, P.q[0] * R.d0));
+                const double u1 = fma(P.q[5], R.d2, fma(P.q[4], R.d1, P.q[3] * R.d0));
+                const double u2 = fma(P.q[8], R.d2, fma(P.q[7], R.d1, P.q[6] * R.d0));
+                const double x0 = fma(P.q[10], u2, -(P.q[11] * u1)), x1 = fma(P.q[11], u0, -(P.q[9] * u2));
+                const double x2 = fma(P.q[9], u1, -(P.q[10] * u0));
+                dd = fma(u2, u2, fma(u1, u1, u0 * u0));
+                mm = fma(x2, x2, fma(x1, x1, x0 * x0));
+            }
+            double kap = mm / dd;
+            if (fc.cutoff && fabs(kap - fc.lam2) <= (double)P.ext.x)
+                kap = kappa_fp64(sc.means, sc.log_scales, sc.quats, fc.origin[0], fc.origin[1], fc.origin[2], g, d[0],
+                                 d[1], d[2]);
+            const double x = (double)sc.opacity_logits[g];
+            const double sig = x >= 0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x));
+            double u = sig * exp(-0.5 * kap);
+            if (fc.cutoff && !(kap <= fc.lam2)) u = 0.0;
+            t = u < kMaxBlendT ? u : kMaxBlendT;
+        }
+        const int n = min(32, e1 - base);
+        for (int j = 0; j < n; ++j) {
+            const double tj = __shfl_sync(0xffffffffu, t, j);
+            const uint32_t gj = __shfl_sync(0xffffffffu, g, j);
+            if (!(rem >= kMinRemaining)) {
+                alive = false;
+                break;
+            }
+            ++ne;
+            const float4 col = payload[gj].col;
+            const double w = rem * tj;
+            cr += w * col.x;
+            cg += w * col.y;
+            cb += w * col.z;
+            rem = rem * (1.0 - tj);
+            cnt += tj > 0;
+        }
+    }
+    if (lane == 0) {
+        color[(int64_t)p * 3 + 0] = (float)(cr + rem * fc.bg[0]);
+        color[(int64_t)p * 3 + 1] = (float)(cg + rem * fc.bg[1]);
+        color[(int64_t)p * 3 + 2] = (float)(cb + rem * fc.bg[2]);
+        remaining[p] = (float)rem;
         count[p] = cnt;
         n_eval[p] = ne;
     }
-    if (rechecks_out) {
-        rechecks = __reduce_add_sync(0xffffffffu, rechecks);
-        if ((tid & 31) == 0 && rechecks) atomicAdd(rechecks_out, (unsigned long long)rechecks);
-    }
+}
+
+template <bool kBEAP>
+__global__ void __launch_bounds__(128) k_fixup(FrameConst fc, geer_scene sc, const int4 *__restrict__ items,
+                                               const int32_t *__restrict__ pix_list,
+                                               const double2 *__restrict__ col_sc, const double2 *__restrict__ row_sc,
+                                               const double *__restrict__ dir64, const int32_t *__restrict__ ranges,
+                                               const uint32_t *__restrict__ order, const Payload *__restrict__ payload,
+                                               const unsigned long long *__restrict__ counters,
+                                               const int32_t *__restrict__ fixup_list, float *__restrict__ color,
+                                               float *__restrict__ remaining, int32_t *__restrict__ count,
+                                               int32_t *__restrict__ n_eval) {
+    const int lane = threadIdx.x & 31;
+    const int n_fix = (int)counters[2];
+    const int n_warps = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
+    for (int wg = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); wg < n_fix; wg += n_warps)
+        fixup_pixel<kBEAP>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload, fixup_list[wg], lane,
+                           color, remaining, count, n_eval);
 }
 
 // ------------------------------------------------------------------------------ K6
@@ -259,28 +537,44 @@ __device__ __forceinline__ float warp_transpose_reduce16(float v[16], int lane) 
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+// Reverse-order backward (renderer.py:259-310).  The producer streams the
+// tile's first max_n entries back to front; each lane walks its pixel's alive
+// entries (index < n_eval) from the last to the first, recovering
+// T_i = T_{i+1} / (1 - t_i) from the forward's final remaining, and the warp
+// adds its 16 per-entry partials to the Gaussian's accumulators.
 template <bool kBEAP>
-__global__ void __launch_bounds__(kRasterThreads, 2)
+__global__ void __launch_bounds__(kPipeThreads, 2)
     k_backward(FrameConst fc, geer_scene sc, const int4 *__restrict__ items, const int32_t *__restrict__ n_items,
                const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
                const double2 *__restrict__ row_sc, const double *__restrict__ dir64,
                const int32_t *__restrict__ ranges, const uint32_t *__restrict__ order,
-               const Payload *__restrict__ payload, const float *__restrict__ remaining,
-               const int32_t *__restrict__ n_eval, const float *__restrict__ dl_dimage, float4 *__restrict__ accum) {
-    constexpr int kWarps = kRasterThreads / 32;
-    __shared__ Payload sbuf[kBwdBatch];
-    __shared__ uint32_t sgid[kBwdBatch];
-    __shared__ float red[kWarps][kBwdBatch][16];
+               const Payload *__restrict__ payload, const GradPayload *__restrict__ gpayload,
+               const float *__restrict__ remaining, const int32_t *__restrict__ n_eval,
+               const float *__restrict__ dl_dimage, float *__restrict__ accum) {
+    __shared__ PipeSmem S;
     __shared__ int smax;
     if ((int)blockIdx.x >= *n_items) return;
     const int4 it = items[blockIdx.x];
+    const int e0 = ranges[it.x];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool valid = tid < it.z;
+    const bool valid = warp < kConsumerWarps && tid < it.z;
     const int p = valid ? pix_list[it.y + tid] : 0;
+    const int ne = valid ? n_eval[p] : 0;
+    if (tid == 0) smax = 0;
+    __syncthreads();
+    const int wmax = __reduce_max_sync(0xffffffffu, ne);
+    if (lane == 0 && wmax > 0) atomicMax(&smax, wmax);
+    pipe_init(S);  // (its __syncthreads also publishes smax)
+    const int max_n = smax;
+    if (max_n == 0) return;
+    if (warp == kConsumerWarps) {
+        pipe_produce<true>(S, order, payload, gpayload, e0, max_n, false);
+        return;
+    }
     double d64[3] = {0.0, 0.0, 1.0};
     if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
+    const Ray64 R = make_ray(d64);
     const float dx = (float)d64[0], dy = (float)d64[1], dz = (float)d64[2];
-    const int ne = valid ? n_eval[p] : 0;
     const float t_fin = valid ? remaining[p] : 0.f;
     float gl0 = 0.f, gl1 = 0.f, gl2 = 0.f;
     if (valid) {
@@ -288,44 +582,28 @@ __global__ void __launch_bounds__(kRasterThreads, 2)
         gl1 = dl_dimage[(int64_t)p * 3 + 1];
         gl2 = dl_dimage[(int64_t)p * 3 + 2];
     }
-    // renderer.py:279-280: background term scaled by the final remaining
     const float bgt0 = t_fin * fc.bg[0], bgt1 = t_fin * fc.bg[1], bgt2 = t_fin * fc.bg[2];
-    if (tid == 0) smax = 0;
-    __syncthreads();
-    const int wmax = __reduce_max_sync(0xffffffffu, ne);
-    if (lane == 0 && wmax > 0) atomicMax(&smax, wmax);
-    __syncthreads();
-    const int max_n = smax;
-    if (max_n == 0) return;
-    const int e0 = ranges[it.x];
-
-    float T = t_fin;                  // transmittance in front of the current entry, walked back
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f;  // occlusion suffix (renderer.py:283)
+    float T = t_fin, s0 = 0.f, s1 = 0.f, s2 = 0.f;
     int dummy = 0;
-    for (int hi = max_n; hi > 0; hi -= kBwdBatch) {
-        const int lo = max(0, hi - kBwdBatch);
-        const int n = hi - lo;
-        for (int i = tid; i < n * 5; i += kRasterThreads) {
-            const int e = i / 5, part = i - e * 5;
-            const uint32_t g = __ldg(order + e0 + lo + e);
-            cp_async16(reinterpret_cast<float4 *>(&sbuf[e]) + part, reinterpret_cast<const float4 *>(payload + g) + part);
-            if (part == 0) sgid[e] = g;
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
-        const bool warp_live = __any_sync(0xffffffffu, lo < ne);
-        for (int jj = n - 1; jj >= 0; --jj) {
-            const int i = lo + jj;
-            float v[16];
+    unsigned phase = 0;
+    int s = 0;
+    int hi = max_n;  // local index one past the current stage
+    for (;;) {
+        mbar_wait(&S.full[s], phase);
+        const int n = S.count[s];
+        if (n == 0) break;
+        const int lo = hi - n;
+        if (lo < wmax) {  // some lane of this warp has alive entries in the stage
+            for (int jj = n - 1; jj >= 0; --jj) {
+                const int i = lo + jj;
+                if (i >= wmax) continue;
+                float v[16];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) v[k] = 0.f;
-            const bool active = i < ne;
-            if (warp_live) {
-                if (active) {
-                    const Payload &P = sbuf[jj];
-                    PairEval e;
-                    eval_pair(P, dx, dy, dz, fc, sc, sgid[jj], d64, e, dummy);
+                for (int k = 0; k < 16; ++k) v[k] = 0.f;
+                const Payload &P = S.ring[s][jj];
+                if (i < ne) {
+                    PairT e;
+                    eval_t(P, R, fc, sc, S.gid[s][jj], e, dummy);
                     const float omt = __fsub_rn(1.0f, e.t);
                     const float inv = 1.0f / omt;
                     T = __fdiv_rn(T, omt);  // T_i = T_{i+1} / (1 - t_i)
@@ -342,54 +620,45 @@ __global__ void __launch_bounds__(kRasterThreads, 2)
                     v[13] = w * gl0;  // renderer.py:309 dcol
                     v[14] = w * gl1;
                     v[15] = w * gl2;
-                    // renderer.py:289-302 (gate: t > 0 and u < 0.999)
-                    if (e.t > 0.0f && e.u < kMaxBlendTF) {
+                    if (e.t > 0.0f && e.u < kMaxBlendTF) {  // renderer.py:289-290 gate
+                        // canonical ray (fp32): d_u = W d, m = o_u x d_u (renderer.py:96-99)
+                        const GradPayload &G = S.gring[s][jj];
+                        const float du0 = G.r0.x * dx + G.r0.y * dy + G.r0.z * dz;
+                        const float du1 = G.r1.x * dx + G.r1.y * dy + G.r1.z * dz;
+                        const float du2 = G.r2.x * dx + G.r2.y * dy + G.r2.z * dz;
+                        const float o0 = G.r0.w, o1 = G.r1.w, o2 = G.r2.w;
+                        const float m0 = o1 * du2 - o2 * du1, m1 = o2 * du0 - o0 * du2, m2 = o0 * du1 - o1 * du0;
                         v[12] = dl_dt * e.alpha;
                         const float dk = -0.5f * dl_dt * e.u;
-                        const float coef = 2.0f * dk * e.rdd;  // dl_dm = coef * m
-                        const float lm0 = coef * e.m0, lm1 = coef * e.m1, lm2 = coef * e.m2;
-                        // dl_do = d_u x dl_dm
-                        v[9] = e.du1 * lm2 - e.du2 * lm1;
-                        v[10] = e.du2 * lm0 - e.du0 * lm2;
-                        v[11] = e.du0 * lm1 - e.du1 * lm0;
-                        // dl_dd = -(2 kappa dk / dd) d_u + dl_dm x o_u
-                        const float sc_ = e.kap * coef;
-                        const float o0 = P.r0.w, o1 = P.r1.w, o2 = P.r2.w;
-                        const float dd0 = -sc_ * e.du0 + (lm1 * o2 - lm2 * o1);
-                        const float dd1 = -sc_ * e.du1 + (lm2 * o0 - lm0 * o2);
-                        const float dd2 = -sc_ * e.du2 + (lm0 * o1 - lm1 * o0);
-                        // renderer.py:304 dW_rc = sum_p dl_dd (x) d_p
-                        v[0] = dd0 * dx; v[1] = dd0 * dy; v[2] = dd0 * dz;
+                        const float coef = 2.0f * dk / e.dd;  // dl_dm = coef * m
+                        const float lm0 = coef * m0, lm1 = coef * m1, lm2 = coef * m2;
+                        v[9] = du1 * lm2 - du2 * lm1;  // dl_do = d_u x dl_dm
+                        v[10] = du2 * lm0 - du0 * lm2;
+                        v[11] = du0 * lm1 - du1 * lm0;
+                        const float sc_ = e.kap * coef;  // dl_dd = -(2 kappa dk / dd) d_u + dl_dm x o_u
+                        const float dd0 = -sc_ * du0 + (lm1 * o2 - lm2 * o1);
+                        const float dd1 = -sc_ * du1 + (lm2 * o0 - lm0 * o2);
+                        const float dd2 = -sc_ * du2 + (lm0 * o1 - lm1 * o0);
+                        v[0] = dd0 * dx; v[1] = dd0 * dy; v[2] = dd0 * dz;  // renderer.py:304 dW_rc
                         v[3] = dd1 * dx; v[4] = dd1 * dy; v[5] = dd1 * dz;
                         v[6] = dd2 * dx; v[7] = dd2 * dy; v[8] = dd2 * dz;
                     }
                 }
                 const float tot = warp_transpose_reduce16(v, lane);
-                if ((lane & 1) == 0) red[warp][jj][lane >> 1] = tot;
-            } else if (lane < 16) {
-                red[warp][jj][lane] = 0.f;
+                if ((lane & 1) == 0 && tot != 0.0f)
+                    atomicAdd(accum + (int64_t)S.gid[s][jj] * 16 + (lane >> 1), tot);
             }
         }
-        __syncthreads();
-        // CTA reduction over warps; one float4 atomic per 4 partials
-        for (int idx = tid; idx < n * 4; idx += kRasterThreads) {
-            const int jj = idx >> 2, q = idx & 3;
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
-                acc.x += red[w][jj][q * 4 + 0];
-                acc.y += red[w][jj][q * 4 + 1];
-                acc.z += red[w][jj][q * 4 + 2];
-                acc.w += red[w][jj][q * 4 + 3];
-            }
-            if (acc.x != 0.f || acc.y != 0.f || acc.z != 0.f || acc.w != 0.f)
-                atomicAdd(accum + (int64_t)sgid[jj] * 4 + q, acc);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[s]);
+        hi = lo;
+        if (++s == kStages) {
+            s = 0;
+            phase ^= 1;
         }
-        __syncthreads();
     }
 }
 
-// ------------------------------------------------------------------------------ small kernels
 
 __global__ void k_sum_i32(const int32_t *v, int64_t n, unsigned long long *out) {
     unsigned long long s = 0;
@@ -427,33 +696,38 @@ static int grid_for(int64_t n) { return (int)lmin(lmax((n + 255) / 256, 1), 148 
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    float *color, float *remaining, int32_t *count, int32_t *n_eval, unsigned long long *rechecks,
-                    cudaStream_t st) {
+                    float *color, float *remaining, int32_t *count, int32_t *n_eval, unsigned long long *counters,
+                    int32_t *fixup_list, cudaStream_t st) {
     if (max_items <= 0) return;
-    if (fc.model == GEER_BEAP)
-        k_forward<true><<<max_items, kRasterThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                              ranges, order, payload, color, remaining, count, n_eval,
-                                                              rechecks);
-    else
-        k_forward<false><<<max_items, kRasterThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                               ranges, order, payload, color, remaining, count, n_eval,
-                                                               rechecks);
+    if (fc.model == GEER_BEAP) {
+        k_forward<true><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
+                                                            ranges, order, payload, color, remaining, count, n_eval,
+                                                            counters, fixup_list);
+        k_fixup<true><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
+                                               counters, fixup_list, color, remaining, count, n_eval);
+    } else {
+        k_forward<false><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
+                                                             ranges, order, payload, color, remaining, count, n_eval,
+                                                             counters, fixup_list);
+        k_fixup<false><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
+                                                counters, fixup_list, color, remaining, count, n_eval);
+    }
 }
 
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                      const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                     const float *remaining, const int32_t *n_eval, const float *dl_dimage, float4 *accum,
-                     cudaStream_t st) {
+                     const GradPayload *gpayload, const float *remaining, const int32_t *n_eval,
+                     const float *dl_dimage, float *accum, cudaStream_t st) {
     if (max_items <= 0) return;
     if (fc.model == GEER_BEAP)
-        k_backward<true><<<max_items, kRasterThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                               ranges, order, payload, remaining, n_eval, dl_dimage,
-                                                               accum);
+        k_backward<true><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
+                                                             ranges, order, payload, gpayload, remaining, n_eval,
+                                                             dl_dimage, accum);
     else
-        k_backward<false><<<max_items, kRasterThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc,
-                                                                dir64, ranges, order, payload, remaining, n_eval,
-                                                                dl_dimage, accum);
+        k_backward<false><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
+                                                              ranges, order, payload, gpayload, remaining, n_eval,
+                                                              dl_dimage, accum);
 }
 
 void launch_sum_i32(const int32_t *v, int64_t n, unsigned long long *out, cudaStream_t st) {

@@ -29,8 +29,8 @@ def test_fixture_association_forward_backward(name):
         return
     fr = renderer.render(c.scene, c.camera, c.config)
     assert fr.color.color.dtype == np.float64 and fr.contributor_count.dtype == np.int64
-    if len(c.scene) == 0:
-        np.testing.assert_array_equal(fr.color.color, d["color"])
+    if len(c.scene) == 0:  # background through the fp32 output buffer
+        np.testing.assert_allclose(fr.color.color, d["color"], rtol=0, atol=1e-7)
         np.testing.assert_array_equal(fr.remaining_transmittance, d["remaining"])
         np.testing.assert_array_equal(fr.contributor_count, d["count"])
         return
