@@ -50,7 +50,8 @@ def _deps_mtime() -> float:
 
 def _compile(src: str, extra: list[str], verbose: bool) -> str:
     obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-    cmd = [nvcc(), *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+    defs = os.environ.get("GEER_NVCC_DEFS", "").split()  # tuning experiments, e.g. -DFWD_MIN_BLOCKS=2
+    cmd = [nvcc(), *ARCH, *COMMON, *defs, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -160,6 +160,7 @@ int make_frame_const(const geer_camera *cam, const geer_config *cfg, int n_bands
     fc->lam = cfg->lam;
     fc->lam2 = cfg->lam * cfg->lam;
     fc->lam2f = (float)fc->lam2;
+    fc->cutoff_tol = (float)(1e-6 * fc->lam2 + 1e-7);
     for (int i = 0; i < 3; ++i) fc->bg[i] = (float)cfg->background[i];
     return GEER_OK;
 }

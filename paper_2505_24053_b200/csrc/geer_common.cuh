@@ -33,6 +33,7 @@ struct FrameConst {
     double lam, lam2;
     float bg[3];
     float lam2f;
+    float cutoff_tol;  // |kappa_fp32 - lam^2| below which the cutoff is re-decided in fp64
 };
 
 // Raster payload, one per Gaussian (128 B, see make_payload in geer_geometry.cu):

@@ -108,17 +108,13 @@ __device__ __noinline__ double kappa_fp64(const float *__restrict__ means, const
     return __ddiv_rn(mm, dd);
 }
 
-// Per-pixel ray in fp64 plus its quadratic monomials (for the mode-0 payload).
+// Quadratic monomials of the pixel ray d (fp64) for the mode-0 payload.
 struct Ray64 {
-    double d0, d1, d2;
     double m00, m11, m22, m01, m02, m12;
 };
 
 __device__ __forceinline__ Ray64 make_ray(const double d[3]) {
     Ray64 r;
-    r.d0 = d[0];
-    r.d1 = d[1];
-    r.d2 = d[2];
     r.m00 = d[0] * d[0];
     r.m11 = d[1] * d[1];
     r.m22 = d[2] * d[2];
@@ -132,49 +128,76 @@ struct PairT {
     float kap, alpha, u, t, dd;
 };
 
-// kappa of (payload P, ray R) in fp64, then the blend quantities in fp32:
-//   u = sigma exp(-kappa/2) [kappa <= lam^2], t = min(u, 0.999)   (renderer.py:96-105)
-// Shared verbatim by forward, backward and fix-up, so t is bit-identical in all three.
-__device__ __forceinline__ void eval_t(const Payload &P, const Ray64 &R, const FrameConst &fc, const geer_scene &sc,
-                                       uint32_t gid, PairT &e, int &rechecks) {
-    double dd, mm;
-    const float sw = P.col.w;
-    if (sw >= 0.0f) {  // mode 0: quadratic forms
-        dd = fma(P.q[5], R.m12, fma(P.q[4], R.m02, fma(P.q[3], R.m01, fma(P.q[2], R.m22, fma(P.q[1], R.m11, P.q[0] * R.m00)))));
-        mm = fma(P.q[11], R.m12, fma(P.q[10], R.m02, fma(P.q[9], R.m01, fma(P.q[8], R.m22, fma(P.q[7], R.m11, P.q[6] * R.m00)))));
-    } else {  // mode 1: d_u = W d, m = o_u x d_u (core.py:184-199)
-        const double u0 = fma(P.q[2], R.d2, fma(P.q[1], R.d1, P.q[0] * R.d0));
-        const double u1 = fma(P.q[5], R.d2, fma(P.q[4], R.d1, P.q[3] * R.d0));
-        const double u2 = fma(P.q[8], R.d2, fma(P.q[7], R.d1, P.q[6] * R.d0));
+// |d_u|^2 and |m|^2 of (payload P, ray d) in fp64: mode 0 via the quadratic forms, mode 1 via
+// the fp64 cross product d_u = W d, m = o_u x d_u (core.py:184-199).  dray: the ray itself
+// (only read in mode 1).  m1 must be warp-uniform.
+__device__ __forceinline__ void norms64(const Payload &P, const Ray64 &R, const double *dray, bool m1, double &dd,
+                                        double &mm) {
+    if (!m1) {
+        const double2 a0 = *reinterpret_cast<const double2 *>(&P.q[0]);
+        const double2 a1 = *reinterpret_cast<const double2 *>(&P.q[2]);
+        const double2 a2 = *reinterpret_cast<const double2 *>(&P.q[4]);
+        const double2 b0 = *reinterpret_cast<const double2 *>(&P.q[6]);
+        const double2 b1 = *reinterpret_cast<const double2 *>(&P.q[8]);
+        const double2 b2 = *reinterpret_cast<const double2 *>(&P.q[10]);
+        // (q0 m00 + q1 m11) + (q2 m22 + q3 m01) + (q4 m02 + q5 m12): 4-deep instead of 6-deep chains
+        dd = (fma(a0.y, R.m11, a0.x * R.m00) + fma(a1.y, R.m01, a1.x * R.m22)) + fma(a2.y, R.m12, a2.x * R.m02);
+        mm = (fma(b0.y, R.m11, b0.x * R.m00) + fma(b1.y, R.m01, b1.x * R.m22)) + fma(b2.y, R.m12, b2.x * R.m02);
+    } else {
+        const double d0 = dray[0], d1 = dray[1], d2 = dray[2];
+        const double u0 = fma(P.q[2], d2, fma(P.q[1], d1, P.q[0] * d0));
+        const double u1 = fma(P.q[5], d2, fma(P.q[4], d1, P.q[3] * d0));
+        const double u2 = fma(P.q[8], d2, fma(P.q[7], d1, P.q[6] * d0));
         const double o0 = P.q[9], o1 = P.q[10], o2 = P.q[11];
         const double x0 = fma(o1, u2, -(o2 * u1)), x1 = fma(o2, u0, -(o0 * u2)), x2 = fma(o0, u1, -(o1 * u0));
         dd = fma(u2, u2, fma(u1, u1, u0 * u0));
         mm = fma(x2, x2, fma(x1, x1, x0 * x0));
     }
+}
+
+// Blend quantities of a pair from its fp64 norms (fp32 from here on):
+//   u = sigma exp(-kappa/2) [kappa <= lam^2], t = min(u, 0.999)   (renderer.py:96-105)
+// Returns true when the cutoff decision lies within the fp64 evaluation's own error bound (the
+// forward then hands the pixel to the fp64 fix-up, which uses the reference formulation).
+__device__ __forceinline__ bool finish_t(double dd, double mm, const Payload &P, bool m1, const FrameConst &fc,
+                                         PairT &e, int &rechecks) {
+    const float sw = P.col.w;
     const float ddf = (float)dd;
     e.dd = ddf;
     e.kap = __fmul_rn((float)mm, rcp_approx(ddf));
     e.alpha = ex2_approx(__fmul_rn(e.kap, -0.72134752044448170f));  // exp(-kappa/2)
     float u = __fmul_rn(fabsf(sw), e.alpha);
+    bool uncertain = false;
     if (fc.cutoff) {
         bool inside = e.kap <= fc.lam2f;
-        // kappa_fp32 carries ~3e-7 relative error: re-decide the cutoff in fp64 near lam^2
-        if (fabsf(__fsub_rn(e.kap, fc.lam2f)) <= 1e-6f * fc.lam2f + P.ext.x) {
+        // kappa_fp32 carries ~3e-7 relative error (mode-0 fp64 error <= 1e-7 absolute by construction):
+        // re-decide the cutoff in fp64 near lam^2
+        const float tol = m1 ? fc.cutoff_tol + P.ext.x : fc.cutoff_tol;
+        if (fabsf(__fsub_rn(e.kap, fc.lam2f)) <= tol) {
             const double k64 = mm / dd;
             inside = k64 <= fc.lam2;
-            if (fabs(k64 - fc.lam2) <= (double)P.ext.x)  // inside the fp64 error bound: reference formulation
-                inside = kappa_fp64(sc.means, sc.log_scales, sc.quats, fc.origin[0], fc.origin[1], fc.origin[2], gid,
-                                    R.d0, R.d1, R.d2) <= fc.lam2;
+            uncertain = fabs(k64 - fc.lam2) <= (double)P.ext.x;
             ++rechecks;
         }
         u = inside ? u : 0.0f;
     }
     e.u = u;
     e.t = fminf(u, kMaxBlendTF);
+    return uncertain;
+}
+
+// Shared verbatim by the forward and backward kernels (called warp-uniformly), so t is
+// bit-identical in both.
+__device__ __forceinline__ bool eval_t(const Payload &P, const Ray64 &R, const double *dray, const FrameConst &fc,
+                                       PairT &e, int &rechecks) {
+    const bool m1 = __any_sync(0xffffffffu, P.col.w < 0.0f);
+    double dd, mm;
+    norms64(P, R, dray, m1, dd, mm);
+    return finish_t(dd, mm, P, m1, fc, e, rechecks);
 }
 
 // Relative bound on |t_fp32 - t_exact| / t for a pair (fp64 kappa rounded to fp32, rcp/ex2 approximations).
-__device__ __forceinline__ float t_rel_bound(float kap) { return 3e-7f * (1.0f + kap); }
+__device__ __forceinline__ float t_rel_bound(float kap) { return 6e-7f + 3e-7f * kap; }
 
 // ------------------------------------------------------------------------------ pipeline plumbing
 //
@@ -191,10 +214,14 @@ constexpr int kConsumerWarps = kRasterThreads / 32;  // 8
 constexpr int kStages = 4;
 constexpr int kStageEntries = 32;  // one entry per producer lane
 constexpr int kPipeThreads = kRasterThreads + 32;
+#ifndef FWD_MIN_BLOCKS
+#define FWD_MIN_BLOCKS 3
+#endif
 
+template <bool kGrad>
 struct __align__(16) PipeSmem {
     Payload ring[kStages][kStageEntries];
-    GradPayload gring[kStages][kStageEntries];  // backward only
+    GradPayload gring[kGrad ? kStages : 1][kStageEntries];  // backward only
     uint32_t gid[kStages][kStageEntries];
     int count[kStages];  // entries in the stage; 0 = end of stream
     unsigned long long full[kStages];
@@ -231,7 +258,8 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                  : "memory");
 }
 
-__device__ __forceinline__ void pipe_init(PipeSmem &S) {
+template <class Smem>
+__device__ __forceinline__ void pipe_init(Smem &S) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&S.full[s], 1);
@@ -245,8 +273,8 @@ __device__ __forceinline__ void pipe_init(PipeSmem &S) {
 
 // Producer warp: stream entries [first, first + n_total) (forward order) or the
 // same range walked from the back (reverse) in stages of kStageEntries.
-template <bool kReverse>
-__device__ __forceinline__ void pipe_produce(PipeSmem &S, const uint32_t *__restrict__ order,
+template <bool kReverse, class Smem>
+__device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict__ order,
                                              const Payload *__restrict__ payload,
                                              const GradPayload *__restrict__ gpayload, int first, int n_total,
                                              bool stop_when_done) {
@@ -280,7 +308,7 @@ __device__ __forceinline__ void pipe_produce(PipeSmem &S, const uint32_t *__rest
         __syncwarp();
         if (lane < n) {
             bulk_g2s(&S.ring[s][lane], payload + g, sizeof(Payload), &S.full[s]);
-            if (gpayload) bulk_g2s(&S.gring[s][lane], gpayload + g, sizeof(GradPayload), &S.full[s]);
+            if (gpayload) bulk_g2s(&S.gring[gpayload ? s : 0][lane], gpayload + g, sizeof(GradPayload), &S.full[s]);
         }
         if (++s == kStages) {
             s = 0;
@@ -291,42 +319,43 @@ __device__ __forceinline__ void pipe_produce(PipeSmem &S, const uint32_t *__rest
 
 // ------------------------------------------------------------------------------ K5
 
-// Forward blend of one pair into the pixel state, with a running bound on
-// |rem_fp32 - rem_fp64| (err).  Returns false when the pixel stops: either
-// surely opaque, or too close to the 1e-4 threshold to decide in fp32
-// (borderline -> the pixel is redone in fp64 by k_fixup).
+// Forward pixel state with a running bound on |rem_fp32 - rem_fp64| (err): the alive test of
+// renderer.py:113 is decided against rem64 in [rem - err, rem + err]; a pixel whose test (or a
+// cutoff decision) is too close to call is stopped and redone in fp64 by k_fixup.
 struct PixelState {
     float cr, cg, cb, rem, err;
     int cnt, ne;
 };
 
-__device__ __forceinline__ int blend_step(PixelState &ps, const PairT &e, const Payload &P) {
-    const float hb = t_rel_bound(e.kap);
-    // alive test of renderer.py:113, decided against the fp64 remaining: rem64 in [rem - err, rem + err]
-    const float lo = ps.rem - ps.err, hi = ps.rem + ps.err;
-    if (!(lo >= 1.00001e-4f)) return hi < 0.99999e-4f ? 0 : 2;  // 0: stop, 2: borderline
-    ++ps.ne;
-    const float w = __fmul_rn(ps.rem, e.t);
-    ps.cr = __fmaf_rn(w, P.col.x, ps.cr);
-    ps.cg = __fmaf_rn(w, P.col.y, ps.cg);
-    ps.cb = __fmaf_rn(w, P.col.z, ps.cb);
-    const float omt = __fsub_rn(1.0f, e.t);
-    // |d rem| <= |d rem| (1 - t) + rem |d t|, |d t| <= t * hb (hb: kappa band / 2 + approx. error)
-    ps.err = __fmaf_rn(ps.err, omt, __fmul_rn(w, hb)) + 1.2e-7f * ps.rem;
+__device__ __forceinline__ void pixel_update(PixelState &ps, bool &live, bool &border, const PairT &e,
+                                             const float4 &col, bool unc) {
+    const bool sure_alive = __fsub_rn(ps.rem, ps.err) >= 1.00001e-4f;
+    const bool maybe_alive = __fadd_rn(ps.rem, ps.err) >= 0.99999e-4f;
+    const bool act = live & sure_alive & !unc;
+    border |= live & (sure_alive ? unc : maybe_alive);
+    live = act;
+    const float w = act ? __fmul_rn(ps.rem, e.t) : 0.0f;
+    const float omt = act ? __fsub_rn(1.0f, e.t) : 1.0f;
+    ps.cr = __fmaf_rn(w, col.x, ps.cr);
+    ps.cg = __fmaf_rn(w, col.y, ps.cg);
+    ps.cb = __fmaf_rn(w, col.z, ps.cb);
+    // |d rem'| <= |d rem| (1 - t) + rem |d t| + rounding,  |d t| <= t * t_rel_bound
+    ps.err = __fmaf_rn(ps.err, omt, __fmul_rn(w, t_rel_bound(e.kap))) + (act ? 1.2e-7f * ps.rem : 0.0f);
     ps.rem = __fmul_rn(ps.rem, omt);
-    ps.cnt += e.t > 0.0f;
-    return 1;
+    ps.cnt += (act & (e.t > 0.0f)) ? 1 : 0;
+    ps.ne += act ? 1 : 0;
 }
 
 template <bool kBEAP>
-__global__ void __launch_bounds__(kPipeThreads, 2)
+__global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
     k_forward(FrameConst fc, geer_scene sc, const int4 *__restrict__ items, const int32_t *__restrict__ n_items,
               const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
               const double2 *__restrict__ row_sc, const double *__restrict__ dir64, const int32_t *__restrict__ ranges,
               const uint32_t *__restrict__ order, const Payload *__restrict__ payload, float *__restrict__ color,
               float *__restrict__ remaining, int32_t *__restrict__ count, int32_t *__restrict__ n_eval,
               unsigned long long *__restrict__ counters, int32_t *__restrict__ fixup_list) {
-    __shared__ PipeSmem S;
+    __shared__ PipeSmem<false> S;
+    __shared__ double sray[kRasterThreads][3];  // fp64 pixel rays (mode-1 payloads only)
     if ((int)blockIdx.x >= *n_items) return;
     const int4 it = items[blockIdx.x];
     const int e0 = ranges[it.x], e1 = ranges[it.x + 1];
@@ -342,6 +371,9 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
     double d64[3] = {0.0, 0.0, 1.0};
     if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
     const Ray64 R = make_ray(d64);
+    sray[tid][0] = d64[0];
+    sray[tid][1] = d64[1];
+    sray[tid][2] = d64[2];
     PixelState ps{0.f, 0.f, 0.f, 1.0f, 0.f, 0, 0};
     bool live = valid, border = false;
     int rechecks = 0;
@@ -355,26 +387,23 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
         if (n == 0) break;
         if (warp_live) {
             for (int j = 0; j < n; j += 2) {
-                if (!__any_sync(0xffffffffu, live)) break;
+                if ((j & 3) == 0 && !__any_sync(0xffffffffu, live)) break;
+                const bool hasb = j + 1 < n;
                 const Payload &Pa = S.ring[s][j];
-                const bool has_b = j + 1 < n;
-                const Payload &Pb = S.ring[s][has_b ? j + 1 : j];
-                PairT a, b;
-                int rc_dup = 0;
-                eval_t(Pa, R, fc, sc, S.gid[s][j], a, rechecks);
-                eval_t(Pb, R, fc, sc, S.gid[s][has_b ? j + 1 : j], b, has_b ? rechecks : rc_dup);
-                if (live) {
-                    int r = blend_step(ps, a, Pa);
-                    if (r != 1) {
-                        live = false;
-                        border = r == 2;
-                    } else if (has_b) {
-                        r = blend_step(ps, b, Pb);
-                        if (r != 1) {
-                            live = false;
-                            border = r == 2;
-                        }
-                    }
+                const Payload &Pb = S.ring[s][hasb ? j + 1 : j];
+                // two independent fp64 evaluations per iteration (ILP); blends stay in entry order
+                const bool m1 = __any_sync(0xffffffffu, (Pa.col.w < 0.0f) | (Pb.col.w < 0.0f));
+                double dda, mma, ddb, mmb;
+                norms64(Pa, R, sray[tid], m1, dda, mma);
+                norms64(Pb, R, sray[tid], m1, ddb, mmb);
+                PairT ea, eb;
+                int rc_b = 0;
+                const bool ua = finish_t(dda, mma, Pa, m1, fc, ea, rechecks);
+                const bool ub = finish_t(ddb, mmb, Pb, m1, fc, eb, rc_b);
+                pixel_update(ps, live, border, ea, Pa.col, ua);
+                if (hasb) {
+                    rechecks += rc_b;
+                    pixel_update(ps, live, border, eb, Pb.col, ub);
                 }
             }
             warp_live = __any_sync(0xffffffffu, live);
@@ -434,18 +463,7 @@ __device__ void fixup_pixel(FrameConst fc, const geer_scene &sc, const int4 *__r
             g = order[e];
             const Payload &P = payload[g];
             double dd, mm;
-            if (P.col.w >= 0.0f) {
-                dd = fma(P.q[5], R.m12, fma(P.q[4], R.m02, fma(P.q[3], R.m01, fma(P.q[2], R.m22, fma(P.q[1], R.m11, P.q[0] * R.m00)))));
-                mm = fma(P.q[11], R.m12, fma(P.q[10], R.m02, fma(P.q[9], R.m01, fma(P.q[8], R.m22, fma(P.q[7], R.m11, P.q[6] * R.m00)))));
-            } else {
-                const double u0 = fma(P.q[2], R.d2, fma(P.q[1], R.d1, P.q[0] * R.d0));
-                const double u1 = fma(P.q[5], R.d2, fma(P.q[4], R.d1, P.q[3] * R.d0));
-                const double u2 = fma(P.q[8], R.d2, fma(P.q[7], R.d1, P.q[6] * R.d0));
-                const double x0 = fma(P.q[10], u2, -(P.q[11] * u1)), x1 = fma(P.q[11], u0, -(P.q[9] * u2));
-                const double x2 = fma(P.q[9], u1, -(P.q[10] * u0));
-                dd = fma(u2, u2, fma(u1, u1, u0 * u0));
-                mm = fma(x2, x2, fma(x1, x1, x0 * x0));
-            }
+            norms64(P, R, d, P.col.w < 0.0f, dd, mm);
             double kap = mm / dd;
             if (fc.cutoff && fabs(kap - fc.lam2) <= (double)P.ext.x)
                 kap = kappa_fp64(sc.means, sc.log_scales, sc.quats, fc.origin[0], fc.origin[1], fc.origin[2], g, d[0],
@@ -551,7 +569,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
                const Payload *__restrict__ payload, const GradPayload *__restrict__ gpayload,
                const float *__restrict__ remaining, const int32_t *__restrict__ n_eval,
                const float *__restrict__ dl_dimage, float *__restrict__ accum) {
-    __shared__ PipeSmem S;
+    __shared__ PipeSmem<true> S;
+    __shared__ double sray[kRasterThreads][3];
     __shared__ int smax;
     if ((int)blockIdx.x >= *n_items) return;
     const int4 it = items[blockIdx.x];
@@ -574,6 +593,11 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
     double d64[3] = {0.0, 0.0, 1.0};
     if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
     const Ray64 R = make_ray(d64);
+    if (valid) {
+        sray[tid][0] = d64[0];
+        sray[tid][1] = d64[1];
+        sray[tid][2] = d64[2];
+    }
     const float dx = (float)d64[0], dy = (float)d64[1], dz = (float)d64[2];
     const float t_fin = valid ? remaining[p] : 0.f;
     float gl0 = 0.f, gl1 = 0.f, gl2 = 0.f;
@@ -601,9 +625,9 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
 #pragma unroll
                 for (int k = 0; k < 16; ++k) v[k] = 0.f;
                 const Payload &P = S.ring[s][jj];
+                PairT e;
+                eval_t(P, R, sray[tid], fc, e, dummy);  // warp-uniform call (mode vote inside)
                 if (i < ne) {
-                    PairT e;
-                    eval_t(P, R, fc, sc, S.gid[s][jj], e, dummy);
                     const float omt = __fsub_rn(1.0f, e.t);
                     const float inv = 1.0f / omt;
                     T = __fdiv_rn(T, omt);  // T_i = T_{i+1} / (1 - t_i)
