@@ -306,7 +306,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         int32_t *fix = ENSURE(int32_t, c->fixup, npx);
         launch_forward(fc, sc, c->max_items, (const int4 *)c->items.p, (const int32_t *)c->n_items.p,
                        (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
-                       (const double *)c->dir64.p, ranges, order, payload, color, remaining, count, ne,
+                       (const double *)c->dir64.p, ranges, order, payload, flags, color, remaining, count, ne,
                        c->d_counters, fix, st);
         c->fwd_remaining = remaining;
         c->have_raster = true;
@@ -335,7 +335,8 @@ int run_backward(geer_ctx *c, const float *dl_dimage, bool f64_out, void *const 
     launch_backward(fc, sc, c->max_items, (const int4 *)c->items.p, (const int32_t *)c->n_items.p,
                     (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
                     (const double *)c->dir64.p, (const int32_t *)c->tile_ranges.p, (const uint32_t *)c->order.p,
-                    (const Payload *)c->payload.p, (const GradPayload *)c->gpayload.p, c->fwd_remaining, (const int32_t *)c->n_eval.p,
+                    (const Payload *)c->payload.p, (const GradPayload *)c->gpayload.p, (const uint8_t *)c->flags.p,
+                    c->fwd_remaining, (const int32_t *)c->n_eval.p,
                     dl_dimage, accum, st);
     if (f64_out)
         launch_finalize<double>(fc, sc, (const float4 *)accum, (const uint8_t *)c->flags.p, (double *)gout[0], (double *)gout[1],

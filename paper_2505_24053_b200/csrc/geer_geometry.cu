@@ -436,7 +436,7 @@ __device__ int axis_tiles(double t_aa, double t_a2, double t22, double r0, doubl
 // exceeds 1e-7 (|o_u| cond > ~7e3: tiny, far or very anisotropic Gaussians) the payload
 // instead carries W and o_u (mode 1) and the raster uses the fp64 cross product, the
 // reference's own formulation (core.py:184-199), whose error grows only like |o_u|.
-__device__ void make_payload(const double W[9], const double ou[3], const double rgb[3], double sigma, double cond,
+__device__ bool make_payload(const double W[9], const double ou[3], const double rgb[3], double sigma, double cond,
                              double lam, Payload &pl, GradPayload &gp) {
     const double u64 = 1.1102230246251565e-16;
     const double on2 = ou[0] * ou[0] + ou[1] * ou[1] + ou[2] * ou[2];
@@ -468,6 +468,7 @@ __device__ void make_payload(const double W[9], const double ou[3], const double
     gp.r0 = make_float4((float)W[0], (float)W[1], (float)W[2], (float)ou[0]);
     gp.r1 = make_float4((float)W[3], (float)W[4], (float)W[5], (float)ou[1]);
     gp.r2 = make_float4((float)W[6], (float)W[7], (float)W[8], (float)ou[2]);
+    return mode1;
 }
 
 __global__ void __launch_bounds__(128) k_preprocess(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x,
@@ -557,11 +558,12 @@ __global__ void __launch_bounds__(128) k_preprocess(FrameConst fc, geer_scene sc
     double smax = fmax(s[0], fmax(s[1], s[2])), smin = fmin(s[0], fmin(s[1], s[2]));
     Payload pl;
     GradPayload gp;
-    make_payload(W, ou, rgb, sigma, smax / smin, fc.lam, pl, gp);
+    const bool mode1 = make_payload(W, ou, rgb, sigma, smax / smin, fc.lam, pl, gp);
     payload[g] = pl;
     gpayload[g] = gp;
 
-    uint8_t fl = (uint8_t)(gate << 3);
+    // flags: bit0 keep, bit1 clamped, bits3-5 SH clamp gate per channel, bit6 payload mode 1
+    uint8_t fl = (uint8_t)((gate << 3) | (mode1 ? 64 : 0));
     int64_t n_ent = 0;
     AxisRanges ar;
     for (int i = 0; i < 3; ++i) ar.x[i] = ar.y[i] = 0;

@@ -56,13 +56,13 @@ void tile_ranges(const uint32_t *sorted_tiles, int64_t n_entries, int n_tiles, i
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    float *color, float *remaining, int32_t *count, int32_t *n_eval, unsigned long long *counters,
-                    int32_t *fixup_list, cudaStream_t st);
+                    const uint8_t *flags, float *color, float *remaining, int32_t *count, int32_t *n_eval,
+                    unsigned long long *counters, int32_t *fixup_list, cudaStream_t st);
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                      const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                     const GradPayload *gpayload, const float *remaining, const int32_t *n_eval, const float *dl_dimage, float *accum,
-                     cudaStream_t st);
+                     const GradPayload *gpayload, const uint8_t *flags, const float *remaining,
+                     const int32_t *n_eval, const float *dl_dimage, float *accum, cudaStream_t st);
 void launch_sum_i32(const int32_t *v, int64_t n, unsigned long long *out, cudaStream_t st);
 void launch_convert_f64_f32(const double *in, float *out, int64_t n, cudaStream_t st);
 void launch_convert_f32_f64(const float *in, double *out, int64_t n, cudaStream_t st);

@@ -224,6 +224,7 @@ struct __align__(16) PipeSmem {
     GradPayload gring[kGrad ? kStages : 1][kStageEntries];  // backward only
     uint32_t gid[kStages][kStageEntries];
     int count[kStages];  // entries in the stage; 0 = end of stream
+    int mode1[kStages];  // 1 if any entry of the stage carries a mode-1 (cross-product) payload
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     int done_warps;
@@ -276,7 +277,8 @@ __device__ __forceinline__ void pipe_init(Smem &S) {
 template <bool kReverse, class Smem>
 __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict__ order,
                                              const Payload *__restrict__ payload,
-                                             const GradPayload *__restrict__ gpayload, int first, int n_total,
+                                             const GradPayload *__restrict__ gpayload,
+                                             const uint8_t *__restrict__ flags, int first, int n_total,
                                              bool stop_when_done) {
     const unsigned per_entry = (unsigned)(sizeof(Payload) + (gpayload ? sizeof(GradPayload) : 0));
     const int lane = threadIdx.x & 31;
@@ -297,12 +299,16 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
         // reverse: stage b holds entries [first + n_total - done - n, first + n_total - done)
         const int base = kReverse ? first + n_total - done - n : first + done;
         uint32_t g = 0;
+        bool m1 = false;
         if (lane < n) {
             g = __ldg(order + base + lane);
             S.gid[s][lane] = g;
+            m1 = (__ldg(flags + g) >> 6) & 1;
         }
+        const bool any_m1 = __any_sync(0xffffffffu, m1);
         if (lane == 0) {
             S.count[s] = n;
+            S.mode1[s] = any_m1 ? 1 : 0;
             mbar_arrive_expect_tx(&S.full[s], n * per_entry);
         }
         __syncwarp();
@@ -323,27 +329,54 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
 // renderer.py:113 is decided against rem64 in [rem - err, rem + err]; a pixel whose test (or a
 // cutoff decision) is too close to call is stopped and redone in fp64 by k_fixup.
 struct PixelState {
-    float cr, cg, cb, rem, err;
-    int cnt, ne;
+    float cr, cg, cb;
+    float r;     // remaining transmittance while the pixel is live, 0 once it stopped
+    float rfin;  // remaining transmittance at the stop
+    float err;   // bound on |r_fp32 - r_fp64|
+    int cnt, ne, border;
 };
 
-__device__ __forceinline__ void pixel_update(PixelState &ps, bool &live, bool &border, const PairT &e,
-                                             const float4 &col, bool unc) {
-    const bool sure_alive = __fsub_rn(ps.rem, ps.err) >= 1.00001e-4f;
-    const bool maybe_alive = __fadd_rn(ps.rem, ps.err) >= 0.99999e-4f;
-    const bool act = live & sure_alive & !unc;
-    border |= live & (sure_alive ? unc : maybe_alive);
-    live = act;
-    const float w = act ? __fmul_rn(ps.rem, e.t) : 0.0f;
-    const float omt = act ? __fsub_rn(1.0f, e.t) : 1.0f;
+// One front-to-back step (renderer.py:111-117).  The alive test (:113) is made against the fp64
+// remaining, known to lie in [r - err, r + err]; a pixel stops either surely opaque, or
+// "borderline" (test or cutoff too close to call) and is then redone in fp64 by k_fixup.
+// Stopped pixels carry r = 0, which turns every later update into a no-op without branches.
+__device__ __forceinline__ void pixel_update(PixelState &ps, const PairT &e, const float4 &col, bool unc) {
+    const bool live = ps.r > 0.0f;
+    const bool sure_alive = __fsub_rn(ps.r, ps.err) >= 1.00001e-4f;
+    const bool stop = live & (!sure_alive | unc);
+    ps.border |= (stop & (unc | (__fadd_rn(ps.r, ps.err) >= 0.99999e-4f))) ? 1 : 0;
+    ps.rfin = stop ? ps.r : ps.rfin;
+    ps.r = stop ? 0.0f : ps.r;
+    const float w = __fmul_rn(ps.r, e.t);
+    const float omt = __fsub_rn(1.0f, e.t);
     ps.cr = __fmaf_rn(w, col.x, ps.cr);
     ps.cg = __fmaf_rn(w, col.y, ps.cg);
     ps.cb = __fmaf_rn(w, col.z, ps.cb);
-    // |d rem'| <= |d rem| (1 - t) + rem |d t| + rounding,  |d t| <= t * t_rel_bound
-    ps.err = __fmaf_rn(ps.err, omt, __fmul_rn(w, t_rel_bound(e.kap))) + (act ? 1.2e-7f * ps.rem : 0.0f);
-    ps.rem = __fmul_rn(ps.rem, omt);
-    ps.cnt += (act & (e.t > 0.0f)) ? 1 : 0;
-    ps.ne += act ? 1 : 0;
+    // |d r'| <= |d r| (1 - t) + r |d t| + rounding,  |d t| <= t * t_rel_bound
+    ps.err = __fmaf_rn(ps.r, 1.2e-7f, __fmaf_rn(ps.err, omt, __fmul_rn(w, t_rel_bound(e.kap))));
+    ps.ne += ps.r > 0.0f ? 1 : 0;
+    ps.cnt += w > 0.0f ? 1 : 0;
+    ps.r = __fmul_rn(ps.r, omt);
+}
+
+// One stage of entries for one consumer warp.  kGeneric: the stage holds mode-1 payloads, so the
+// payload mode is decided per entry; otherwise every entry is a mode-0 quadratic form.
+template <bool kGeneric>
+__device__ __forceinline__ void consume_stage(const Payload *ring, int n, const Ray64 &R, const double *dray,
+                                              const FrameConst &fc, PixelState &ps, int &rechecks) {
+    for (int j0 = 0; j0 < n; j0 += 4) {
+        if (!__any_sync(0xffffffffu, ps.r > 0.0f)) break;
+        const int j1 = min(j0 + 4, n);
+        for (int j = j0; j < j1; ++j) {
+            const Payload &P = ring[j];
+            const bool m1 = kGeneric ? __any_sync(0xffffffffu, P.col.w < 0.0f) : false;
+            double dd, mm;
+            norms64(P, R, dray, m1, dd, mm);
+            PairT e;
+            const bool unc = finish_t(dd, mm, P, m1, fc, e, rechecks);
+            pixel_update(ps, e, P.col, unc);
+        }
+    }
 }
 
 template <bool kBEAP>
@@ -351,9 +384,10 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
     k_forward(FrameConst fc, geer_scene sc, const int4 *__restrict__ items, const int32_t *__restrict__ n_items,
               const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
               const double2 *__restrict__ row_sc, const double *__restrict__ dir64, const int32_t *__restrict__ ranges,
-              const uint32_t *__restrict__ order, const Payload *__restrict__ payload, float *__restrict__ color,
-              float *__restrict__ remaining, int32_t *__restrict__ count, int32_t *__restrict__ n_eval,
-              unsigned long long *__restrict__ counters, int32_t *__restrict__ fixup_list) {
+              const uint32_t *__restrict__ order, const Payload *__restrict__ payload,
+              const uint8_t *__restrict__ flags, float *__restrict__ color, float *__restrict__ remaining,
+              int32_t *__restrict__ count, int32_t *__restrict__ n_eval, unsigned long long *__restrict__ counters,
+              int32_t *__restrict__ fixup_list) {
     __shared__ PipeSmem<false> S;
     __shared__ double sray[kRasterThreads][3];  // fp64 pixel rays (mode-1 payloads only)
     if ((int)blockIdx.x >= *n_items) return;
@@ -362,7 +396,7 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
     pipe_init(S);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == kConsumerWarps) {
-        pipe_produce<false>(S, order, payload, nullptr, e0, e1 - e0, true);
+        pipe_produce<false>(S, order, payload, nullptr, flags, e0, e1 - e0, true);
         return;
     }
     const int tid = threadIdx.x;
@@ -374,10 +408,9 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
     sray[tid][0] = d64[0];
     sray[tid][1] = d64[1];
     sray[tid][2] = d64[2];
-    PixelState ps{0.f, 0.f, 0.f, 1.0f, 0.f, 0, 0};
-    bool live = valid, border = false;
+    PixelState ps{0.f, 0.f, 0.f, valid ? 1.0f : 0.0f, 1.0f, 0.f, 0, 0, 0};
     int rechecks = 0;
-    bool warp_live = __any_sync(0xffffffffu, live);
+    bool warp_live = __any_sync(0xffffffffu, valid);
     if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
     unsigned phase = 0;
     int s = 0;
@@ -386,27 +419,11 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
         const int n = S.count[s];
         if (n == 0) break;
         if (warp_live) {
-            for (int j = 0; j < n; j += 2) {
-                if ((j & 3) == 0 && !__any_sync(0xffffffffu, live)) break;
-                const bool hasb = j + 1 < n;
-                const Payload &Pa = S.ring[s][j];
-                const Payload &Pb = S.ring[s][hasb ? j + 1 : j];
-                // two independent fp64 evaluations per iteration (ILP); blends stay in entry order
-                const bool m1 = __any_sync(0xffffffffu, (Pa.col.w < 0.0f) | (Pb.col.w < 0.0f));
-                double dda, mma, ddb, mmb;
-                norms64(Pa, R, sray[tid], m1, dda, mma);
-                norms64(Pb, R, sray[tid], m1, ddb, mmb);
-                PairT ea, eb;
-                int rc_b = 0;
-                const bool ua = finish_t(dda, mma, Pa, m1, fc, ea, rechecks);
-                const bool ub = finish_t(ddb, mmb, Pb, m1, fc, eb, rc_b);
-                pixel_update(ps, live, border, ea, Pa.col, ua);
-                if (hasb) {
-                    rechecks += rc_b;
-                    pixel_update(ps, live, border, eb, Pb.col, ub);
-                }
-            }
-            warp_live = __any_sync(0xffffffffu, live);
+            if (!S.mode1[s])
+                consume_stage<false>(S.ring[s], n, R, sray[tid], fc, ps, rechecks);
+            else
+                consume_stage<true>(S.ring[s], n, R, sray[tid], fc, ps, rechecks);
+            warp_live = __any_sync(0xffffffffu, ps.r > 0.0f);
             if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
         }
         __syncwarp();
@@ -417,14 +434,15 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
         }
     }
     if (valid) {
+        const float rem = ps.r > 0.0f ? ps.r : ps.rfin;  // live to the end of the list, or stopped
         // renderer.py:118 background with the final remaining transmittance
-        color[(int64_t)p * 3 + 0] = __fmaf_rn(ps.rem, fc.bg[0], ps.cr);
-        color[(int64_t)p * 3 + 1] = __fmaf_rn(ps.rem, fc.bg[1], ps.cg);
-        color[(int64_t)p * 3 + 2] = __fmaf_rn(ps.rem, fc.bg[2], ps.cb);
-        remaining[p] = ps.rem;
+        color[(int64_t)p * 3 + 0] = __fmaf_rn(rem, fc.bg[0], ps.cr);
+        color[(int64_t)p * 3 + 1] = __fmaf_rn(rem, fc.bg[1], ps.cg);
+        color[(int64_t)p * 3 + 2] = __fmaf_rn(rem, fc.bg[2], ps.cb);
+        remaining[p] = rem;
         count[p] = ps.cnt;
         n_eval[p] = ps.ne;
-        if (border) {
+        if (ps.border) {
             unsigned long long slot = atomicAdd(&counters[2], 1ull);
             fixup_list[slot] = (int32_t)(((int64_t)blockIdx.x << 8) | tid);  // work item, thread
         }
@@ -567,7 +585,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
                const double2 *__restrict__ row_sc, const double *__restrict__ dir64,
                const int32_t *__restrict__ ranges, const uint32_t *__restrict__ order,
                const Payload *__restrict__ payload, const GradPayload *__restrict__ gpayload,
-               const float *__restrict__ remaining, const int32_t *__restrict__ n_eval,
+               const uint8_t *__restrict__ flags, const float *__restrict__ remaining, const int32_t *__restrict__ n_eval,
                const float *__restrict__ dl_dimage, float *__restrict__ accum) {
     __shared__ PipeSmem<true> S;
     __shared__ double sray[kRasterThreads][3];
@@ -587,7 +605,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
     const int max_n = smax;
     if (max_n == 0) return;
     if (warp == kConsumerWarps) {
-        pipe_produce<true>(S, order, payload, gpayload, e0, max_n, false);
+        pipe_produce<true>(S, order, payload, gpayload, flags, e0, max_n, false);
         return;
     }
     double d64[3] = {0.0, 0.0, 1.0};
@@ -720,19 +738,19 @@ static int grid_for(int64_t n) { return (int)lmin(lmax((n + 255) / 256, 1), 148 
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    float *color, float *remaining, int32_t *count, int32_t *n_eval, unsigned long long *counters,
-                    int32_t *fixup_list, cudaStream_t st) {
+                    const uint8_t *flags, float *color, float *remaining, int32_t *count, int32_t *n_eval,
+                    unsigned long long *counters, int32_t *fixup_list, cudaStream_t st) {
     if (max_items <= 0) return;
     if (fc.model == GEER_BEAP) {
         k_forward<true><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                            ranges, order, payload, color, remaining, count, n_eval,
-                                                            counters, fixup_list);
+                                                            ranges, order, payload, flags, color, remaining, count,
+                                                            n_eval, counters, fixup_list);
         k_fixup<true><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                counters, fixup_list, color, remaining, count, n_eval);
     } else {
         k_forward<false><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                             ranges, order, payload, color, remaining, count, n_eval,
-                                                             counters, fixup_list);
+                                                             ranges, order, payload, flags, color, remaining, count,
+                                                             n_eval, counters, fixup_list);
         k_fixup<false><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                 counters, fixup_list, color, remaining, count, n_eval);
     }
@@ -741,17 +759,17 @@ void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, c
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                      const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                     const GradPayload *gpayload, const float *remaining, const int32_t *n_eval,
-                     const float *dl_dimage, float *accum, cudaStream_t st) {
+                     const GradPayload *gpayload, const uint8_t *flags, const float *remaining,
+                     const int32_t *n_eval, const float *dl_dimage, float *accum, cudaStream_t st) {
     if (max_items <= 0) return;
     if (fc.model == GEER_BEAP)
         k_backward<true><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                             ranges, order, payload, gpayload, remaining, n_eval,
-                                                             dl_dimage, accum);
+                                                             ranges, order, payload, gpayload, flags, remaining,
+                                                             n_eval, dl_dimage, accum);
     else
         k_backward<false><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                              ranges, order, payload, gpayload, remaining, n_eval,
-                                                              dl_dimage, accum);
+                                                              ranges, order, payload, gpayload, flags, remaining,
+                                                              n_eval, dl_dimage, accum);
 }
 
 void launch_sum_i32(const int32_t *v, int64_t n, unsigned long long *out, cudaStream_t st) {
