@@ -228,6 +228,7 @@ struct __align__(16) PipeSmem {
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     int done_warps;
+    int stop;  // producer will not fill any more stages
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -242,6 +243,20 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, u
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_drop(unsigned long long *bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive_drop.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long *bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
     asm volatile(
@@ -267,6 +282,7 @@ __device__ __forceinline__ void pipe_init(Smem &S) {
             mbar_init(&S.empty[s], kConsumerWarps);
         }
         S.done_warps = 0;
+        S.stop = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -283,18 +299,21 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
     const unsigned per_entry = (unsigned)(sizeof(Payload) + (gpayload ? sizeof(GradPayload) : 0));
     const int lane = threadIdx.x & 31;
     unsigned phase = 0;
-    int s = 0;
-    for (int b = 0;; ++b) {
+    int s = 0, b = 0;
+    bool sentinel = false;
+    for (;; ++b) {
         const int done = kStageEntries * b;
-        int n = min(kStageEntries, n_total - done);
-        if (n > 0 && stop_when_done && *((volatile int *)&S.done_warps) == kConsumerWarps) n = 0;
+        const int n = min(kStageEntries, n_total - done);
+        // every consumer warp has dropped out: stop streaming (no sentinel needed)
+        if (stop_when_done && *((volatile int *)&S.done_warps) == kConsumerWarps) break;
         mbar_wait(&S.empty[s], phase ^ 1);
         if (n <= 0) {
             if (lane == 0) {
                 S.count[s] = 0;
                 mbar_arrive(&S.full[s]);
             }
-            return;
+            sentinel = true;
+            break;
         }
         // reverse: stage b holds entries [first + n_total - done - n, first + n_total - done)
         const int base = kReverse ? first + n_total - done - n : first + done;
@@ -316,6 +335,34 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
             bulk_g2s(&S.ring[s][lane], payload + g, sizeof(Payload), &S.full[s]);
             if (gpayload) bulk_g2s(&S.gring[gpayload ? s : 0][lane], gpayload + g, sizeof(GradPayload), &S.full[s]);
         }
+        if (++s == kStages) {
+            s = 0;
+            phase ^= 1;
+        }
+    }
+    if (lane == 0) *((volatile int *)&S.stop) = 1;
+    // No bulk copy may still be writing shared memory when the CTA retires: wait for the fills
+    // nobody may have waited for.  (After a sentinel, fill b - kStages is known to be consumed and
+    // its slot's barrier has moved on to the sentinel's phase, so it is excluded.)
+    const int oldest = sentinel ? b - kStages + 1 : b - kStages;
+    for (int f = b - 1; f >= 0 && f >= oldest; --f) mbar_wait(&S.full[f % kStages], (f / kStages) & 1);
+}
+
+// A consumer warp whose pixels are all opaque leaves the pipeline: it releases the current stage
+// with arrive_drop and drops out of each later stage's "empty" barrier at the phase it would have
+// released (waiting for that stage's fill first, so the phase is the right one), unless the
+// producer has stopped filling.
+__device__ __forceinline__ void pipe_drop_out(PipeSmem<false> &S, int s, unsigned phase) {
+    const int lane = threadIdx.x & 31;
+    for (int k = 0; k < kStages; ++k) {
+        if (k > 0) {
+            bool ready = false;
+            while (!(ready = mbar_try_wait(&S.full[s], phase)))
+                if (*((volatile int *)&S.stop)) break;
+            if (!ready || S.count[s] == 0) return;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_drop(&S.empty[s]);
         if (++s == kStages) {
             s = 0;
             phase ^= 1;
@@ -425,6 +472,10 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
                 consume_stage<true>(S.ring[s], n, R, sray[tid], fc, ps, rechecks);
             warp_live = __any_sync(0xffffffffu, ps.r > 0.0f);
             if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
+        }
+        if (!warp_live) {  // all 32 pixels opaque: leave the pipeline, stop issuing
+            pipe_drop_out(S, s, phase);
+            break;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[s]);
