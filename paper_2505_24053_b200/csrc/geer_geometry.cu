@@ -388,43 +388,57 @@ __device__ int axis_tiles(double t_aa, double t_a2, double t22, double r0, doubl
         ni = 2;
     }
     const double wlo = edges[0], whi = edges[n_edges - 1];
-    int a0[3], a1[3], na = 0;
-    for (int k = 0; k < ni; ++k) {
-        double lo2 = wlo > ilo[k] ? wlo : ilo[k];
-        double hi2 = whi < ihi[k] ? whi : ihi[k];
-        if (lo2 > hi2) continue;
-        int i0 = max(ss_right(edges, n_edges, lo2) - 1, 0);
-        int i1 = min(ss_left(edges, n_edges, hi2), n_edges - 1);
-        if (i0 >= i1) continue;
-        a0[na] = i0;
-        a1[na] = i1;
-        ++na;
-    }
-    // sort by start, merge overlapping/adjacent
-    for (int i = 1; i < na; ++i)
-        for (int j = i; j > 0 && a0[j] < a0[j - 1]; --j) {
-            int t0 = a0[j]; a0[j] = a0[j - 1]; a0[j - 1] = t0;
-            int t1 = a1[j]; a1[j] = a1[j - 1]; a1[j - 1] = t1;
+    // tile-index range of each interval after window clipping (association.py:373-388); empty -> [BIG, BIG)
+    const int BIG = 1 << 20;
+    int a0[3], a1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        a0[k] = BIG;
+        a1[k] = BIG;
+        if (k < ni) {
+            const double lo2 = wlo > ilo[k] ? wlo : ilo[k];
+            const double hi2 = whi < ihi[k] ? whi : ihi[k];
+            if (!(lo2 > hi2)) {
+                const int i0 = max(ss_right(edges, n_edges, lo2) - 1, 0);
+                const int i1 = min(ss_left(edges, n_edges, hi2), n_edges - 1);
+                if (i0 < i1) {
+                    a0[k] = i0;
+                    a1[k] = i1;
+                }
+            }
         }
-    int nm = 0, cnt = 0;
-    int m0[3], m1[3];
-    for (int i = 0; i < na; ++i) {
-        if (nm > 0 && a0[i] <= m1[nm - 1]) {
-            m1[nm - 1] = max(m1[nm - 1], a1[i]);
+    }
+    // sort the three ranges by start (network), then merge overlapping/adjacent ones (set union)
+    auto cs = [&](int i, int j) {
+        if (a0[j] < a0[i]) {
+            int t = a0[i]; a0[i] = a0[j]; a0[j] = t;
+            t = a1[i]; a1[i] = a1[j]; a1[j] = t;
+        }
+    };
+    cs(0, 1);
+    cs(1, 2);
+    cs(0, 1);
+    // merge 1 into 0, then 2 into the last kept
+    int m0 = a0[0], m1 = a1[0], n0 = BIG, n1 = BIG, p0 = BIG, p1 = BIG;
+    if (a0[1] < BIG) {
+        if (a0[1] <= m1) m1 = max(m1, a1[1]);
+        else { n0 = a0[1]; n1 = a1[1]; }
+    }
+    if (a0[2] < BIG) {
+        if (n0 < BIG) {
+            if (a0[2] <= n1) n1 = max(n1, a1[2]);
+            else { p0 = a0[2]; p1 = a1[2]; }
+        } else if (a0[2] <= m1) {
+            m1 = max(m1, a1[2]);
         } else {
-            m0[nm] = a0[i];
-            m1[nm] = a1[i];
-            ++nm;
+            n0 = a0[2]; n1 = a1[2];
         }
     }
-    for (int i = 0; i < 3; ++i) {
-        if (i < nm) {
-            out[i] = (uint32_t)m0[i] | ((uint32_t)m1[i] << 16);
-            cnt += m1[i] - m0[i];
-        } else {
-            out[i] = 0;
-        }
-    }
+    int cnt = 0;
+    out[0] = out[1] = out[2] = 0;
+    if (m0 < BIG) { out[0] = (uint32_t)m0 | ((uint32_t)m1 << 16); cnt += m1 - m0; }
+    if (n0 < BIG) { out[1] = (uint32_t)n0 | ((uint32_t)n1 << 16); cnt += n1 - n0; }
+    if (p0 < BIG) { out[2] = (uint32_t)p0 | ((uint32_t)p1 << 16); cnt += p1 - p0; }
     return cnt;
 }
 
@@ -471,41 +485,25 @@ __device__ bool make_payload(const double W[9], const double ou[3], const double
     return mode1;
 }
 
-__global__ void __launch_bounds__(128) k_preprocess(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x,
-                                                    const double *__restrict__ medges_y, Payload *__restrict__ payload,
-                                                    GradPayload *__restrict__ gpayload, uint32_t *__restrict__ depth_key, int64_t *__restrict__ count,
-                                                    AxisRanges *__restrict__ ranges, uint8_t *__restrict__ flags,
-                                                    double *__restrict__ mu_out, double *__restrict__ depth_out,
-                                                    int *__restrict__ err) {
+// K1a: exact fp64 association of one Gaussian (association.py:82-88, 148-224, 343-350, 373-451)
+__global__ void __launch_bounds__(128) k_associate(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x,
+                                                   const double *__restrict__ medges_y, uint32_t *__restrict__ depth_key,
+                                                   int64_t *__restrict__ count, AxisRanges *__restrict__ ranges,
+                                                   uint8_t *__restrict__ flags, double *__restrict__ mu_out,
+                                                   double *__restrict__ depth_out, int *__restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *sex = reinterpret_cast<double *>(smem_raw);
     double *sey = sex + (fc.n_x + 1);
-    // SH staging area, 16-byte aligned for the float4 copies
-    float *ssh = reinterpret_cast<float *>(smem_raw + ((sizeof(double) * (fc.n_x + fc.n_y + 2) + 15) & ~(size_t)15));
-    const int nb3 = sc.n_bands * 3;
     for (int i = threadIdx.x; i <= fc.n_x; i += blockDim.x) sex[i] = medges_x[i];
     for (int i = threadIdx.x; i <= fc.n_y; i += blockDim.x) sey[i] = medges_y[i];
-    // stage this block's SH block (contiguous) into smem with coalesced loads
-    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
-    const int cnt_b = (int)min((int64_t)blockDim.x, sc.n - g0);
-    {
-        const float *src = sc.sh + g0 * nb3;
-        const int total = cnt_b * nb3;
-        if ((((uintptr_t)src) & 15) == 0 && (total & 3) == 0) {
-            const float4 *s4 = reinterpret_cast<const float4 *>(src);
-            float4 *d4 = reinterpret_cast<float4 *>(ssh);
-            for (int i = threadIdx.x; i < total / 4; i += blockDim.x) d4[i] = __ldg(s4 + i);
-        } else {
-            for (int i = threadIdx.x; i < total; i += blockDim.x) ssh[i] = __ldg(src + i);
-        }
-    }
     __syncthreads();
-    const int64_t g = g0 + threadIdx.x;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= sc.n) return;
 
     const double *R = fc.R;
-    double mean[3] = {sc.means[g * 3 + 0], sc.means[g * 3 + 1], sc.means[g * 3 + 2]};
-    float q4[4] = {sc.quats[g * 4 + 0], sc.quats[g * 4 + 1], sc.quats[g * 4 + 2], sc.quats[g * 4 + 3]};
+    const double mean[3] = {sc.means[g * 3 + 0], sc.means[g * 3 + 1], sc.means[g * 3 + 2]};
+    const float4 q4v = *reinterpret_cast<const float4 *>(sc.quats + g * 4);
+    const float q4[4] = {q4v.x, q4v.y, q4v.z, q4v.w};
     double rot[9], s[3];
     quat_rot(q4, rot);
     for (int i = 0; i < 3; ++i) s[i] = exp((double)sc.log_scales[g * 3 + i]);
@@ -525,45 +523,12 @@ __global__ void __launch_bounds__(128) k_preprocess(FrameConst fc, geer_scene sc
                 for (int k = 0; k < 3; ++k) acc += R[i * 3 + j] * cov[j * 3 + k] * R[l * 3 + k];
             covc[i * 3 + l] = acc;
         }
-    double depth = sqrt(mu[0] * mu[0] + mu[1] * mu[1] + mu[2] * mu[2]);
+    const double depth = sqrt(mu[0] * mu[0] + mu[1] * mu[1] + mu[2] * mu[2]);
     if (mu_out) {
         for (int i = 0; i < 3; ++i) mu_out[g * 3 + i] = mu[i];
         depth_out[g] = depth;
     }
-
-    // fp32 raster payload (renderer.py:78-80): W = S^-1 R^T, o_u = W (o - mean), rgb, sigma
-    double W[9];
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) W[i * 3 + j] = rot[j * 3 + i] / s[i];
-    double rel[3] = {fc.origin[0] - mean[0], fc.origin[1] - mean[1], fc.origin[2] - mean[2]};
-    double ou[3];
-    for (int i = 0; i < 3; ++i) ou[i] = W[i * 3 + 0] * rel[0] + W[i * 3 + 1] * rel[1] + W[i * 3 + 2] * rel[2];
-    double sigma = sigmoid((double)sc.opacity_logits[g]);
-    // renderer.py:57-70 sh_colors
-    double vd[3] = {mean[0] - fc.origin[0], mean[1] - fc.origin[1], mean[2] - fc.origin[2]};
-    double vn = sqrt(vd[0] * vd[0] + vd[1] * vd[1] + vd[2] * vd[2]);
-    vn = vn > 1e-12 ? vn : 1e-12;
-    double basis[16];
-    sh_basis(vd[0] / vn, vd[1] / vn, vd[2] / vn, basis);
-    const float *shg = ssh + threadIdx.x * nb3;
-    double rgb[3];
-    uint8_t gate = 0;
-    for (int c = 0; c < 3; ++c) {
-        double pre = 0.0;
-        for (int b = 0; b < sc.n_bands; ++b) pre += basis[b] * (double)shg[b * 3 + c];
-        pre += 0.5;
-        if (pre > 0) gate |= (uint8_t)(1u << c);
-        rgb[c] = pre > 0.0 ? pre : 0.0;
-    }
-    double smax = fmax(s[0], fmax(s[1], s[2])), smin = fmin(s[0], fmin(s[1], s[2]));
-    Payload pl;
-    GradPayload gp;
-    const bool mode1 = make_payload(W, ou, rgb, sigma, smax / smin, fc.lam, pl, gp);
-    payload[g] = pl;
-    gpayload[g] = gp;
-
-    // flags: bit0 keep, bit1 clamped, bits3-5 SH clamp gate per channel, bit6 payload mode 1
-    uint8_t fl = (uint8_t)((gate << 3) | (mode1 ? 64 : 0));
+    uint8_t fl = 0;
     int64_t n_ent = 0;
     AxisRanges ar;
     for (int i = 0; i < 3; ++i) ar.x[i] = ar.y[i] = 0;
@@ -581,17 +546,17 @@ __global__ void __launch_bounds__(128) k_preprocess(FrameConst fc, geer_scene sc
         } else {
             // np.linalg.cholesky (LAPACK potf2, lower) operation sequence: reciprocal-pivot column
             // scaling and fma dot products (see oracle/geer_oracle.c)
-            double a00 = covc[0];
+            const double a00 = covc[0];
             bool pd = a00 > 0.0;
             if (pd) {
-                double l00 = sqrt(a00), r0 = 1.0 / l00;
-                double l10 = covc[3] * r0, l20 = covc[6] * r0;
-                double a11 = covc[4] - l10 * l10;
+                const double l00 = sqrt(a00), r0 = 1.0 / l00;
+                const double l10 = covc[3] * r0, l20 = covc[6] * r0;
+                const double a11 = covc[4] - l10 * l10;
                 pd = a11 > 0.0;
                 if (pd) {
-                    double l11 = sqrt(a11);
-                    double l21 = (covc[7] - l20 * l10) * (1.0 / l11);
-                    double a22 = covc[8] - __fma_rn(l21, l21, l20 * l20);
+                    const double l11 = sqrt(a11);
+                    const double l21 = (covc[7] - l20 * l10) * (1.0 / l11);
+                    const double a22 = covc[8] - __fma_rn(l21, l21, l20 * l20);
                     pd = a22 > 0.0;
                 }
             }
@@ -602,22 +567,24 @@ __global__ void __launch_bounds__(128) k_preprocess(FrameConst fc, geer_scene sc
         }
         if (ok) {
             const double lam2 = fc.lam * fc.lam;
-            double t00 = lam2 * covc[0] - mu[0] * mu[0];
-            double t02 = lam2 * covc[2] - mu[0] * mu[2];
-            double t11 = lam2 * covc[4] - mu[1] * mu[1];
-            double t12 = lam2 * covc[5] - mu[1] * mu[2];
-            double t22 = lam2 * covc[8] - mu[2] * mu[2];
-            double scale = fmax(fmax(fmax(fabs(t00), fabs(t02)), fmax(fabs(t11), fabs(t12))), fmax(fabs(t22), 1e-300));
+            const double t00 = lam2 * covc[0] - mu[0] * mu[0];
+            const double t02 = lam2 * covc[2] - mu[0] * mu[2];
+            const double t11 = lam2 * covc[4] - mu[1] * mu[1];
+            const double t12 = lam2 * covc[5] - mu[1] * mu[2];
+            const double t22 = lam2 * covc[8] - mu[2] * mu[2];
+            const double scale =
+                fmax(fmax(fmax(fabs(t00), fabs(t02)), fmax(fabs(t11), fabs(t12))), fmax(fabs(t22), 1e-300));
             bool clamped = false;
             double rt0 = 0, rt1 = 0, rp0 = 0, rp1 = 0;
             if (fabs(t22) < 1e-12 * scale) {
                 clamped = true;
             } else {
-                bool okt = quadratic_roots(t22, t02, t00, rt0, rt1);
-                bool okp = quadratic_roots(t22, t12, t11, rp0, rp1);
+                const bool okt = quadratic_roots(t22, t02, t00, rt0, rt1);
+                const bool okp = quadratic_roots(t22, t12, t11, rp0, rp1);
                 clamped = !okt || !okp;
             }
-            bool keep = !(clamped && sigma < kMinClampedOpacity);  // association.py:343-350
+            const double sigma = sigmoid((double)sc.opacity_logits[g]);
+            const bool keep = !(clamped && sigma < kMinClampedOpacity);  // association.py:343-350
             if (clamped) fl |= 2;
             if (keep) {
                 fl |= 1;
@@ -626,8 +593,8 @@ __global__ void __launch_bounds__(128) k_preprocess(FrameConst fc, geer_scene sc
                     ar.y[0] = (uint32_t)fc.n_y << 16;
                     n_ent = (int64_t)fc.n_x * fc.n_y;
                 } else {
-                    int cx = axis_tiles(t00, t02, t22, rt0, rt1, sex, fc.n_x + 1, ar.x);
-                    int cy = axis_tiles(t11, t12, t22, rp0, rp1, sey, fc.n_y + 1, ar.y);
+                    const int cx = axis_tiles(t00, t02, t22, rt0, rt1, sex, fc.n_x + 1, ar.x);
+                    const int cy = axis_tiles(t11, t12, t22, rp0, rp1, sey, fc.n_y + 1, ar.y);
                     n_ent = (int64_t)cx * cy;
                 }
             }
@@ -637,90 +604,167 @@ __global__ void __launch_bounds__(128) k_preprocess(FrameConst fc, geer_scene sc
     ranges[g] = ar;
     flags[g] = fl;
     // association.py:335-340 key bits (depth > 0): f32 bits | 0x80000000; non-emitting last
-    uint32_t kb = __float_as_uint((float)depth) | 0x80000000u;
+    const uint32_t kb = __float_as_uint((float)depth) | 0x80000000u;
     depth_key[g] = n_ent > 0 ? kb : 0xFFFFFFFFu;
+}
+
+// K1b: raster payload of one Gaussian (renderer.py:57-81): W, o_u, the fp64 quadratic forms, SH colour.
+// Only the pixel-side arithmetic of the raster depends on these values (not the association), so
+// reciprocals replace divisions here.  NB = SH band count (compile-time: static register arrays).
+template <int NB>
+__global__ void __launch_bounds__(128) k_payload(FrameConst fc, geer_scene sc, Payload *__restrict__ payload,
+                                                 GradPayload *__restrict__ gpayload, uint8_t *__restrict__ flags) {
+    __shared__ __align__(16) float ssh[128 * NB * 3];
+    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
+    const int cnt_b = (int)lmin((int64_t)blockDim.x, sc.n - g0);
+    {
+        // stage this block's SH coefficients (contiguous) with coalesced loads
+        const float *src = sc.sh + g0 * NB * 3;
+        const int total = cnt_b * NB * 3;
+        if ((((uintptr_t)src) & 15) == 0 && (total & 3) == 0) {
+            const float4 *s4 = reinterpret_cast<const float4 *>(src);
+            float4 *d4 = reinterpret_cast<float4 *>(ssh);
+            for (int i = threadIdx.x; i < total / 4; i += blockDim.x) d4[i] = __ldg(s4 + i);
+        } else {
+            for (int i = threadIdx.x; i < total; i += blockDim.x) ssh[i] = __ldg(src + i);
+        }
+    }
+    __syncthreads();
+    const int64_t g = g0 + threadIdx.x;
+    if (g >= sc.n) return;
+    const double mean[3] = {sc.means[g * 3 + 0], sc.means[g * 3 + 1], sc.means[g * 3 + 2]};
+    const float4 q4v = *reinterpret_cast<const float4 *>(sc.quats + g * 4);
+    const float q4[4] = {q4v.x, q4v.y, q4v.z, q4v.w};
+    double rot[9], s[3], is[3];
+    quat_rot(q4, rot);
+    for (int i = 0; i < 3; ++i) {
+        s[i] = exp((double)sc.log_scales[g * 3 + i]);
+        is[i] = exp(-(double)sc.log_scales[g * 3 + i]);
+    }
+    // renderer.py:78-79: W = S^-1 R^T, o_u = W (o - mean)
+    double W[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) W[i * 3 + j] = rot[j * 3 + i] * is[i];
+    const double rel[3] = {fc.origin[0] - mean[0], fc.origin[1] - mean[1], fc.origin[2] - mean[2]};
+    double ou[3];
+    for (int i = 0; i < 3; ++i) ou[i] = W[i * 3 + 0] * rel[0] + W[i * 3 + 1] * rel[1] + W[i * 3 + 2] * rel[2];
+    const double sigma = sigmoid((double)sc.opacity_logits[g]);
+    // renderer.py:57-70 sh_colors (view direction from the optical centre, stop-gradient)
+    const double vd[3] = {-rel[0], -rel[1], -rel[2]};
+    double vn = sqrt(vd[0] * vd[0] + vd[1] * vd[1] + vd[2] * vd[2]);
+    const double ivn = 1.0 / (vn > 1e-12 ? vn : 1e-12);
+    double basis[16];
+    sh_basis(vd[0] * ivn, vd[1] * ivn, vd[2] * ivn, basis);
+    const float *shg = ssh + threadIdx.x * NB * 3;
+    double rgb[3];
+    uint8_t gate = 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double pre = 0.0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) pre += basis[b] * (double)shg[b * 3 + c];
+        pre += 0.5;
+        if (pre > 0) gate |= (uint8_t)(1u << c);
+        rgb[c] = pre > 0.0 ? pre : 0.0;
+    }
+    const double smax = fmax(s[0], fmax(s[1], s[2])), smin = fmin(s[0], fmin(s[1], s[2]));
+    Payload pl;
+    GradPayload gp;
+    const bool mode1 = make_payload(W, ou, rgb, sigma, smax / smin, fc.lam, pl, gp);
+    payload[g] = pl;
+    gpayload[g] = gp;
+    // flags: bit0 keep, bit1 clamped (K1a), bits3-5 SH clamp gate per channel, bit6 payload mode 1
+    flags[g] = (uint8_t)(flags[g] | (gate << 3) | (mode1 ? 64 : 0));
 }
 
 // ---------------------------------------------------------------- K7
 
-// accum layout per Gaussian (16 f32): dW_rc (9, row-major), sum dl/do_u (3), sum dsigma, sum dcol (3)
-template <typename T>
+// accum layout per Gaussian (16 f32): dW_rc (9, row-major), sum dl/do_u (3), sum dsigma, sum dcol (3).
+// fp32 arithmetic (the accumulators are fp32 already); renderer.py:304-307, 204-231, 332.
+template <typename T, int NB>
 __global__ void __launch_bounds__(128) k_finalize(FrameConst fc, geer_scene sc, const float4 *__restrict__ accum,
                                                   const uint8_t *__restrict__ flags, T *dmeans, T *dlog_scales,
                                                   T *dquats, T *dopac, T *dsh, int accumulate) {
-    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (g >= sc.n) return;
     float a[16];
+#pragma unroll
     for (int i = 0; i < 4; ++i) {
-        float4 v = accum[g * 4 + i];
+        const float4 v = accum[g * 4 + i];
         a[i * 4 + 0] = v.x;
         a[i * 4 + 1] = v.y;
         a[i * 4 + 2] = v.z;
         a[i * 4 + 3] = v.w;
     }
-    double mean[3] = {sc.means[g * 3 + 0], sc.means[g * 3 + 1], sc.means[g * 3 + 2]};
-    float q4[4] = {sc.quats[g * 4 + 0], sc.quats[g * 4 + 1], sc.quats[g * 4 + 2], sc.quats[g * 4 + 3]};
-    double rot[9], s[3], W[9];
-    quat_rot(q4, rot);
-    for (int i = 0; i < 3; ++i) s[i] = exp((double)sc.log_scales[g * 3 + i]);
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) W[i * 3 + j] = rot[j * 3 + i] / s[i];
-    double rel[3] = {fc.origin[0] - mean[0], fc.origin[1] - mean[1], fc.origin[2] - mean[2]};
-    double dos[3] = {a[9], a[10], a[11]};
-    // renderer.py:304-307: dW = dW_rc + (sum dl/do) (o - mu)^T ; dmu = -W^T sum dl/do
-    double dw[9];
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) dw[i * 3 + j] = (double)a[i * 3 + j] + dos[i] * rel[j];
-    double dmu[3];
-    for (int i = 0; i < 3; ++i) dmu[i] = -(W[0 * 3 + i] * dos[0] + W[1 * 3 + i] * dos[1] + W[2 * 3 + i] * dos[2]);
-    // renderer.py:204-231
-    double dls[3];
-    for (int k = 0; k < 3; ++k) {
-        double acc = dw[k * 3 + 0] * rot[0 * 3 + k] + dw[k * 3 + 1] * rot[1 * 3 + k] + dw[k * 3 + 2] * rot[2 * 3 + k];
-        dls[k] = (-acc / (s[k] * s[k])) * s[k];
-    }
-    double q0 = q4[0], q1 = q4[1], q2 = q4[2], q3 = q4[3];
-    double qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-    double r = q0 / qn, i = q1 / qn, j = q2 / qn, k = q3 / qn;
-    const double D[4][9] = {
-        {0, k, -j, -k, 0, i, j, -i, 0},
-        {0, j, k, j, -2 * i, r, k, -r, -2 * i},
-        {-2 * j, i, -r, i, 0, k, r, k, -2 * j},
-        {-2 * k, r, i, -r, -2 * k, j, i, j, 0},
-    };
-    double dqr[4];
-    for (int mm = 0; mm < 4; ++mm) {
-        double acc = 0.0;
-        for (int aa = 0; aa < 3; ++aa)
-            for (int bb = 0; bb < 3; ++bb) acc += dw[aa * 3 + bb] * (2.0 * D[mm][aa * 3 + bb] * (1.0 / s[aa]));
-        dqr[mm] = acc;
-    }
-    double qh[4] = {q0 / qn, q1 / qn, q2 / qn, q3 / qn};
-    double dot = dqr[0] * qh[0] + dqr[1] * qh[1] + dqr[2] * qh[2] + dqr[3] * qh[3];
+    const float mean[3] = {sc.means[g * 3 + 0], sc.means[g * 3 + 1], sc.means[g * 3 + 2]};
+    const float4 q4v = *reinterpret_cast<const float4 *>(sc.quats + g * 4);
+    const float q0 = q4v.x, q1 = q4v.y, q2 = q4v.z, q3 = q4v.w;
+    const float qn = sqrtf(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+    const float iqn = 1.0f / qn;
+    const float r = q0 * iqn, i = q1 * iqn, j = q2 * iqn, k = q3 * iqn;
+    const float rot[9] = {1 - 2 * (j * j + k * k), 2 * (i * j - r * k), 2 * (i * k + r * j),
+                          2 * (i * j + r * k), 1 - 2 * (i * i + k * k), 2 * (j * k - r * i),
+                          2 * (i * k - r * j), 2 * (j * k + r * i), 1 - 2 * (i * i + j * j)};
+    float is[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) is[c] = __expf(-sc.log_scales[g * 3 + c]);
+    const float rel[3] = {(float)fc.origin[0] - mean[0], (float)fc.origin[1] - mean[1], (float)fc.origin[2] - mean[2]};
+    const float dos[3] = {a[9], a[10], a[11]};
+    // renderer.py:304-307: dW = dW_rc + (sum dl/do) (o - mu)^T ; dmu = -W^T sum dl/do, W[i][j] = rot[j][i] / s_i
+    float dw[9];
+#pragma unroll
+    for (int x = 0; x < 3; ++x)
+#pragma unroll
+        for (int y = 0; y < 3; ++y) dw[x * 3 + y] = fmaf(dos[x], rel[y], a[x * 3 + y]);
+    float dmu[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        dmu[c] = -(rot[c * 3 + 0] * is[0] * dos[0] + rot[c * 3 + 1] * is[1] * dos[1] + rot[c * 3 + 2] * is[2] * dos[2]);
+    // renderer.py:208-209: dlog_s_k = -(sum_j dW[k][j] R[j][k]) / s_k
+    float dls[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        dls[c] = -(dw[c * 3 + 0] * rot[0 * 3 + c] + dw[c * 3 + 1] * rot[1 * 3 + c] + dw[c * 3 + 2] * rot[2 * 3 + c]) * is[c];
+    // renderer.py:211-230: dq_raw_m = sum_ab dW[a][b] 2 D_m[a][b] / s_a, then the normalisation Jacobian
+    float e[9];
+#pragma unroll
+    for (int x = 0; x < 3; ++x)
+#pragma unroll
+        for (int y = 0; y < 3; ++y) e[x * 3 + y] = 2.0f * dw[x * 3 + y] * is[x];
+    const float dqr0 = e[1] * k - e[2] * j - e[3] * k + e[5] * i + e[6] * j - e[7] * i;
+    const float dqr1 = e[1] * j + e[2] * k + e[3] * j - 2 * i * e[4] + e[5] * r + e[6] * k - e[7] * r - 2 * i * e[8];
+    const float dqr2 = -2 * j * e[0] + e[1] * i - e[2] * r + e[3] * i + e[5] * k + e[6] * r + e[7] * k - 2 * j * e[8];
+    const float dqr3 = -2 * k * e[0] + e[1] * r + e[2] * i - e[3] * r - 2 * k * e[4] + e[5] * j + e[6] * i + e[7] * j;
+    const float dot = dqr0 * r + dqr1 * i + dqr2 * j + dqr3 * k;
     // renderer.py:332 dsh = basis (x) (dcol * gate), view direction stop-gradient
-    double vd[3] = {mean[0] - fc.origin[0], mean[1] - fc.origin[1], mean[2] - fc.origin[2]};
-    double vn = sqrt(vd[0] * vd[0] + vd[1] * vd[1] + vd[2] * vd[2]);
-    vn = vn > 1e-12 ? vn : 1e-12;
+    const float vx = -rel[0], vy = -rel[1], vz = -rel[2];
+    const float ivn = 1.0f / fmaxf(sqrtf(vx * vx + vy * vy + vz * vz), 1e-12f);
     double basis[16];
-    sh_basis(vd[0] / vn, vd[1] / vn, vd[2] / vn, basis);
-    uint8_t gate = flags[g] >> 3;
-    double dcol[3];
-    for (int c = 0; c < 3; ++c) dcol[c] = ((gate >> c) & 1) ? (double)a[13 + c] : 0.0;
-
-    const bool acc = accumulate & GEER_ACCUMULATE;
-    auto put = [&](T *p, int64_t idx, double v) { p[idx] = acc ? (T)((double)p[idx] + v) : (T)v; };
-    for (int c = 0; c < 3; ++c) put(dmeans, g * 3 + c, dmu[c]);
-    for (int c = 0; c < 3; ++c) put(dlog_scales, g * 3 + c, dls[c]);
-    for (int mm = 0; mm < 4; ++mm) put(dquats, g * 4 + mm, (dqr[mm] - dot * qh[mm]) / qn);
-    double dsig = (double)a[12];
+    sh_basis((double)(vx * ivn), (double)(vy * ivn), (double)(vz * ivn), basis);
+    const uint8_t gate = flags[g] >> 3;
+    float dcol[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) dcol[c] = ((gate >> c) & 1) ? a[13 + c] : 0.0f;
+    float dsig = a[12];
     if (accumulate & GEER_OPACITY_LOGIT) {  // trainer.py:208-217 stored_grads: chain through the logit
-        double sg = sigmoid((double)sc.opacity_logits[g]);
-        dsig = dsig * sg * (1.0 - sg);
+        const float sg = 1.0f / (1.0f + __expf(-sc.opacity_logits[g]));
+        dsig = dsig * sg * (1.0f - sg);
     }
+    const bool acc = accumulate & GEER_ACCUMULATE;
+    auto put = [&](T *p, int64_t idx, float v) { p[idx] = acc ? (T)((double)p[idx] + (double)v) : (T)v; };
+#pragma unroll
+    for (int c = 0; c < 3; ++c) put(dmeans, g * 3 + c, dmu[c]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) put(dlog_scales, g * 3 + c, dls[c]);
+    put(dquats, g * 4 + 0, (dqr0 - dot * r) * iqn);
+    put(dquats, g * 4 + 1, (dqr1 - dot * i) * iqn);
+    put(dquats, g * 4 + 2, (dqr2 - dot * j) * iqn);
+    put(dquats, g * 4 + 3, (dqr3 - dot * k) * iqn);
     put(dopac, g, dsig);
-    const int nb = sc.n_bands;
-    for (int b = 0; b < nb; ++b)
-        for (int c = 0; c < 3; ++c) put(dsh, (g * nb + b) * 3 + c, basis[b] * dcol[c]);
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) put(dsh, (g * NB + b) * 3 + c, (float)basis[b] * dcol[c]);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -764,31 +808,43 @@ void launch_item_fill(int n_tiles, const int32_t *tile_off, const int32_t *item_
     k_item_fill<<<(n_tiles + 255) / 256, 256, 0, st>>>(n_tiles, tile_off, item_off, items, n_items);
 }
 
-size_t preprocess_smem(const FrameConst &fc) {
-    return ((sizeof(double) * (fc.n_x + fc.n_y + 2) + 15) & ~(size_t)15) + sizeof(float) * 128 * fc.n_bands * 3;
-}
+size_t preprocess_smem(const FrameConst &fc) { return sizeof(double) * (fc.n_x + fc.n_y + 2); }
 
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
-                       Payload *payload, GradPayload *gpayload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges, uint8_t *flags,
-                       double *mu_out, double *depth_out, int *err, cudaStream_t st) {
+                       Payload *payload, GradPayload *gpayload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges,
+                       uint8_t *flags, double *mu_out, double *depth_out, int *err, cudaStream_t st) {
     if (sc.n == 0) return;
-    size_t smem = preprocess_smem(fc);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_preprocess, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
+    const int blocks = (int)((sc.n + 127) / 128);
+    k_associate<<<blocks, 128, preprocess_smem(fc), st>>>(fc, sc, medges_x, medges_y, depth_key, count, ranges, flags,
+                                                          mu_out, depth_out, err);
+    switch (sc.n_bands) {
+#define GEER_NB_CASE(NB) \
+    case NB: k_payload<NB><<<blocks, 128, 0, st>>>(fc, sc, payload, gpayload, flags); break;
+        GEER_NB_CASE(1) GEER_NB_CASE(2) GEER_NB_CASE(3) GEER_NB_CASE(4) GEER_NB_CASE(5) GEER_NB_CASE(6)
+        GEER_NB_CASE(7) GEER_NB_CASE(8) GEER_NB_CASE(9) GEER_NB_CASE(10) GEER_NB_CASE(11) GEER_NB_CASE(12)
+        GEER_NB_CASE(13) GEER_NB_CASE(14) GEER_NB_CASE(15) GEER_NB_CASE(16)
+#undef GEER_NB_CASE
+        default: break;
     }
-    int blocks = (int)((sc.n + 127) / 128);
-    k_preprocess<<<blocks, 128, smem, st>>>(fc, sc, medges_x, medges_y, payload, gpayload, depth_key, count, ranges, flags,
-                                            mu_out, depth_out, err);
 }
 
 template <typename T>
 void launch_finalize(const FrameConst &fc, const geer_scene &sc, const float4 *accum, const uint8_t *flags, T *dmeans,
                      T *dlog_scales, T *dquats, T *dopac, T *dsh, int accumulate, cudaStream_t st) {
     if (sc.n == 0) return;
-    int blocks = (int)((sc.n + 127) / 128);
-    k_finalize<T><<<blocks, 128, 0, st>>>(fc, sc, accum, flags, dmeans, dlog_scales, dquats, dopac, dsh, accumulate);
+    const int blocks = (int)((sc.n + 127) / 128);
+    switch (sc.n_bands) {
+#define GEER_NB_CASE(NB)                                                                                           \
+    case NB:                                                                                                       \
+        k_finalize<T, NB><<<blocks, 128, 0, st>>>(fc, sc, accum, flags, dmeans, dlog_scales, dquats, dopac, dsh, \
+                                                  accumulate);                                                     \
+        break;
+        GEER_NB_CASE(1) GEER_NB_CASE(2) GEER_NB_CASE(3) GEER_NB_CASE(4) GEER_NB_CASE(5) GEER_NB_CASE(6)
+        GEER_NB_CASE(7) GEER_NB_CASE(8) GEER_NB_CASE(9) GEER_NB_CASE(10) GEER_NB_CASE(11) GEER_NB_CASE(12)
+        GEER_NB_CASE(13) GEER_NB_CASE(14) GEER_NB_CASE(15) GEER_NB_CASE(16)
+#undef GEER_NB_CASE
+        default: break;
+    }
 }
 template void launch_finalize<float>(const FrameConst &, const geer_scene &, const float4 *, const uint8_t *, float *,
                                      float *, float *, float *, float *, int, cudaStream_t);
