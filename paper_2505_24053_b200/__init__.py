@@ -9,3 +9,16 @@ raises.
 """
 
 __version__ = "0.1.0"
+
+
+def install(with_graph: bool = False):
+    """Patch a live ``raygauss`` so its render / render_backward / build_render_graph run here (dropin.py)."""
+    from .dropin import install as _install
+
+    return _install(with_graph)
+
+
+def uninstall():
+    from .dropin import uninstall as _uninstall
+
+    _uninstall()

@@ -38,6 +38,19 @@ def shard(n_items: int, rank: int, world: int) -> range:
     return range(start, start + base + (1 if rank < extra else 0))
 
 
+def allreduce_grads(buf: torch.Tensor, world: int) -> torch.Tensor:
+    """Sum the flat per-rank gradient buffer over all ranks in place (ONE collective per step).
+
+    NCCL over NVLink/NVSwitch on the GPU box; gloo in the CPU tests.  World size 1
+    is a no-op, so the 1-GPU step runs no collective at all.
+    """
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM)
+    return buf
+
+
 class FlatScene:
     """A DeviceScene whose five tensors are views of one contiguous fp32 buffer."""
 
@@ -133,10 +146,7 @@ class MultiViewTrainer:
             self.renderer.backward(dl, grads=self.grads.scene, accumulate=True, opacity_logit=True)
             if compute_loss:
                 loss += float((color - target).abs().mean())
-        if self.world > 1:
-            import torch.distributed as dist
-
-            dist.all_reduce(self.grads.buf, op=dist.ReduceOp.SUM)
+        allreduce_grads(self.grads.buf, self.world)
         self.t += 1
         _lib.check(self.lib.geer_adam(self.params.buf.data_ptr(), self.grads.buf.data_ptr(), self.m.data_ptr(),
                                       self.v.data_ptr(), self.lr.data_ptr(), self.params.numel, ctypes.c_float(0.9),

@@ -1,0 +1,37 @@
+"""install() rebinds the reference's entry points (incl. the trainer's by-name imports) and restores them.
+
+Needs the reference package importable (this build container); skipped elsewhere.
+The GPU-side behaviour of the patched functions is covered by test_gpu_parity.py.
+"""
+
+import os
+import sys
+
+import pytest
+
+REF = "/root/reference/pkg/src"
+pytestmark = pytest.mark.skipif(not os.path.isdir(REF), reason="reference package not present")
+
+
+def test_install_patches_renderer_association_and_trainer():
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import raygauss.association as ra
+    import raygauss.renderer as rr
+    import raygauss.trainer as rt
+
+    import paper_2505_24053_b200 as pkg
+    from paper_2505_24053_b200 import dropin
+
+    orig = (rr.render, rr.render_backward, ra.build_render_graph, rt.render, rt.render_backward)
+    patched = pkg.install()
+    try:
+        assert set(patched) == {"raygauss.renderer.render", "raygauss.renderer.render_backward",
+                                "raygauss.association.build_render_graph", "raygauss.trainer.render",
+                                "raygauss.trainer.render_backward"}
+        assert rr.render is rt.render and rr.render is not orig[0]
+        assert rr.render_backward is dropin.render_backward is rt.render_backward
+        assert ra.build_render_graph is dropin.build_render_graph
+    finally:
+        pkg.uninstall()
+    assert (rr.render, rr.render_backward, ra.build_render_graph, rt.render, rt.render_backward) == orig
