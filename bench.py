@@ -308,6 +308,9 @@ def run_ours(args):
     extra["frame"] = {"entries": int(st["n_entries"]), "tiles": int(st["n_tiles"]),
                       "work_items": int(st["n_work_items"]), "evaluated_pairs": int(pairs),
                       "pairs_per_pixel": pairs / n_px, "kappa_rechecks": int(st["kappa_rechecks"]),
+                      "fixup_pixels": int(st["fixup_pixels"]),
+                      "warp_entries": int(st["warp_entries"]),
+                      "issued_pairs_over_evaluated": 32 * st["warp_entries"] / max(pairs, 1),
                       "clamped": int(st["clamped"])}
 
     # ---- fwd + bwd ms per view (config 3)

@@ -67,8 +67,11 @@ typedef struct geer_config {
     int32_t tile_px;
     int32_t support_cutoff;
     int32_t threads;
-    int32_t pad_;
+    int32_t flags; /* GEER_CFG_* debug switches (0 = default behaviour) */
 } geer_config;
+
+/* Disable the per-warp PBF culling of the raster (results are identical; for tests). */
+#define GEER_CFG_NO_CULL 1
 
 /* Device scene: fp32 SoA in the reference's stored spaces (scene.py:35-51). */
 typedef struct geer_scene {
@@ -110,6 +113,7 @@ typedef struct geer_stats {
     int64_t kappa_rechecks;   /* fp64 re-evaluations of the kappa cutoff */
     int64_t fixup_pixels;     /* pixels recomposited in fp64 (early stop too close to call in fp32) */
     int64_t clamped;          /* clamped & kept particles */
+    int64_t warp_entries;     /* forward (warp, entry) evaluations after PBF culling */
     float ms_prep, ms_dup, ms_sort, ms_render, ms_total; /* CUDA-event stage times (if timing on) */
     float ms_backward;
 } geer_stats;

@@ -47,7 +47,7 @@ class GeerCamera(ctypes.Structure):
 class GeerConfig(ctypes.Structure):
     _fields_ = [
         ("lam", ctypes.c_double), ("background", ctypes.c_double * 3), ("tile_px", ctypes.c_int32),
-        ("support_cutoff", ctypes.c_int32), ("threads", ctypes.c_int32), ("pad_", ctypes.c_int32),
+        ("support_cutoff", ctypes.c_int32), ("threads", ctypes.c_int32), ("flags", ctypes.c_int32),
     ]
 
 
@@ -73,7 +73,7 @@ class GeerStats(ctypes.Structure):
         ("n_gaussians", ctypes.c_int64), ("n_entries", ctypes.c_int64), ("n_tiles", ctypes.c_int64),
         ("n_work_items", ctypes.c_int64), ("evaluated_pairs", ctypes.c_int64), ("kappa_rechecks", ctypes.c_int64),
         ("fixup_pixels", ctypes.c_int64),
-        ("clamped", ctypes.c_int64),
+        ("clamped", ctypes.c_int64), ("warp_entries", ctypes.c_int64),
         ("ms_prep", ctypes.c_float), ("ms_dup", ctypes.c_float), ("ms_sort", ctypes.c_float),
         ("ms_render", ctypes.c_float), ("ms_total", ctypes.c_float), ("ms_backward", ctypes.c_float),
     ]
@@ -162,13 +162,17 @@ def camera_struct(camera) -> GeerCamera:
     return c
 
 
-def config_struct(config) -> GeerConfig:
+GEER_CFG_NO_CULL = 1
+
+
+def config_struct(config, flags: int = 0) -> GeerConfig:
     g = GeerConfig()
     g.lam = float(config.lam)
     g.background[:] = [float(v) for v in np.asarray(config.background, dtype=np.float64).reshape(3)]
     g.tile_px = int(config.tile_px)
     g.support_cutoff = 1 if config.support_cutoff else 0
     g.threads = int(getattr(config, "threads", 1) or 0)
+    g.flags = int(flags)
     return g
 
 

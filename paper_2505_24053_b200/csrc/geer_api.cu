@@ -64,17 +64,17 @@ struct geer_ctx {
     int max_items = 0;
     const float *fwd_remaining = nullptr;  // remaining written by the last forward (backward input)
     float ms[6] = {};
-    unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs, [2] fp64 fix-up pixels
+    unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs, [2] fix-up pixels, [3] warp-entries
     int *d_err = nullptr;
     int64_t *h_hdr = nullptr;  // pinned: [0] total entries, [1] error code
     // camera buffers
     Buf col_sc, row_sc, medges_x, medges_y, edges_x, edges_y, dir64, theta, phi, minmax, pixel_tile, pixel_tile_sorted,
         pix_iota, pix_list, tile_count, tile_off, item_count, item_off, items, n_items;
     // per-Gaussian buffers
-    Buf payload, gpayload, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, cnt_sorted, offs, ranges_ax, flags, mu_c,
+    Buf payload, gpayload, box, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, cnt_sorted, offs, ranges_ax, flags, mu_c,
         depth;
     // per-entry buffers
-    Buf tile_keys, tile_keys_sorted, gids, order, tile_ranges;
+    Buf tile_keys, tile_keys_sorted, gids, order, tile_ranges, block_rank;
     // per-pixel buffers
     Buf color, remaining, count_px, n_eval, dl32, fixup;
     // backward
@@ -143,6 +143,8 @@ int make_frame_const(const geer_camera *cam, const geer_config *cfg, int n_bands
     fc->n_tiles = fc->n_x * fc->n_y;
     fc->n_bands = n_bands;
     fc->cutoff = cfg->support_cutoff ? 1 : 0;
+    // per-warp PBF culling is exact only under the support cutoff (renderer.py:103-105)
+    fc->cull = (cfg->support_cutoff && !(cfg->flags & GEER_CFG_NO_CULL)) ? 1 : 0;
     for (int i = 0; i < 9; ++i) fc->R[i] = cam->rotation[i];
     for (int i = 0; i < 3; ++i) fc->t[i] = cam->translation[i];
     // camera.py:71-74: o = -R^T t
@@ -231,7 +233,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     c->have_frame = false;
     c->have_raster = false;
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
-    GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 3 * sizeof(unsigned long long), st));
+    GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), st));
     GEER_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
     rc = camera_setup(c, want_export, st);
     if (rc) return rc;
@@ -239,6 +241,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     // ---- K1 preprocess
     Payload *payload = ENSURE(Payload, c->payload, n);
     GradPayload *gpayload = ENSURE(GradPayload, c->gpayload, n);
+    float4 *box = ENSURE(float4, c->box, n);
     uint32_t *dkey = ENSURE(uint32_t, c->depth_key, n);
     uint32_t *dkey_s = ENSURE(uint32_t, c->depth_key_sorted, n);
     int32_t *giota = ENSURE(int32_t, c->gid_iota, n);
@@ -255,7 +258,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     }
     int32_t *ranges = ENSURE(int32_t, c->tile_ranges, fc.n_tiles + 1);
     launch_preprocess(fc, sc, (const double *)c->medges_x.p, (const double *)c->medges_y.p, payload, gpayload, dkey, cnt, ar,
-                      flags, mu, dep, c->d_err, st);
+                      flags, box, mu, dep, c->d_err, st);
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[1], st));
 
     // ---- dup: depth order, scan, header D2H, emit
@@ -286,7 +289,8 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     uint32_t *tks = ENSURE(uint32_t, c->tile_keys_sorted, total);
     uint32_t *gids = ENSURE(uint32_t, c->gids, total);
     uint32_t *order = ENSURE(uint32_t, c->order, total);
-    emit_entries(offs, gsorted, ar, fc.n_x, total, n, tk, gids, st);
+    int32_t *brank = ENSURE(int32_t, c->block_rank, emit_blocks(total) + 1);
+    emit_entries(offs, gsorted, ar, fc.n_x, total, n, brank, tk, gids, st);
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[2], st));
 
     // ---- sort: stable tile sort + ranges
@@ -306,7 +310,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         int32_t *fix = ENSURE(int32_t, c->fixup, npx);
         launch_forward(fc, sc, c->max_items, (const int4 *)c->items.p, (const int32_t *)c->n_items.p,
                        (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
-                       (const double *)c->dir64.p, ranges, order, payload, flags, color, remaining, count, ne,
+                       (const double *)c->dir64.p, ranges, order, payload, flags, box, color, remaining, count, ne,
                        c->d_counters, fix, st);
         c->fwd_remaining = remaining;
         c->have_raster = true;
@@ -336,7 +340,7 @@ int run_backward(geer_ctx *c, const float *dl_dimage, bool f64_out, void *const 
                     (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
                     (const double *)c->dir64.p, (const int32_t *)c->tile_ranges.p, (const uint32_t *)c->order.p,
                     (const Payload *)c->payload.p, (const GradPayload *)c->gpayload.p, (const uint8_t *)c->flags.p,
-                    c->fwd_remaining, (const int32_t *)c->n_eval.p,
+                    (const float4 *)c->box.p, c->fwd_remaining, (const int32_t *)c->n_eval.p,
                     dl_dimage, accum, st);
     if (f64_out)
         launch_finalize<double>(fc, sc, (const float4 *)accum, (const uint8_t *)c->flags.p, (double *)gout[0], (double *)gout[1],
@@ -429,7 +433,7 @@ geer_ctx *geer_create(int device) {
     c->device = device;
     bool ok = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) == cudaSuccess;
     for (int i = 0; i < 6 && ok; ++i) ok = cudaEventCreate(&c->ev[i]) == cudaSuccess;
-    ok = ok && cudaMalloc(&c->d_counters, 3 * sizeof(unsigned long long)) == cudaSuccess;
+    ok = ok && cudaMalloc(&c->d_counters, 4 * sizeof(unsigned long long)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->d_err, sizeof(int)) == cudaSuccess;
     ok = ok && cudaMallocHost(&c->h_hdr, 2 * sizeof(int64_t)) == cudaSuccess;
     if (!ok) {
@@ -446,10 +450,10 @@ void geer_destroy(geer_ctx *c) {
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     Buf *bufs[] = {&c->col_sc, &c->row_sc, &c->medges_x, &c->medges_y, &c->edges_x, &c->edges_y, &c->dir64,
                    &c->theta, &c->phi, &c->minmax, &c->pixel_tile, &c->pixel_tile_sorted, &c->pix_iota, &c->pix_list,
-                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->payload, &c->gpayload,
+                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->payload, &c->gpayload, &c->box,
                    &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted, &c->count, &c->cnt_sorted,
                    &c->offs, &c->ranges_ax, &c->flags, &c->mu_c, &c->depth, &c->tile_keys, &c->tile_keys_sorted,
-                   &c->gids, &c->order, &c->tile_ranges, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,
+                   &c->gids, &c->order, &c->tile_ranges, &c->block_rank, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,
                    &c->accum, &c->temp, &c->h64_means, &c->h64_log, &c->h64_quats, &c->h64_op, &c->h64_sh,
                    &c->s32_means, &c->s32_log, &c->s32_quats, &c->s32_op, &c->s32_sh, &c->out64, &c->g64};
     for (Buf *b : bufs) free_buf(*b);
@@ -514,7 +518,7 @@ int geer_frame_stats(geer_ctx *c, geer_stats *out) {
         GEER_CUDA(cudaDeviceSynchronize());
         GEER_CUDA(cudaMemsetAsync(c->d_counters + 1, 0, sizeof(unsigned long long), st));
         launch_sum_i32((const int32_t *)c->n_eval.p, (int64_t)c->fc.width * c->fc.height, c->d_counters + 1, st);
-        unsigned long long h[3];
+        unsigned long long h[4];
         int32_t nit = 0;
         GEER_CUDA(cudaMemcpyAsync(h, c->d_counters, sizeof(h), cudaMemcpyDeviceToHost, st));
         GEER_CUDA(cudaMemcpyAsync(&nit, c->n_items.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -522,6 +526,7 @@ int geer_frame_stats(geer_ctx *c, geer_stats *out) {
         out->kappa_rechecks = (int64_t)h[0];
         out->evaluated_pairs = (int64_t)h[1];
         out->fixup_pixels = (int64_t)h[2];
+        out->warp_entries = (int64_t)h[3];
         out->n_work_items = nit;
     }
     if (c->have_frame && c->scene.n > 0) {

@@ -27,7 +27,8 @@ constexpr int kBwdBatch = 32;        // entries per backward reduction batch
 struct FrameConst {
     int width, height, model, tile_px;
     int n_x, n_y, n_tiles, n_bands;
-    int cutoff, pad_;
+    int cutoff;
+    int cull;  // per-warp PBF culling of raster entries (support cutoff on and not disabled)
     double R[9], t[3], origin[3];
     double fov_x, fov_y, fx, fy, cx, cy, k[4];
     double lam, lam2;

@@ -352,10 +352,16 @@ __device__ __forceinline__ void cswap(double &a, double &b) {
     }
 }
 
+// Absolute mirror-space margin of the raster's per-warp PBF culling bounds: far above the fp64
+// rounding of the interval endpoints, far below a pixel (1920 px over 180 deg: ~8e-4 per pixel).
+constexpr double kCullMargin = 1e-6;
+
 // association.py:189-217 + :373-388 + union (:435-446): merged disjoint tile-index ranges of one axis.
-// Returns the tile count; ranges packed lo | hi << 16 (empty slots = 0).
+// Returns the tile count; ranges packed lo | hi << 16 (empty slots = 0).  hull_lo/hull_hi: fp32
+// bounds (rounded outward, widened by kCullMargin) of the arcs' union restricted to the open front
+// half |m| < 1, where every camera-frame ray with z > 0 has its mirror coordinate; empty -> (+inf, -inf).
 __device__ int axis_tiles(double t_aa, double t_a2, double t22, double r0, double r1, const double *edges, int n_edges,
-                          uint32_t out[3]) {
+                          uint32_t out[3], float &hull_lo, float &hull_hi) {
     double c[4];
     mirror_candidates(r0, c[0], c[1]);
     mirror_candidates(r1, c[2], c[3]);
@@ -386,6 +392,18 @@ __device__ int axis_tiles(double t_aa, double t_a2, double t22, double r0, doubl
         ilo[0] = c[0]; ihi[0] = c[1];
         ilo[1] = c[2]; ihi[1] = c[3];
         ni = 2;
+    }
+    {
+        double hl = INFINITY, hh = -INFINITY;
+        for (int k = 0; k < ni; ++k) {
+            const double lo = ilo[k] > -1.0 ? ilo[k] : -1.0, hi = ihi[k] < 1.0 ? ihi[k] : 1.0;
+            if (lo <= hi) {
+                hl = lo < hl ? lo : hl;
+                hh = hi > hh ? hi : hh;
+            }
+        }
+        hull_lo = hl <= hh ? __double2float_rd(hl - kCullMargin) : INFINITY;
+        hull_hi = hl <= hh ? __double2float_ru(hh + kCullMargin) : -INFINITY;
     }
     const double wlo = edges[0], whi = edges[n_edges - 1];
     // tile-index range of each interval after window clipping (association.py:373-388); empty -> [BIG, BIG)
@@ -489,7 +507,8 @@ __device__ bool make_payload(const double W[9], const double ou[3], const double
 __global__ void __launch_bounds__(128) k_associate(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x,
                                                    const double *__restrict__ medges_y, uint32_t *__restrict__ depth_key,
                                                    int64_t *__restrict__ count, AxisRanges *__restrict__ ranges,
-                                                   uint8_t *__restrict__ flags, double *__restrict__ mu_out,
+                                                   uint8_t *__restrict__ flags, float4 *__restrict__ box,
+                                                   double *__restrict__ mu_out,
                                                    double *__restrict__ depth_out, int *__restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *sex = reinterpret_cast<double *>(smem_raw);
@@ -532,6 +551,8 @@ __global__ void __launch_bounds__(128) k_associate(FrameConst fc, geer_scene sc,
     int64_t n_ent = 0;
     AxisRanges ar;
     for (int i = 0; i < 3; ++i) ar.x[i] = ar.y[i] = 0;
+    // raster culling bounds in mirror space (x_lo, x_hi, y_lo, y_hi); clamped: everything
+    float4 bx = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
     // association.py:417-419 near cull
     if (depth >= kNearLimit) {
         // association.py:154-160 symmetric + positive-definite (Cholesky pivots)
@@ -593,8 +614,8 @@ __global__ void __launch_bounds__(128) k_associate(FrameConst fc, geer_scene sc,
                     ar.y[0] = (uint32_t)fc.n_y << 16;
                     n_ent = (int64_t)fc.n_x * fc.n_y;
                 } else {
-                    const int cx = axis_tiles(t00, t02, t22, rt0, rt1, sex, fc.n_x + 1, ar.x);
-                    const int cy = axis_tiles(t11, t12, t22, rp0, rp1, sey, fc.n_y + 1, ar.y);
+                    const int cx = axis_tiles(t00, t02, t22, rt0, rt1, sex, fc.n_x + 1, ar.x, bx.x, bx.y);
+                    const int cy = axis_tiles(t11, t12, t22, rp0, rp1, sey, fc.n_y + 1, ar.y, bx.z, bx.w);
                     n_ent = (int64_t)cx * cy;
                 }
             }
@@ -602,6 +623,7 @@ __global__ void __launch_bounds__(128) k_associate(FrameConst fc, geer_scene sc,
     }
     count[g] = n_ent;
     ranges[g] = ar;
+    box[g] = bx;
     flags[g] = fl;
     // association.py:335-340 key bits (depth > 0): f32 bits | 0x80000000; non-emitting last
     const uint32_t kb = __float_as_uint((float)depth) | 0x80000000u;
@@ -614,7 +636,8 @@ __global__ void __launch_bounds__(128) k_associate(FrameConst fc, geer_scene sc,
 template <int NB>
 __global__ void __launch_bounds__(128) k_payload(FrameConst fc, geer_scene sc, Payload *__restrict__ payload,
                                                  GradPayload *__restrict__ gpayload, uint8_t *__restrict__ flags) {
-    __shared__ __align__(16) float ssh[128 * NB * 3];
+    // SH staging, then payload staging (176 B = 44 floats per Gaussian)
+    __shared__ __align__(16) float ssh[128 * (NB * 3 > 44 ? NB * 3 : 44)];
     const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
     const int cnt_b = (int)lmin((int64_t)blockDim.x, sc.n - g0);
     {
@@ -630,8 +653,8 @@ __global__ void __launch_bounds__(128) k_payload(FrameConst fc, geer_scene sc, P
         }
     }
     __syncthreads();
-    const int64_t g = g0 + threadIdx.x;
-    if (g >= sc.n) return;
+    const bool live = threadIdx.x < cnt_b;  // threads past the end compute a copy of row 0 (not stored)
+    const int64_t g = g0 + (live ? threadIdx.x : 0);
     const double mean[3] = {sc.means[g * 3 + 0], sc.means[g * 3 + 1], sc.means[g * 3 + 2]};
     const float4 q4v = *reinterpret_cast<const float4 *>(sc.quats + g * 4);
     const float q4[4] = {q4v.x, q4v.y, q4v.z, q4v.w};
@@ -655,7 +678,7 @@ __global__ void __launch_bounds__(128) k_payload(FrameConst fc, geer_scene sc, P
     const double ivn = 1.0 / (vn > 1e-12 ? vn : 1e-12);
     double basis[16];
     sh_basis(vd[0] * ivn, vd[1] * ivn, vd[2] * ivn, basis);
-    const float *shg = ssh + threadIdx.x * NB * 3;
+    const float *shg = ssh + (live ? threadIdx.x : 0) * NB * 3;
     double rgb[3];
     uint8_t gate = 0;
 #pragma unroll
@@ -671,13 +694,42 @@ __global__ void __launch_bounds__(128) k_payload(FrameConst fc, geer_scene sc, P
     Payload pl;
     GradPayload gp;
     const bool mode1 = make_payload(W, ou, rgb, sigma, smax / smin, fc.lam, pl, gp);
-    payload[g] = pl;
-    gpayload[g] = gp;
     // flags: bit0 keep, bit1 clamped (K1a), bits3-5 SH clamp gate per channel, bit6 payload mode 1
-    flags[g] = (uint8_t)(flags[g] | (gate << 3) | (mode1 ? 64 : 0));
+    if (live) flags[g] = (uint8_t)(flags[g] | (gate << 3) | (mode1 ? 64 : 0));
+    // coalesced stores: stage the block's 128-B payloads and 48-B grad payloads in shared memory
+    // (reusing the SH staging buffer) and write them out as contiguous float4 runs
+    float4 *sp = reinterpret_cast<float4 *>(ssh);
+    float4 *sg = sp + 128 * (sizeof(Payload) / 16);
+    __syncthreads();  // every thread is done reading its SH coefficients
+    const float4 *plv = reinterpret_cast<const float4 *>(&pl);
+    const float4 *gpv = reinterpret_cast<const float4 *>(&gp);
+#pragma unroll
+    for (int k = 0; k < (int)(sizeof(Payload) / 16); ++k) sp[threadIdx.x * (sizeof(Payload) / 16) + k] = plv[k];
+#pragma unroll
+    for (int k = 0; k < (int)(sizeof(GradPayload) / 16); ++k) sg[threadIdx.x * (sizeof(GradPayload) / 16) + k] = gpv[k];
+    __syncthreads();
+    float4 *dp = reinterpret_cast<float4 *>(payload + g0);
+    float4 *dg = reinterpret_cast<float4 *>(gpayload + g0);
+    for (int i = threadIdx.x; i < cnt_b * (int)(sizeof(Payload) / 16); i += blockDim.x) dp[i] = sp[i];
+    for (int i = threadIdx.x; i < cnt_b * (int)(sizeof(GradPayload) / 16); i += blockDim.x) dg[i] = sg[i];
 }
 
 // ---------------------------------------------------------------- K7
+
+// Coalesced block store of per-Gaussian rows: thread i holds row i (width values) of this block's
+// cnt rows; rows go through shared memory so the global stores are contiguous (the SoA gradient
+// arrays have 1..48 values per Gaussian, which would otherwise be strided partial-sector writes).
+template <typename T, int W>
+__device__ __forceinline__ void store_rows(float *sm, const float (&v)[W], int cnt, T *dst, bool acc) {
+    __syncthreads();  // previous round's readers are done
+#pragma unroll
+    for (int k = 0; k < W; ++k) sm[threadIdx.x * (W | 1) + k] = v[k];  // odd stride: no bank conflicts
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt * W; i += blockDim.x) {
+        const float x = sm[(i / W) * (W | 1) + i % W];
+        dst[i] = acc ? (T)((double)dst[i] + (double)x) : (T)x;
+    }
+}
 
 // accum layout per Gaussian (16 f32): dW_rc (9, row-major), sum dl/do_u (3), sum dsigma, sum dcol (3).
 // fp32 arithmetic (the accumulators are fp32 already); renderer.py:304-307, 204-231, 332.
@@ -685,8 +737,10 @@ template <typename T, int NB>
 __global__ void __launch_bounds__(128) k_finalize(FrameConst fc, geer_scene sc, const float4 *__restrict__ accum,
                                                   const uint8_t *__restrict__ flags, T *dmeans, T *dlog_scales,
                                                   T *dquats, T *dopac, T *dsh, int accumulate) {
-    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (g >= sc.n) return;
+    __shared__ float sm[128 * ((NB * 3 | 1) > 5 ? (NB * 3 | 1) : 5)];  // widest row: max(NB * 3, 4), odd stride
+    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
+    const int cnt = (int)lmin((int64_t)blockDim.x, sc.n - g0);
+    const int64_t g = g0 + (threadIdx.x < cnt ? threadIdx.x : 0);
     float a[16];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -751,20 +805,18 @@ __global__ void __launch_bounds__(128) k_finalize(FrameConst fc, geer_scene sc, 
         dsig = dsig * sg * (1.0f - sg);
     }
     const bool acc = accumulate & GEER_ACCUMULATE;
-    auto put = [&](T *p, int64_t idx, float v) { p[idx] = acc ? (T)((double)p[idx] + (double)v) : (T)v; };
-#pragma unroll
-    for (int c = 0; c < 3; ++c) put(dmeans, g * 3 + c, dmu[c]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) put(dlog_scales, g * 3 + c, dls[c]);
-    put(dquats, g * 4 + 0, (dqr0 - dot * r) * iqn);
-    put(dquats, g * 4 + 1, (dqr1 - dot * i) * iqn);
-    put(dquats, g * 4 + 2, (dqr2 - dot * j) * iqn);
-    put(dquats, g * 4 + 3, (dqr3 - dot * k) * iqn);
-    put(dopac, g, dsig);
+    const float dq[4] = {(dqr0 - dot * r) * iqn, (dqr1 - dot * i) * iqn, (dqr2 - dot * j) * iqn, (dqr3 - dot * k) * iqn};
+    const float dop[1] = {dsig};
+    float dshv[NB * 3];
 #pragma unroll
     for (int b = 0; b < NB; ++b)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) put(dsh, (g * NB + b) * 3 + c, (float)basis[b] * dcol[c]);
+        for (int c = 0; c < 3; ++c) dshv[b * 3 + c] = (float)basis[b] * dcol[c];
+    store_rows<T, 3>(sm, dmu, cnt, dmeans + g0 * 3, acc);
+    store_rows<T, 3>(sm, dls, cnt, dlog_scales + g0 * 3, acc);
+    store_rows<T, 4>(sm, dq, cnt, dquats + g0 * 4, acc);
+    store_rows<T, 1>(sm, dop, cnt, dopac + g0, acc);
+    store_rows<T, NB * 3>(sm, dshv, cnt, dsh + g0 * NB * 3, acc);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -812,11 +864,11 @@ size_t preprocess_smem(const FrameConst &fc) { return sizeof(double) * (fc.n_x +
 
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
                        Payload *payload, GradPayload *gpayload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges,
-                       uint8_t *flags, double *mu_out, double *depth_out, int *err, cudaStream_t st) {
+                       uint8_t *flags, float4 *box, double *mu_out, double *depth_out, int *err, cudaStream_t st) {
     if (sc.n == 0) return;
     const int blocks = (int)((sc.n + 127) / 128);
     k_associate<<<blocks, 128, preprocess_smem(fc), st>>>(fc, sc, medges_x, medges_y, depth_key, count, ranges, flags,
-                                                          mu_out, depth_out, err);
+                                                          box, mu_out, depth_out, err);
     switch (sc.n_bands) {
 #define GEER_NB_CASE(NB) \
     case NB: k_payload<NB><<<blocks, 128, 0, st>>>(fc, sc, payload, gpayload, flags); break;

@@ -24,7 +24,7 @@ void launch_item_fill(int n_tiles, const int32_t *tile_off, const int32_t *item_
 size_t preprocess_smem(const FrameConst &fc);
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
                        Payload *payload, GradPayload *gpayload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges, uint8_t *flags,
-                       double *mu_out, double *depth_out, int *err, cudaStream_t st);
+                       float4 *box, double *mu_out, double *depth_out, int *err, cudaStream_t st);
 template <typename T>
 void launch_finalize(const FrameConst &fc, const geer_scene &sc, const float4 *accum, const uint8_t *flags, T *dmeans,
                      T *dlog_scales, T *dquats, T *dopac, T *dsh, int accumulate, cudaStream_t st);
@@ -43,8 +43,10 @@ void sort_depth(void *temp, size_t temp_bytes, const uint32_t *keys_in, uint32_t
 void gather_counts(const int32_t *sorted_gid, const int64_t *count, int64_t *cnt_sorted, int64_t n, cudaStream_t st);
 void inclusive_scan_i64(void *temp, size_t temp_bytes, const int64_t *in, int64_t *out, int64_t n, cudaStream_t st);
 void exclusive_scan_i32(void *temp, size_t temp_bytes, const int32_t *in, int32_t *out, int64_t n, cudaStream_t st);
+int64_t emit_blocks(int64_t n_entries);
 void emit_entries(const int64_t *offs, const int32_t *sorted_gid, const AxisRanges *ranges, int n_x,
-                  int64_t n_entries, int64_t n, uint32_t *tile_keys, uint32_t *gids, cudaStream_t st);
+                  int64_t n_entries, int64_t n, int32_t *block_rank, uint32_t *tile_keys, uint32_t *gids,
+                  cudaStream_t st);
 void sort_tiles(void *temp, size_t temp_bytes, const uint32_t *keys_in, uint32_t *keys_out, const uint32_t *vals_in,
                 uint32_t *vals_out, int64_t n, int n_bits, cudaStream_t st);
 void sort_pixels(void *temp, size_t temp_bytes, const int32_t *keys_in, int32_t *keys_out, const int32_t *vals_in,
@@ -56,12 +58,12 @@ void tile_ranges(const uint32_t *sorted_tiles, int64_t n_entries, int n_tiles, i
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    const uint8_t *flags, float *color, float *remaining, int32_t *count, int32_t *n_eval,
+                    const uint8_t *flags, const float4 *box, float *color, float *remaining, int32_t *count, int32_t *n_eval,
                     unsigned long long *counters, int32_t *fixup_list, cudaStream_t st);
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                      const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                     const GradPayload *gpayload, const uint8_t *flags, const float *remaining,
+                     const GradPayload *gpayload, const uint8_t *flags, const float4 *box, const float *remaining,
                      const int32_t *n_eval, const float *dl_dimage, float *accum, cudaStream_t st);
 void launch_sum_i32(const int32_t *v, int64_t n, unsigned long long *out, cudaStream_t st);
 void launch_convert_f64_f32(const double *in, float *out, int64_t n, cudaStream_t st);

@@ -211,7 +211,10 @@ __device__ __forceinline__ float t_rel_bound(float kap) { return 6e-7f + 3e-7f *
 // consumer warp is done.
 
 constexpr int kConsumerWarps = kRasterThreads / 32;  // 8
-constexpr int kStages = 4;
+#ifndef GEER_STAGES
+#define GEER_STAGES 4
+#endif
+constexpr int kStages = GEER_STAGES;
 constexpr int kStageEntries = 32;  // one entry per producer lane
 constexpr int kPipeThreads = kRasterThreads + 32;
 #ifndef FWD_MIN_BLOCKS
@@ -220,11 +223,15 @@ constexpr int kPipeThreads = kRasterThreads + 32;
 
 template <bool kGrad>
 struct __align__(16) PipeSmem {
-    Payload ring[kStages][kStageEntries];
+    Payload ring[kStages][kStageEntries + 1];  // slot kStageEntries: a null entry (t = 0 for every ray)
     GradPayload gring[kGrad ? kStages : 1][kStageEntries];  // backward only
     uint32_t gid[kStages][kStageEntries];
     int count[kStages];  // entries in the stage; 0 = end of stream
     int mode1[kStages];  // 1 if any entry of the stage carries a mode-1 (cross-product) payload
+    uint32_t mask[kStages][kConsumerWarps];  // per consumer warp: entries of the stage its patch may see
+    uint8_t idx[kStages][kConsumerWarps][kStageEntries + 4];  // the same entries as a list, padded with null slots
+    int cnt[kStages][kConsumerWarps];                          // entries in that list
+    float4 patch[kConsumerWarps];            // per consumer warp: mirror-space bounds of its pixels
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     int done_warps;
@@ -283,6 +290,13 @@ __device__ __forceinline__ void pipe_init(Smem &S) {
         }
         S.done_warps = 0;
         S.stop = 0;
+        // null entry: |d_u|^2 = |d|^2, |m|^2 = 0, sigma = 0  ->  kappa = 0, t = 0 exactly (a no-op)
+        for (int s = 0; s < kStages; ++s) {
+            Payload &z = S.ring[s][kStageEntries];
+            for (int i = 0; i < 12; ++i) z.q[i] = i < 3 ? 1.0 : 0.0;
+            z.col = make_float4(0.f, 0.f, 0.f, 0.f);
+            z.ext = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -294,8 +308,8 @@ template <bool kReverse, class Smem>
 __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict__ order,
                                              const Payload *__restrict__ payload,
                                              const GradPayload *__restrict__ gpayload,
-                                             const uint8_t *__restrict__ flags, int first, int n_total,
-                                             bool stop_when_done) {
+                                             const uint8_t *__restrict__ flags, const float4 *__restrict__ box,
+                                             bool cull, int first, int n_total, bool stop_when_done) {
     const unsigned per_entry = (unsigned)(sizeof(Payload) + (gpayload ? sizeof(GradPayload) : 0));
     const int lane = threadIdx.x & 31;
     unsigned phase = 0;
@@ -319,12 +333,31 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
         const int base = kReverse ? first + n_total - done - n : first + done;
         uint32_t g = 0;
         bool m1 = false;
+        float4 bx = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
         if (lane < n) {
             g = __ldg(order + base + lane);
             S.gid[s][lane] = g;
             m1 = (__ldg(flags + g) >> 6) & 1;
+            if (cull) bx = __ldg(box + g);
         }
         const bool any_m1 = __any_sync(0xffffffffu, m1);
+        // Per-warp PBF culling: a pixel ray can have kappa <= lam^2 only if its camera-frame mirror
+        // coordinates lie inside the Gaussian's PBF intervals (association.py:189-217); entries whose
+        // bounds miss a warp's whole pixel patch contribute exactly nothing to it (t = 0).
+        uint32_t my_mask = 0;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w) {
+            const float4 P = S.patch[w];
+            const bool ov = lane < n && !(bx.y < P.x || bx.x > P.y || bx.w < P.z || bx.z > P.w);
+            const uint32_t m = __ballot_sync(0xffffffffu, ov);
+            if (lane == w) my_mask = m;
+            const int c = __popc(m);
+            if (ov) S.idx[s][w][__popc(m & ((1u << lane) - 1u))] = (uint8_t)lane;
+            if (lane < 4) S.idx[s][w][c + lane] = (uint8_t)kStageEntries;  // pad to a multiple of 4
+            if (lane == 0) S.cnt[s][w] = c;
+        }
+        if (lane < kConsumerWarps) S.mask[s][lane] = my_mask;
+        __syncwarp();
         if (lane == 0) {
             S.count[s] = n;
             S.mode1[s] = any_m1 ? 1 : 0;
@@ -380,51 +413,206 @@ struct PixelState {
     float r;     // remaining transmittance while the pixel is live, 0 once it stopped
     float rfin;  // remaining transmittance at the stop
     float err;   // bound on |r_fp32 - r_fp64|
+    float efin;  // err at a threshold stop (-1: none)
     int cnt, ne, border;
 };
 
-// One front-to-back step (renderer.py:111-117).  The alive test (:113) is made against the fp64
-// remaining, known to lie in [r - err, r + err]; a pixel stops either surely opaque, or
-// "borderline" (test or cutoff too close to call) and is then redone in fp64 by k_fixup.
-// Stopped pixels carry r = 0, which turns every later update into a no-op without branches.
-__device__ __forceinline__ void pixel_update(PixelState &ps, const PairT &e, const float4 &col, bool unc) {
-    const bool live = ps.r > 0.0f;
-    const bool sure_alive = __fsub_rn(ps.r, ps.err) >= 1.00001e-4f;
-    const bool stop = live & (!sure_alive | unc);
-    ps.border |= (stop & (unc | (__fadd_rn(ps.r, ps.err) >= 0.99999e-4f))) ? 1 : 0;
-    ps.rfin = stop ? ps.r : ps.rfin;
-    ps.r = stop ? 0.0f : ps.r;
-    const float w = __fmul_rn(ps.r, e.t);
-    const float omt = __fsub_rn(1.0f, e.t);
+// One front-to-back step (renderer.py:111-117) of a live pixel, followed by the alive test of the
+// NEXT entry (renderer.py:113: remaining >= 1e-4), made here against the fp64 remaining known to lie
+// in [r - err, r + err].  A pixel stops either surely opaque or "borderline" (test, or this entry's
+// cutoff, too close to call: redone in fp64 by k_fixup; see pixel_border).  Stopped pixels carry
+// r = 0, which turns every later update into a no-op without branches, and an entry with t = 0
+// changes nothing, so skipping it (PBF culling, null padding entries) is exact.
+__device__ __forceinline__ void pixel_update(PixelState &ps, float kap, float t, const float4 &col, bool unc, int jne) {
+    if (unc) {  // rare: this entry's cutoff is undecidable in fp64 -> whole pixel to the fp64 fix-up
+        ps.border |= ps.r > 0.0f ? 1 : 0;
+        ps.rfin = ps.r > 0.0f ? ps.r : ps.rfin;
+        ps.r = 0.0f;
+    }
+    const float w = __fmul_rn(ps.r, t);
+    const float omt = __fsub_rn(1.0f, t);
     ps.cr = __fmaf_rn(w, col.x, ps.cr);
     ps.cg = __fmaf_rn(w, col.y, ps.cg);
     ps.cb = __fmaf_rn(w, col.z, ps.cb);
-    // |d r'| <= |d r| (1 - t) + r |d t| + rounding,  |d t| <= t * t_rel_bound
-    ps.err = __fmaf_rn(ps.r, 1.2e-7f, __fmaf_rn(ps.err, omt, __fmul_rn(w, t_rel_bound(e.kap))));
-    ps.ne += ps.r > 0.0f ? 1 : 0;
+    // |d r'| <= |d r| (1 - t) + r |d t| + rounding (none when t = 0),  |d t| <= t * t_rel_bound
+    ps.err = __fmaf_rn(ps.err, omt, __fmaf_rn(w, t_rel_bound(kap), w > 0.0f ? __fmul_rn(ps.r, 1.2e-7f) : 0.0f));
     ps.cnt += w > 0.0f ? 1 : 0;
     ps.r = __fmul_rn(ps.r, omt);
+    const bool stop = (ps.r > 0.0f) & (__fsub_rn(ps.r, ps.err) < 1.00001e-4f);
+    ps.rfin = stop ? ps.r : ps.rfin;
+    ps.efin = stop ? ps.err : ps.efin;
+    ps.ne = stop ? jne : ps.ne;  // alive entries: this one and every one before it (renderer.py:113)
+    ps.r = stop ? 0.0f : ps.r;
 }
 
-// One stage of entries for one consumer warp.  kGeneric: the stage holds mode-1 payloads, so the
-// payload mode is decided per entry; otherwise every entry is a mode-0 quadratic form.
-template <bool kGeneric>
-__device__ __forceinline__ void consume_stage(const Payload *ring, int n, const Ray64 &R, const double *dray,
-                                              const FrameConst &fc, PixelState &ps, int &rechecks) {
-    for (int j0 = 0; j0 < n; j0 += 4) {
-        if (!__any_sync(0xffffffffu, ps.r > 0.0f)) break;
-        const int j1 = min(j0 + 4, n);
-        for (int j = j0; j < j1; ++j) {
-            const Payload &P = ring[j];
-            const bool m1 = kGeneric ? __any_sync(0xffffffffu, P.col.w < 0.0f) : false;
+// A pixel that stopped on the threshold is borderline when the fp64 remaining could still be >= 1e-4.
+__device__ __forceinline__ bool pixel_border(const PixelState &ps) {
+    return ps.border || (ps.r == 0.0f && ps.efin >= 0.0f && __fadd_rn(ps.rfin, ps.efin) >= 0.99999e-4f);
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double2 lds_d2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+
+// Mode-0 norms from a payload at shared address pa (same arithmetic as norms64).
+__device__ __forceinline__ void norms64_smem(uint32_t pa, const Ray64 &R, double &dd, double &mm) {
+    const double2 a0 = lds_d2(pa + 0), a1 = lds_d2(pa + 16), a2 = lds_d2(pa + 32);
+    const double2 b0 = lds_d2(pa + 48), b1 = lds_d2(pa + 64), b2 = lds_d2(pa + 80);
+    dd = (fma(a0.y, R.m11, a0.x * R.m00) + fma(a1.y, R.m01, a1.x * R.m22)) + fma(a2.y, R.m12, a2.x * R.m02);
+    mm = (fma(b0.y, R.m11, b0.x * R.m00) + fma(b1.y, R.m01, b1.x * R.m22)) + fma(b2.y, R.m12, b2.x * R.m02);
+}
+
+constexpr uint32_t kColOff = 96;  // offsetof(Payload, col)
+constexpr uint32_t kExtOff = 112; // offsetof(Payload, ext)
+
+// The entries of one stage that this warp's PBF mask keeps, front to back, four at a time (the list
+// is padded with null entries, which are exact no-ops).  Culled entries change nothing; the alive
+// count is recorded when a pixel stops (base: entries of the tile before this stage).
+//
+// Stage of mode-1 payloads (rare: tiny, far or very anisotropic Gaussians): the payload mode is
+// decided per entry and each entry runs the reference formulation via finish_t.
+__device__ __forceinline__ void consume_stage_generic(PipeSmem<false> &S, int s, int warp, int base, const Ray64 &R,
+                                                      const double *dray, const FrameConst &fc, PixelState &ps,
+                                                      int &rechecks, int &went) {
+    const int cnt = S.cnt[s][warp];
+    int k0 = 0;
+    for (; k0 < cnt; k0 += 4) {
+        if (k0 > 0 && !__any_sync(0xffffffffu, ps.r > 0.0f)) break;  // warp opaque
+        const uint32_t q = *reinterpret_cast<const uint32_t *>(&S.idx[s][warp][k0]);
+#pragma unroll 1
+        for (int u = 0; u < 4; ++u) {
+            const int j = (q >> (8 * u)) & 0xFF;
+            const Payload &P = S.ring[s][j];
+            const bool m1 = __any_sync(0xffffffffu, P.col.w < 0.0f);
             double dd, mm;
             norms64(P, R, dray, m1, dd, mm);
             PairT e;
             const bool unc = finish_t(dd, mm, P, m1, fc, e, rechecks);
-            pixel_update(ps, e, P.col, unc);
+            pixel_update(ps, e.kap, e.t, P.col, unc, base + j + 1);
         }
     }
+    went += k0 < cnt ? k0 : cnt;
 }
+
+// Stage of mode-0 payloads (the common case): four entries' t first (independent work, explicit
+// shared loads), one warp vote for the rare fp64 cutoff re-decisions, then the four serial pixel
+// updates.  t is bit-identical to finish_t's (the backward recomputes it with eval_t).
+#ifndef GEER_FWD_GROUP
+#define GEER_FWD_GROUP 2
+#endif
+constexpr int kFwdGroup = GEER_FWD_GROUP;  // entries evaluated together (ILP vs registers)
+
+template <bool kCutoff>
+__device__ __forceinline__ void consume_stage_fast(PipeSmem<false> &S, int s, int warp, int base, const Ray64 &R,
+                                                   const FrameConst &fc, PixelState &ps, int &rechecks, int &went) {
+    const int cnt = S.cnt[s][warp];
+    const uint32_t rb = smem_u32(&S.ring[s][0]);
+    const uint32_t ib = smem_u32(&S.idx[s][warp][0]);
+    int k0 = 0;
+    for (; k0 < cnt; k0 += kFwdGroup) {
+        if (k0 > 0 && !__any_sync(0xffffffffu, ps.r > 0.0f)) break;  // warp opaque
+        const uint32_t q = kFwdGroup == 4 ? lds_u32(ib + k0) : (lds_u32(ib + (k0 & ~3)) >> (8 * (k0 & 3)));
+        float kap[kFwdGroup], t[kFwdGroup];
+        uint32_t pa[kFwdGroup];
+        bool near[kFwdGroup], unc[kFwdGroup];
+        bool any_near = false;
+#pragma unroll
+        for (int u = 0; u < kFwdGroup; ++u) {
+            pa[u] = rb + ((q >> (8 * u)) & 0xFF) * (uint32_t)sizeof(Payload);
+            double dd, mm;
+            norms64_smem(pa[u], R, dd, mm);
+            const float sw = lds_f32(pa[u] + kColOff + 12);
+            kap[u] = __fmul_rn((float)mm, rcp_approx((float)dd));
+            float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u], -0.72134752044448170f)));
+            near[u] = false;
+            unc[u] = false;
+            if (kCutoff) {
+                near[u] = fabsf(__fsub_rn(kap[u], fc.lam2f)) <= fc.cutoff_tol;
+                any_near |= near[u];
+                uu = kap[u] <= fc.lam2f ? uu : 0.0f;
+            }
+            t[u] = fminf(uu, kMaxBlendTF);
+        }
+        if (kCutoff && __any_sync(0xffffffffu, any_near)) {
+#pragma unroll
+            for (int u = 0; u < kFwdGroup; ++u) {  // (fully unrolled: the arrays stay in registers)
+                if (!near[u]) continue;
+                double dd, mm;
+                norms64_smem(pa[u], R, dd, mm);
+                const double k64 = mm / dd;
+                const float sw = lds_f32(pa[u] + kColOff + 12);
+                const float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u], -0.72134752044448170f)));
+                t[u] = k64 <= fc.lam2 ? fminf(uu, kMaxBlendTF) : 0.0f;
+                unc[u] = fabs(k64 - fc.lam2) <= (double)lds_f32(pa[u] + kExtOff);
+                ++rechecks;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kFwdGroup; ++u) {
+            const float4 col = lds_f4(pa[u] + kColOff);
+            pixel_update(ps, kap[u], t[u], col, unc[u], base + (int)((pa[u] - rb) / (uint32_t)sizeof(Payload)) + 1);
+        }
+    }
+    went += k0 < cnt ? k0 : cnt;
+}
+
+// Camera-frame mirror coordinates of a world ray (the CSF/PBF space of association.py:91-126):
+// m = tan(angle / 2) of its (x, z) and (y, z) projections, outward-rounded to fp32.  Rays with
+// z <= 0 on an axis leave that axis unbounded (no culling there).
+__device__ __forceinline__ float4 ray_mirror_bounds(const FrameConst &fc, const double d[3]) {
+    double c[3];
+    for (int i = 0; i < 3; ++i) c[i] = fma(fc.R[i * 3 + 2], d[2], fma(fc.R[i * 3 + 1], d[1], fc.R[i * 3 + 0] * d[0]));
+    float4 b = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
+    if (c[2] > 0.0) {
+        const double mx = c[0] / (sqrt(c[0] * c[0] + c[2] * c[2]) + c[2]);
+        const double my = c[1] / (sqrt(c[1] * c[1] + c[2] * c[2]) + c[2]);
+        b = make_float4(__double2float_rd(mx), __double2float_ru(mx), __double2float_rd(my), __double2float_ru(my));
+    }
+    return b;
+}
+
+// Warp-wide union of the lanes' mirror bounds (lanes without a pixel contribute nothing); lane 0
+// stores it as the warp's patch for the producer's culling masks.
+__device__ __forceinline__ void publish_patch(float4 *patch, int warp, int lane, bool valid, float4 b) {
+    if (!valid) b = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        b.x = fminf(b.x, __shfl_xor_sync(0xffffffffu, b.x, o));
+        b.y = fmaxf(b.y, __shfl_xor_sync(0xffffffffu, b.y, o));
+        b.z = fminf(b.z, __shfl_xor_sync(0xffffffffu, b.z, o));
+        b.w = fmaxf(b.w, __shfl_xor_sync(0xffffffffu, b.w, o));
+    }
+    if (lane == 0 && warp < kConsumerWarps) patch[warp] = b;
+}
+
+#ifdef GEER_CTA_TIMING
+// Tuning instrumentation (build with -DGEER_CTA_TIMING): per raster CTA start / end %globaltimer
+// (ns), SM id and warp-entries, read back by geer_debug_cta_times (scripts/cta_timing.py).
+__device__ unsigned long long g_cta_t0[1 << 16], g_cta_t1[1 << 16];
+__device__ int g_cta_sm[1 << 16], g_cta_went[1 << 16];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 
 template <bool kBEAP>
 __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
@@ -432,44 +620,56 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
               const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
               const double2 *__restrict__ row_sc, const double *__restrict__ dir64, const int32_t *__restrict__ ranges,
               const uint32_t *__restrict__ order, const Payload *__restrict__ payload,
-              const uint8_t *__restrict__ flags, float *__restrict__ color, float *__restrict__ remaining,
-              int32_t *__restrict__ count, int32_t *__restrict__ n_eval, unsigned long long *__restrict__ counters,
-              int32_t *__restrict__ fixup_list) {
+              const uint8_t *__restrict__ flags, const float4 *__restrict__ box, float *__restrict__ color,
+              float *__restrict__ remaining, int32_t *__restrict__ count, int32_t *__restrict__ n_eval,
+              unsigned long long *__restrict__ counters, int32_t *__restrict__ fixup_list) {
     __shared__ PipeSmem<false> S;
     __shared__ double sray[kRasterThreads][3];  // fp64 pixel rays (mode-1 payloads only)
     if ((int)blockIdx.x >= *n_items) return;
     const int4 it = items[blockIdx.x];
     const int e0 = ranges[it.x], e1 = ranges[it.x + 1];
-    pipe_init(S);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp == kConsumerWarps) {
-        pipe_produce<false>(S, order, payload, nullptr, flags, e0, e1 - e0, true);
-        return;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef GEER_CTA_TIMING
+    if (tid == 0 && blockIdx.x < (1u << 16)) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        g_cta_t0[blockIdx.x] = gtimer();
+        g_cta_sm[blockIdx.x] = (int)smid;
+        g_cta_t1[blockIdx.x] = 0;
+        g_cta_went[blockIdx.x] = 0;
     }
-    const int tid = threadIdx.x;
+#endif
     const bool valid = tid < it.z;
     const int p = valid ? pix_list[it.y + tid] : 0;
     double d64[3] = {0.0, 0.0, 1.0};
     if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
+    if (warp < kConsumerWarps) publish_patch(S.patch, warp, lane, valid, ray_mirror_bounds(fc, d64));
+    pipe_init(S);  // (its __syncthreads also publishes the patches)
+    if (warp == kConsumerWarps) {
+        pipe_produce<false>(S, order, payload, nullptr, flags, box, fc.cull != 0, e0, e1 - e0, true);
+        return;
+    }
     const Ray64 R = make_ray(d64);
     sray[tid][0] = d64[0];
     sray[tid][1] = d64[1];
     sray[tid][2] = d64[2];
-    PixelState ps{0.f, 0.f, 0.f, valid ? 1.0f : 0.0f, 1.0f, 0.f, 0, 0, 0};
-    int rechecks = 0;
+    PixelState ps{0.f, 0.f, 0.f, valid ? 1.0f : 0.0f, 1.0f, 0.f, -1.0f, 0, 0, 0};
+    int rechecks = 0, went = 0;
     bool warp_live = __any_sync(0xffffffffu, valid);
     if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
     unsigned phase = 0;
-    int s = 0;
+    int s = 0, base = 0;
     for (;;) {
         mbar_wait(&S.full[s], phase);
         const int n = S.count[s];
         if (n == 0) break;
         if (warp_live) {
-            if (!S.mode1[s])
-                consume_stage<false>(S.ring[s], n, R, sray[tid], fc, ps, rechecks);
+            if (S.mode1[s])
+                consume_stage_generic(S, s, warp, base, R, sray[tid], fc, ps, rechecks, went);
+            else if (fc.cutoff)
+                consume_stage_fast<true>(S, s, warp, base, R, fc, ps, rechecks, went);
             else
-                consume_stage<true>(S.ring[s], n, R, sray[tid], fc, ps, rechecks);
+                consume_stage_fast<false>(S, s, warp, base, R, fc, ps, rechecks, went);
             warp_live = __any_sync(0xffffffffu, ps.r > 0.0f);
             if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
         }
@@ -479,11 +679,13 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.empty[s]);
+        base += n;
         if (++s == kStages) {
             s = 0;
             phase ^= 1;
         }
     }
+    if (ps.r > 0.0f) ps.ne = e1 - e0;  // alive through the whole list
     if (valid) {
         const float rem = ps.r > 0.0f ? ps.r : ps.rfin;  // live to the end of the list, or stopped
         // renderer.py:118 background with the final remaining transmittance
@@ -493,13 +695,20 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
         remaining[p] = rem;
         count[p] = ps.cnt;
         n_eval[p] = ps.ne;
-        if (ps.border) {
+        if (pixel_border(ps)) {
             unsigned long long slot = atomicAdd(&counters[2], 1ull);
             fixup_list[slot] = (int32_t)(((int64_t)blockIdx.x << 8) | tid);  // work item, thread
         }
     }
     rechecks = __reduce_add_sync(0xffffffffu, rechecks);
     if (lane == 0 && rechecks) atomicAdd(&counters[0], (unsigned long long)rechecks);
+    if (lane == 0 && went) atomicAdd(&counters[3], (unsigned long long)went);
+#ifdef GEER_CTA_TIMING
+    if (lane == 0 && blockIdx.x < (1u << 16)) {
+        atomicMax(&g_cta_t1[blockIdx.x], gtimer());
+        atomicAdd(&g_cta_went[blockIdx.x], went);
+    }
+#endif
 }
 
 // ------------------------------------------------------------------------------ fp64 fix-up of borderline pixels
@@ -636,7 +845,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
                const double2 *__restrict__ row_sc, const double *__restrict__ dir64,
                const int32_t *__restrict__ ranges, const uint32_t *__restrict__ order,
                const Payload *__restrict__ payload, const GradPayload *__restrict__ gpayload,
-               const uint8_t *__restrict__ flags, const float *__restrict__ remaining, const int32_t *__restrict__ n_eval,
+               const uint8_t *__restrict__ flags, const float4 *__restrict__ box, const float *__restrict__ remaining,
+               const int32_t *__restrict__ n_eval,
                const float *__restrict__ dl_dimage, float *__restrict__ accum) {
     __shared__ PipeSmem<true> S;
     __shared__ double sray[kRasterThreads][3];
@@ -652,15 +862,16 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
     __syncthreads();
     const int wmax = __reduce_max_sync(0xffffffffu, ne);
     if (lane == 0 && wmax > 0) atomicMax(&smax, wmax);
-    pipe_init(S);  // (its __syncthreads also publishes smax)
+    double d64[3] = {0.0, 0.0, 1.0};
+    if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
+    if (warp < kConsumerWarps) publish_patch(S.patch, warp, lane, valid, ray_mirror_bounds(fc, d64));
+    pipe_init(S);  // (its __syncthreads also publishes smax and the patches)
     const int max_n = smax;
     if (max_n == 0) return;
     if (warp == kConsumerWarps) {
-        pipe_produce<true>(S, order, payload, gpayload, flags, e0, max_n, false);
+        pipe_produce<true>(S, order, payload, gpayload, flags, box, fc.cull != 0, e0, max_n, false);
         return;
     }
-    double d64[3] = {0.0, 0.0, 1.0};
-    if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
     const Ray64 R = make_ray(d64);
     if (valid) {
         sray[tid][0] = d64[0];
@@ -687,9 +898,13 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
         if (n == 0) break;
         const int lo = hi - n;
         if (lo < wmax) {  // some lane of this warp has alive entries in the stage
-            for (int jj = n - 1; jj >= 0; --jj) {
+            // entries the PBF mask keeps (culled ones have t = 0: no gradient, T unchanged), below wmax
+            uint32_t msk = S.mask[s][warp];
+            if (wmax - lo < 32) msk &= (1u << (wmax - lo)) - 1u;
+            while (msk) {
+                const int jj = 31 - __clz(msk);
+                msk &= ~(1u << jj);
                 const int i = lo + jj;
-                if (i >= wmax) continue;
                 float v[16];
 #pragma unroll
                 for (int k = 0; k < 16; ++k) v[k] = 0.f;
@@ -789,18 +1004,18 @@ static int grid_for(int64_t n) { return (int)lmin(lmax((n + 255) / 256, 1), 148 
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    const uint8_t *flags, float *color, float *remaining, int32_t *count, int32_t *n_eval,
-                    unsigned long long *counters, int32_t *fixup_list, cudaStream_t st) {
+                    const uint8_t *flags, const float4 *box, float *color, float *remaining, int32_t *count,
+                    int32_t *n_eval, unsigned long long *counters, int32_t *fixup_list, cudaStream_t st) {
     if (max_items <= 0) return;
     if (fc.model == GEER_BEAP) {
         k_forward<true><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                            ranges, order, payload, flags, color, remaining, count,
+                                                            ranges, order, payload, flags, box, color, remaining, count,
                                                             n_eval, counters, fixup_list);
         k_fixup<true><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                counters, fixup_list, color, remaining, count, n_eval);
     } else {
         k_forward<false><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                             ranges, order, payload, flags, color, remaining, count,
+                                                             ranges, order, payload, flags, box, color, remaining, count,
                                                              n_eval, counters, fixup_list);
         k_fixup<false><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                 counters, fixup_list, color, remaining, count, n_eval);
@@ -810,16 +1025,16 @@ void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, c
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                      const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                     const GradPayload *gpayload, const uint8_t *flags, const float *remaining,
+                     const GradPayload *gpayload, const uint8_t *flags, const float4 *box, const float *remaining,
                      const int32_t *n_eval, const float *dl_dimage, float *accum, cudaStream_t st) {
     if (max_items <= 0) return;
     if (fc.model == GEER_BEAP)
         k_backward<true><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                             ranges, order, payload, gpayload, flags, remaining,
+                                                             ranges, order, payload, gpayload, flags, box, remaining,
                                                              n_eval, dl_dimage, accum);
     else
         k_backward<false><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                              ranges, order, payload, gpayload, flags, remaining,
+                                                              ranges, order, payload, gpayload, flags, box, remaining,
                                                               n_eval, dl_dimage, accum);
 }
 
@@ -842,3 +1057,15 @@ void launch_fill_background(const FrameConst &fc, float *color, float *remaining
 }
 
 }  // namespace geer
+
+#ifdef GEER_CTA_TIMING
+extern "C" int geer_debug_cta_times(unsigned long long *t0, unsigned long long *t1, int *sm, int *went, int n) {
+    if (n > (1 << 16)) n = 1 << 16;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(t0, geer::g_cta_t0, sizeof(unsigned long long) * n);
+    cudaMemcpyFromSymbol(t1, geer::g_cta_t1, sizeof(unsigned long long) * n);
+    cudaMemcpyFromSymbol(sm, geer::g_cta_sm, sizeof(int) * n);
+    cudaMemcpyFromSymbol(went, geer::g_cta_went, sizeof(int) * n);
+    return (int)cudaGetLastError();
+}
+#endif

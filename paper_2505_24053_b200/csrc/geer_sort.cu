@@ -115,6 +115,18 @@ __device__ __forceinline__ int range_len(const uint32_t r[3]) {
 // their offsets are staged in shared memory and each thread binary-searches
 // its entry's rank there (coalesced writes, no per-Gaussian load imbalance).
 constexpr int kEmitPerBlock = 1024;
+
+// block_rank[b] = depth rank owning entry b * kEmitPerBlock; block_rank[n_blocks] = rank of the last
+// entry.  One thread per rank: a rank owns the block starts inside its [offs[r], offs[r+1]).
+__global__ void k_block_ranks(const int64_t *__restrict__ offs, int64_t n, int64_t n_entries, int n_blocks,
+                              int32_t *__restrict__ block_rank) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t lo = offs[r], hi = offs[r + 1];
+        if (lo == hi) continue;
+        for (int64_t b = (lo + kEmitPerBlock - 1) / kEmitPerBlock; b * kEmitPerBlock < hi; ++b) block_rank[b] = (int32_t)r;
+        if (lo <= n_entries - 1 && n_entries - 1 < hi) block_rank[n_blocks] = (int32_t)r;
+    }
+}
 __device__ __forceinline__ int64_t upper_rank(const int64_t *offs, int64_t lo, int64_t hi, int64_t e) {
     // largest r in [lo, hi] with offs[r] <= e
     while (lo < hi) {
@@ -123,17 +135,15 @@ __device__ __forceinline__ int64_t upper_rank(const int64_t *offs, int64_t lo, i
     }
     return lo;
 }
-__global__ void __launch_bounds__(256) k_emit(const int64_t *__restrict__ offs, const int32_t *__restrict__ sorted_gid,
+__global__ void __launch_bounds__(256) k_emit(const int64_t *__restrict__ offs, const int32_t *__restrict__ block_rank,
+                                              const int32_t *__restrict__ sorted_gid,
                                               const AxisRanges *__restrict__ ranges, int n_x, int64_t n_entries,
                                               int64_t n, uint32_t *__restrict__ tile_keys, uint32_t *__restrict__ gids) {
     __shared__ int64_t s_off[kEmitPerBlock + 2];
-    __shared__ int64_t s_r0, s_r1;
     const int64_t e_begin = (int64_t)blockIdx.x * kEmitPerBlock;
     const int64_t e_last = min(e_begin + kEmitPerBlock, n_entries) - 1;
-    if (threadIdx.x == 0) s_r0 = upper_rank(offs, 0, n, e_begin);
-    if (threadIdx.x == 32) s_r1 = upper_rank(offs, 0, n, e_last);
-    __syncthreads();
-    const int64_t r0 = s_r0, r1 = s_r1;
+    // ranks owning this block's first entry and (at most) the next block's first entry
+    const int64_t r0 = block_rank[blockIdx.x], r1 = block_rank[blockIdx.x + 1];
     const int span = (int)(r1 - r0 + 1);  // <= kEmitPerBlock + 1
     for (int i = threadIdx.x; i <= span; i += blockDim.x) s_off[i] = offs[r0 + i];
     __syncthreads();
@@ -153,11 +163,15 @@ __global__ void __launch_bounds__(256) k_emit(const int64_t *__restrict__ offs, 
     }
 }
 
+int64_t emit_blocks(int64_t n_entries) { return (n_entries + kEmitPerBlock - 1) / kEmitPerBlock; }
+
 void emit_entries(const int64_t *offs, const int32_t *sorted_gid, const AxisRanges *ranges, int n_x,
-                  int64_t n_entries, int64_t n, uint32_t *tile_keys, uint32_t *gids, cudaStream_t st) {
+                  int64_t n_entries, int64_t n, int32_t *block_rank, uint32_t *tile_keys, uint32_t *gids,
+                  cudaStream_t st) {
     if (n_entries <= 0) return;
-    int64_t blocks = (n_entries + kEmitPerBlock - 1) / kEmitPerBlock;
-    k_emit<<<(unsigned)blocks, 256, 0, st>>>(offs, sorted_gid, ranges, n_x, n_entries, n, tile_keys, gids);
+    const int64_t blocks = emit_blocks(n_entries);
+    k_block_ranks<<<(unsigned)lmin((n + 255) / 256, 148 * 16), 256, 0, st>>>(offs, n, n_entries, (int)blocks, block_rank);
+    k_emit<<<(unsigned)blocks, 256, 0, st>>>(offs, block_rank, sorted_gid, ranges, n_x, n_entries, n, tile_keys, gids);
 }
 
 // ranges[t] = first entry with tile >= t (np.searchsorted(tiles, arange(n_tiles + 1)))

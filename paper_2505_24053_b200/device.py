@@ -74,8 +74,12 @@ class DeviceRenderer:
     def set_timing(self, on: bool):
         self.ctx.set_timing(on)
 
-    def forward(self, scene: DeviceScene, camera, config, out=None):
-        """Returns (color (H,W,3) f32, remaining (H,W) f32, count (H,W) i32) CUDA tensors."""
+    def forward(self, scene: DeviceScene, camera, config, out=None, flags: int = 0):
+        """Returns (color (H,W,3) f32, remaining (H,W) f32, count (H,W) i32) CUDA tensors.
+
+        ``flags``: ``_lib.GEER_CFG_*`` debug switches (e.g. ``GEER_CFG_NO_CULL``); results do not
+        depend on them.
+        """
         h, w = int(camera.height), int(camera.width)
         dev = scene.means.device
         if out is None:
@@ -85,7 +89,7 @@ class DeviceRenderer:
         color, remaining, count = out
         s = scene.struct()
         cam = _lib.camera_struct(camera)
-        cfg = _lib.config_struct(config)
+        cfg = _lib.config_struct(config, flags)
         stream = torch.cuda.current_stream(dev).cuda_stream
         _lib.check(self.ctx._lib.geer_forward(self.ctx.ptr, ctypes.byref(s), ctypes.byref(cam), ctypes.byref(cfg),
                                               color.data_ptr(), remaining.data_ptr(), count.data_ptr(), stream))

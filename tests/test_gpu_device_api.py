@@ -83,3 +83,23 @@ def test_l1_grad_and_adam_kernels():
         v_ref = 0.999 * v_ref + 0.001 * grad * grad
         p_ref = p_ref - 1e-3 * (m_ref / (1 - 0.9 ** step)) / (torch.sqrt(v_ref / (1 - 0.999 ** step)) + 1e-15)
     torch.testing.assert_close(p, p_ref, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("config_name,n,w,h", [("C2", 50_000, 640, 360), ("C5", 40_000, 480, 270),
+                                               ("C1", 10_000, 256, 256)])
+def test_pbf_culling_is_exact(config_name, n, w, h):
+    """Per-warp PBF culling skips only pairs with t = 0: forward outputs are bit-identical with it off."""
+    scene = synth.config_scene(config_name, n=n)
+    cam = synth.config_camera(config_name, width=w, height=h)
+    cfg = renderer.RenderConfig(background=np.array([0.3, 0.1, 0.2]))
+    ds = DeviceScene.from_scene(scene)
+    r = DeviceRenderer(0)
+    on = [t.clone() for t in r.forward(ds, cam, cfg)]
+    st_on = r.stats()
+    off = [t.clone() for t in r.forward(ds, cam, cfg, flags=_lib.GEER_CFG_NO_CULL)]
+    st_off = r.stats()
+    torch.cuda.synchronize()
+    for a, b in zip(on, off):
+        assert torch.equal(a, b)
+    assert st_on["evaluated_pairs"] == st_off["evaluated_pairs"]
+    assert st_on["warp_entries"] <= st_off["warp_entries"]
