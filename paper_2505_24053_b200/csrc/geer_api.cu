@@ -69,7 +69,7 @@ struct geer_ctx {
     int64_t *h_hdr = nullptr;  // pinned: [0] total entries, [1] error code
     // camera buffers
     Buf col_sc, row_sc, medges_x, medges_y, edges_x, edges_y, dir64, theta, phi, minmax, pixel_tile, pixel_tile_sorted,
-        pix_iota, pix_list, tile_count, tile_off, item_count, item_off, items, n_items;
+        pix_iota, pix_list, tile_count, tile_off, item_count, item_off, items, n_items, work, n_work;
     // per-Gaussian buffers
     Buf payload, gpayload, box, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, cnt_sorted, offs, ranges_ax, flags, mu_c,
         depth;
@@ -301,6 +301,9 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         sort_tiles(tmp, b, tk, tks, gids, order, total, bits, st);
     }
     tile_ranges(tks, total, fc.n_tiles, ranges, st);
+    int4 *work = ENSURE(int4, c->work, c->max_items);
+    int32_t *nwork = ENSURE(int32_t, c->n_work, 2);
+    order_items((const int4 *)c->items.p, (const int32_t *)c->n_items.p, ranges, c->max_items, work, nwork, st);
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[3], st));
     c->have_frame = true;
 
@@ -308,7 +311,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     if (color) {
         int32_t *ne = ENSURE(int32_t, c->n_eval, npx);
         int32_t *fix = ENSURE(int32_t, c->fixup, npx);
-        launch_forward(fc, sc, c->max_items, (const int4 *)c->items.p, (const int32_t *)c->n_items.p,
+        launch_forward(fc, sc, c->max_items, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
                        (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
                        (const double *)c->dir64.p, ranges, order, payload, flags, box, color, remaining, count, ne,
                        c->d_counters, fix, st);
@@ -336,7 +339,7 @@ int run_backward(geer_ctx *c, const float *dl_dimage, bool f64_out, void *const 
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
     float *accum = ENSURE(float, c->accum, sc.n * 16);
     if (sc.n > 0) GEER_CUDA(cudaMemsetAsync(accum, 0, sizeof(float) * 16 * sc.n, st));
-    launch_backward(fc, sc, c->max_items, (const int4 *)c->items.p, (const int32_t *)c->n_items.p,
+    launch_backward(fc, sc, c->max_items, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
                     (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
                     (const double *)c->dir64.p, (const int32_t *)c->tile_ranges.p, (const uint32_t *)c->order.p,
                     (const Payload *)c->payload.p, (const GradPayload *)c->gpayload.p, (const uint8_t *)c->flags.p,
@@ -450,7 +453,7 @@ void geer_destroy(geer_ctx *c) {
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     Buf *bufs[] = {&c->col_sc, &c->row_sc, &c->medges_x, &c->medges_y, &c->edges_x, &c->edges_y, &c->dir64,
                    &c->theta, &c->phi, &c->minmax, &c->pixel_tile, &c->pixel_tile_sorted, &c->pix_iota, &c->pix_list,
-                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->payload, &c->gpayload, &c->box,
+                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->work, &c->n_work, &c->payload, &c->gpayload, &c->box,
                    &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted, &c->count, &c->cnt_sorted,
                    &c->offs, &c->ranges_ax, &c->flags, &c->mu_c, &c->depth, &c->tile_keys, &c->tile_keys_sorted,
                    &c->gids, &c->order, &c->tile_ranges, &c->block_rank, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,
@@ -521,7 +524,7 @@ int geer_frame_stats(geer_ctx *c, geer_stats *out) {
         unsigned long long h[4];
         int32_t nit = 0;
         GEER_CUDA(cudaMemcpyAsync(h, c->d_counters, sizeof(h), cudaMemcpyDeviceToHost, st));
-        GEER_CUDA(cudaMemcpyAsync(&nit, c->n_items.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        GEER_CUDA(cudaMemcpyAsync(&nit, c->n_work.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));  // items with entries
         GEER_CUDA(cudaStreamSynchronize(st));
         out->kappa_rechecks = (int64_t)h[0];
         out->evaluated_pairs = (int64_t)h[1];

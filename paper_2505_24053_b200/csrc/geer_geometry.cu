@@ -636,8 +636,8 @@ __global__ void __launch_bounds__(128) k_associate(FrameConst fc, geer_scene sc,
 template <int NB>
 __global__ void __launch_bounds__(128) k_payload(FrameConst fc, geer_scene sc, Payload *__restrict__ payload,
                                                  GradPayload *__restrict__ gpayload, uint8_t *__restrict__ flags) {
-    // SH staging, then payload staging (176 B = 44 floats per Gaussian)
-    __shared__ __align__(16) float ssh[128 * (NB * 3 > 44 ? NB * 3 : 44)];
+    // SH staging, then payload staging (9 + 3 float4 = 48 floats per Gaussian, padded rows)
+    __shared__ __align__(16) float ssh[128 * (NB * 3 > 48 ? NB * 3 : 48)];
     const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
     const int cnt_b = (int)lmin((int64_t)blockDim.x, sc.n - g0);
     {
@@ -698,20 +698,22 @@ __global__ void __launch_bounds__(128) k_payload(FrameConst fc, geer_scene sc, P
     if (live) flags[g] = (uint8_t)(flags[g] | (gate << 3) | (mode1 ? 64 : 0));
     // coalesced stores: stage the block's 128-B payloads and 48-B grad payloads in shared memory
     // (reusing the SH staging buffer) and write them out as contiguous float4 runs
+    // rows padded to 9 float4 (payload) and kept at 3 float4 (grad payload): conflict-free 16-B stores
+    constexpr int kP = sizeof(Payload) / 16, kPP = kP + 1, kG = sizeof(GradPayload) / 16;
     float4 *sp = reinterpret_cast<float4 *>(ssh);
-    float4 *sg = sp + 128 * (sizeof(Payload) / 16);
+    float4 *sg = sp + 128 * kPP;
     __syncthreads();  // every thread is done reading its SH coefficients
     const float4 *plv = reinterpret_cast<const float4 *>(&pl);
     const float4 *gpv = reinterpret_cast<const float4 *>(&gp);
 #pragma unroll
-    for (int k = 0; k < (int)(sizeof(Payload) / 16); ++k) sp[threadIdx.x * (sizeof(Payload) / 16) + k] = plv[k];
+    for (int k = 0; k < kP; ++k) sp[threadIdx.x * kPP + k] = plv[k];
 #pragma unroll
-    for (int k = 0; k < (int)(sizeof(GradPayload) / 16); ++k) sg[threadIdx.x * (sizeof(GradPayload) / 16) + k] = gpv[k];
+    for (int k = 0; k < kG; ++k) sg[threadIdx.x * kG + k] = gpv[k];
     __syncthreads();
     float4 *dp = reinterpret_cast<float4 *>(payload + g0);
     float4 *dg = reinterpret_cast<float4 *>(gpayload + g0);
-    for (int i = threadIdx.x; i < cnt_b * (int)(sizeof(Payload) / 16); i += blockDim.x) dp[i] = sp[i];
-    for (int i = threadIdx.x; i < cnt_b * (int)(sizeof(GradPayload) / 16); i += blockDim.x) dg[i] = sg[i];
+    for (int i = threadIdx.x; i < cnt_b * kP; i += blockDim.x) dp[i] = sp[(i / kP) * kPP + i % kP];
+    for (int i = threadIdx.x; i < cnt_b * kG; i += blockDim.x) dg[i] = sg[i];
 }
 
 // ---------------------------------------------------------------- K7

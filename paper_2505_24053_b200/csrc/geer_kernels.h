@@ -53,6 +53,8 @@ void sort_pixels(void *temp, size_t temp_bytes, const int32_t *keys_in, int32_t 
                  int32_t *vals_out, int64_t n, int n_bits, cudaStream_t st);
 size_t sort_pixels_temp_bytes(int64_t n, int n_bits);
 void tile_ranges(const uint32_t *sorted_tiles, int64_t n_entries, int n_tiles, int32_t *ranges, cudaStream_t st);
+void order_items(const int4 *items, const int32_t *n_items, const int32_t *ranges, int max_items, int4 *work,
+                 int32_t *n_work, cudaStream_t st);
 
 // geer_raster.cu (fp32 raster forward / backward)
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,

@@ -515,7 +515,7 @@ __device__ __forceinline__ void consume_stage_generic(PipeSmem<false> &S, int s,
 // shared loads), one warp vote for the rare fp64 cutoff re-decisions, then the four serial pixel
 // updates.  t is bit-identical to finish_t's (the backward recomputes it with eval_t).
 #ifndef GEER_FWD_GROUP
-#define GEER_FWD_GROUP 2
+#define GEER_FWD_GROUP 4
 #endif
 constexpr int kFwdGroup = GEER_FWD_GROUP;  // entries evaluated together (ILP vs registers)
 
@@ -625,10 +625,24 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
               unsigned long long *__restrict__ counters, int32_t *__restrict__ fixup_list) {
     __shared__ PipeSmem<false> S;
     __shared__ double sray[kRasterThreads][3];  // fp64 pixel rays (mode-1 payloads only)
-    if ((int)blockIdx.x >= *n_items) return;
-    const int4 it = items[blockIdx.x];
-    const int e0 = ranges[it.x], e1 = ranges[it.x + 1];
+    // n_items: [0] items with entries (work[0, n0)), [1] empty items (work[max_items - n1, max_items))
+    const int n_full = n_items[0];
+    if ((int)blockIdx.x >= n_full + n_items[1]) return;
+    const int4 it = items[(int)blockIdx.x < n_full ? blockIdx.x : gridDim.x - 1 - (blockIdx.x - n_full)];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if ((int)blockIdx.x >= n_full) {  // tile without entries: background only (renderer.py:118)
+        if (tid < it.z) {
+            const int p = pix_list[it.y + tid];
+            color[(int64_t)p * 3 + 0] = fc.bg[0];
+            color[(int64_t)p * 3 + 1] = fc.bg[1];
+            color[(int64_t)p * 3 + 2] = fc.bg[2];
+            remaining[p] = 1.0f;
+            count[p] = 0;
+            n_eval[p] = 0;
+        }
+        return;
+    }
+    const int e0 = ranges[it.x], e1 = ranges[it.x + 1];
 #ifdef GEER_CTA_TIMING
     if (tid == 0 && blockIdx.x < (1u << 16)) {
         unsigned smid;
@@ -851,7 +865,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
     __shared__ PipeSmem<true> S;
     __shared__ double sray[kRasterThreads][3];
     __shared__ int smax;
-    if ((int)blockIdx.x >= *n_items) return;
+    if ((int)blockIdx.x >= n_items[0]) return;  // tiles without entries have no gradient
     const int4 it = items[blockIdx.x];
     const int e0 = ranges[it.x];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -911,6 +925,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
                 const Payload &P = S.ring[s][jj];
                 PairT e;
                 eval_t(P, R, sray[tid], fc, e, dummy);  // warp-uniform call (mode vote inside)
+                // t = 0 (or not alive) on every lane: T, the suffix and all 16 partials are unchanged
+                if (!__any_sync(0xffffffffu, i < ne && e.t > 0.0f)) continue;
                 if (i < ne) {
                     const float omt = __fsub_rn(1.0f, e.t);
                     const float inv = 1.0f / omt;

@@ -127,39 +127,70 @@ __global__ void k_block_ranks(const int64_t *__restrict__ offs, int64_t n, int64
         if (lo <= n_entries - 1 && n_entries - 1 < hi) block_rank[n_blocks] = (int32_t)r;
     }
 }
-__device__ __forceinline__ int64_t upper_rank(const int64_t *offs, int64_t lo, int64_t hi, int64_t e) {
-    // largest r in [lo, hi] with offs[r] <= e
-    while (lo < hi) {
-        int64_t mid = (lo + hi + 1) >> 1;
-        if (offs[mid] <= e) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
+// One block = kEmitPerBlock consecutive entries (4 per thread).  The block's ranks are staged
+// once (gid, axis ranges, local start), each rank marks the position of its first entry, and an
+// inclusive max-scan over the positions gives every entry its rank; entries are then decoded from
+// shared memory and written with coalesced stores.
 __global__ void __launch_bounds__(256) k_emit(const int64_t *__restrict__ offs, const int32_t *__restrict__ block_rank,
                                               const int32_t *__restrict__ sorted_gid,
                                               const AxisRanges *__restrict__ ranges, int n_x, int64_t n_entries,
                                               int64_t n, uint32_t *__restrict__ tile_keys, uint32_t *__restrict__ gids) {
-    __shared__ int64_t s_off[kEmitPerBlock + 2];
+    __shared__ int s_pos[kEmitPerBlock];
+    __shared__ int s_start[kEmitPerBlock + 1];
+    __shared__ uint32_t s_g[kEmitPerBlock + 1];
+    __shared__ AxisRanges s_ar[kEmitPerBlock + 1];
+    __shared__ int s_wmax[8];
     const int64_t e_begin = (int64_t)blockIdx.x * kEmitPerBlock;
-    const int64_t e_last = min(e_begin + kEmitPerBlock, n_entries) - 1;
+    const int n_here = (int)lmin(kEmitPerBlock, n_entries - e_begin);
     // ranks owning this block's first entry and (at most) the next block's first entry
     const int64_t r0 = block_rank[blockIdx.x], r1 = block_rank[blockIdx.x + 1];
     const int span = (int)(r1 - r0 + 1);  // <= kEmitPerBlock + 1
-    for (int i = threadIdx.x; i <= span; i += blockDim.x) s_off[i] = offs[r0 + i];
+    for (int j = threadIdx.x; j < kEmitPerBlock; j += blockDim.x) s_pos[j] = 0;
     __syncthreads();
-    for (int j = threadIdx.x; j < kEmitPerBlock; j += blockDim.x) {
-        const int64_t e = e_begin + j;
-        if (e > e_last) break;
-        const int rl = (int)upper_rank(s_off, 0, span - 1, e);
-        const int32_t g = sorted_gid[r0 + rl];
-        const AxisRanges ar = ranges[g];
+    for (int i = threadIdx.x; i < span; i += blockDim.x) {
+        const int st = (int)(offs[r0 + i] - e_begin);  // < 0 only for rank r0
+        const uint32_t g = (uint32_t)sorted_gid[r0 + i];
+        s_start[i] = st;
+        s_g[i] = g;
+        s_ar[i] = ranges[g];
+        if (st >= 0 && st < kEmitPerBlock) s_pos[st] = i;
+    }
+    __syncthreads();
+    // inclusive max-scan of s_pos (local ranks increase with position)
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    int v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = s_pos[4 * t + u];
+#pragma unroll
+    for (int u = 1; u < 4; ++u) v[u] = max(v[u], v[u - 1]);
+    int run = v[3];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, run, o);
+        if (lane >= o) run = max(run, y);
+    }
+    if (lane == 31) s_wmax[warp] = run;
+    __syncthreads();
+    int carry = 0;
+    for (int w = 0; w < warp; ++w) carry = max(carry, s_wmax[w]);
+    int prev = __shfl_up_sync(0xffffffffu, run, 1);
+    prev = max(lane > 0 ? prev : 0, carry);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s_pos[4 * t + u] = max(v[u], prev);
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int j = u * 256 + t;
+        if (j >= n_here) break;
+        const int rl = s_pos[j];
+        const AxisRanges ar = s_ar[rl];
         const int cx = range_len(ar.x);
-        const int k = (int)(e - s_off[rl]);
+        const int k = j - s_start[rl];
         const int ky = k / cx;
         const int iy = range_index(ar.y, ky);
         const int ix = range_index(ar.x, k - ky * cx);
-        tile_keys[e] = (uint32_t)(iy * n_x + ix);
-        gids[e] = (uint32_t)g;
+        tile_keys[e_begin + j] = (uint32_t)(iy * n_x + ix);
+        gids[e_begin + j] = s_g[rl];
     }
 }
 
@@ -181,6 +212,41 @@ __global__ void k_ranges(const uint32_t *__restrict__ tiles, int64_t n_entries, 
         int cur = e == n_entries ? n_tiles : (int)tiles[e];
         for (int t = prev + 1; t <= cur; ++t) ranges[t] = (int32_t)e;
     }
+}
+
+// Raster work order: items of tiles with entries fill work[] from the front, the empty ones (which
+// only write the background) from the back.  n_work[0] = items with entries, n_work[1] = empty
+// items (both zeroed before the launch).  The order among full items does not affect results.
+__global__ void k_order_items(const int4 *__restrict__ items, const int32_t *__restrict__ n_items,
+                              const int32_t *__restrict__ ranges, int max_items, int4 *__restrict__ work,
+                              int32_t *__restrict__ n_work) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool in = i < *n_items;
+    int4 it = make_int4(0, 0, 0, 0);
+    bool full = false;
+    if (in) {
+        it = items[i];
+        full = ranges[it.x + 1] > ranges[it.x];
+    }
+    // warp-aggregated slots
+    const unsigned mf = __ballot_sync(0xffffffffu, in && full), me = __ballot_sync(0xffffffffu, in && !full);
+    const int lane = threadIdx.x & 31;
+    int bf = 0, be = 0;
+    if (lane == 0) {
+        if (mf) bf = atomicAdd(&n_work[0], __popc(mf));
+        if (me) be = atomicAdd(&n_work[1], __popc(me));
+    }
+    bf = __shfl_sync(0xffffffffu, bf, 0);
+    be = __shfl_sync(0xffffffffu, be, 0);
+    const unsigned lt = (1u << lane) - 1u;
+    if (in && full) work[bf + __popc(mf & lt)] = it;
+    if (in && !full) work[max_items - 1 - (be + __popc(me & lt))] = it;
+}
+
+void order_items(const int4 *items, const int32_t *n_items, const int32_t *ranges, int max_items, int4 *work,
+                 int32_t *n_work, cudaStream_t st) {
+    cudaMemsetAsync(n_work, 0, 2 * sizeof(int32_t), st);
+    k_order_items<<<(max_items + 255) / 256, 256, 0, st>>>(items, n_items, ranges, max_items, work, n_work);
 }
 
 void tile_ranges(const uint32_t *sorted_tiles, int64_t n_entries, int n_tiles, int32_t *ranges, cudaStream_t st) {

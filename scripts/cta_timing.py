@@ -49,3 +49,7 @@ order = np.argsort(-dur)[:10]
 print("longest CTAs (us, warp-entries):", [(round(dur[i] / 1e3, 1), int(went[i])) for i in order])
 print("ns per warp-entry (CTAs with >1000):", float(np.median(dur[went > 1000] / went[went > 1000])))
 print("stats", st)
+A = np.vstack([np.ones_like(went, dtype=np.float64), went.astype(np.float64)]).T
+coef, *_ = np.linalg.lstsq(A, dur.astype(np.float64), rcond=None)
+print("fit: CTA ns = %.0f + %.1f * warp_entries" % (coef[0], coef[1]))
+print("CTAs with 0 warp-entries:", int((went == 0).sum()), "mean dur us", float(dur[went == 0].mean() / 1e3) if (went == 0).any() else 0)
