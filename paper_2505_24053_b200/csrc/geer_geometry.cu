@@ -503,21 +503,16 @@ __device__ bool make_payload(const double W[9], const double ou[3], const double
     return mode1;
 }
 
-// K1a: exact fp64 association of one Gaussian (association.py:82-88, 148-224, 343-350, 373-451)
-__global__ void __launch_bounds__(128) k_associate(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x,
-                                                   const double *__restrict__ medges_y, uint32_t *__restrict__ depth_key,
-                                                   int64_t *__restrict__ count, AxisRanges *__restrict__ ranges,
-                                                   uint8_t *__restrict__ flags, float4 *__restrict__ box,
-                                                   double *__restrict__ mu_out,
-                                                   double *__restrict__ depth_out, int *__restrict__ err) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *sex = reinterpret_cast<double *>(smem_raw);
-    double *sey = sex + (fc.n_x + 1);
-    for (int i = threadIdx.x; i <= fc.n_x; i += blockDim.x) sex[i] = medges_x[i];
-    for (int i = threadIdx.x; i <= fc.n_y; i += blockDim.x) sey[i] = medges_y[i];
-    __syncthreads();
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= sc.n) return;
+__device__ __forceinline__ void named_barrier(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// K1a: exact fp64 association of one Gaussian (association.py:82-88, 148-224, 343-350, 373-451).
+// sex / sey: the mirror tile edges in shared memory.  Returns the keep / clamped flag bits.
+__device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, const double *sex, const double *sey,
+                                 int64_t g, uint32_t *__restrict__ depth_key, int64_t *__restrict__ count,
+                                 AxisRanges *__restrict__ ranges, float4 *__restrict__ box,
+                                 double *__restrict__ mu_out, double *__restrict__ depth_out, int *__restrict__ err) {
 
     const double *R = fc.R;
     const double mean[3] = {sc.means[g * 3 + 0], sc.means[g * 3 + 1], sc.means[g * 3 + 2]};
@@ -624,22 +619,22 @@ __global__ void __launch_bounds__(128) k_associate(FrameConst fc, geer_scene sc,
     count[g] = n_ent;
     ranges[g] = ar;
     box[g] = bx;
-    flags[g] = fl;
     // association.py:335-340 key bits (depth > 0): f32 bits | 0x80000000; non-emitting last
     const uint32_t kb = __float_as_uint((float)depth) | 0x80000000u;
     depth_key[g] = n_ent > 0 ? kb : 0xFFFFFFFFu;
+    return fl;
 }
 
 // K1b: raster payload of one Gaussian (renderer.py:57-81): W, o_u, the fp64 quadratic forms, SH colour.
 // Only the pixel-side arithmetic of the raster depends on these values (not the association), so
 // reciprocals replace divisions here.  NB = SH band count (compile-time: static register arrays).
+// Runs on a group of 128 threads (lt = 0..127) that synchronises with named barrier 2; ssh: SH
+// staging, then payload staging (9 + 3 float4 = 48 floats per Gaussian, padded rows).  Returns the
+// SH clamp gate (bits 3-5) and payload-mode (bit 6) flag bits of Gaussian g0 + lt.
 template <int NB>
-__global__ void __launch_bounds__(128) k_payload(FrameConst fc, geer_scene sc, Payload *__restrict__ payload,
-                                                 GradPayload *__restrict__ gpayload, uint8_t *__restrict__ flags) {
-    // SH staging, then payload staging (9 + 3 float4 = 48 floats per Gaussian, padded rows)
-    __shared__ __align__(16) float ssh[128 * (NB * 3 > 48 ? NB * 3 : 48)];
-    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
-    const int cnt_b = (int)lmin((int64_t)blockDim.x, sc.n - g0);
+__device__ uint8_t payload_block(const FrameConst &fc, const geer_scene &sc, float *ssh, int64_t g0, int cnt_b, int lt,
+                                 Payload *__restrict__ payload, GradPayload *__restrict__ gpayload) {
+    const int nthr = 128;
     {
         // stage this block's SH coefficients (contiguous) with coalesced loads
         const float *src = sc.sh + g0 * NB * 3;
@@ -647,14 +642,14 @@ __global__ void __launch_bounds__(128) k_payload(FrameConst fc, geer_scene sc, P
         if ((((uintptr_t)src) & 15) == 0 && (total & 3) == 0) {
             const float4 *s4 = reinterpret_cast<const float4 *>(src);
             float4 *d4 = reinterpret_cast<float4 *>(ssh);
-            for (int i = threadIdx.x; i < total / 4; i += blockDim.x) d4[i] = __ldg(s4 + i);
+            for (int i = lt; i < total / 4; i += nthr) d4[i] = __ldg(s4 + i);
         } else {
-            for (int i = threadIdx.x; i < total; i += blockDim.x) ssh[i] = __ldg(src + i);
+            for (int i = lt; i < total; i += nthr) ssh[i] = __ldg(src + i);
         }
     }
-    __syncthreads();
-    const bool live = threadIdx.x < cnt_b;  // threads past the end compute a copy of row 0 (not stored)
-    const int64_t g = g0 + (live ? threadIdx.x : 0);
+    named_barrier(2, 128);
+    const bool live = lt < cnt_b;  // threads past the end compute a copy of row 0 (not stored)
+    const int64_t g = g0 + (live ? lt : 0);
     const double mean[3] = {sc.means[g * 3 + 0], sc.means[g * 3 + 1], sc.means[g * 3 + 2]};
     const float4 q4v = *reinterpret_cast<const float4 *>(sc.quats + g * 4);
     const float q4[4] = {q4v.x, q4v.y, q4v.z, q4v.w};
@@ -678,7 +673,7 @@ __global__ void __launch_bounds__(128) k_payload(FrameConst fc, geer_scene sc, P
     const double ivn = 1.0 / (vn > 1e-12 ? vn : 1e-12);
     double basis[16];
     sh_basis(vd[0] * ivn, vd[1] * ivn, vd[2] * ivn, basis);
-    const float *shg = ssh + (live ? threadIdx.x : 0) * NB * 3;
+    const float *shg = ssh + (live ? lt : 0) * NB * 3;
     double rgb[3];
     uint8_t gate = 0;
 #pragma unroll
@@ -695,25 +690,58 @@ __global__ void __launch_bounds__(128) k_payload(FrameConst fc, geer_scene sc, P
     GradPayload gp;
     const bool mode1 = make_payload(W, ou, rgb, sigma, smax / smin, fc.lam, pl, gp);
     // flags: bit0 keep, bit1 clamped (K1a), bits3-5 SH clamp gate per channel, bit6 payload mode 1
-    if (live) flags[g] = (uint8_t)(flags[g] | (gate << 3) | (mode1 ? 64 : 0));
+    const uint8_t bits = (uint8_t)((gate << 3) | (mode1 ? 64 : 0));
     // coalesced stores: stage the block's 128-B payloads and 48-B grad payloads in shared memory
     // (reusing the SH staging buffer) and write them out as contiguous float4 runs
     // rows padded to 9 float4 (payload) and kept at 3 float4 (grad payload): conflict-free 16-B stores
     constexpr int kP = sizeof(Payload) / 16, kPP = kP + 1, kG = sizeof(GradPayload) / 16;
     float4 *sp = reinterpret_cast<float4 *>(ssh);
     float4 *sg = sp + 128 * kPP;
-    __syncthreads();  // every thread is done reading its SH coefficients
+    named_barrier(2, 128);  // every thread is done reading its SH coefficients
     const float4 *plv = reinterpret_cast<const float4 *>(&pl);
     const float4 *gpv = reinterpret_cast<const float4 *>(&gp);
 #pragma unroll
-    for (int k = 0; k < kP; ++k) sp[threadIdx.x * kPP + k] = plv[k];
+    for (int k = 0; k < kP; ++k) sp[lt * kPP + k] = plv[k];
 #pragma unroll
-    for (int k = 0; k < kG; ++k) sg[threadIdx.x * kG + k] = gpv[k];
-    __syncthreads();
+    for (int k = 0; k < kG; ++k) sg[lt * kG + k] = gpv[k];
+    named_barrier(2, 128);
     float4 *dp = reinterpret_cast<float4 *>(payload + g0);
     float4 *dg = reinterpret_cast<float4 *>(gpayload + g0);
-    for (int i = threadIdx.x; i < cnt_b * kP; i += blockDim.x) dp[i] = sp[(i / kP) * kPP + i % kP];
-    for (int i = threadIdx.x; i < cnt_b * kG; i += blockDim.x) dg[i] = sg[i];
+    for (int i = lt; i < cnt_b * kP; i += nthr) dp[i] = sp[(i / kP) * kPP + i % kP];
+    for (int i = lt; i < cnt_b * kG; i += nthr) dg[i] = sg[i];
+    return bits;
+}
+
+// K1: one block = 128 Gaussians; threads 0-127 run the exact fp64 association, threads 128-255 the
+// raster payload of the same Gaussians (the first is fp64-issue-bound, the second latency-bound,
+// so co-resident they overlap), then the flag bits of both are merged.
+template <int NB>
+__global__ void __launch_bounds__(256, 3)
+    k_preprocess(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x, const double *__restrict__ medges_y,
+                 Payload *__restrict__ payload, GradPayload *__restrict__ gpayload, uint32_t *__restrict__ depth_key,
+                 int64_t *__restrict__ count, AxisRanges *__restrict__ ranges, uint8_t *__restrict__ flags,
+                 float4 *__restrict__ box, double *__restrict__ mu_out, double *__restrict__ depth_out,
+                 int *__restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(16) float ssh[128 * (NB * 3 > 48 ? NB * 3 : 48)];
+    __shared__ uint8_t sfl[2][128];
+    const int64_t g0 = (int64_t)blockIdx.x * 128;
+    const int cnt_b = (int)lmin(128, sc.n - g0);
+    const int lt = threadIdx.x & 127;
+    if (threadIdx.x < 128) {
+        double *sex = reinterpret_cast<double *>(smem_raw);
+        double *sey = sex + (fc.n_x + 1);
+        for (int i = lt; i <= fc.n_x; i += 128) sex[i] = medges_x[i];
+        for (int i = lt; i <= fc.n_y; i += 128) sey[i] = medges_y[i];
+        named_barrier(1, 128);
+        sfl[0][lt] = lt < cnt_b ? associate_one(fc, sc, sex, sey, g0 + lt, depth_key, count, ranges, box, mu_out,
+                                                depth_out, err)
+                                : 0;
+    } else {
+        sfl[1][lt] = payload_block<NB>(fc, sc, ssh, g0, cnt_b, lt, payload, gpayload);
+    }
+    __syncthreads();
+    if (threadIdx.x < cnt_b) flags[g0 + threadIdx.x] = (uint8_t)(sfl[0][threadIdx.x] | sfl[1][threadIdx.x]);
 }
 
 // ---------------------------------------------------------------- K7
@@ -869,11 +897,13 @@ void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double 
                        uint8_t *flags, float4 *box, double *mu_out, double *depth_out, int *err, cudaStream_t st) {
     if (sc.n == 0) return;
     const int blocks = (int)((sc.n + 127) / 128);
-    k_associate<<<blocks, 128, preprocess_smem(fc), st>>>(fc, sc, medges_x, medges_y, depth_key, count, ranges, flags,
-                                                          box, mu_out, depth_out, err);
     switch (sc.n_bands) {
-#define GEER_NB_CASE(NB) \
-    case NB: k_payload<NB><<<blocks, 128, 0, st>>>(fc, sc, payload, gpayload, flags); break;
+#define GEER_NB_CASE(NB)                                                                                            \
+    case NB:                                                                                                        \
+        k_preprocess<NB><<<blocks, 256, preprocess_smem(fc), st>>>(fc, sc, medges_x, medges_y, payload, gpayload,   \
+                                                                   depth_key, count, ranges, flags, box, mu_out,   \
+                                                                   depth_out, err);                                \
+        break;
         GEER_NB_CASE(1) GEER_NB_CASE(2) GEER_NB_CASE(3) GEER_NB_CASE(4) GEER_NB_CASE(5) GEER_NB_CASE(6)
         GEER_NB_CASE(7) GEER_NB_CASE(8) GEER_NB_CASE(9) GEER_NB_CASE(10) GEER_NB_CASE(11) GEER_NB_CASE(12)
         GEER_NB_CASE(13) GEER_NB_CASE(14) GEER_NB_CASE(15) GEER_NB_CASE(16)
