@@ -929,8 +929,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
                 if (!__any_sync(0xffffffffu, i < ne && e.t > 0.0f)) continue;
                 if (i < ne) {
                     const float omt = __fsub_rn(1.0f, e.t);
-                    const float inv = 1.0f / omt;
-                    T = __fdiv_rn(T, omt);  // T_i = T_{i+1} / (1 - t_i)
+                    const float inv = rcp_approx(omt);  // 1 - t >= 0.001: ~1 ulp
+                    T = T * inv;                        // T_i = T_{i+1} / (1 - t_i)
                     const float w = T * e.t;
                     const float c0 = P.col.x, c1 = P.col.y, c2 = P.col.z;
                     // renderer.py:284-287

@@ -112,6 +112,20 @@ def _ctx(device: int = 0) -> _lib.Context:
     return _lib.default_context(device)
 
 
+def _host_empty(shape, dtype) -> np.ndarray:
+    """A fresh numpy array in page-locked memory (torch's caching host allocator).
+
+    The device->host copies of the outputs then run at full PCIe speed instead of
+    faulting in fresh pageable pages (measured 17 ms vs 1.5 ms for a 1080p frame);
+    blocks are recycled once the caller drops the previous result.
+    """
+    import torch
+
+    t = torch.empty(shape, dtype={np.float64: torch.float64, np.int64: torch.int64}[np.dtype(dtype).type],
+                    pin_memory=True)
+    return t.numpy()
+
+
 def render(scene, camera, config: RenderConfig | None = None, *, return_graph: bool = False,
            device: int = 0) -> FrameOutput:
     """Render ``scene`` through ``camera`` (renderer.py:123-176) on the GPU.
@@ -124,9 +138,9 @@ def render(scene, camera, config: RenderConfig | None = None, *, return_graph: b
     validate_camera(camera)
     h, w = int(camera.height), int(camera.width)
     hs = _HostScene(scene)
-    color = np.empty((h, w, 3), dtype=np.float64)
-    remaining = np.empty((h, w), dtype=np.float64)
-    count = np.empty((h, w), dtype=np.int64)
+    color = _host_empty((h, w, 3), np.float64)
+    remaining = _host_empty((h, w), np.float64)
+    count = _host_empty((h, w), np.int64)
     ctx = _ctx(device)
     cam = _lib.camera_struct(camera)
     cfg = _lib.config_struct(config)
@@ -145,10 +159,12 @@ def render_backward(scene, camera, dl_dimage: np.ndarray, config: RenderConfig |
     config = config or RenderConfig()
     validate_camera(camera)
     hs = _HostScene(scene)
-    grads = SceneGrads(np.zeros((hs.n, 3)), np.zeros((hs.n, 3)), np.zeros((hs.n, 4)), np.zeros(hs.n),
-                       np.zeros((hs.n, hs.n_bands, 3)))
     if hs.n == 0:
-        return grads
+        return SceneGrads(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 4)), np.zeros(0),
+                          np.zeros((0, hs.n_bands, 3)))
+    grads = SceneGrads(_host_empty((hs.n, 3), np.float64), _host_empty((hs.n, 3), np.float64),
+                       _host_empty((hs.n, 4), np.float64), _host_empty((hs.n,), np.float64),
+                       _host_empty((hs.n, hs.n_bands, 3), np.float64))
     h, w = int(camera.height), int(camera.width)
     dl = np.ascontiguousarray(np.asarray(dl_dimage, dtype=np.float64).reshape(h, w, 3))
     ctx = _ctx(device)
