@@ -60,6 +60,7 @@ struct geer_ctx {
     geer_scene scene{};
     bool have_frame = false;
     bool have_raster = false;
+    bool keys16 = false;  // tile keys stored as uint16
     int64_t n_entries = 0;
     int max_items = 0;
     const float *fwd_remaining = nullptr;  // remaining written by the last forward (backward input)
@@ -285,22 +286,37 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     if (total >= ((int64_t)1 << 31) - 1)
         return fail(GEER_ERR_NOMEM, "render graph has %lld entries (limit 2^31)", (long long)total);
     c->n_entries = total;
-    uint32_t *tk = ENSURE(uint32_t, c->tile_keys, total);
-    uint32_t *tks = ENSURE(uint32_t, c->tile_keys_sorted, total);
+    // tile keys: u16 when every tile id fits (2 B less per entry and pass in the sort)
+    c->keys16 = fc.n_tiles <= 65536;
+    const size_t kbytes = c->keys16 ? 2 : 4;
+    void *tk = ENSURE(char, c->tile_keys, total * kbytes);
+    void *tks = ENSURE(char, c->tile_keys_sorted, total * kbytes);
     uint32_t *gids = ENSURE(uint32_t, c->gids, total);
     uint32_t *order = ENSURE(uint32_t, c->order, total);
     int32_t *brank = ENSURE(int32_t, c->block_rank, emit_blocks(total) + 1);
-    emit_entries(offs, gsorted, ar, fc.n_x, total, n, brank, tk, gids, st);
+    if (c->keys16)
+        emit_entries(offs, gsorted, ar, fc.n_x, total, n, brank, (uint16_t *)tk, gids, st);
+    else
+        emit_entries(offs, gsorted, ar, fc.n_x, total, n, brank, (uint32_t *)tk, gids, st);
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[2], st));
 
     // ---- sort: stable tile sort + ranges
     if (total > 0) {
         int bits = ceil_log2(fc.n_tiles);
-        size_t b = sort_tiles_temp_bytes(total, bits);
-        void *tmp = ENSURE(char, c->temp, b);
-        sort_tiles(tmp, b, tk, tks, gids, order, total, bits, st);
+        if (c->keys16) {
+            size_t b = sort_tiles_temp_bytes<uint16_t>(total, bits);
+            void *tmp = ENSURE(char, c->temp, b);
+            sort_tiles(tmp, b, (const uint16_t *)tk, (uint16_t *)tks, gids, order, total, bits, st);
+        } else {
+            size_t b = sort_tiles_temp_bytes<uint32_t>(total, bits);
+            void *tmp = ENSURE(char, c->temp, b);
+            sort_tiles(tmp, b, (const uint32_t *)tk, (uint32_t *)tks, gids, order, total, bits, st);
+        }
     }
-    tile_ranges(tks, total, fc.n_tiles, ranges, st);
+    if (c->keys16)
+        tile_ranges((const uint16_t *)tks, total, fc.n_tiles, ranges, st);
+    else
+        tile_ranges((const uint32_t *)tks, total, fc.n_tiles, ranges, st);
     int4 *work = ENSURE(int4, c->work, c->max_items);
     int32_t *nwork = ENSURE(int32_t, c->n_work, 2);
     order_items((const int4 *)c->items.p, (const int32_t *)c->n_items.p, ranges, c->max_items, work, nwork, st);
@@ -585,8 +601,20 @@ int geer_graph_export(geer_ctx *c, int64_t *order, int64_t *entry_tile, int64_t 
     const int64_t n = c->scene.n, E = c->n_entries, npx = (int64_t)fc.width * fc.height;
     int rc = d2h_u32_as_i64(c->order.p, order, E);
     if (rc) return rc;
-    rc = d2h_u32_as_i64(c->tile_keys_sorted.p, entry_tile, E);
-    if (rc) return rc;
+    if (c->keys16 && entry_tile && E > 0) {
+        uint16_t *tmp = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)E);
+        if (!tmp) return fail(GEER_ERR_NOMEM, "host allocation failed");
+        cudaError_t e = cudaMemcpy(tmp, c->tile_keys_sorted.p, sizeof(uint16_t) * (size_t)E, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) {
+            free(tmp);
+            return fail(GEER_ERR_CUDA, "graph export copy failed: %s", cudaGetErrorString(e));
+        }
+        for (int64_t i = 0; i < E; ++i) entry_tile[i] = (int64_t)tmp[i];
+        free(tmp);
+    } else {
+        rc = d2h_u32_as_i64(c->tile_keys_sorted.p, entry_tile, E);
+        if (rc) return rc;
+    }
     if (ranges) {
         rc = d2h_u32_as_i64(c->tile_ranges.p, ranges, fc.n_tiles + 1);
         if (rc) return rc;

@@ -750,10 +750,12 @@ __device__ void fixup_pixel(FrameConst fc, const geer_scene &sc, const int4 *__r
         const int e = base + lane;
         double t = 0.0;
         uint32_t g = 0;
+        float4 cl = make_float4(0.f, 0.f, 0.f, 0.f);
         if (e < e1) {
             // fp64 kappa (payload quadratic forms / cross product), fp64 exp: renderer.py:96-105 in fp64
             g = order[e];
             const Payload &P = payload[g];
+            cl = P.col;
             double dd, mm;
             norms64(P, R, d, P.col.w < 0.0f, dd, mm);
             double kap = mm / dd;
@@ -769,13 +771,13 @@ __device__ void fixup_pixel(FrameConst fc, const geer_scene &sc, const int4 *__r
         const int n = min(32, e1 - base);
         for (int j = 0; j < n; ++j) {
             const double tj = __shfl_sync(0xffffffffu, t, j);
-            const uint32_t gj = __shfl_sync(0xffffffffu, g, j);
+            const float4 col = make_float4(__shfl_sync(0xffffffffu, cl.x, j), __shfl_sync(0xffffffffu, cl.y, j),
+                                           __shfl_sync(0xffffffffu, cl.z, j), 0.f);
             if (!(rem >= kMinRemaining)) {
                 alive = false;
                 break;
             }
             ++ne;
-            const float4 col = payload[gj].col;
             const double w = rem * tj;
             cr += w * col.x;
             cg += w * col.y;

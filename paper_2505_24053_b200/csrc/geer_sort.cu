@@ -40,13 +40,15 @@ size_t scan_i32_temp_bytes(int64_t n) {
     return bytes;
 }
 
+template <typename K>
 size_t sort_tiles_temp_bytes(int64_t n_entries, int n_bits) {
     size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)n_entries, 0,
-                                    n_bits > 0 ? n_bits : 1);
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const K *)nullptr, (K *)nullptr, (const uint32_t *)nullptr,
+                                    (uint32_t *)nullptr, (int)n_entries, 0, n_bits > 0 ? n_bits : 1);
     return bytes;
 }
+template size_t sort_tiles_temp_bytes<uint16_t>(int64_t, int);
+template size_t sort_tiles_temp_bytes<uint32_t>(int64_t, int);
 
 size_t sort_pixels_temp_bytes(int64_t n, int n_bits) {
     size_t bytes = 0;
@@ -60,11 +62,16 @@ void sort_depth(void *temp, size_t temp_bytes, const uint32_t *keys_in, uint32_t
     cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n, 0, 32, st);
 }
 
-void sort_tiles(void *temp, size_t temp_bytes, const uint32_t *keys_in, uint32_t *keys_out, const uint32_t *vals_in,
+template <typename K>
+void sort_tiles(void *temp, size_t temp_bytes, const K *keys_in, K *keys_out, const uint32_t *vals_in,
                 uint32_t *vals_out, int64_t n, int n_bits, cudaStream_t st) {
     cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n, 0,
                                     n_bits > 0 ? n_bits : 1, st);
 }
+template void sort_tiles<uint16_t>(void *, size_t, const uint16_t *, uint16_t *, const uint32_t *, uint32_t *, int64_t,
+                                   int, cudaStream_t);
+template void sort_tiles<uint32_t>(void *, size_t, const uint32_t *, uint32_t *, const uint32_t *, uint32_t *, int64_t,
+                                   int, cudaStream_t);
 
 void sort_pixels(void *temp, size_t temp_bytes, const int32_t *keys_in, int32_t *keys_out, const int32_t *vals_in,
                  int32_t *vals_out, int64_t n, int n_bits, cudaStream_t st) {
@@ -131,10 +138,11 @@ __global__ void k_block_ranks(const int64_t *__restrict__ offs, int64_t n, int64
 // once (gid, axis ranges, local start), each rank marks the position of its first entry, and an
 // inclusive max-scan over the positions gives every entry its rank; entries are then decoded from
 // shared memory and written with coalesced stores.
+template <typename K>
 __global__ void __launch_bounds__(256) k_emit(const int64_t *__restrict__ offs, const int32_t *__restrict__ block_rank,
                                               const int32_t *__restrict__ sorted_gid,
                                               const AxisRanges *__restrict__ ranges, int n_x, int64_t n_entries,
-                                              int64_t n, uint32_t *__restrict__ tile_keys, uint32_t *__restrict__ gids) {
+                                              int64_t n, K *__restrict__ tile_keys, uint32_t *__restrict__ gids) {
     __shared__ int s_pos[kEmitPerBlock];
     __shared__ int s_start[kEmitPerBlock + 1];
     __shared__ uint32_t s_g[kEmitPerBlock + 1];
@@ -189,24 +197,30 @@ __global__ void __launch_bounds__(256) k_emit(const int64_t *__restrict__ offs, 
         const int ky = k / cx;
         const int iy = range_index(ar.y, ky);
         const int ix = range_index(ar.x, k - ky * cx);
-        tile_keys[e_begin + j] = (uint32_t)(iy * n_x + ix);
+        tile_keys[e_begin + j] = (K)(iy * n_x + ix);
         gids[e_begin + j] = s_g[rl];
     }
 }
 
 int64_t emit_blocks(int64_t n_entries) { return (n_entries + kEmitPerBlock - 1) / kEmitPerBlock; }
 
+template <typename K>
 void emit_entries(const int64_t *offs, const int32_t *sorted_gid, const AxisRanges *ranges, int n_x,
-                  int64_t n_entries, int64_t n, int32_t *block_rank, uint32_t *tile_keys, uint32_t *gids,
+                  int64_t n_entries, int64_t n, int32_t *block_rank, K *tile_keys, uint32_t *gids,
                   cudaStream_t st) {
     if (n_entries <= 0) return;
     const int64_t blocks = emit_blocks(n_entries);
     k_block_ranks<<<(unsigned)lmin((n + 255) / 256, 148 * 16), 256, 0, st>>>(offs, n, n_entries, (int)blocks, block_rank);
-    k_emit<<<(unsigned)blocks, 256, 0, st>>>(offs, block_rank, sorted_gid, ranges, n_x, n_entries, n, tile_keys, gids);
+    k_emit<K><<<(unsigned)blocks, 256, 0, st>>>(offs, block_rank, sorted_gid, ranges, n_x, n_entries, n, tile_keys, gids);
 }
+template void emit_entries<uint16_t>(const int64_t *, const int32_t *, const AxisRanges *, int, int64_t, int64_t,
+                                     int32_t *, uint16_t *, uint32_t *, cudaStream_t);
+template void emit_entries<uint32_t>(const int64_t *, const int32_t *, const AxisRanges *, int, int64_t, int64_t,
+                                     int32_t *, uint32_t *, uint32_t *, cudaStream_t);
 
 // ranges[t] = first entry with tile >= t (np.searchsorted(tiles, arange(n_tiles + 1)))
-__global__ void k_ranges(const uint32_t *__restrict__ tiles, int64_t n_entries, int n_tiles, int32_t *__restrict__ ranges) {
+template <typename K>
+__global__ void k_ranges(const K *__restrict__ tiles, int64_t n_entries, int n_tiles, int32_t *__restrict__ ranges) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= n_entries; e += (int64_t)gridDim.x * blockDim.x) {
         int prev = e == 0 ? -1 : (int)tiles[e - 1];
         int cur = e == n_entries ? n_tiles : (int)tiles[e];
@@ -249,9 +263,12 @@ void order_items(const int4 *items, const int32_t *n_items, const int32_t *range
     k_order_items<<<(max_items + 255) / 256, 256, 0, st>>>(items, n_items, ranges, max_items, work, n_work);
 }
 
-void tile_ranges(const uint32_t *sorted_tiles, int64_t n_entries, int n_tiles, int32_t *ranges, cudaStream_t st) {
+template <typename K>
+void tile_ranges(const K *sorted_tiles, int64_t n_entries, int n_tiles, int32_t *ranges, cudaStream_t st) {
     int blocks = (int)lmin((n_entries + 1 + 255) / 256, 148 * 16);
-    k_ranges<<<blocks, 256, 0, st>>>(sorted_tiles, n_entries, n_tiles, ranges);
+    k_ranges<K><<<blocks, 256, 0, st>>>(sorted_tiles, n_entries, n_tiles, ranges);
 }
+template void tile_ranges<uint16_t>(const uint16_t *, int64_t, int, int32_t *, cudaStream_t);
+template void tile_ranges<uint32_t>(const uint32_t *, int64_t, int, int32_t *, cudaStream_t);
 
 }  // namespace geer
