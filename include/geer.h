@@ -168,6 +168,11 @@ int geer_l1_grad(const float *color, const float *target, const uint8_t *mask, f
 int geer_adam(float *param, const float *grad, float *m, float *v, const float *lr, int64_t n, float beta1,
               float beta2, float eps, int32_t step, void *stream);
 
+/* ---- diagnostics ------------------------------------------------------------- */
+/* Measured FP32 FMA throughput of the device (scalar FFMA and packed FFMA2 chains), TFLOP/s: the
+ * roofline denominator of the FP32-bound raster kernels (bench.py). */
+int geer_measure_fp32_peak(int device, double *tflops_scalar, double *tflops_packed);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,7 +30,7 @@ MODEL_IDS = {"pinhole": 0, "kb": 1, "beap": 2}
 EXPORTED = (
     "geer_abi_version", "geer_last_error", "geer_create", "geer_destroy", "geer_set_timing", "geer_forward",
     "geer_backward", "geer_frame_stats", "geer_graph_info", "geer_graph_export", "geer_build_graph_host",
-    "geer_render_host", "geer_render_backward_host", "geer_l1_grad", "geer_adam",
+    "geer_render_host", "geer_render_backward_host", "geer_l1_grad", "geer_adam", "geer_measure_fp32_peak",
 )
 
 
@@ -121,6 +121,7 @@ def load():
             "geer_render_backward_host": ([P, P, P, P, P, P], I),
             "geer_l1_grad": ([P, P, P, P, I64, F, P], I),
             "geer_adam": ([P, P, P, P, P, I64, F, F, F, ctypes.c_int32, P], I),
+            "geer_measure_fp32_peak": ([I, P, P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

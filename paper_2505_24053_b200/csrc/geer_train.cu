@@ -68,3 +68,70 @@ int geer_adam(float *param, const float *grad, float *m, float *v, const float *
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- diagnostics: FP32 FMA peak
+// The raster's roofline denominator (MEASURED_PEAKS.json has HBM and bf16 only): every thread runs
+// independent FMA chains, scalar FFMA or packed FFMA2 (fma.rn.f32x2, sm_100a); flops = 2 per lane-FMA.
+namespace {
+template <bool kPacked>
+__global__ void __launch_bounds__(256) k_fma_peak(float *out, int iters, float b) {
+    float a[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[k] = threadIdx.x * 1e-3f + k;
+    for (int i = 0; i < iters; ++i) {
+        if (kPacked) {
+#pragma unroll
+            for (int k = 0; k < 16; k += 2) {
+                unsigned long long x = ((unsigned long long)__float_as_uint(a[k + 1]) << 32) | __float_as_uint(a[k]);
+                const unsigned long long y = ((unsigned long long)__float_as_uint(b) << 32) | __float_as_uint(b);
+                asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(x) : "l"(y));
+                a[k] = __uint_as_float((unsigned)x);
+                a[k + 1] = __uint_as_float((unsigned)(x >> 32));
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) a[k] = fmaf(a[k], b, b);
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += a[k];
+    if (s == 12345.678f) out[0] = s;  // keep the chains alive
+}
+}  // namespace
+
+extern "C" int geer_measure_fp32_peak(int device, double *tflops_scalar, double *tflops_packed) {
+    if (cudaSetDevice(device) != cudaSuccess) return GEER_ERR_CUDA;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    float *out = nullptr;
+    if (cudaMalloc(&out, sizeof(float)) != cudaSuccess) return GEER_ERR_CUDA;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 4096, blocks = sms * 8;
+    double res[2] = {0, 0};
+    for (int packed = 0; packed < 2; ++packed) {
+        float best = 1e30f;
+        for (int rep = 0; rep < 4; ++rep) {
+            cudaEventRecord(e0);
+            if (packed)
+                k_fma_peak<true><<<blocks, 256>>>(out, iters, 0.999f);
+            else
+                k_fma_peak<false><<<blocks, 256>>>(out, iters, 0.999f);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (rep > 0 && ms < best) best = ms;  // first launch is warm-up
+        }
+        const double flops = 2.0 * 16.0 * iters * (double)blocks * 256.0;
+        res[packed] = flops / (best * 1e-3) / 1e12;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (tflops_scalar) *tflops_scalar = res[0];
+    if (tflops_packed) *tflops_packed = res[1];
+    return cudaGetLastError() == cudaSuccess ? GEER_OK : GEER_ERR_CUDA;
+}
