@@ -412,6 +412,13 @@ def run_ours(args):
         except Exception as exc:
             extra["train_step"] = {"error": repr(exc)}
 
+    # ---- config 5: 6M Gaussians, 3840x2160 equidistant (KB, k = 0) fisheye, forward (each rank one view)
+    if not args.no_c5:
+        try:
+            extra["c5"] = run_c5(args, rank, world, local)
+        except Exception as exc:
+            extra["c5"] = {"error": repr(exc)}
+
     # ---- CPU baseline (rank 0, N=1 only): the fp64 C port of the reference path on this host
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -443,6 +450,46 @@ def run_ours(args):
     barrier(world)
 
 
+def run_c5(args, rank, world, local):
+    """BASELINE config 5 forward: K frames timed with CUDA events (max over ranks), stage times, stats."""
+    import torch
+
+    from paper_2505_24053_b200 import renderer, synth
+    from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene
+
+    scene = synth.config_scene("C5")
+    cam = synth.config_camera("C5")
+    ds = DeviceScene.from_scene(scene, device=f"cuda:{local}")
+    del scene
+    r = DeviceRenderer(local)
+    cfg = renderer.RenderConfig()
+    out = (torch.empty((cam.height, cam.width, 3), dtype=torch.float32, device="cuda"),
+           torch.empty((cam.height, cam.width), dtype=torch.float32, device="cuda"),
+           torch.empty((cam.height, cam.width), dtype=torch.int32, device="cuda"))
+    for _ in range(3):
+        r.forward(ds, cam, cfg, out=out)
+    torch.cuda.synchronize()
+    k = max(3, min(args.steps, 10))
+    barrier(world)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(k):
+        r.forward(ds, cam, cfg, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = allreduce_max(e0.elapsed_time(e1), world) / k
+    r.set_timing(True)
+    r.forward(ds, cam, cfg, out=out)
+    st = r.stats()
+    r.set_timing(False)
+    return {"workload": "C5: 6M Gaussians, 3840x2160 equidistant KB fisheye (hFoV 180 deg), forward",
+            "fps": world * 1e3 / ms, "ms_per_frame": ms, "mrays_per_s": world * 1e3 / ms * cam.width * cam.height / 1e6,
+            "steps": k, "entries": int(st["n_entries"]), "work_items": int(st["n_work_items"]),
+            "evaluated_pairs": int(st["evaluated_pairs"]),
+            "stages_ms": {key: st["ms_" + key] for key in ("prep", "dup", "sort", "render", "total")}}
+
+
 def _pinned_copy(a):
     import torch
 
@@ -463,6 +510,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -111,3 +111,16 @@ def test_full_c2_association_and_forward_vs_oracle():
     rep = P.assert_image_close(fr.color.color, fr.remaining_transmittance, fr.contributor_count, of.color,
                                of.remaining, of.count)
     print("C2 image parity", rep, "entries", len(g.order))
+
+
+def test_full_c3_backward_vs_oracle():
+    """BASELINE config 3 at full size: 1M-Gaussian gradients (means/scales/rotations/opacity/SH) vs the oracle."""
+    scene = synth.config_scene("C2")
+    cam = synth.config_camera("C2")
+    cfg = renderer.RenderConfig()
+    dl = np.random.default_rng(1).standard_normal((1080, 1920, 3)) / (1080 * 1920)
+    og = O.build_render_graph(scene, cam)
+    ob = O.render_backward(scene, cam, dl, cfg, graph=og)
+    gr = renderer.render_backward(scene, cam, dl, cfg)
+    rep = P.assert_grads_close(gr, vars(ob))
+    print("C3 gradient parity", rep)
