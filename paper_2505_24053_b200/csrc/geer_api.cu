@@ -72,7 +72,7 @@ struct geer_ctx {
     Buf col_sc, row_sc, medges_x, medges_y, edges_x, edges_y, dir64, theta, phi, minmax, pixel_tile, pixel_tile_sorted,
         pix_iota, pix_list, tile_count, tile_off, item_count, item_off, items, n_items, work, n_work;
     // per-Gaussian buffers
-    Buf payload, gpayload, box, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, cnt_sorted, offs, ranges_ax, flags, mu_c,
+    Buf payload, gpayload, cull, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, cnt_sorted, offs, ranges_ax, flags, mu_c,
         depth;
     // per-entry buffers
     Buf tile_keys, tile_keys_sorted, gids, order, tile_ranges, block_rank;
@@ -242,7 +242,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     // ---- K1 preprocess
     Payload *payload = ENSURE(Payload, c->payload, n);
     GradPayload *gpayload = ENSURE(GradPayload, c->gpayload, n);
-    float4 *box = ENSURE(float4, c->box, n);
+    Cull *cull = ENSURE(Cull, c->cull, n);
     uint32_t *dkey = ENSURE(uint32_t, c->depth_key, n);
     uint32_t *dkey_s = ENSURE(uint32_t, c->depth_key_sorted, n);
     int32_t *giota = ENSURE(int32_t, c->gid_iota, n);
@@ -259,7 +259,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     }
     int32_t *ranges = ENSURE(int32_t, c->tile_ranges, fc.n_tiles + 1);
     launch_preprocess(fc, sc, (const double *)c->medges_x.p, (const double *)c->medges_y.p, payload, gpayload, dkey, cnt, ar,
-                      flags, box, mu, dep, c->d_err, st);
+                      flags, cull, mu, dep, c->d_err, st);
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[1], st));
 
     // ---- dup: depth order, scan, header D2H, emit
@@ -329,7 +329,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         int32_t *fix = ENSURE(int32_t, c->fixup, npx);
         launch_forward(fc, sc, c->max_items, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
                        (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
-                       (const double *)c->dir64.p, ranges, order, payload, flags, box, color, remaining, count, ne,
+                       (const double *)c->dir64.p, ranges, order, payload, flags, cull, color, remaining, count, ne,
                        c->d_counters, fix, st);
         c->fwd_remaining = remaining;
         c->have_raster = true;
@@ -359,7 +359,7 @@ int run_backward(geer_ctx *c, const float *dl_dimage, bool f64_out, void *const 
                     (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
                     (const double *)c->dir64.p, (const int32_t *)c->tile_ranges.p, (const uint32_t *)c->order.p,
                     (const Payload *)c->payload.p, (const GradPayload *)c->gpayload.p, (const uint8_t *)c->flags.p,
-                    (const float4 *)c->box.p, c->fwd_remaining, (const int32_t *)c->n_eval.p,
+                    (const Cull *)c->cull.p, c->fwd_remaining, (const int32_t *)c->n_eval.p,
                     dl_dimage, accum, st);
     if (f64_out)
         launch_finalize<double>(fc, sc, (const float4 *)accum, (const uint8_t *)c->flags.p, (double *)gout[0], (double *)gout[1],
@@ -469,7 +469,7 @@ void geer_destroy(geer_ctx *c) {
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     Buf *bufs[] = {&c->col_sc, &c->row_sc, &c->medges_x, &c->medges_y, &c->edges_x, &c->edges_y, &c->dir64,
                    &c->theta, &c->phi, &c->minmax, &c->pixel_tile, &c->pixel_tile_sorted, &c->pix_iota, &c->pix_list,
-                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->work, &c->n_work, &c->payload, &c->gpayload, &c->box,
+                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->work, &c->n_work, &c->payload, &c->gpayload, &c->cull,
                    &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted, &c->count, &c->cnt_sorted,
                    &c->offs, &c->ranges_ax, &c->flags, &c->mu_c, &c->depth, &c->tile_keys, &c->tile_keys_sorted,
                    &c->gids, &c->order, &c->tile_ranges, &c->block_rank, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,

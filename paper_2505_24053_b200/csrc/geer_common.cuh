@@ -54,6 +54,14 @@ struct __align__(16) GradPayload {
     float4 r0, r1, r2;
 };
 
+// Raster culling record of one Gaussian (48 B, written by K1, streamed with the payload):
+//   box  = PBF hull in camera-frame mirror space (x_lo, x_hi, y_lo, y_hi), outward-rounded
+//   k0, k1 = visual-cone matrix K (K00, K11, K22, K01 | K02, K12, lambda_max bound, 0), see cone_misses
+struct __align__(16) Cull {
+    float4 box;
+    float4 k0, k1;
+};
+
 // Per-axis tile ranges: up to 3 disjoint [lo, hi) pairs packed lo | hi << 16.
 struct AxisRanges {
     uint32_t x[3];

@@ -511,7 +511,7 @@ __device__ __forceinline__ void named_barrier(int id, int count) {
 // sex / sey: the mirror tile edges in shared memory.  Returns the keep / clamped flag bits.
 __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, const double *sex, const double *sey,
                                  int64_t g, uint32_t *__restrict__ depth_key, int64_t *__restrict__ count,
-                                 AxisRanges *__restrict__ ranges, float4 *__restrict__ box,
+                                 AxisRanges *__restrict__ ranges, Cull *__restrict__ cull,
                                  double *__restrict__ mu_out, double *__restrict__ depth_out, int *__restrict__ err) {
 
     const double *R = fc.R;
@@ -548,6 +548,11 @@ __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, con
     for (int i = 0; i < 3; ++i) ar.x[i] = ar.y[i] = 0;
     // raster culling bounds in mirror space (x_lo, x_hi, y_lo, y_hi); clamped: everything
     float4 bx = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
+    // raster culling: the visual cone of the lam-ellipsoid (camera frame, full line).  With P = Sigma_c^-1,
+    // nu = P mu, a = mu^T nu - lam^2 > 0 (camera outside):  kappa(d) <= lam^2  <=>  d^T K d >= 0,
+    // K = nu nu^T - a P, stored divided by nu^T nu (then lambda_max(K) <= 1).  .b.z: lambda_max bound
+    // (inf: never cull, e.g. clamped or camera inside)
+    float4 ca = make_float4(0.f, 0.f, 0.f, 0.f), cb = make_float4(0.f, 0.f, INFINITY, 0.f);
     // association.py:417-419 near cull
     if (depth >= kNearLimit) {
         // association.py:154-160 symmetric + positive-definite (Cholesky pivots)
@@ -612,13 +617,37 @@ __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, con
                     const int cx = axis_tiles(t00, t02, t22, rt0, rt1, sex, fc.n_x + 1, ar.x, bx.x, bx.y);
                     const int cy = axis_tiles(t11, t12, t22, rp0, rp1, sey, fc.n_y + 1, ar.y, bx.z, bx.w);
                     n_ent = (int64_t)cx * cy;
+                    // Q = R_c R(q): camera frame <- Gaussian axes;  P = Q diag(1/s^2) Q^T
+                    double Q[9], P[9], nu[3];
+                    for (int i = 0; i < 3; ++i)
+                        for (int j = 0; j < 3; ++j)
+                            Q[i * 3 + j] = R[i * 3 + 0] * rot[0 * 3 + j] + R[i * 3 + 1] * rot[1 * 3 + j] +
+                                           R[i * 3 + 2] * rot[2 * 3 + j];
+                    const double is2[3] = {1.0 / (s[0] * s[0]), 1.0 / (s[1] * s[1]), 1.0 / (s[2] * s[2])};
+                    for (int i = 0; i < 3; ++i)
+                        for (int j = 0; j < 3; ++j)
+                            P[i * 3 + j] = Q[i * 3 + 0] * is2[0] * Q[j * 3 + 0] + Q[i * 3 + 1] * is2[1] * Q[j * 3 + 1] +
+                                           Q[i * 3 + 2] * is2[2] * Q[j * 3 + 2];
+                    for (int i = 0; i < 3; ++i) nu[i] = P[i * 3 + 0] * mu[0] + P[i * 3 + 1] * mu[1] + P[i * 3 + 2] * mu[2];
+                    const double a = mu[0] * nu[0] + mu[1] * nu[1] + mu[2] * nu[2] - lam2;
+                    const double nn = nu[0] * nu[0] + nu[1] * nu[1] + nu[2] * nu[2];
+                    if (a > 0.0 && nn > 0.0) {
+                        const double in = 1.0 / nn;
+                        auto K = [&](int i, int j) { return (float)((nu[i] * nu[j] - a * P[i * 3 + j]) * in); };
+                        ca = make_float4(K(0, 0), K(1, 1), K(2, 2), K(0, 1));
+                        cb = make_float4(K(0, 2), K(1, 2), 1.0f, 0.f);
+                    }
                 }
             }
         }
     }
     count[g] = n_ent;
     ranges[g] = ar;
-    box[g] = bx;
+    Cull cr;
+    cr.box = bx;
+    cr.k0 = ca;
+    cr.k1 = cb;
+    cull[g] = cr;
     // association.py:335-340 key bits (depth > 0): f32 bits | 0x80000000; non-emitting last
     const uint32_t kb = __float_as_uint((float)depth) | 0x80000000u;
     depth_key[g] = n_ent > 0 ? kb : 0xFFFFFFFFu;
@@ -720,8 +749,8 @@ __global__ void __launch_bounds__(256, 3)
     k_preprocess(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x, const double *__restrict__ medges_y,
                  Payload *__restrict__ payload, GradPayload *__restrict__ gpayload, uint32_t *__restrict__ depth_key,
                  int64_t *__restrict__ count, AxisRanges *__restrict__ ranges, uint8_t *__restrict__ flags,
-                 float4 *__restrict__ box, double *__restrict__ mu_out, double *__restrict__ depth_out,
-                 int *__restrict__ err) {
+                 Cull *__restrict__ cull, double *__restrict__ mu_out,
+                 double *__restrict__ depth_out, int *__restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(16) float ssh[128 * (NB * 3 > 48 ? NB * 3 : 48)];
     __shared__ uint8_t sfl[2][128];
@@ -734,8 +763,8 @@ __global__ void __launch_bounds__(256, 3)
         for (int i = lt; i <= fc.n_x; i += 128) sex[i] = medges_x[i];
         for (int i = lt; i <= fc.n_y; i += 128) sey[i] = medges_y[i];
         named_barrier(1, 128);
-        sfl[0][lt] = lt < cnt_b ? associate_one(fc, sc, sex, sey, g0 + lt, depth_key, count, ranges, box, mu_out,
-                                                depth_out, err)
+        sfl[0][lt] = lt < cnt_b ? associate_one(fc, sc, sex, sey, g0 + lt, depth_key, count, ranges, cull,
+                                                mu_out, depth_out, err)
                                 : 0;
     } else {
         sfl[1][lt] = payload_block<NB>(fc, sc, ssh, g0, cnt_b, lt, payload, gpayload);
@@ -894,14 +923,16 @@ size_t preprocess_smem(const FrameConst &fc) { return sizeof(double) * (fc.n_x +
 
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
                        Payload *payload, GradPayload *gpayload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges,
-                       uint8_t *flags, float4 *box, double *mu_out, double *depth_out, int *err, cudaStream_t st) {
+                       uint8_t *flags, Cull *cull, double *mu_out, double *depth_out, int *err,
+                       cudaStream_t st) {
     if (sc.n == 0) return;
     const int blocks = (int)((sc.n + 127) / 128);
     switch (sc.n_bands) {
 #define GEER_NB_CASE(NB)                                                                                            \
     case NB:                                                                                                        \
         k_preprocess<NB><<<blocks, 256, preprocess_smem(fc), st>>>(fc, sc, medges_x, medges_y, payload, gpayload,   \
-                                                                   depth_key, count, ranges, flags, box, mu_out,   \
+                                                                   depth_key, count, ranges, flags, cull,          \
+                                                                   mu_out,                                         \
                                                                    depth_out, err);                                \
         break;
         GEER_NB_CASE(1) GEER_NB_CASE(2) GEER_NB_CASE(3) GEER_NB_CASE(4) GEER_NB_CASE(5) GEER_NB_CASE(6)

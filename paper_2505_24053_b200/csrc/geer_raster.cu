@@ -225,13 +225,13 @@ template <bool kGrad>
 struct __align__(16) PipeSmem {
     Payload ring[kStages][kStageEntries + 1];  // slot kStageEntries: a null entry (t = 0 for every ray)
     GradPayload gring[kGrad ? kStages : 1][kStageEntries];  // backward only
+    Cull cring[kStages][kStageEntries];                     // culling records of the stage's entries
     uint32_t gid[kStages][kStageEntries];
     int count[kStages];  // entries in the stage; 0 = end of stream
-    int mode1[kStages];  // 1 if any entry of the stage carries a mode-1 (cross-product) payload
-    uint32_t mask[kStages][kConsumerWarps];  // per consumer warp: entries of the stage its patch may see
-    uint8_t idx[kStages][kConsumerWarps][kStageEntries + 4];  // the same entries as a list, padded with null slots
-    int cnt[kStages][kConsumerWarps];                          // entries in that list
+    uint8_t idx[kStages][kConsumerWarps][kStageEntries + 4];  // per warp: its kept entries, padded with null slots
     float4 patch[kConsumerWarps];            // per consumer warp: mirror-space bounds of its pixels
+    float4 pcone[kConsumerWarps];            // per consumer warp: cone around its pixel rays (cam frame)
+                                             // (unit axis c, cos^2 beta), see cone_misses
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     int done_warps;
@@ -302,24 +302,53 @@ __device__ __forceinline__ void pipe_init(Smem &S) {
     __syncthreads();
 }
 
+// True when no ray of a warp's cone can meet the Gaussian's lam-ellipsoid along its full line.
+// A ray d meets it iff g(d) = d^T K d >= 0 (K from k_preprocess: the ellipsoid's visual cone,
+// equivalent to kappa(d) <= lam^2).  For unit d within angle beta <= 45 deg of the cone axis c:
+// g(d) <= cos^2(beta) g(c) + sin(2 beta) |P_perp K c| + sin^2(beta) lambda_max(K)  (for g(c) < 0).
+// The test is made on squares, with a margin far above the fp32 error of K (entries <= ~1 after
+// normalisation).  pc = (c, cos^2 beta); tb.z = lambda_max bound (+inf: never culled).
+__device__ __forceinline__ bool cone_misses(const float4 &ta, const float4 &tb, const float4 &pc) {
+    const float t00 = ta.x, t11 = ta.y, t22 = ta.z, t01 = ta.w, t02 = tb.x, t12 = tb.y, lmax = tb.z;  // K entries
+    const float tc0 = t00 * pc.x + t01 * pc.y + t02 * pc.z;
+    const float tc1 = t01 * pc.x + t11 * pc.y + t12 * pc.z;
+    const float tc2 = t02 * pc.x + t12 * pc.y + t22 * pc.z;
+    const float gc = tc0 * pc.x + tc1 * pc.y + tc2 * pc.z;
+    const float p2 = fmaxf(tc0 * tc0 + tc1 * tc1 + tc2 * tc2 - gc * gc, 0.0f);  // |P_perp T c|^2
+    const float c2 = pc.w, s2 = 1.0f - pc.w;                                      // cos^2, sin^2 beta
+    const float tnorm = fabsf(t00) + fabsf(t11) + fabsf(t22) + 2.0f * (fabsf(t01) + fabsf(t02) + fabsf(t12));
+    const float lhs = c2 * gc + s2 * fmaxf(lmax, 0.0f) + 1e-5f * tnorm + 1e-30f;  // must be < -sin(2b) p
+    return lhs < 0.0f && lhs * lhs > 4.0f * s2 * c2 * p2;                          // sin^2(2b) = 4 s2 c2
+}
+
 // Producer warp: stream entries [first, first + n_total) (forward order) or the
 // same range walked from the back (reverse) in stages of kStageEntries.
 template <bool kReverse, class Smem>
 __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict__ order,
                                              const Payload *__restrict__ payload,
-                                             const GradPayload *__restrict__ gpayload,
-                                             const uint8_t *__restrict__ flags, const float4 *__restrict__ box,
-                                             bool cull, int first, int n_total, bool stop_when_done) {
-    const unsigned per_entry = (unsigned)(sizeof(Payload) + (gpayload ? sizeof(GradPayload) : 0));
+                                             const GradPayload *__restrict__ gpayload, const Cull *__restrict__ cull,
+                                             int first, int n_total, bool stop_when_done) {
+    const unsigned per_entry =
+        (unsigned)(sizeof(Payload) + (gpayload ? sizeof(GradPayload) : 0) + (cull ? sizeof(Cull) : 0));
     const int lane = threadIdx.x & 31;
+    // gid of this lane's entry in stage bb (the order load runs one stage ahead of the copies)
+    auto load_gid = [&](int bb) -> uint32_t {
+        const int done = kStageEntries * bb;
+        const int n = min(kStageEntries, n_total - done);
+        const int base = kReverse ? first + n_total - done - n : first + done;
+        return lane < n ? __ldg(order + base + lane) : 0u;
+    };
     unsigned phase = 0;
     int s = 0, b = 0;
     bool sentinel = false;
+    uint32_t g_next = load_gid(0);
     for (;; ++b) {
         const int done = kStageEntries * b;
         const int n = min(kStageEntries, n_total - done);
         // every consumer warp has dropped out: stop streaming (no sentinel needed)
         if (stop_when_done && *((volatile int *)&S.done_warps) == kConsumerWarps) break;
+        const uint32_t g = g_next;
+        if (n > 0) g_next = load_gid(b + 1);
         mbar_wait(&S.empty[s], phase ^ 1);
         if (n <= 0) {
             if (lane == 0) {
@@ -329,44 +358,17 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
             sentinel = true;
             break;
         }
-        // reverse: stage b holds entries [first + n_total - done - n, first + n_total - done)
-        const int base = kReverse ? first + n_total - done - n : first + done;
-        uint32_t g = 0;
-        bool m1 = false;
-        float4 bx = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
-        if (lane < n) {
-            g = __ldg(order + base + lane);
-            S.gid[s][lane] = g;
-            m1 = (__ldg(flags + g) >> 6) & 1;
-            if (cull) bx = __ldg(box + g);
-        }
-        const bool any_m1 = __any_sync(0xffffffffu, m1);
-        // Per-warp PBF culling: a pixel ray can have kappa <= lam^2 only if its camera-frame mirror
-        // coordinates lie inside the Gaussian's PBF intervals (association.py:189-217); entries whose
-        // bounds miss a warp's whole pixel patch contribute exactly nothing to it (t = 0).
-        uint32_t my_mask = 0;
-#pragma unroll
-        for (int w = 0; w < kConsumerWarps; ++w) {
-            const float4 P = S.patch[w];
-            const bool ov = lane < n && !(bx.y < P.x || bx.x > P.y || bx.w < P.z || bx.z > P.w);
-            const uint32_t m = __ballot_sync(0xffffffffu, ov);
-            if (lane == w) my_mask = m;
-            const int c = __popc(m);
-            if (ov) S.idx[s][w][__popc(m & ((1u << lane) - 1u))] = (uint8_t)lane;
-            if (lane < 4) S.idx[s][w][c + lane] = (uint8_t)kStageEntries;  // pad to a multiple of 4
-            if (lane == 0) S.cnt[s][w] = c;
-        }
-        if (lane < kConsumerWarps) S.mask[s][lane] = my_mask;
+        if (lane < n) S.gid[s][lane] = g;
         __syncwarp();
         if (lane == 0) {
             S.count[s] = n;
-            S.mode1[s] = any_m1 ? 1 : 0;
             mbar_arrive_expect_tx(&S.full[s], n * per_entry);
         }
         __syncwarp();
         if (lane < n) {
             bulk_g2s(&S.ring[s][lane], payload + g, sizeof(Payload), &S.full[s]);
             if (gpayload) bulk_g2s(&S.gring[gpayload ? s : 0][lane], gpayload + g, sizeof(GradPayload), &S.full[s]);
+            if (cull) bulk_g2s(&S.cring[s][lane], cull + g, sizeof(Cull), &S.full[s]);
         }
         if (++s == kStages) {
             s = 0;
@@ -379,6 +381,28 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
     // its slot's barrier has moved on to the sentinel's phase, so it is excluded.)
     const int oldest = sentinel ? b - kStages + 1 : b - kStages;
     for (int f = b - 1; f >= 0 && f >= oldest; --f) mbar_wait(&S.full[f % kStages], (f / kStages) & 1);
+}
+
+// Per-warp culling of one stage (run by the consumer warp itself, one entry per lane): an entry is
+// kept unless its PBF hull misses the warp's mirror-space patch or its visual cone misses the warp's
+// ray cone (both conservative: a dropped entry has kappa > lam^2, i.e. t = 0, on every pixel of the
+// warp).  Writes the warp's compacted, null-padded entry list; returns the kept count and (via m)
+// the kept mask.
+template <class Smem>
+__device__ __forceinline__ int stage_keep(Smem &S, int s, int warp, int lane, int n, bool cull, const float4 &patch,
+                                          const float4 &pcone, uint32_t &m) {
+    bool ov = lane < n;
+    if (cull && ov) {
+        const Cull &C = S.cring[s][lane];
+        const float4 bx = C.box;
+        ov = !(bx.y < patch.x || bx.x > patch.y || bx.w < patch.z || bx.z > patch.w) && !cone_misses(C.k0, C.k1, pcone);
+    }
+    m = __ballot_sync(0xffffffffu, ov);
+    const int c = __popc(m);
+    if (ov) S.idx[s][warp][__popc(m & ((1u << lane) - 1u))] = (uint8_t)lane;
+    if (lane < 4) S.idx[s][warp][c + lane] = (uint8_t)kStageEntries;  // pad to a multiple of 4
+    __syncwarp();
+    return c;
 }
 
 // A consumer warp whose pixels are all opaque leaves the pipeline: it releases the current stage
@@ -488,10 +512,9 @@ constexpr uint32_t kExtOff = 112; // offsetof(Payload, ext)
 //
 // Stage of mode-1 payloads (rare: tiny, far or very anisotropic Gaussians): the payload mode is
 // decided per entry and each entry runs the reference formulation via finish_t.
-__device__ __forceinline__ void consume_stage_generic(PipeSmem<false> &S, int s, int warp, int base, const Ray64 &R,
-                                                      const double *dray, const FrameConst &fc, PixelState &ps,
-                                                      int &rechecks, int &went) {
-    const int cnt = S.cnt[s][warp];
+__device__ __forceinline__ void consume_stage_generic(PipeSmem<false> &S, int s, int warp, int cnt, int base,
+                                                      const Ray64 &R, const double *dray, const FrameConst &fc,
+                                                      PixelState &ps, int &rechecks, int &went) {
     int k0 = 0;
     for (; k0 < cnt; k0 += 4) {
         if (k0 > 0 && !__any_sync(0xffffffffu, ps.r > 0.0f)) break;  // warp opaque
@@ -520,9 +543,13 @@ __device__ __forceinline__ void consume_stage_generic(PipeSmem<false> &S, int s,
 constexpr int kFwdGroup = GEER_FWD_GROUP;  // entries evaluated together (ILP vs registers)
 
 template <bool kCutoff>
-__device__ __forceinline__ void consume_stage_fast(PipeSmem<false> &S, int s, int warp, int base, const Ray64 &R,
-                                                   const FrameConst &fc, PixelState &ps, int &rechecks, int &went) {
-    const int cnt = S.cnt[s][warp];
+__device__ __forceinline__ void consume_stage_fast(PipeSmem<false> &S, int s, int warp, int cnt, int base,
+                                                   const Ray64 &R, const FrameConst &fc, PixelState &ps, int &rechecks,
+                                                   int &went) {
+#ifdef GEER_EXP_NOCOMPUTE
+    went += cnt;
+    return;  // tuning experiment: the pipeline alone (results are wrong)
+#endif
     const uint32_t rb = smem_u32(&S.ring[s][0]);
     const uint32_t ib = smem_u32(&S.idx[s][warp][0]);
     int k0 = 0;
@@ -588,6 +615,39 @@ __device__ __forceinline__ float4 ray_mirror_bounds(const FrameConst &fc, const 
     return b;
 }
 
+// Cone around a warp's pixel rays in the camera frame: axis c = normalised sum of the lanes' rays,
+// sin^2(beta) = max over lanes of |c x d|^2 / |d|^2, widened by 2% + 1e-9 for rounding (no
+// transcendental functions: this runs once per CTA on every consumer thread).
+__device__ __forceinline__ void publish_cone(float4 *pcone, const FrameConst &fc, int warp, int lane, bool valid,
+                                             const double d[3]) {
+    double c[3];
+    for (int i = 0; i < 3; ++i)
+        c[i] = valid ? fma(fc.R[i * 3 + 2], d[2], fma(fc.R[i * 3 + 1], d[1], fc.R[i * 3 + 0] * d[0])) : 0.0;
+    double sx = c[0], sy = c[1], sz = c[2];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        sz += __shfl_xor_sync(0xffffffffu, sz, o);
+    }
+    const double nrm2 = sx * sx + sy * sy + sz * sz;
+    float sin2 = 0.f;
+    if (valid && nrm2 > 0.0) {
+        const double x0 = sy * c[2] - sz * c[1], x1 = sz * c[0] - sx * c[2], x2 = sx * c[1] - sy * c[0];
+        const double dn2 = c[0] * c[0] + c[1] * c[1] + c[2] * c[2];
+        sin2 = (float)((x0 * x0 + x1 * x1 + x2 * x2) / (nrm2 * dn2));  // |c_hat x d_hat|^2
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sin2 = fmaxf(sin2, __shfl_xor_sync(0xffffffffu, sin2, o));
+    sin2 = fmaf(sin2, 1.02f, 1e-9f);
+    if (lane == 0 && warp < kConsumerWarps) {
+        const float inv = nrm2 > 0.0 ? (float)(1.0 / sqrt(nrm2)) : 0.f;
+        // the bound needs beta <= 45 deg (sin^2 <= 0.5); cos^2 = 0 disables the test otherwise
+        pcone[warp] = nrm2 > 0.0 && sin2 < 0.5f ? make_float4((float)sx * inv, (float)sy * inv, (float)sz * inv, 1.0f - sin2)
+                                                : make_float4(0.f, 0.f, 1.f, 0.f);
+    }
+}
+
 // Warp-wide union of the lanes' mirror bounds (lanes without a pixel contribute nothing); lane 0
 // stores it as the warp's patch for the producer's culling masks.
 __device__ __forceinline__ void publish_patch(float4 *patch, int warp, int lane, bool valid, float4 b) {
@@ -620,7 +680,7 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
               const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
               const double2 *__restrict__ row_sc, const double *__restrict__ dir64, const int32_t *__restrict__ ranges,
               const uint32_t *__restrict__ order, const Payload *__restrict__ payload,
-              const uint8_t *__restrict__ flags, const float4 *__restrict__ box, float *__restrict__ color,
+              const uint8_t *__restrict__ flags, const Cull *__restrict__ cull, float *__restrict__ color,
               float *__restrict__ remaining, int32_t *__restrict__ count, int32_t *__restrict__ n_eval,
               unsigned long long *__restrict__ counters, int32_t *__restrict__ fixup_list) {
     __shared__ PipeSmem<false> S;
@@ -657,16 +717,20 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
     const int p = valid ? pix_list[it.y + tid] : 0;
     double d64[3] = {0.0, 0.0, 1.0};
     if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
-    if (warp < kConsumerWarps) publish_patch(S.patch, warp, lane, valid, ray_mirror_bounds(fc, d64));
+    if (warp < kConsumerWarps) {
+        publish_patch(S.patch, warp, lane, valid, ray_mirror_bounds(fc, d64));
+        publish_cone(S.pcone, fc, warp, lane, valid, d64);
+    }
     pipe_init(S);  // (its __syncthreads also publishes the patches)
     if (warp == kConsumerWarps) {
-        pipe_produce<false>(S, order, payload, nullptr, flags, box, fc.cull != 0, e0, e1 - e0, true);
+        pipe_produce<false>(S, order, payload, nullptr, fc.cull ? cull : nullptr, e0, e1 - e0, true);
         return;
     }
     const Ray64 R = make_ray(d64);
     sray[tid][0] = d64[0];
     sray[tid][1] = d64[1];
     sray[tid][2] = d64[2];
+    const float4 my_patch = S.patch[warp], my_cone = S.pcone[warp];
     PixelState ps{0.f, 0.f, 0.f, valid ? 1.0f : 0.0f, 1.0f, 0.f, -1.0f, 0, 0, 0};
     int rechecks = 0, went = 0;
     bool warp_live = __any_sync(0xffffffffu, valid);
@@ -678,12 +742,15 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
         const int n = S.count[s];
         if (n == 0) break;
         if (warp_live) {
-            if (S.mode1[s])
-                consume_stage_generic(S, s, warp, base, R, sray[tid], fc, ps, rechecks, went);
+            uint32_t m;
+            const int cnt = stage_keep(S, s, warp, lane, n, fc.cull != 0, my_patch, my_cone, m);
+            // a mode-1 (cross-product) payload anywhere in the stage selects the generic path
+            if (__any_sync(0xffffffffu, lane < n && S.ring[s][lane].col.w < 0.0f))
+                consume_stage_generic(S, s, warp, cnt, base, R, sray[tid], fc, ps, rechecks, went);
             else if (fc.cutoff)
-                consume_stage_fast<true>(S, s, warp, base, R, fc, ps, rechecks, went);
+                consume_stage_fast<true>(S, s, warp, cnt, base, R, fc, ps, rechecks, went);
             else
-                consume_stage_fast<false>(S, s, warp, base, R, fc, ps, rechecks, went);
+                consume_stage_fast<false>(S, s, warp, cnt, base, R, fc, ps, rechecks, went);
             warp_live = __any_sync(0xffffffffu, ps.r > 0.0f);
             if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
         }
@@ -861,7 +928,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
                const double2 *__restrict__ row_sc, const double *__restrict__ dir64,
                const int32_t *__restrict__ ranges, const uint32_t *__restrict__ order,
                const Payload *__restrict__ payload, const GradPayload *__restrict__ gpayload,
-               const uint8_t *__restrict__ flags, const float4 *__restrict__ box, const float *__restrict__ remaining,
+               const uint8_t *__restrict__ flags, const Cull *__restrict__ cull, const float *__restrict__ remaining,
                const int32_t *__restrict__ n_eval,
                const float *__restrict__ dl_dimage, float *__restrict__ accum) {
     __shared__ PipeSmem<true> S;
@@ -880,12 +947,15 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
     if (lane == 0 && wmax > 0) atomicMax(&smax, wmax);
     double d64[3] = {0.0, 0.0, 1.0};
     if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
-    if (warp < kConsumerWarps) publish_patch(S.patch, warp, lane, valid, ray_mirror_bounds(fc, d64));
+    if (warp < kConsumerWarps) {
+        publish_patch(S.patch, warp, lane, valid, ray_mirror_bounds(fc, d64));
+        publish_cone(S.pcone, fc, warp, lane, valid, d64);
+    }
     pipe_init(S);  // (its __syncthreads also publishes smax and the patches)
     const int max_n = smax;
     if (max_n == 0) return;
     if (warp == kConsumerWarps) {
-        pipe_produce<true>(S, order, payload, gpayload, flags, box, fc.cull != 0, e0, max_n, false);
+        pipe_produce<true>(S, order, payload, gpayload, fc.cull ? cull : nullptr, e0, max_n, false);
         return;
     }
     const Ray64 R = make_ray(d64);
@@ -895,6 +965,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
         sray[tid][2] = d64[2];
     }
     const float dx = (float)d64[0], dy = (float)d64[1], dz = (float)d64[2];
+    const float4 my_patch = S.patch[warp], my_cone = S.pcone[warp];
     const float t_fin = valid ? remaining[p] : 0.f;
     float gl0 = 0.f, gl1 = 0.f, gl2 = 0.f;
     if (valid) {
@@ -914,8 +985,9 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
         if (n == 0) break;
         const int lo = hi - n;
         if (lo < wmax) {  // some lane of this warp has alive entries in the stage
-            // entries the PBF mask keeps (culled ones have t = 0: no gradient, T unchanged), below wmax
-            uint32_t msk = S.mask[s][warp];
+            // entries the culling keeps (culled ones have t = 0: no gradient, T unchanged), below wmax
+            uint32_t msk;
+            stage_keep(S, s, warp, lane, n, fc.cull != 0, my_patch, my_cone, msk);
             if (wmax - lo < 32) msk &= (1u << (wmax - lo)) - 1u;
             while (msk) {
                 const int jj = 31 - __clz(msk);
@@ -1022,18 +1094,18 @@ static int grid_for(int64_t n) { return (int)lmin(lmax((n + 255) / 256, 1), 148 
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    const uint8_t *flags, const float4 *box, float *color, float *remaining, int32_t *count,
+                    const uint8_t *flags, const Cull *cull, float *color, float *remaining, int32_t *count,
                     int32_t *n_eval, unsigned long long *counters, int32_t *fixup_list, cudaStream_t st) {
     if (max_items <= 0) return;
     if (fc.model == GEER_BEAP) {
         k_forward<true><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                            ranges, order, payload, flags, box, color, remaining, count,
+                                                            ranges, order, payload, flags, cull, color, remaining, count,
                                                             n_eval, counters, fixup_list);
         k_fixup<true><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                counters, fixup_list, color, remaining, count, n_eval);
     } else {
         k_forward<false><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                             ranges, order, payload, flags, box, color, remaining, count,
+                                                             ranges, order, payload, flags, cull, color, remaining, count,
                                                              n_eval, counters, fixup_list);
         k_fixup<false><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                 counters, fixup_list, color, remaining, count, n_eval);
@@ -1043,16 +1115,16 @@ void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, c
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                      const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                     const GradPayload *gpayload, const uint8_t *flags, const float4 *box, const float *remaining,
+                     const GradPayload *gpayload, const uint8_t *flags, const Cull *cull, const float *remaining,
                      const int32_t *n_eval, const float *dl_dimage, float *accum, cudaStream_t st) {
     if (max_items <= 0) return;
     if (fc.model == GEER_BEAP)
         k_backward<true><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                             ranges, order, payload, gpayload, flags, box, remaining,
+                                                             ranges, order, payload, gpayload, flags, cull, remaining,
                                                              n_eval, dl_dimage, accum);
     else
         k_backward<false><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                              ranges, order, payload, gpayload, flags, box, remaining,
+                                                              ranges, order, payload, gpayload, flags, cull, remaining,
                                                               n_eval, dl_dimage, accum);
 }
 
