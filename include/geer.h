@@ -114,6 +114,7 @@ typedef struct geer_stats {
     int64_t fixup_pixels;     /* pixels recomposited in fp64 (early stop too close to call in fp32) */
     int64_t clamped;          /* clamped & kept particles */
     int64_t warp_entries;     /* forward (warp, entry) evaluations after PBF culling */
+    int64_t streamed_entries; /* forward entries streamed into shared memory (all raster CTAs) */
     float ms_prep, ms_dup, ms_sort, ms_render, ms_total; /* CUDA-event stage times (if timing on) */
     float ms_backward;
 } geer_stats;

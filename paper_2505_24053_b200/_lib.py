@@ -73,7 +73,7 @@ class GeerStats(ctypes.Structure):
         ("n_gaussians", ctypes.c_int64), ("n_entries", ctypes.c_int64), ("n_tiles", ctypes.c_int64),
         ("n_work_items", ctypes.c_int64), ("evaluated_pairs", ctypes.c_int64), ("kappa_rechecks", ctypes.c_int64),
         ("fixup_pixels", ctypes.c_int64),
-        ("clamped", ctypes.c_int64), ("warp_entries", ctypes.c_int64),
+        ("clamped", ctypes.c_int64), ("warp_entries", ctypes.c_int64), ("streamed_entries", ctypes.c_int64),
         ("ms_prep", ctypes.c_float), ("ms_dup", ctypes.c_float), ("ms_sort", ctypes.c_float),
         ("ms_render", ctypes.c_float), ("ms_total", ctypes.c_float), ("ms_backward", ctypes.c_float),
     ]

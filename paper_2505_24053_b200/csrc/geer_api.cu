@@ -8,6 +8,8 @@
 //   render: K5 raster
 // The backward (K6 + K7) reuses the forward's graph, payload and per-pixel
 // (n_eval, remaining) state held in the context.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdint.h>
@@ -48,6 +50,28 @@ struct Buf {
     size_t cap = 0;
 };
 
+// TMA tensor map over an array of fixed-size rows (payloads), for the raster's gather4 copies.
+int make_row_map(CUtensorMap *map, const void *base, int64_t rows, int row_bytes) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return fail(GEER_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
+        encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)(row_bytes / 4), (cuuint64_t)(rows > 0 ? rows : 1)};
+    const cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+    const cuuint32_t box[2] = {(cuuint32_t)(row_bytes / 4), 1};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(GEER_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return GEER_OK;
+}
+
 }  // namespace
 
 struct geer_ctx {
@@ -63,16 +87,17 @@ struct geer_ctx {
     bool keys16 = false;  // tile keys stored as uint16
     int64_t n_entries = 0;
     int max_items = 0;
+    CUtensorMap pay_map, gpay_map;  // gather4 maps over the payload / grad payload arrays
     const float *fwd_remaining = nullptr;  // remaining written by the last forward (backward input)
     float ms[6] = {};
-    unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs, [2] fix-up pixels, [3] warp-entries
+    unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs, [2] fix-up pixels, [3] warp-entries, [4] streamed entries
     int *d_err = nullptr;
     int64_t *h_hdr = nullptr;  // pinned: [0] total entries, [1] error code
     // camera buffers
     Buf col_sc, row_sc, medges_x, medges_y, edges_x, edges_y, dir64, theta, phi, minmax, pixel_tile, pixel_tile_sorted,
         pix_iota, pix_list, tile_count, tile_off, item_count, item_off, items, n_items, work, n_work;
     // per-Gaussian buffers
-    Buf payload, gpayload, cull, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, cnt_sorted, offs, ranges_ax, flags, mu_c,
+    Buf payload, gpayload, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, cnt_sorted, offs, ranges_ax, flags, mu_c,
         depth;
     // per-entry buffers
     Buf tile_keys, tile_keys_sorted, gids, order, tile_ranges, block_rank;
@@ -234,7 +259,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     c->have_frame = false;
     c->have_raster = false;
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
-    GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), st));
+    GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 5 * sizeof(unsigned long long), st));
     GEER_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
     rc = camera_setup(c, want_export, st);
     if (rc) return rc;
@@ -242,7 +267,6 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     // ---- K1 preprocess
     Payload *payload = ENSURE(Payload, c->payload, n);
     GradPayload *gpayload = ENSURE(GradPayload, c->gpayload, n);
-    Cull *cull = ENSURE(Cull, c->cull, n);
     uint32_t *dkey = ENSURE(uint32_t, c->depth_key, n);
     uint32_t *dkey_s = ENSURE(uint32_t, c->depth_key_sorted, n);
     int32_t *giota = ENSURE(int32_t, c->gid_iota, n);
@@ -258,8 +282,12 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         dep = ENSURE(double, c->depth, n);
     }
     int32_t *ranges = ENSURE(int32_t, c->tile_ranges, fc.n_tiles + 1);
+    rc = make_row_map(&c->pay_map, payload, n, (int)sizeof(Payload));
+    if (rc) return rc;
+    rc = make_row_map(&c->gpay_map, gpayload, n, (int)sizeof(GradPayload));
+    if (rc) return rc;
     launch_preprocess(fc, sc, (const double *)c->medges_x.p, (const double *)c->medges_y.p, payload, gpayload, dkey, cnt, ar,
-                      flags, cull, mu, dep, c->d_err, st);
+                      flags, mu, dep, c->d_err, st);
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[1], st));
 
     // ---- dup: depth order, scan, header D2H, emit
@@ -329,7 +357,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         int32_t *fix = ENSURE(int32_t, c->fixup, npx);
         launch_forward(fc, sc, c->max_items, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
                        (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
-                       (const double *)c->dir64.p, ranges, order, payload, flags, cull, color, remaining, count, ne,
+                       (const double *)c->dir64.p, ranges, order, payload, c->pay_map, flags, color, remaining, count, ne,
                        c->d_counters, fix, st);
         c->fwd_remaining = remaining;
         c->have_raster = true;
@@ -358,8 +386,8 @@ int run_backward(geer_ctx *c, const float *dl_dimage, bool f64_out, void *const 
     launch_backward(fc, sc, c->max_items, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
                     (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
                     (const double *)c->dir64.p, (const int32_t *)c->tile_ranges.p, (const uint32_t *)c->order.p,
-                    (const Payload *)c->payload.p, (const GradPayload *)c->gpayload.p, (const uint8_t *)c->flags.p,
-                    (const Cull *)c->cull.p, c->fwd_remaining, (const int32_t *)c->n_eval.p,
+                    c->pay_map, c->gpay_map, (const uint8_t *)c->flags.p,
+                    c->fwd_remaining, (const int32_t *)c->n_eval.p,
                     dl_dimage, accum, st);
     if (f64_out)
         launch_finalize<double>(fc, sc, (const float4 *)accum, (const uint8_t *)c->flags.p, (double *)gout[0], (double *)gout[1],
@@ -452,7 +480,7 @@ geer_ctx *geer_create(int device) {
     c->device = device;
     bool ok = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) == cudaSuccess;
     for (int i = 0; i < 6 && ok; ++i) ok = cudaEventCreate(&c->ev[i]) == cudaSuccess;
-    ok = ok && cudaMalloc(&c->d_counters, 4 * sizeof(unsigned long long)) == cudaSuccess;
+    ok = ok && cudaMalloc(&c->d_counters, 5 * sizeof(unsigned long long)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->d_err, sizeof(int)) == cudaSuccess;
     ok = ok && cudaMallocHost(&c->h_hdr, 2 * sizeof(int64_t)) == cudaSuccess;
     if (!ok) {
@@ -469,7 +497,7 @@ void geer_destroy(geer_ctx *c) {
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     Buf *bufs[] = {&c->col_sc, &c->row_sc, &c->medges_x, &c->medges_y, &c->edges_x, &c->edges_y, &c->dir64,
                    &c->theta, &c->phi, &c->minmax, &c->pixel_tile, &c->pixel_tile_sorted, &c->pix_iota, &c->pix_list,
-                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->work, &c->n_work, &c->payload, &c->gpayload, &c->cull,
+                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->work, &c->n_work, &c->payload, &c->gpayload,
                    &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted, &c->count, &c->cnt_sorted,
                    &c->offs, &c->ranges_ax, &c->flags, &c->mu_c, &c->depth, &c->tile_keys, &c->tile_keys_sorted,
                    &c->gids, &c->order, &c->tile_ranges, &c->block_rank, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,
@@ -537,7 +565,7 @@ int geer_frame_stats(geer_ctx *c, geer_stats *out) {
         GEER_CUDA(cudaDeviceSynchronize());
         GEER_CUDA(cudaMemsetAsync(c->d_counters + 1, 0, sizeof(unsigned long long), st));
         launch_sum_i32((const int32_t *)c->n_eval.p, (int64_t)c->fc.width * c->fc.height, c->d_counters + 1, st);
-        unsigned long long h[4];
+        unsigned long long h[5];
         int32_t nit = 0;
         GEER_CUDA(cudaMemcpyAsync(h, c->d_counters, sizeof(h), cudaMemcpyDeviceToHost, st));
         GEER_CUDA(cudaMemcpyAsync(&nit, c->n_work.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));  // items with entries
@@ -546,6 +574,7 @@ int geer_frame_stats(geer_ctx *c, geer_stats *out) {
         out->evaluated_pairs = (int64_t)h[1];
         out->fixup_pixels = (int64_t)h[2];
         out->warp_entries = (int64_t)h[3];
+        out->streamed_entries = (int64_t)h[4];
         out->n_work_items = nit;
     }
     if (c->have_frame && c->scene.n > 0) {

@@ -37,29 +37,31 @@ struct FrameConst {
     float cutoff_tol;  // |kappa_fp32 - lam^2| below which the cutoff is re-decided in fp64
 };
 
-// Raster payload, one per Gaussian (128 B, see make_payload in geer_geometry.cu):
-//   q[12]  mode 0: quadratic forms of |d_u|^2 and |m|^2 in the ray d:
-//                  (A00, A11, A22, 2A01, 2A02, 2A12, B00, B11, B22, 2B01, 2B02, 2B12)
-//          mode 1: W (row-major) and o_u for the fp64 cross-product evaluation
-//   col  = (r, g, b, sigma); sigma < 0 flags mode 1
-//   ext  = (absolute kappa error bound of the fp64 evaluation, 0, 0, 0)
-struct __align__(16) Payload {
-    double q[12];
-    float4 col;
-    float4 ext;
-};
-
-// fp32 W rows and o_u (w component) for the backward's gradient vectors.
-struct __align__(16) GradPayload {
-    float4 r0, r1, r2;
-};
-
 // Raster culling record of one Gaussian (48 B, written by K1, streamed with the payload):
 //   box  = PBF hull in camera-frame mirror space (x_lo, x_hi, y_lo, y_hi), outward-rounded
 //   k0, k1 = visual-cone matrix K (K00, K11, K22, K01 | K02, K12, lambda_max bound, 0), see cone_misses
 struct __align__(16) Cull {
     float4 box;
     float4 k0, k1;
+};
+
+// Raster payload, one per Gaussian (176 B, see make_payload in geer_geometry.cu; one bulk copy):
+//   q[12]  mode 0: quadratic forms of |d_u|^2 and |m|^2 in the ray d:
+//                  (A00, A11, A22, 2A01, 2A02, 2A12, B00, B11, B22, 2B01, 2B02, 2B12)
+//          mode 1: W (row-major) and o_u for the fp64 cross-product evaluation
+//   col  = (r, g, b, sigma); sigma < 0 flags mode 1
+//   ext  = (absolute kappa error bound of the fp64 evaluation, 0, 0, 0)
+//   cull = the culling record (written by the association half of K1)
+struct __align__(16) Payload {
+    double q[12];
+    float4 col;
+    float4 ext;
+    Cull cull;
+};
+
+// fp32 W rows and o_u (w component) for the backward's gradient vectors.
+struct __align__(16) GradPayload {
+    float4 r0, r1, r2;
 };
 
 // Per-axis tile ranges: up to 3 disjoint [lo, hi) pairs packed lo | hi << 16.

@@ -511,7 +511,7 @@ __device__ __forceinline__ void named_barrier(int id, int count) {
 // sex / sey: the mirror tile edges in shared memory.  Returns the keep / clamped flag bits.
 __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, const double *sex, const double *sey,
                                  int64_t g, uint32_t *__restrict__ depth_key, int64_t *__restrict__ count,
-                                 AxisRanges *__restrict__ ranges, Cull *__restrict__ cull,
+                                 AxisRanges *__restrict__ ranges, Cull &cr,
                                  double *__restrict__ mu_out, double *__restrict__ depth_out, int *__restrict__ err) {
 
     const double *R = fc.R;
@@ -643,11 +643,9 @@ __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, con
     }
     count[g] = n_ent;
     ranges[g] = ar;
-    Cull cr;
     cr.box = bx;
     cr.k0 = ca;
     cr.k1 = cb;
-    cull[g] = cr;
     // association.py:335-340 key bits (depth > 0): f32 bits | 0x80000000; non-emitting last
     const uint32_t kb = __float_as_uint((float)depth) | 0x80000000u;
     depth_key[g] = n_ent > 0 ? kb : 0xFFFFFFFFu;
@@ -660,6 +658,11 @@ __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, con
 // Runs on a group of 128 threads (lt = 0..127) that synchronises with named barrier 2; ssh: SH
 // staging, then payload staging (9 + 3 float4 = 48 floats per Gaussian, padded rows).  Returns the
 // SH clamp gate (bits 3-5) and payload-mode (bit 6) flag bits of Gaussian g0 + lt.
+constexpr int kPayHead = offsetof(Payload, cull) / 16;    // float4s of a payload before its culling record
+constexpr int kPayRow = sizeof(Payload) / 16;             // float4s of a payload
+constexpr int kStageRow = kPayHead + 1;                   // padded staging row
+constexpr int kGradRow = sizeof(GradPayload) / 16;
+
 template <int NB>
 __device__ uint8_t payload_block(const FrameConst &fc, const geer_scene &sc, float *ssh, int64_t g0, int cnt_b, int lt,
                                  Payload *__restrict__ payload, GradPayload *__restrict__ gpayload) {
@@ -720,24 +723,18 @@ __device__ uint8_t payload_block(const FrameConst &fc, const geer_scene &sc, flo
     const bool mode1 = make_payload(W, ou, rgb, sigma, smax / smin, fc.lam, pl, gp);
     // flags: bit0 keep, bit1 clamped (K1a), bits3-5 SH clamp gate per channel, bit6 payload mode 1
     const uint8_t bits = (uint8_t)((gate << 3) | (mode1 ? 64 : 0));
-    // coalesced stores: stage the block's 128-B payloads and 48-B grad payloads in shared memory
-    // (reusing the SH staging buffer) and write them out as contiguous float4 runs
-    // rows padded to 9 float4 (payload) and kept at 3 float4 (grad payload): conflict-free 16-B stores
-    constexpr int kP = sizeof(Payload) / 16, kPP = kP + 1, kG = sizeof(GradPayload) / 16;
+    // stage the block's payloads (first 8 float4; the culling record comes from the association
+    // half) and grad payloads in shared memory, reusing the SH buffer: k_preprocess writes them out
+    // as contiguous float4 runs.  Rows padded to 9 float4: conflict-free 16-B stores.
     float4 *sp = reinterpret_cast<float4 *>(ssh);
-    float4 *sg = sp + 128 * kPP;
+    float4 *sg = sp + 128 * kStageRow;
     named_barrier(2, 128);  // every thread is done reading its SH coefficients
     const float4 *plv = reinterpret_cast<const float4 *>(&pl);
     const float4 *gpv = reinterpret_cast<const float4 *>(&gp);
 #pragma unroll
-    for (int k = 0; k < kP; ++k) sp[lt * kPP + k] = plv[k];
+    for (int k = 0; k < kPayHead; ++k) sp[lt * kStageRow + k] = plv[k];
 #pragma unroll
-    for (int k = 0; k < kG; ++k) sg[lt * kG + k] = gpv[k];
-    named_barrier(2, 128);
-    float4 *dp = reinterpret_cast<float4 *>(payload + g0);
-    float4 *dg = reinterpret_cast<float4 *>(gpayload + g0);
-    for (int i = lt; i < cnt_b * kP; i += nthr) dp[i] = sp[(i / kP) * kPP + i % kP];
-    for (int i = lt; i < cnt_b * kG; i += nthr) dg[i] = sg[i];
+    for (int k = 0; k < kGradRow; ++k) sg[lt * kGradRow + k] = gpv[k];
     return bits;
 }
 
@@ -749,10 +746,12 @@ __global__ void __launch_bounds__(256, 3)
     k_preprocess(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x, const double *__restrict__ medges_y,
                  Payload *__restrict__ payload, GradPayload *__restrict__ gpayload, uint32_t *__restrict__ depth_key,
                  int64_t *__restrict__ count, AxisRanges *__restrict__ ranges, uint8_t *__restrict__ flags,
-                 Cull *__restrict__ cull, double *__restrict__ mu_out,
+                 double *__restrict__ mu_out,
                  double *__restrict__ depth_out, int *__restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ __align__(16) float ssh[128 * (NB * 3 > 48 ? NB * 3 : 48)];
+    constexpr int kStageFloats = (kStageRow + kGradRow) * 4;  // payload-head + grad-payload staging
+    __shared__ __align__(16) float ssh[128 * (NB * 3 > kStageFloats ? NB * 3 : kStageFloats)];
+    __shared__ Cull scull[128];
     __shared__ uint8_t sfl[2][128];
     const int64_t g0 = (int64_t)blockIdx.x * 128;
     const int cnt_b = (int)lmin(128, sc.n - g0);
@@ -763,7 +762,7 @@ __global__ void __launch_bounds__(256, 3)
         for (int i = lt; i <= fc.n_x; i += 128) sex[i] = medges_x[i];
         for (int i = lt; i <= fc.n_y; i += 128) sey[i] = medges_y[i];
         named_barrier(1, 128);
-        sfl[0][lt] = lt < cnt_b ? associate_one(fc, sc, sex, sey, g0 + lt, depth_key, count, ranges, cull,
+        sfl[0][lt] = lt < cnt_b ? associate_one(fc, sc, sex, sey, g0 + lt, depth_key, count, ranges, scull[lt],
                                                 mu_out, depth_out, err)
                                 : 0;
     } else {
@@ -771,6 +770,17 @@ __global__ void __launch_bounds__(256, 3)
     }
     __syncthreads();
     if (threadIdx.x < cnt_b) flags[g0 + threadIdx.x] = (uint8_t)(sfl[0][threadIdx.x] | sfl[1][threadIdx.x]);
+    // coalesced write-out of the block's payload rows (head + culling record) and grad payloads
+    const float4 *sp = reinterpret_cast<const float4 *>(ssh);
+    const float4 *sg = sp + 128 * kStageRow;
+    const float4 *scv = reinterpret_cast<const float4 *>(scull);
+    float4 *dp = reinterpret_cast<float4 *>(payload + g0);
+    float4 *dg = reinterpret_cast<float4 *>(gpayload + g0);
+    for (int i = threadIdx.x; i < cnt_b * kPayRow; i += blockDim.x) {
+        const int r = i / kPayRow, k = i - r * kPayRow;
+        dp[i] = k < kPayHead ? sp[r * kStageRow + k] : scv[r * (sizeof(Cull) / 16) + (k - kPayHead)];
+    }
+    for (int i = threadIdx.x; i < cnt_b * kGradRow; i += blockDim.x) dg[i] = sg[i];
 }
 
 // ---------------------------------------------------------------- K7
@@ -923,7 +933,7 @@ size_t preprocess_smem(const FrameConst &fc) { return sizeof(double) * (fc.n_x +
 
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
                        Payload *payload, GradPayload *gpayload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges,
-                       uint8_t *flags, Cull *cull, double *mu_out, double *depth_out, int *err,
+                       uint8_t *flags, double *mu_out, double *depth_out, int *err,
                        cudaStream_t st) {
     if (sc.n == 0) return;
     const int blocks = (int)((sc.n + 127) / 128);
@@ -931,7 +941,7 @@ void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double 
 #define GEER_NB_CASE(NB)                                                                                            \
     case NB:                                                                                                        \
         k_preprocess<NB><<<blocks, 256, preprocess_smem(fc), st>>>(fc, sc, medges_x, medges_y, payload, gpayload,   \
-                                                                   depth_key, count, ranges, flags, cull,          \
+                                                                   depth_key, count, ranges, flags,                \
                                                                    mu_out,                                         \
                                                                    depth_out, err);                                \
         break;

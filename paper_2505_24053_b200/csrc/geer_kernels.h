@@ -1,6 +1,7 @@
 // geer_kernels.h — host-side launchers shared between the translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -24,7 +25,7 @@ void launch_item_fill(int n_tiles, const int32_t *tile_off, const int32_t *item_
 size_t preprocess_smem(const FrameConst &fc);
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
                        Payload *payload, GradPayload *gpayload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges, uint8_t *flags,
-                       Cull *cull, double *mu_out, double *depth_out, int *err, cudaStream_t st);
+                       double *mu_out, double *depth_out, int *err, cudaStream_t st);
 template <typename T>
 void launch_finalize(const FrameConst &fc, const geer_scene &sc, const float4 *accum, const uint8_t *flags, T *dmeans,
                      T *dlog_scales, T *dquats, T *dopac, T *dsh, int accumulate, cudaStream_t st);
@@ -64,12 +65,12 @@ void order_items(const int4 *items, const int32_t *n_items, const int32_t *range
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    const uint8_t *flags, const Cull *cull, float *color, float *remaining, int32_t *count, int32_t *n_eval,
+                    const CUtensorMap &pay_map, const uint8_t *flags, float *color, float *remaining, int32_t *count, int32_t *n_eval,
                     unsigned long long *counters, int32_t *fixup_list, cudaStream_t st);
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
-                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                     const GradPayload *gpayload, const uint8_t *flags, const Cull *cull,
+                     const double *dir64, const int32_t *ranges, const uint32_t *order, const CUtensorMap &pay_map,
+                     const CUtensorMap &gpay_map, const uint8_t *flags,
                      const float *remaining,
                      const int32_t *n_eval, const float *dl_dimage, float *accum, cudaStream_t st);
 void launch_sum_i32(const int32_t *v, int64_t n, unsigned long long *out, cudaStream_t st);

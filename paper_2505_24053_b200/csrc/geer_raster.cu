@@ -18,6 +18,7 @@
 // entries back to front, forms the 16 per-(pixel, Gaussian) partials,
 // warp-reduces them with a shuffle transpose, CTA-reduces them in shared
 // memory and issues one vector atomic per 4 partials per entry.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -221,11 +222,17 @@ constexpr int kPipeThreads = kRasterThreads + 32;
 #define FWD_MIN_BLOCKS 3
 #endif
 
+constexpr int kRingGroupBytes = 768;    // 4 x 176-B payloads (704 B), padded to a multiple of 128
+constexpr int kGringGroupBytes = 256;   // 4 x 48-B grad payloads (192 B), padded
+constexpr int kRingGroups = kStageEntries / 4 + 1;
+static_assert(sizeof(Payload) * 4 <= kRingGroupBytes && sizeof(GradPayload) * 4 <= kGringGroupBytes, "ring layout");
+
 template <bool kGrad>
-struct __align__(16) PipeSmem {
-    Payload ring[kStages][kStageEntries + 1];  // slot kStageEntries: a null entry (t = 0 for every ray)
-    GradPayload gring[kGrad ? kStages : 1][kStageEntries];  // backward only
-    Cull cring[kStages][kStageEntries];                     // culling records of the stage's entries
+struct __align__(128) PipeSmem {
+    // Entries land in groups of 4 (one TMA gather4 per group), each group 128-B aligned; group
+    // kStageEntries / 4 holds the null entry (t = 0 for every ray).  Use ring_at / gring_at.
+    alignas(128) unsigned char ring[kStages][kRingGroups][kRingGroupBytes];
+    alignas(128) unsigned char gring[kGrad ? kStages : 1][kStageEntries / 4][kGringGroupBytes];  // backward only
     uint32_t gid[kStages][kStageEntries];
     int count[kStages];  // entries in the stage; 0 = end of stream
     uint8_t idx[kStages][kConsumerWarps][kStageEntries + 4];  // per warp: its kept entries, padded with null slots
@@ -237,6 +244,23 @@ struct __align__(16) PipeSmem {
     int done_warps;
     int stop;  // producer will not fill any more stages
 };
+
+// The dynamic shared window starts after the static allocations: align the pipeline state to 128 B
+// (TMA destinations) by hand; launches reserve sizeof + 128 bytes.
+__device__ __forceinline__ unsigned char *align128(unsigned char *p) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+    return p + ((128u - (a & 127u)) & 127u);
+}
+
+__device__ __forceinline__ uint32_t ring_off(int j) { return (uint32_t)((j >> 2) * kRingGroupBytes + (j & 3) * (int)sizeof(Payload)); }
+template <class Smem>
+__device__ __forceinline__ Payload &ring_at(Smem &S, int s, int j) {
+    return *reinterpret_cast<Payload *>(&S.ring[s][0][0] + ring_off(j));
+}
+template <class Smem>
+__device__ __forceinline__ const GradPayload &gring_at(Smem &S, int s, int j) {
+    return *reinterpret_cast<const GradPayload *>(&S.gring[s][j >> 2][(j & 3) * sizeof(GradPayload)]);
+}
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -274,6 +298,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
         "r"(parity)
         : "memory");
 }
+// TMA gather4: rows r[0..3] of a 2D row-major tensor (one row = one payload) into 4 consecutive
+// rows at dst (128-B aligned), completion counted on bar (sm_100a UTMALDG.2D.GATHER4).
+__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *map, const uint32_t r[4],
+                                            unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(0), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(smem_u32(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
@@ -292,7 +327,7 @@ __device__ __forceinline__ void pipe_init(Smem &S) {
         S.stop = 0;
         // null entry: |d_u|^2 = |d|^2, |m|^2 = 0, sigma = 0  ->  kappa = 0, t = 0 exactly (a no-op)
         for (int s = 0; s < kStages; ++s) {
-            Payload &z = S.ring[s][kStageEntries];
+            Payload &z = ring_at(S, s, kStageEntries);
             for (int i = 0; i < 12; ++i) z.q[i] = i < 3 ? 1.0 : 0.0;
             z.col = make_float4(0.f, 0.f, 0.f, 0.f);
             z.ext = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -323,13 +358,11 @@ __device__ __forceinline__ bool cone_misses(const float4 &ta, const float4 &tb, 
 
 // Producer warp: stream entries [first, first + n_total) (forward order) or the
 // same range walked from the back (reverse) in stages of kStageEntries.
-template <bool kReverse, class Smem>
-__device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict__ order,
-                                             const Payload *__restrict__ payload,
-                                             const GradPayload *__restrict__ gpayload, const Cull *__restrict__ cull,
-                                             int first, int n_total, bool stop_when_done) {
-    const unsigned per_entry =
-        (unsigned)(sizeof(Payload) + (gpayload ? sizeof(GradPayload) : 0) + (cull ? sizeof(Cull) : 0));
+template <bool kReverse, bool kGradMaps, class Smem>
+__device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict__ order, const CUtensorMap *pay_map,
+                                             const CUtensorMap *gpay_map, int first, int n_total, bool stop_when_done,
+                                             unsigned long long *streamed = nullptr) {
+    const unsigned per_group = (unsigned)(4 * (sizeof(Payload) + (kGradMaps ? sizeof(GradPayload) : 0)));
     const int lane = threadIdx.x & 31;
     // gid of this lane's entry in stage bb (the order load runs one stage ahead of the copies)
     auto load_gid = [&](int bb) -> uint32_t {
@@ -362,13 +395,18 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
         __syncwarp();
         if (lane == 0) {
             S.count[s] = n;
-            mbar_arrive_expect_tx(&S.full[s], n * per_entry);
+            mbar_arrive_expect_tx(&S.full[s], ((n + 3) >> 2) * per_group);
         }
         __syncwarp();
-        if (lane < n) {
-            bulk_g2s(&S.ring[s][lane], payload + g, sizeof(Payload), &S.full[s]);
-            if (gpayload) bulk_g2s(&S.gring[gpayload ? s : 0][lane], gpayload + g, sizeof(GradPayload), &S.full[s]);
-            if (cull) bulk_g2s(&S.cring[s][lane], cull + g, sizeof(Cull), &S.full[s]);
+        // lane k < ceil(n / 4) gathers rows of entries 4k..4k+3 (a partial last group repeats its
+        // last entry, so every gather moves 4 whole rows)
+        const int ng = (n + 3) >> 2;
+        uint32_t rows[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rows[q] = __shfl_sync(0xffffffffu, g, min(4 * (lane & 7) + q, n - 1));
+        if (lane < ng) {
+            tma_gather4(&S.ring[s][lane][0], pay_map, rows, &S.full[s]);
+            if (kGradMaps) tma_gather4(&S.gring[kGradMaps ? s : 0][lane][0], gpay_map, rows, &S.full[s]);
         }
         if (++s == kStages) {
             s = 0;
@@ -379,6 +417,7 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
     // No bulk copy may still be writing shared memory when the CTA retires: wait for the fills
     // nobody may have waited for.  (After a sentinel, fill b - kStages is known to be consumed and
     // its slot's barrier has moved on to the sentinel's phase, so it is excluded.)
+    if (streamed && lane == 0) atomicAdd(streamed, (unsigned long long)min(n_total, kStageEntries * b));
     const int oldest = sentinel ? b - kStages + 1 : b - kStages;
     for (int f = b - 1; f >= 0 && f >= oldest; --f) mbar_wait(&S.full[f % kStages], (f / kStages) & 1);
 }
@@ -393,7 +432,7 @@ __device__ __forceinline__ int stage_keep(Smem &S, int s, int warp, int lane, in
                                           const float4 &pcone, uint32_t &m) {
     bool ov = lane < n;
     if (cull && ov) {
-        const Cull &C = S.cring[s][lane];
+        const Cull &C = ring_at(S, s, lane).cull;
         const float4 bx = C.box;
         ov = !(bx.y < patch.x || bx.x > patch.y || bx.w < patch.z || bx.z > patch.w) && !cone_misses(C.k0, C.k1, pcone);
     }
@@ -522,7 +561,7 @@ __device__ __forceinline__ void consume_stage_generic(PipeSmem<false> &S, int s,
 #pragma unroll 1
         for (int u = 0; u < 4; ++u) {
             const int j = (q >> (8 * u)) & 0xFF;
-            const Payload &P = S.ring[s][j];
+            const Payload &P = ring_at(S, s, j);
             const bool m1 = __any_sync(0xffffffffu, P.col.w < 0.0f);
             double dd, mm;
             norms64(P, R, dray, m1, dd, mm);
@@ -550,7 +589,7 @@ __device__ __forceinline__ void consume_stage_fast(PipeSmem<false> &S, int s, in
     went += cnt;
     return;  // tuning experiment: the pipeline alone (results are wrong)
 #endif
-    const uint32_t rb = smem_u32(&S.ring[s][0]);
+    const uint32_t rb = smem_u32(&S.ring[s][0][0]);
     const uint32_t ib = smem_u32(&S.idx[s][warp][0]);
     int k0 = 0;
     for (; k0 < cnt; k0 += kFwdGroup) {
@@ -558,11 +597,13 @@ __device__ __forceinline__ void consume_stage_fast(PipeSmem<false> &S, int s, in
         const uint32_t q = kFwdGroup == 4 ? lds_u32(ib + k0) : (lds_u32(ib + (k0 & ~3)) >> (8 * (k0 & 3)));
         float kap[kFwdGroup], t[kFwdGroup];
         uint32_t pa[kFwdGroup];
+        int jj[kFwdGroup];
         bool near[kFwdGroup], unc[kFwdGroup];
         bool any_near = false;
 #pragma unroll
         for (int u = 0; u < kFwdGroup; ++u) {
-            pa[u] = rb + ((q >> (8 * u)) & 0xFF) * (uint32_t)sizeof(Payload);
+            jj[u] = (q >> (8 * u)) & 0xFF;
+            pa[u] = rb + ring_off(jj[u]);
             double dd, mm;
             norms64_smem(pa[u], R, dd, mm);
             const float sw = lds_f32(pa[u] + kColOff + 12);
@@ -594,7 +635,7 @@ __device__ __forceinline__ void consume_stage_fast(PipeSmem<false> &S, int s, in
 #pragma unroll
         for (int u = 0; u < kFwdGroup; ++u) {
             const float4 col = lds_f4(pa[u] + kColOff);
-            pixel_update(ps, kap[u], t[u], col, unc[u], base + (int)((pa[u] - rb) / (uint32_t)sizeof(Payload)) + 1);
+            pixel_update(ps, kap[u], t[u], col, unc[u], base + jj[u] + 1);
         }
     }
     went += k0 < cnt ? k0 : cnt;
@@ -679,11 +720,12 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
     k_forward(FrameConst fc, geer_scene sc, const int4 *__restrict__ items, const int32_t *__restrict__ n_items,
               const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
               const double2 *__restrict__ row_sc, const double *__restrict__ dir64, const int32_t *__restrict__ ranges,
-              const uint32_t *__restrict__ order, const Payload *__restrict__ payload,
-              const uint8_t *__restrict__ flags, const Cull *__restrict__ cull, float *__restrict__ color,
+              const uint32_t *__restrict__ order, const __grid_constant__ CUtensorMap pay_map,
+              const uint8_t *__restrict__ flags, float *__restrict__ color,
               float *__restrict__ remaining, int32_t *__restrict__ count, int32_t *__restrict__ n_eval,
               unsigned long long *__restrict__ counters, int32_t *__restrict__ fixup_list) {
-    __shared__ PipeSmem<false> S;
+    extern __shared__ __align__(16) unsigned char dsmem[];  // PipeSmem (dynamic: deep rings exceed 48 KB)
+    PipeSmem<false> &S = *reinterpret_cast<PipeSmem<false> *>(align128(dsmem));
     __shared__ double sray[kRasterThreads][3];  // fp64 pixel rays (mode-1 payloads only)
     // n_items: [0] items with entries (work[0, n0)), [1] empty items (work[max_items - n1, max_items))
     const int n_full = n_items[0];
@@ -723,7 +765,7 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
     }
     pipe_init(S);  // (its __syncthreads also publishes the patches)
     if (warp == kConsumerWarps) {
-        pipe_produce<false>(S, order, payload, nullptr, fc.cull ? cull : nullptr, e0, e1 - e0, true);
+        pipe_produce<false, false>(S, order, &pay_map, nullptr, e0, e1 - e0, true, &counters[4]);
         return;
     }
     const Ray64 R = make_ray(d64);
@@ -745,7 +787,7 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
             uint32_t m;
             const int cnt = stage_keep(S, s, warp, lane, n, fc.cull != 0, my_patch, my_cone, m);
             // a mode-1 (cross-product) payload anywhere in the stage selects the generic path
-            if (__any_sync(0xffffffffu, lane < n && S.ring[s][lane].col.w < 0.0f))
+            if (__any_sync(0xffffffffu, lane < n && ring_at(S, s, lane).col.w < 0.0f))
                 consume_stage_generic(S, s, warp, cnt, base, R, sray[tid], fc, ps, rechecks, went);
             else if (fc.cutoff)
                 consume_stage_fast<true>(S, s, warp, cnt, base, R, fc, ps, rechecks, went);
@@ -927,11 +969,12 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
                const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
                const double2 *__restrict__ row_sc, const double *__restrict__ dir64,
                const int32_t *__restrict__ ranges, const uint32_t *__restrict__ order,
-               const Payload *__restrict__ payload, const GradPayload *__restrict__ gpayload,
-               const uint8_t *__restrict__ flags, const Cull *__restrict__ cull, const float *__restrict__ remaining,
+               const __grid_constant__ CUtensorMap pay_map, const __grid_constant__ CUtensorMap gpay_map,
+               const uint8_t *__restrict__ flags, const float *__restrict__ remaining,
                const int32_t *__restrict__ n_eval,
                const float *__restrict__ dl_dimage, float *__restrict__ accum) {
-    __shared__ PipeSmem<true> S;
+    extern __shared__ __align__(16) unsigned char dsmem[];
+    PipeSmem<true> &S = *reinterpret_cast<PipeSmem<true> *>(align128(dsmem));
     __shared__ double sray[kRasterThreads][3];
     __shared__ int smax;
     if ((int)blockIdx.x >= n_items[0]) return;  // tiles without entries have no gradient
@@ -955,7 +998,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
     const int max_n = smax;
     if (max_n == 0) return;
     if (warp == kConsumerWarps) {
-        pipe_produce<true>(S, order, payload, gpayload, fc.cull ? cull : nullptr, e0, max_n, false);
+        pipe_produce<true, true>(S, order, &pay_map, &gpay_map, e0, max_n, false);
         return;
     }
     const Ray64 R = make_ray(d64);
@@ -996,7 +1039,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
                 float v[16];
 #pragma unroll
                 for (int k = 0; k < 16; ++k) v[k] = 0.f;
-                const Payload &P = S.ring[s][jj];
+                const Payload &P = ring_at(S, s, jj);
                 PairT e;
                 eval_t(P, R, sray[tid], fc, e, dummy);  // warp-uniform call (mode vote inside)
                 // t = 0 (or not alive) on every lane: T, the suffix and all 16 partials are unchanged
@@ -1020,7 +1063,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
                     v[15] = w * gl2;
                     if (e.t > 0.0f && e.u < kMaxBlendTF) {  // renderer.py:289-290 gate
                         // canonical ray (fp32): d_u = W d, m = o_u x d_u (renderer.py:96-99)
-                        const GradPayload &G = S.gring[s][jj];
+                        const GradPayload &G = gring_at(S, s, jj);
                         const float du0 = G.r0.x * dx + G.r0.y * dy + G.r0.z * dz;
                         const float du1 = G.r1.x * dx + G.r1.y * dy + G.r1.z * dz;
                         const float du2 = G.r2.x * dx + G.r2.y * dy + G.r2.z * dz;
@@ -1091,21 +1134,33 @@ __global__ void k_fill_bg(FrameConst fc, float *color, float *remaining, int32_t
 
 static int grid_for(int64_t n) { return (int)lmin(lmax((n + 255) / 256, 1), 148 * 8); }
 
+// Dynamic shared memory above 48 KB needs an explicit opt-in per kernel (done once).
+static void raster_smem_optin() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<false>) + 128);
+    cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<false>) + 128);
+    cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<true>) + 128);
+    cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<true>) + 128);
+}
+
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    const uint8_t *flags, const Cull *cull, float *color, float *remaining, int32_t *count,
+                    const CUtensorMap &pay_map, const uint8_t *flags, float *color, float *remaining, int32_t *count,
                     int32_t *n_eval, unsigned long long *counters, int32_t *fixup_list, cudaStream_t st) {
     if (max_items <= 0) return;
+    raster_smem_optin();
     if (fc.model == GEER_BEAP) {
-        k_forward<true><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                            ranges, order, payload, flags, cull, color, remaining, count,
+        k_forward<true><<<max_items, kPipeThreads, sizeof(PipeSmem<false>) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
+                                                            ranges, order, pay_map, flags, color, remaining, count,
                                                             n_eval, counters, fixup_list);
         k_fixup<true><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                counters, fixup_list, color, remaining, count, n_eval);
     } else {
-        k_forward<false><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                             ranges, order, payload, flags, cull, color, remaining, count,
+        k_forward<false><<<max_items, kPipeThreads, sizeof(PipeSmem<false>) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
+                                                             ranges, order, pay_map, flags, color, remaining, count,
                                                              n_eval, counters, fixup_list);
         k_fixup<false><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                 counters, fixup_list, color, remaining, count, n_eval);
@@ -1114,17 +1169,18 @@ void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, c
 
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
-                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                     const GradPayload *gpayload, const uint8_t *flags, const Cull *cull, const float *remaining,
+                     const double *dir64, const int32_t *ranges, const uint32_t *order, const CUtensorMap &pay_map,
+                     const CUtensorMap &gpay_map, const uint8_t *flags, const float *remaining,
                      const int32_t *n_eval, const float *dl_dimage, float *accum, cudaStream_t st) {
     if (max_items <= 0) return;
+    raster_smem_optin();
     if (fc.model == GEER_BEAP)
-        k_backward<true><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                             ranges, order, payload, gpayload, flags, cull, remaining,
+        k_backward<true><<<max_items, kPipeThreads, sizeof(PipeSmem<true>) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
+                                                             ranges, order, pay_map, gpay_map, flags, remaining,
                                                              n_eval, dl_dimage, accum);
     else
-        k_backward<false><<<max_items, kPipeThreads, 0, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                              ranges, order, payload, gpayload, flags, cull, remaining,
+        k_backward<false><<<max_items, kPipeThreads, sizeof(PipeSmem<true>) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
+                                                              ranges, order, pay_map, gpay_map, flags, remaining,
                                                               n_eval, dl_dimage, accum);
 }
 

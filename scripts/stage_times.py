@@ -26,5 +26,5 @@ for _ in range(7):
     r.forward(ds, cam, cfg)
     r.backward(dl)
     st.append(r.stats())
-keys = ["ms_prep", "ms_dup", "ms_sort", "ms_render", "ms_total", "ms_backward", "fixup_pixels", "kappa_rechecks", "warp_entries", "evaluated_pairs"]
+keys = ["ms_prep", "ms_dup", "ms_sort", "ms_render", "ms_total", "ms_backward", "fixup_pixels", "kappa_rechecks", "warp_entries", "evaluated_pairs", "streamed_entries"]
 print(json.dumps({k: float(np.median([s[k] for s in st])) for k in keys}))
