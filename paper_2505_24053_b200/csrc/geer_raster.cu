@@ -236,9 +236,6 @@ struct __align__(128) PipeSmem {
     uint32_t gid[kStages][kStageEntries];
     int count[kStages];  // entries in the stage; 0 = end of stream
     uint8_t idx[kStages][kConsumerWarps][kStageEntries + 4];  // per warp: its kept entries, padded with null slots
-    float4 patch[kConsumerWarps];            // per consumer warp: mirror-space bounds of its pixels
-    float4 pcone[kConsumerWarps];            // per consumer warp: cone around its pixel rays (cam frame)
-                                             // (unit axis c, cos^2 beta), see cone_misses
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     int done_warps;
@@ -659,8 +656,7 @@ __device__ __forceinline__ float4 ray_mirror_bounds(const FrameConst &fc, const 
 // Cone around a warp's pixel rays in the camera frame: axis c = normalised sum of the lanes' rays,
 // sin^2(beta) = max over lanes of |c x d|^2 / |d|^2, widened by 2% + 1e-9 for rounding (no
 // transcendental functions: this runs once per CTA on every consumer thread).
-__device__ __forceinline__ void publish_cone(float4 *pcone, const FrameConst &fc, int warp, int lane, bool valid,
-                                             const double d[3]) {
+__device__ __forceinline__ float4 warp_cone(const FrameConst &fc, bool valid, const double d[3]) {
     double c[3];
     for (int i = 0; i < 3; ++i)
         c[i] = valid ? fma(fc.R[i * 3 + 2], d[2], fma(fc.R[i * 3 + 1], d[1], fc.R[i * 3 + 0] * d[0])) : 0.0;
@@ -681,17 +677,15 @@ __device__ __forceinline__ void publish_cone(float4 *pcone, const FrameConst &fc
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sin2 = fmaxf(sin2, __shfl_xor_sync(0xffffffffu, sin2, o));
     sin2 = fmaf(sin2, 1.02f, 1e-9f);
-    if (lane == 0 && warp < kConsumerWarps) {
-        const float inv = nrm2 > 0.0 ? (float)(1.0 / sqrt(nrm2)) : 0.f;
-        // the bound needs beta <= 45 deg (sin^2 <= 0.5); cos^2 = 0 disables the test otherwise
-        pcone[warp] = nrm2 > 0.0 && sin2 < 0.5f ? make_float4((float)sx * inv, (float)sy * inv, (float)sz * inv, 1.0f - sin2)
-                                                : make_float4(0.f, 0.f, 1.f, 0.f);
-    }
+    const float inv = nrm2 > 0.0 ? (float)(1.0 / sqrt(nrm2)) : 0.f;
+    // the bound needs beta <= 45 deg (sin^2 <= 0.5); cos^2 = 0 disables the test otherwise
+    return nrm2 > 0.0 && sin2 < 0.5f ? make_float4((float)sx * inv, (float)sy * inv, (float)sz * inv, 1.0f - sin2)
+                                     : make_float4(0.f, 0.f, 1.f, 0.f);
 }
 
 // Warp-wide union of the lanes' mirror bounds (lanes without a pixel contribute nothing); lane 0
 // stores it as the warp's patch for the producer's culling masks.
-__device__ __forceinline__ void publish_patch(float4 *patch, int warp, int lane, bool valid, float4 b) {
+__device__ __forceinline__ float4 warp_patch(bool valid, float4 b) {
     if (!valid) b = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -700,7 +694,7 @@ __device__ __forceinline__ void publish_patch(float4 *patch, int warp, int lane,
         b.z = fminf(b.z, __shfl_xor_sync(0xffffffffu, b.z, o));
         b.w = fmaxf(b.w, __shfl_xor_sync(0xffffffffu, b.w, o));
     }
-    if (lane == 0 && warp < kConsumerWarps) patch[warp] = b;
+    return b;
 }
 
 #ifdef GEER_CTA_TIMING
@@ -708,6 +702,7 @@ __device__ __forceinline__ void publish_patch(float4 *patch, int warp, int lane,
 // (ns), SM id and warp-entries, read back by geer_debug_cta_times (scripts/cta_timing.py).
 __device__ unsigned long long g_cta_t0[1 << 16], g_cta_t1[1 << 16];
 __device__ int g_cta_sm[1 << 16], g_cta_went[1 << 16];
+__device__ unsigned long long g_cta_ts[1 << 16], g_cta_tf[1 << 16];  // setup done, first stage ready
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -755,24 +750,25 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
         g_cta_went[blockIdx.x] = 0;
     }
 #endif
-    const bool valid = tid < it.z;
-    const int p = valid ? pix_list[it.y + tid] : 0;
-    double d64[3] = {0.0, 0.0, 1.0};
-    if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
-    if (warp < kConsumerWarps) {
-        publish_patch(S.patch, warp, lane, valid, ray_mirror_bounds(fc, d64));
-        publish_cone(S.pcone, fc, warp, lane, valid, d64);
-    }
-    pipe_init(S);  // (its __syncthreads also publishes the patches)
+    // the producer starts streaming right away; the consumers set up their pixels meanwhile
+    pipe_init(S);
     if (warp == kConsumerWarps) {
         pipe_produce<false, false>(S, order, &pay_map, nullptr, e0, e1 - e0, true, &counters[4]);
         return;
     }
+    const bool valid = tid < it.z;
+    const int p = valid ? pix_list[it.y + tid] : 0;
+    double d64[3] = {0.0, 0.0, 1.0};
+    if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
+    const float4 my_patch = warp_patch(valid, ray_mirror_bounds(fc, d64));
+    const float4 my_cone = warp_cone(fc, valid, d64);
+#ifdef GEER_CTA_TIMING
+    if (tid == 0 && blockIdx.x < (1u << 16)) g_cta_ts[blockIdx.x] = gtimer();
+#endif
     const Ray64 R = make_ray(d64);
     sray[tid][0] = d64[0];
     sray[tid][1] = d64[1];
     sray[tid][2] = d64[2];
-    const float4 my_patch = S.patch[warp], my_cone = S.pcone[warp];
     PixelState ps{0.f, 0.f, 0.f, valid ? 1.0f : 0.0f, 1.0f, 0.f, -1.0f, 0, 0, 0};
     int rechecks = 0, went = 0;
     bool warp_live = __any_sync(0xffffffffu, valid);
@@ -781,6 +777,9 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
     int s = 0, base = 0;
     for (;;) {
         mbar_wait(&S.full[s], phase);
+#ifdef GEER_CTA_TIMING
+        if (tid == 0 && base == 0 && blockIdx.x < (1u << 16)) g_cta_tf[blockIdx.x] = gtimer();
+#endif
         const int n = S.count[s];
         if (n == 0) break;
         if (warp_live) {
@@ -988,19 +987,18 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
     __syncthreads();
     const int wmax = __reduce_max_sync(0xffffffffu, ne);
     if (lane == 0 && wmax > 0) atomicMax(&smax, wmax);
-    double d64[3] = {0.0, 0.0, 1.0};
-    if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
-    if (warp < kConsumerWarps) {
-        publish_patch(S.patch, warp, lane, valid, ray_mirror_bounds(fc, d64));
-        publish_cone(S.pcone, fc, warp, lane, valid, d64);
-    }
-    pipe_init(S);  // (its __syncthreads also publishes smax and the patches)
+    pipe_init(S);  // (its __syncthreads also publishes smax)
     const int max_n = smax;
     if (max_n == 0) return;
     if (warp == kConsumerWarps) {
         pipe_produce<true, true>(S, order, &pay_map, &gpay_map, e0, max_n, false);
         return;
     }
+    // the producer streams while the consumers set up their pixels
+    double d64[3] = {0.0, 0.0, 1.0};
+    if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
+    const float4 my_patch = warp_patch(valid, ray_mirror_bounds(fc, d64));
+    const float4 my_cone = warp_cone(fc, valid, d64);
     const Ray64 R = make_ray(d64);
     if (valid) {
         sray[tid][0] = d64[0];
@@ -1008,7 +1006,6 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
         sray[tid][2] = d64[2];
     }
     const float dx = (float)d64[0], dy = (float)d64[1], dz = (float)d64[2];
-    const float4 my_patch = S.patch[warp], my_cone = S.pcone[warp];
     const float t_fin = valid ? remaining[p] : 0.f;
     float gl0 = 0.f, gl1 = 0.f, gl2 = 0.f;
     if (valid) {
@@ -1205,6 +1202,13 @@ void launch_fill_background(const FrameConst &fc, float *color, float *remaining
 }  // namespace geer
 
 #ifdef GEER_CTA_TIMING
+extern "C" int geer_debug_cta_phases(unsigned long long *ts, unsigned long long *tf, int n) {
+    if (n > (1 << 16)) n = 1 << 16;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(ts, geer::g_cta_ts, sizeof(unsigned long long) * n);
+    cudaMemcpyFromSymbol(tf, geer::g_cta_tf, sizeof(unsigned long long) * n);
+    return (int)cudaGetLastError();
+}
 extern "C" int geer_debug_cta_times(unsigned long long *t0, unsigned long long *t1, int *sm, int *went, int n) {
     if (n > (1 << 16)) n = 1 << 16;
     cudaDeviceSynchronize();

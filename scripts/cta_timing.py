@@ -29,7 +29,15 @@ f = lib.geer_debug_cta_times
 f.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int]
 f(t0.ctypes.data, t1.ctypes.data, sm.ctypes.data, went.ctypes.data, n)
 st = r.stats()
+ts = np.zeros(n, np.uint64); tf = np.zeros(n, np.uint64)
+f2 = lib.geer_debug_cta_phases
+f2.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+f2(ts.ctypes.data, tf.ctypes.data, n)
 ok = t1 > 0
+ph_setup = (ts[ok].astype(np.int64) - t0[ok].astype(np.int64)) / 1e3
+ph_first = (tf[ok].astype(np.int64) - ts[ok].astype(np.int64)) / 1e3
+print("phase us: setup (start -> pipe_init) mean %.2f p50 %.2f; first stage wait mean %.2f p50 %.2f" %
+      (ph_setup.mean(), np.median(ph_setup), ph_first.mean(), np.median(ph_first)))
 t0 = t0[ok].astype(np.int64); t1 = t1[ok].astype(np.int64); sm = sm[ok]; went = went[ok]
 base = t0.min()
 t0 -= base; t1 -= base
