@@ -88,6 +88,9 @@ struct geer_ctx {
     int64_t n_entries = 0;
     int max_items = 0;
     CUtensorMap pay_map, gpay_map;  // gather4 maps over the payload / grad payload arrays
+    // K0 cache: the camera setup depends only on the camera and the tile size
+    bool cam_valid = false, cam_pixel_tile = false;
+    FrameConst cam_fc{};
     const float *fwd_remaining = nullptr;  // remaining written by the last forward (backward input)
     float ms[6] = {};
     unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs, [2] fix-up pixels, [3] warp-entries, [4] streamed entries
@@ -249,6 +252,15 @@ int camera_setup(geer_ctx *c, bool want_pixel_tile, cudaStream_t st) {
     return GEER_OK;
 }
 
+// Whether the K0 outputs in the context are those of this frame's camera (same model, size, tiling,
+// pose and intrinsics, compared bit for bit).
+bool camera_cached(const geer_ctx *c, bool want_pixel_tile) {
+    if (!c->cam_valid || (want_pixel_tile && !c->cam_pixel_tile)) return false;
+    const FrameConst &a = c->cam_fc, &b = c->fc;
+    return a.width == b.width && a.height == b.height && a.model == b.model && a.tile_px == b.tile_px &&
+           memcmp(a.R, b.R, sizeof(a.R)) == 0 && memcmp(&a.fov_x, &b.fov_x, sizeof(double) * 10) == 0;
+}
+
 // Full association (+ raster when color != null) for the scene in c->scene.
 int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, bool want_export, cudaStream_t st) {
     int rc = 0;
@@ -261,8 +273,14 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
     GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 5 * sizeof(unsigned long long), st));
     GEER_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
-    rc = camera_setup(c, want_export, st);
-    if (rc) return rc;
+    if (!camera_cached(c, want_export)) {
+        c->cam_valid = false;
+        rc = camera_setup(c, want_export, st);
+        if (rc) return rc;
+        c->cam_valid = true;
+        c->cam_pixel_tile = want_export || fc.model != GEER_BEAP;
+        c->cam_fc = fc;
+    }
 
     // ---- K1 preprocess
     Payload *payload = ENSURE(Payload, c->payload, n);

@@ -103,3 +103,23 @@ def test_pbf_culling_is_exact(config_name, n, w, h):
         assert torch.equal(a, b)
     assert st_on["evaluated_pairs"] == st_off["evaluated_pairs"]
     assert st_on["warp_entries"] <= st_off["warp_entries"]
+
+
+def test_camera_setup_cache_follows_the_camera():
+    """K0 is cached per camera: alternating poses (same size) must match fresh renders bit for bit."""
+    scene = synth.config_scene("C2", n=20_000)
+    cam_a = synth.config_camera("C2", width=320, height=180)
+    rot, t = synth.look_at((0.7, 0.2, -1.9))
+    from paper_2505_24053_b200.scene import Camera
+
+    cam_b = Camera(width=320, height=180, model="beap", rotation=rot, translation=t, fov_x=cam_a.fov_x,
+                   fov_y=cam_a.fov_y)
+    cfg = renderer.RenderConfig()
+    ds = DeviceScene.from_scene(scene)
+    fresh = {}
+    for name, cam in (("a", cam_a), ("b", cam_b)):
+        fresh[name] = DeviceRenderer(0).forward(ds, cam, cfg)[0].clone()
+    r = DeviceRenderer(0)
+    for name, cam in (("a", cam_a), ("b", cam_b), ("a", cam_a), ("a", cam_a), ("b", cam_b)):
+        col = r.forward(ds, cam, cfg)[0]
+        assert torch.equal(col, fresh[name]), name
