@@ -169,6 +169,14 @@ int geer_l1_grad(const float *color, const float *target, const uint8_t *mask, f
 int geer_adam(float *param, const float *grad, float *m, float *v, const float *lr, int64_t n, float beta1,
               float beta2, float eps, int32_t step, void *stream);
 
+/* Masked (1 - w) L1 + w (1 - SSIM) loss and its image gradient (trainer.py:114-155, SSIM window
+ * trainer.py:26-69) for an (H,W,3) f32 device image against an (H,W,3) f32 target; mask (H,W) u8
+ * (NULL = all valid).  out (device, 3 doubles): total, L1, 1 - SSIM.  workspace: device buffer of
+ * geer_loss_workspace_bytes(H, W). */
+size_t geer_loss_workspace_bytes(int height, int width);
+int geer_loss(const float *color, const float *target, const uint8_t *mask, int height, int width, float ssim_weight,
+              void *workspace, double *out, float *dl_dimage, void *stream);
+
 /* ---- diagnostics ------------------------------------------------------------- */
 /* Measured FP32 FMA throughput of the device (scalar FFMA and packed FFMA2 chains), TFLOP/s: the
  * roofline denominator of the FP32-bound raster kernels (bench.py). */

@@ -33,6 +33,7 @@ UNITS = {
     "geer_sort.cu": [],
     "geer_api.cu": [],
     "geer_train.cu": [],
+    "geer_loss.cu": [],
 }
 
 

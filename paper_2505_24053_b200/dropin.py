@@ -8,7 +8,7 @@
 
 The trainer imports ``render`` / ``render_backward`` by name (trainer.py:23),
 so both ``raygauss.renderer`` and ``raygauss.trainer`` are patched (SURVEY
-§3.3).  Results come back as the reference's OWN dataclasses
+§3.3); ``raygauss.trainer.loss`` (L1 + SSIM, trainer.py:114-155) runs on the GPU too.  Results come back as the reference's OWN dataclasses
 (``raygauss.renderer.FrameOutput`` with a ``raygauss.camera.BEAPImage``,
 ``raygauss.renderer.SceneGrads``, ``raygauss.association.RenderGraph``), so
 code that type-checks or pattern-matches on them keeps working.
@@ -71,9 +71,16 @@ def build_render_graph(scene, camera, lam: float = 3.0, tile_px: int = 16, grid=
     return _to_ref_graph(association.build_render_graph(scene, camera, lam, tile_px), _ref("association"))
 
 
+def loss(rendered, target, ssim_weight: float = 0.2):
+    """``raygauss.trainer.loss`` replacement (trainer.py:114-155): masked L1 + SSIM on the GPU."""
+    from . import train
+
+    return train.loss(rendered, target, ssim_weight)
+
+
 # (module, attribute) pairs that install() rebinds
 TARGETS = (("renderer", "render"), ("renderer", "render_backward"), ("association", "build_render_graph"),
-           ("trainer", "render"), ("trainer", "render_backward"))
+           ("trainer", "render"), ("trainer", "render_backward"), ("trainer", "loss"))
 
 
 def install(with_graph: bool = False) -> list[str]:
@@ -87,7 +94,7 @@ def install(with_graph: bool = False) -> list[str]:
 
     _lib.load()
     repl = {"render": make_render(with_graph), "render_backward": render_backward,
-            "build_render_graph": build_render_graph}
+            "build_render_graph": build_render_graph, "loss": loss}
     patched = []
     for mod_name, attr in TARGETS:
         try:

@@ -38,6 +38,70 @@ def shard(n_items: int, rank: int, world: int) -> range:
     return range(start, start + base + (1 if rank < extra else 0))
 
 
+SSIM_WEIGHT = 0.2  # trainer.py:114 loss(..., ssim_weight=0.2)
+
+
+class LossWorkspace:
+    """Device scratch of geer_loss for one image size (grow-only)."""
+
+    def __init__(self):
+        self.buf = None
+        self.out = None
+
+    def get(self, h: int, w: int, device):
+        nbytes = int(_lib.load().geer_loss_workspace_bytes(h, w))
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(device):
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            self.out = torch.empty(3, dtype=torch.float64, device=device)
+        return self.buf, self.out
+
+
+def loss_device(color: torch.Tensor, target: torch.Tensor, mask: torch.Tensor | None = None,
+                ssim_weight: float = SSIM_WEIGHT, grad: torch.Tensor | None = None,
+                workspace: LossWorkspace | None = None):
+    """trainer.loss (trainer.py:114-155) on device tensors: returns (out, grad).
+
+    ``out`` is a float64 CUDA tensor (total, L1, 1 - SSIM); ``grad`` the (H,W,3) fp32 image gradient.
+    ``mask``: (H,W) bool/uint8 CUDA tensor of valid target pixels (None = all valid).
+    """
+    h, w = int(color.shape[0]), int(color.shape[1])
+    for t in (color, target):
+        if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous() or tuple(t.shape) != (h, w, 3):
+            raise ValueError("color and target must be contiguous (H,W,3) float32 CUDA tensors")
+    m = None
+    if mask is not None:
+        m = mask.to(torch.uint8).contiguous()
+        if tuple(m.shape) != (h, w):
+            raise ValueError("mask must be (H,W)")
+    ws = workspace or LossWorkspace()
+    buf, out = ws.get(h, w, color.device)
+    if grad is None:
+        grad = torch.empty_like(color)
+    stream = torch.cuda.current_stream(color.device).cuda_stream
+    _lib.check(_lib.load().geer_loss(color.data_ptr(), target.data_ptr(), m.data_ptr() if m is not None else None,
+                                     h, w, ctypes.c_float(ssim_weight), buf.data_ptr(), out.data_ptr(),
+                                     grad.data_ptr(), stream))
+    return out, grad
+
+
+def loss(rendered, target, ssim_weight: float = SSIM_WEIGHT, device: int = 0):
+    """Drop-in for raygauss.trainer.loss (trainer.py:114-155): (total, dL/drendered) in float64 numpy.
+
+    ``target`` is a BEAPImage-like object with ``color`` (H,W,3) and ``mask`` (H,W).  The loss and
+    its gradient are computed by the CUDA kernels in fp32 with fp64 sums.
+    """
+    rendered = np.asarray(rendered)
+    tcol = np.asarray(target.color)
+    if rendered.shape != tcol.shape:
+        raise ValueError("rendered and target shapes disagree")  # trainer.py:121-122
+    dev = torch.device(f"cuda:{device}")
+    c = torch.as_tensor(np.ascontiguousarray(rendered, dtype=np.float32), device=dev)
+    t = torch.as_tensor(np.ascontiguousarray(tcol, dtype=np.float32), device=dev)
+    m = torch.as_tensor(np.ascontiguousarray(np.asarray(target.mask, dtype=np.uint8)), device=dev)
+    out, g = loss_device(c, t, m, ssim_weight)
+    return float(out[0].item()), g.double().cpu().numpy()
+
+
 def allreduce_grads(buf: torch.Tensor, world: int) -> torch.Tensor:
     """Sum the flat per-rank gradient buffer over all ranks in place (ONE collective per step).
 
@@ -105,6 +169,8 @@ class MultiViewTrainer:
         self.grad_numel = self.params.numel
         self.last_loss = None
         self._bufs = {}
+        self.ssim_weight = SSIM_WEIGHT
+        self.loss_ws = LossWorkspace()
         self.lib = _lib.load()
 
     @classmethod
@@ -140,12 +206,11 @@ class MultiViewTrainer:
         for cam, target in zip(self.cameras, self.targets):
             color, rem, cnt, dl = self._out(cam)
             self.renderer.forward(self.params.scene, cam, self.config, out=(color, rem, cnt))
-            npx = cam.height * cam.width
-            _lib.check(self.lib.geer_l1_grad(color.data_ptr(), target.data_ptr(), None, dl.data_ptr(), npx,
-                                             ctypes.c_float(1.0 / (npx * 3)), stream))
+            # trainer.py:269 loss(): (1 - w) L1 + w (1 - SSIM) and its image gradient
+            out, _ = loss_device(color, target, None, self.ssim_weight, grad=dl, workspace=self.loss_ws)
             self.renderer.backward(dl, grads=self.grads.scene, accumulate=True, opacity_logit=True)
             if compute_loss:
-                loss += float((color - target).abs().mean())
+                loss += float(out[0].item())
         allreduce_grads(self.grads.buf, self.world)
         self.t += 1
         _lib.check(self.lib.geer_adam(self.params.buf.data_ptr(), self.grads.buf.data_ptr(), self.m.data_ptr(),

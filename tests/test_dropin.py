@@ -23,15 +23,15 @@ def test_install_patches_renderer_association_and_trainer():
     import paper_2505_24053_b200 as pkg
     from paper_2505_24053_b200 import dropin
 
-    orig = (rr.render, rr.render_backward, ra.build_render_graph, rt.render, rt.render_backward)
+    orig = (rr.render, rr.render_backward, ra.build_render_graph, rt.render, rt.render_backward, rt.loss)
     patched = pkg.install()
     try:
         assert set(patched) == {"raygauss.renderer.render", "raygauss.renderer.render_backward",
                                 "raygauss.association.build_render_graph", "raygauss.trainer.render",
-                                "raygauss.trainer.render_backward"}
+                                "raygauss.trainer.render_backward", "raygauss.trainer.loss"}
         assert rr.render is rt.render and rr.render is not orig[0]
         assert rr.render_backward is dropin.render_backward is rt.render_backward
         assert ra.build_render_graph is dropin.build_render_graph
     finally:
         pkg.uninstall()
-    assert (rr.render, rr.render_backward, ra.build_render_graph, rt.render, rt.render_backward) == orig
+    assert (rr.render, rr.render_backward, ra.build_render_graph, rt.render, rt.render_backward, rt.loss) == orig
