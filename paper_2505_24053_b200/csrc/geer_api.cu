@@ -79,6 +79,7 @@ struct geer_ctx {
     cudaStream_t own_stream = nullptr;
     bool timing = false;
     cudaEvent_t ev[6] = {};
+    cudaEvent_t ev_hdr = nullptr;  // the 12-byte frame header has reached the host
     // frame state
     FrameConst fc{};
     geer_scene scene{};
@@ -93,7 +94,7 @@ struct geer_ctx {
     FrameConst cam_fc{};
     const float *fwd_remaining = nullptr;  // remaining written by the last forward (backward input)
     float ms[6] = {};
-    unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs, [2] fix-up pixels, [3] warp-entries, [4] streamed entries
+    unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs, [2] fix-up pixels, [3] warp-entries, [4] streamed entries, [5] graph entries (K1)
     int *d_err = nullptr;
     int64_t *h_hdr = nullptr;  // pinned: [0] total entries, [1] error code
     // camera buffers
@@ -271,7 +272,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     c->have_frame = false;
     c->have_raster = false;
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
-    GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 5 * sizeof(unsigned long long), st));
+    GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 6 * sizeof(unsigned long long), st));
     GEER_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
     if (!camera_cached(c, want_export)) {
         c->cam_valid = false;
@@ -305,11 +306,17 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     rc = make_row_map(&c->gpay_map, gpayload, n, (int)sizeof(GradPayload));
     if (rc) return rc;
     launch_preprocess(fc, sc, (const double *)c->medges_x.p, (const double *)c->medges_y.p, payload, gpayload, dkey, cnt, ar,
-                      flags, mu, dep, c->d_err, st);
+                      flags, mu, dep, c->d_err, c->d_counters + 5, st);
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[1], st));
 
     // ---- dup: depth order, scan, header D2H, emit
+    // The entry total (summed by K1) and the error flag go to the host right after K1; the depth
+    // sort and count scan, which do not need them, are queued before the host waits, so the GPU
+    // never idles on this round trip.
     int64_t total = 0;
+    GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[0], c->d_counters + 5, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[1], c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GEER_CUDA(cudaEventRecord(c->ev_hdr, st));
     if (n > 0) {
         launch_iota(giota, n, st);
         size_t b1 = sort_depth_temp_bytes(n), b2 = scan_temp_bytes(n);
@@ -318,12 +325,8 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         gather_counts(gsorted, cnt, cnts, n, st);
         GEER_CUDA(cudaMemsetAsync(offs, 0, sizeof(int64_t), st));
         inclusive_scan_i64(tmp, b2, cnts, offs + 1, n, st);
-        GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[0], offs + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    } else {
-        c->h_hdr[0] = 0;
     }
-    GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[1], c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
-    GEER_CUDA(cudaStreamSynchronize(st));
+    GEER_CUDA(cudaEventSynchronize(c->ev_hdr));
     int err = (int)(c->h_hdr[1] & 0xFFFFFFFF);
     if (err == GEER_ERR_NOT_PD) return fail(GEER_ERR_NOT_PD, "view covariance must be positive definite");
     if (err == GEER_ERR_NOT_SYMMETRIC) return fail(GEER_ERR_NOT_SYMMETRIC, "view covariance must be symmetric");
@@ -498,7 +501,8 @@ geer_ctx *geer_create(int device) {
     c->device = device;
     bool ok = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) == cudaSuccess;
     for (int i = 0; i < 6 && ok; ++i) ok = cudaEventCreate(&c->ev[i]) == cudaSuccess;
-    ok = ok && cudaMalloc(&c->d_counters, 5 * sizeof(unsigned long long)) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&c->ev_hdr, cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaMalloc(&c->d_counters, 6 * sizeof(unsigned long long)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->d_err, sizeof(int)) == cudaSuccess;
     ok = ok && cudaMallocHost(&c->h_hdr, 2 * sizeof(int64_t)) == cudaSuccess;
     if (!ok) {
@@ -524,6 +528,7 @@ void geer_destroy(geer_ctx *c) {
     for (Buf *b : bufs) free_buf(*b);
     for (int i = 0; i < 6; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    if (c->ev_hdr) cudaEventDestroy(c->ev_hdr);
     if (c->d_counters) cudaFree(c->d_counters);
     if (c->d_err) cudaFree(c->d_err);
     if (c->h_hdr) cudaFreeHost(c->h_hdr);

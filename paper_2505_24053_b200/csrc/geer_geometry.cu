@@ -548,11 +548,6 @@ __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, con
     for (int i = 0; i < 3; ++i) ar.x[i] = ar.y[i] = 0;
     // raster culling bounds in mirror space (x_lo, x_hi, y_lo, y_hi); clamped: everything
     float4 bx = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
-    // raster culling: the visual cone of the lam-ellipsoid (camera frame, full line).  With P = Sigma_c^-1,
-    // nu = P mu, a = mu^T nu - lam^2 > 0 (camera outside):  kappa(d) <= lam^2  <=>  d^T K d >= 0,
-    // K = nu nu^T - a P, stored divided by nu^T nu (then lambda_max(K) <= 1).  .b.z: lambda_max bound
-    // (inf: never cull, e.g. clamped or camera inside)
-    float4 ca = make_float4(0.f, 0.f, 0.f, 0.f), cb = make_float4(0.f, 0.f, INFINITY, 0.f);
     // association.py:417-419 near cull
     if (depth >= kNearLimit) {
         // association.py:154-160 symmetric + positive-definite (Cholesky pivots)
@@ -617,35 +612,13 @@ __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, con
                     const int cx = axis_tiles(t00, t02, t22, rt0, rt1, sex, fc.n_x + 1, ar.x, bx.x, bx.y);
                     const int cy = axis_tiles(t11, t12, t22, rp0, rp1, sey, fc.n_y + 1, ar.y, bx.z, bx.w);
                     n_ent = (int64_t)cx * cy;
-                    // Q = R_c R(q): camera frame <- Gaussian axes;  P = Q diag(1/s^2) Q^T
-                    double Q[9], P[9], nu[3];
-                    for (int i = 0; i < 3; ++i)
-                        for (int j = 0; j < 3; ++j)
-                            Q[i * 3 + j] = R[i * 3 + 0] * rot[0 * 3 + j] + R[i * 3 + 1] * rot[1 * 3 + j] +
-                                           R[i * 3 + 2] * rot[2 * 3 + j];
-                    const double is2[3] = {1.0 / (s[0] * s[0]), 1.0 / (s[1] * s[1]), 1.0 / (s[2] * s[2])};
-                    for (int i = 0; i < 3; ++i)
-                        for (int j = 0; j < 3; ++j)
-                            P[i * 3 + j] = Q[i * 3 + 0] * is2[0] * Q[j * 3 + 0] + Q[i * 3 + 1] * is2[1] * Q[j * 3 + 1] +
-                                           Q[i * 3 + 2] * is2[2] * Q[j * 3 + 2];
-                    for (int i = 0; i < 3; ++i) nu[i] = P[i * 3 + 0] * mu[0] + P[i * 3 + 1] * mu[1] + P[i * 3 + 2] * mu[2];
-                    const double a = mu[0] * nu[0] + mu[1] * nu[1] + mu[2] * nu[2] - lam2;
-                    const double nn = nu[0] * nu[0] + nu[1] * nu[1] + nu[2] * nu[2];
-                    if (a > 0.0 && nn > 0.0) {
-                        const double in = 1.0 / nn;
-                        auto K = [&](int i, int j) { return (float)((nu[i] * nu[j] - a * P[i * 3 + j]) * in); };
-                        ca = make_float4(K(0, 0), K(1, 1), K(2, 2), K(0, 1));
-                        cb = make_float4(K(0, 2), K(1, 2), 1.0f, 0.f);
-                    }
                 }
             }
         }
     }
     count[g] = n_ent;
     ranges[g] = ar;
-    cr.box = bx;
-    cr.k0 = ca;
-    cr.k1 = cb;
+    cr.box = bx;  // (the visual-cone part of the record is written by the payload half)
     // association.py:335-340 key bits (depth > 0): f32 bits | 0x80000000; non-emitting last
     const uint32_t kb = __float_as_uint((float)depth) | 0x80000000u;
     depth_key[g] = n_ent > 0 ? kb : 0xFFFFFFFFu;
@@ -664,8 +637,8 @@ constexpr int kStageRow = kPayHead + 1;                   // padded staging row
 constexpr int kGradRow = sizeof(GradPayload) / 16;
 
 template <int NB>
-__device__ uint8_t payload_block(const FrameConst &fc, const geer_scene &sc, float *ssh, int64_t g0, int cnt_b, int lt,
-                                 Payload *__restrict__ payload, GradPayload *__restrict__ gpayload) {
+__device__ uint8_t payload_block(const FrameConst &fc, const geer_scene &sc, float *ssh, Cull *scull, int64_t g0,
+                                 int cnt_b, int lt) {
     const int nthr = 128;
     {
         // stage this block's SH coefficients (contiguous) with coalesced loads
@@ -717,6 +690,33 @@ __device__ uint8_t payload_block(const FrameConst &fc, const geer_scene &sc, flo
         if (pre > 0) gate |= (uint8_t)(1u << c);
         rgb[c] = pre > 0.0 ? pre : 0.0;
     }
+    // raster culling: the visual cone of the lam-ellipsoid (camera frame, full line).  With
+    // P = Sigma_c^-1 = (W R_c^T)^T (W R_c^T), nu = P mu_c, a = mu_c^T nu - lam^2 > 0 (camera outside):
+    // kappa(d) <= lam^2 <=> d^T K d >= 0, K = nu nu^T - a P, stored divided by nu^T nu (then
+    // lambda_max(K) <= 1).  k1.z is the lambda_max bound (inf: never culled, e.g. camera inside).
+    {
+        double Wc[9], P[9], mc[3], nu[3];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+                Wc[i * 3 + j] = W[i * 3 + 0] * fc.R[j * 3 + 0] + W[i * 3 + 1] * fc.R[j * 3 + 1] + W[i * 3 + 2] * fc.R[j * 3 + 2];
+        for (int i = 0; i < 3; ++i)
+            for (int j = i; j < 3; ++j)
+                P[i * 3 + j] = P[j * 3 + i] = Wc[0 * 3 + i] * Wc[0 * 3 + j] + Wc[1 * 3 + i] * Wc[1 * 3 + j] + Wc[2 * 3 + i] * Wc[2 * 3 + j];
+        for (int i = 0; i < 3; ++i)
+            mc[i] = fc.R[i * 3 + 0] * mean[0] + fc.R[i * 3 + 1] * mean[1] + fc.R[i * 3 + 2] * mean[2] + fc.t[i];
+        for (int i = 0; i < 3; ++i) nu[i] = P[i * 3 + 0] * mc[0] + P[i * 3 + 1] * mc[1] + P[i * 3 + 2] * mc[2];
+        const double a = mc[0] * nu[0] + mc[1] * nu[1] + mc[2] * nu[2] - fc.lam * fc.lam;
+        const double nn = nu[0] * nu[0] + nu[1] * nu[1] + nu[2] * nu[2];
+        Cull &cr = scull[lt];
+        cr.k0 = make_float4(0.f, 0.f, 0.f, 0.f);
+        cr.k1 = make_float4(0.f, 0.f, INFINITY, 0.f);
+        if (a > 0.0 && nn > 0.0) {
+            const double in = 1.0 / nn;
+            auto K = [&](int i, int j) { return (float)((nu[i] * nu[j] - a * P[i * 3 + j]) * in); };
+            cr.k0 = make_float4(K(0, 0), K(1, 1), K(2, 2), K(0, 1));
+            cr.k1 = make_float4(K(0, 2), K(1, 2), 1.0f, 0.f);
+        }
+    }
     const double smax = fmax(s[0], fmax(s[1], s[2])), smin = fmin(s[0], fmin(s[1], s[2]));
     Payload pl;
     GradPayload gp;
@@ -746,8 +746,8 @@ __global__ void __launch_bounds__(256, 3)
     k_preprocess(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x, const double *__restrict__ medges_y,
                  Payload *__restrict__ payload, GradPayload *__restrict__ gpayload, uint32_t *__restrict__ depth_key,
                  int64_t *__restrict__ count, AxisRanges *__restrict__ ranges, uint8_t *__restrict__ flags,
-                 double *__restrict__ mu_out,
-                 double *__restrict__ depth_out, int *__restrict__ err) {
+                 double *__restrict__ mu_out, double *__restrict__ depth_out, int *__restrict__ err,
+                 unsigned long long *__restrict__ total_entries) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int kStageFloats = (kStageRow + kGradRow) * 4;  // payload-head + grad-payload staging
     __shared__ __align__(16) float ssh[128 * (NB * 3 > kStageFloats ? NB * 3 : kStageFloats)];
@@ -762,14 +762,29 @@ __global__ void __launch_bounds__(256, 3)
         for (int i = lt; i <= fc.n_x; i += 128) sex[i] = medges_x[i];
         for (int i = lt; i <= fc.n_y; i += 128) sey[i] = medges_y[i];
         named_barrier(1, 128);
+#ifdef GEER_EXP_NO_ASSOC
+        if (lt < cnt_b) count[g0 + lt] = 0;
+        sfl[0][lt] = 0;
+        if (false)
+#endif
         sfl[0][lt] = lt < cnt_b ? associate_one(fc, sc, sex, sey, g0 + lt, depth_key, count, ranges, scull[lt],
                                                 mu_out, depth_out, err)
                                 : 0;
     } else {
-        sfl[1][lt] = payload_block<NB>(fc, sc, ssh, g0, cnt_b, lt, payload, gpayload);
+#ifndef GEER_EXP_NO_PAYLOAD
+        sfl[1][lt] = payload_block<NB>(fc, sc, ssh, scull, g0, cnt_b, lt);
+#else
+        sfl[1][lt] = 0;
+#endif
     }
     __syncthreads();
     if (threadIdx.x < cnt_b) flags[g0 + threadIdx.x] = (uint8_t)(sfl[0][threadIdx.x] | sfl[1][threadIdx.x]);
+    if (threadIdx.x < 32) {  // the block's entries, for the frame total (one atomic per block)
+        unsigned long long t = 0;
+        for (int i = threadIdx.x; i < cnt_b; i += 32) t += (unsigned long long)count[g0 + i];
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (threadIdx.x == 0 && t) atomicAdd(total_entries, t);
+    }
     // coalesced write-out of the block's payload rows (head + culling record) and grad payloads
     const float4 *sp = reinterpret_cast<const float4 *>(ssh);
     const float4 *sg = sp + 128 * kStageRow;
@@ -934,7 +949,7 @@ size_t preprocess_smem(const FrameConst &fc) { return sizeof(double) * (fc.n_x +
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
                        Payload *payload, GradPayload *gpayload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges,
                        uint8_t *flags, double *mu_out, double *depth_out, int *err,
-                       cudaStream_t st) {
+                       unsigned long long *total_entries, cudaStream_t st) {
     if (sc.n == 0) return;
     const int blocks = (int)((sc.n + 127) / 128);
     switch (sc.n_bands) {
@@ -942,8 +957,7 @@ void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double 
     case NB:                                                                                                        \
         k_preprocess<NB><<<blocks, 256, preprocess_smem(fc), st>>>(fc, sc, medges_x, medges_y, payload, gpayload,   \
                                                                    depth_key, count, ranges, flags,                \
-                                                                   mu_out,                                         \
-                                                                   depth_out, err);                                \
+                                                                   mu_out, depth_out, err, total_entries);         \
         break;
         GEER_NB_CASE(1) GEER_NB_CASE(2) GEER_NB_CASE(3) GEER_NB_CASE(4) GEER_NB_CASE(5) GEER_NB_CASE(6)
         GEER_NB_CASE(7) GEER_NB_CASE(8) GEER_NB_CASE(9) GEER_NB_CASE(10) GEER_NB_CASE(11) GEER_NB_CASE(12)
