@@ -741,8 +741,11 @@ __device__ uint8_t payload_block(const FrameConst &fc, const geer_scene &sc, flo
 // K1: one block = 128 Gaussians; threads 0-127 run the exact fp64 association, threads 128-255 the
 // raster payload of the same Gaussians (the first is fp64-issue-bound, the second latency-bound,
 // so co-resident they overlap), then the flag bits of both are merged.
+#ifndef K1_MIN_BLOCKS
+#define K1_MIN_BLOCKS 4
+#endif
 template <int NB>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, K1_MIN_BLOCKS)
     k_preprocess(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x, const double *__restrict__ medges_y,
                  Payload *__restrict__ payload, GradPayload *__restrict__ gpayload, uint32_t *__restrict__ depth_key,
                  int64_t *__restrict__ count, AxisRanges *__restrict__ ranges, uint8_t *__restrict__ flags,
