@@ -101,8 +101,10 @@ __global__ void k_beap_tables(FrameConst fc, double2 *col_sc, double2 *row_sc, d
 }
 
 // BEAP tiles are tile_px x tile_px pixel blocks (association.py:310-316).  Pixel
-// list of a tile: contiguous block, ordered so that each warp covers an 8x4
-// patch of a 16x16 tile (coherent early stop); other sizes row-major.
+// list of a 16x16 tile: pixel q = half * 128 + w * 32 + lane lies in the 8x8 patch w (2 x 2 patches)
+// at row 4 * half + lane / 8, column lane % 8 — so a raster thread owning pixels q and q + 128 keeps
+// both in its warp's 8x8 patch, and a warp of 32 consecutive q covers an 8x4 half-patch (coherent
+// early stop either way); other tile sizes row-major.
 __global__ void k_beap_csr(FrameConst fc, int32_t *tile_off, int32_t *pix_list, int32_t *pixel_tile) {
     int t = blockIdx.x;
     int tx = t % fc.n_x, ty = t / fc.n_x;
@@ -120,9 +122,9 @@ __global__ void k_beap_csr(FrameConst fc, int32_t *tile_off, int32_t *pix_list, 
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
         int lx, ly;
         if (swz) {
-            int warp = q >> 5, lane = q & 31;
-            lx = (warp & 1) * 8 + (lane & 7);
-            ly = (warp >> 1) * 4 + (lane >> 3);
+            const int half = q >> 7, w = (q >> 5) & 3, lane = q & 31;
+            lx = (w & 1) * 8 + (lane & 7);
+            ly = (w >> 1) * 8 + half * 4 + (lane >> 3);
         } else {
             lx = q % w;
             ly = q / w;

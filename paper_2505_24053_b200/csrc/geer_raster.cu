@@ -227,15 +227,16 @@ constexpr int kGringGroupBytes = 256;   // 4 x 48-B grad payloads (192 B), padde
 constexpr int kRingGroups = kStageEntries / 4 + 1;
 static_assert(sizeof(Payload) * 4 <= kRingGroupBytes && sizeof(GradPayload) * 4 <= kGringGroupBytes, "ring layout");
 
-template <bool kGrad>
+template <bool kGrad, int NW = kConsumerWarps>
 struct __align__(128) PipeSmem {
+    static constexpr int kNW = NW;  // consumer warps
     // Entries land in groups of 4 (one TMA gather4 per group), each group 128-B aligned; group
     // kStageEntries / 4 holds the null entry (t = 0 for every ray).  Use ring_at / gring_at.
     alignas(128) unsigned char ring[kStages][kRingGroups][kRingGroupBytes];
     alignas(128) unsigned char gring[kGrad ? kStages : 1][kStageEntries / 4][kGringGroupBytes];  // backward only
     uint32_t gid[kStages][kStageEntries];
     int count[kStages];  // entries in the stage; 0 = end of stream
-    uint8_t idx[kStages][kConsumerWarps][kStageEntries + 4];  // per warp: its kept entries, padded with null slots
+    uint8_t idx[kStages][NW][kStageEntries + 4];  // per warp: its kept entries, padded with null slots
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     int done_warps;
@@ -318,7 +319,7 @@ __device__ __forceinline__ void pipe_init(Smem &S) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&S.full[s], 1);
-            mbar_init(&S.empty[s], kConsumerWarps);
+            mbar_init(&S.empty[s], Smem::kNW);
         }
         S.done_warps = 0;
         S.stop = 0;
@@ -376,7 +377,7 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
         const int done = kStageEntries * b;
         const int n = min(kStageEntries, n_total - done);
         // every consumer warp has dropped out: stop streaming (no sentinel needed)
-        if (stop_when_done && *((volatile int *)&S.done_warps) == kConsumerWarps) break;
+        if (stop_when_done && *((volatile int *)&S.done_warps) == Smem::kNW) break;
         const uint32_t g = g_next;
         if (n > 0) g_next = load_gid(b + 1);
         mbar_wait(&S.empty[s], phase ^ 1);
@@ -445,7 +446,8 @@ __device__ __forceinline__ int stage_keep(Smem &S, int s, int warp, int lane, in
 // with arrive_drop and drops out of each later stage's "empty" barrier at the phase it would have
 // released (waiting for that stage's fill first, so the phase is the right one), unless the
 // producer has stopped filling.
-__device__ __forceinline__ void pipe_drop_out(PipeSmem<false> &S, int s, unsigned phase) {
+template <class Smem>
+__device__ __forceinline__ void pipe_drop_out(Smem &S, int s, unsigned phase) {
     const int lane = threadIdx.x & 31;
     for (int k = 0; k < kStages; ++k) {
         if (k > 0) {
@@ -542,45 +544,52 @@ __device__ __forceinline__ void norms64_smem(uint32_t pa, const Ray64 &R, double
 constexpr uint32_t kColOff = 96;  // offsetof(Payload, col)
 constexpr uint32_t kExtOff = 112; // offsetof(Payload, ext)
 
-// The entries of one stage that this warp's PBF mask keeps, front to back, four at a time (the list
+// The entries of one stage that this warp's culling keeps, front to back, a few at a time (the list
 // is padded with null entries, which are exact no-ops).  Culled entries change nothing; the alive
-// count is recorded when a pixel stops (base: entries of the tile before this stage).
+// count is recorded when a pixel stops (base: entries of the tile before this stage).  Each thread
+// owns PX pixels: one payload load from shared memory serves all of them.
 //
 // Stage of mode-1 payloads (rare: tiny, far or very anisotropic Gaussians): the payload mode is
 // decided per entry and each entry runs the reference formulation via finish_t.
-__device__ __forceinline__ void consume_stage_generic(PipeSmem<false> &S, int s, int warp, int cnt, int base,
-                                                      const Ray64 &R, const double *dray, const FrameConst &fc,
-                                                      PixelState &ps, int &rechecks, int &went) {
+template <int PX, class Smem>
+__device__ __forceinline__ void consume_stage_generic(Smem &S, int s, int warp, int cnt, int base, const Ray64 (&R)[PX],
+                                                      const double *const (&dray)[PX], const FrameConst &fc,
+                                                      PixelState (&ps)[PX], int &rechecks, int &went) {
     int k0 = 0;
     for (; k0 < cnt; k0 += 4) {
-        if (k0 > 0 && !__any_sync(0xffffffffu, ps.r > 0.0f)) break;  // warp opaque
+        bool live = false;
+#pragma unroll
+        for (int x = 0; x < PX; ++x) live |= ps[x].r > 0.0f;
+        if (k0 > 0 && !__any_sync(0xffffffffu, live)) break;  // warp opaque
         const uint32_t q = *reinterpret_cast<const uint32_t *>(&S.idx[s][warp][k0]);
 #pragma unroll 1
         for (int u = 0; u < 4; ++u) {
             const int j = (q >> (8 * u)) & 0xFF;
             const Payload &P = ring_at(S, s, j);
             const bool m1 = __any_sync(0xffffffffu, P.col.w < 0.0f);
-            double dd, mm;
-            norms64(P, R, dray, m1, dd, mm);
-            PairT e;
-            const bool unc = finish_t(dd, mm, P, m1, fc, e, rechecks);
-            pixel_update(ps, e.kap, e.t, P.col, unc, base + j + 1);
+#pragma unroll
+            for (int x = 0; x < PX; ++x) {
+                double dd, mm;
+                norms64(P, R[x], dray[x], m1, dd, mm);
+                PairT e;
+                const bool unc = finish_t(dd, mm, P, m1, fc, e, rechecks);
+                pixel_update(ps[x], e.kap, e.t, P.col, unc, base + j + 1);
+            }
         }
     }
     went += k0 < cnt ? k0 : cnt;
 }
 
-// Stage of mode-0 payloads (the common case): four entries' t first (independent work, explicit
-// shared loads), one warp vote for the rare fp64 cutoff re-decisions, then the four serial pixel
-// updates.  t is bit-identical to finish_t's (the backward recomputes it with eval_t).
 #ifndef GEER_FWD_GROUP
 #define GEER_FWD_GROUP 4
 #endif
-constexpr int kFwdGroup = GEER_FWD_GROUP;  // entries evaluated together (ILP vs registers)
 
-template <bool kCutoff>
-__device__ __forceinline__ void consume_stage_fast(PipeSmem<false> &S, int s, int warp, int cnt, int base,
-                                                   const Ray64 &R, const FrameConst &fc, PixelState &ps, int &rechecks,
+// Stage of mode-0 payloads (the common case): G entries' t first (independent work, explicit shared
+// loads), one warp vote for the rare fp64 cutoff re-decisions, then the serial pixel updates.  t is
+// bit-identical to finish_t's (the backward recomputes it with eval_t).
+template <bool kCutoff, int PX, int G, class Smem>
+__device__ __forceinline__ void consume_stage_fast(Smem &S, int s, int warp, int cnt, int base, const Ray64 (&R)[PX],
+                                                   const FrameConst &fc, PixelState (&ps)[PX], int &rechecks,
                                                    int &went) {
 #ifdef GEER_EXP_NOCOMPUTE
     went += cnt;
@@ -589,50 +598,66 @@ __device__ __forceinline__ void consume_stage_fast(PipeSmem<false> &S, int s, in
     const uint32_t rb = smem_u32(&S.ring[s][0][0]);
     const uint32_t ib = smem_u32(&S.idx[s][warp][0]);
     int k0 = 0;
-    for (; k0 < cnt; k0 += kFwdGroup) {
-        if (k0 > 0 && !__any_sync(0xffffffffu, ps.r > 0.0f)) break;  // warp opaque
-        const uint32_t q = kFwdGroup == 4 ? lds_u32(ib + k0) : (lds_u32(ib + (k0 & ~3)) >> (8 * (k0 & 3)));
-        float kap[kFwdGroup], t[kFwdGroup];
-        uint32_t pa[kFwdGroup];
-        int jj[kFwdGroup];
-        bool near[kFwdGroup], unc[kFwdGroup];
+    for (; k0 < cnt; k0 += G) {
+        bool live = false;
+#pragma unroll
+        for (int x = 0; x < PX; ++x) live |= ps[x].r > 0.0f;
+        if (k0 > 0 && !__any_sync(0xffffffffu, live)) break;  // warp opaque
+        const uint32_t q = G == 4 ? lds_u32(ib + k0) : (lds_u32(ib + (k0 & ~3)) >> (8 * (k0 & 3)));
+        float kap[G][PX], t[G][PX];
+        uint32_t pa[G];
+        int jj[G];
+        bool near[G][PX], unc[G][PX];
         bool any_near = false;
 #pragma unroll
-        for (int u = 0; u < kFwdGroup; ++u) {
+        for (int u = 0; u < G; ++u) {
             jj[u] = (q >> (8 * u)) & 0xFF;
             pa[u] = rb + ring_off(jj[u]);
-            double dd, mm;
-            norms64_smem(pa[u], R, dd, mm);
+            const double2 a0 = lds_d2(pa[u] + 0), a1 = lds_d2(pa[u] + 16), a2 = lds_d2(pa[u] + 32);
+            const double2 b0 = lds_d2(pa[u] + 48), b1 = lds_d2(pa[u] + 64), b2 = lds_d2(pa[u] + 80);
             const float sw = lds_f32(pa[u] + kColOff + 12);
-            kap[u] = __fmul_rn((float)mm, rcp_approx((float)dd));
-            float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u], -0.72134752044448170f)));
-            near[u] = false;
-            unc[u] = false;
-            if (kCutoff) {
-                near[u] = fabsf(__fsub_rn(kap[u], fc.lam2f)) <= fc.cutoff_tol;
-                any_near |= near[u];
-                uu = kap[u] <= fc.lam2f ? uu : 0.0f;
+#pragma unroll
+            for (int x = 0; x < PX; ++x) {
+                const Ray64 &r = R[x];
+                // (same arithmetic as norms64 mode 0)
+                const double dd = (fma(a0.y, r.m11, a0.x * r.m00) + fma(a1.y, r.m01, a1.x * r.m22)) +
+                                  fma(a2.y, r.m12, a2.x * r.m02);
+                const double mm = (fma(b0.y, r.m11, b0.x * r.m00) + fma(b1.y, r.m01, b1.x * r.m22)) +
+                                  fma(b2.y, r.m12, b2.x * r.m02);
+                kap[u][x] = __fmul_rn((float)mm, rcp_approx((float)dd));
+                float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u][x], -0.72134752044448170f)));
+                near[u][x] = false;
+                unc[u][x] = false;
+                if (kCutoff) {
+                    near[u][x] = fabsf(__fsub_rn(kap[u][x], fc.lam2f)) <= fc.cutoff_tol;
+                    any_near |= near[u][x];
+                    uu = kap[u][x] <= fc.lam2f ? uu : 0.0f;
+                }
+                t[u][x] = fminf(uu, kMaxBlendTF);
             }
-            t[u] = fminf(uu, kMaxBlendTF);
         }
         if (kCutoff && __any_sync(0xffffffffu, any_near)) {
 #pragma unroll
-            for (int u = 0; u < kFwdGroup; ++u) {  // (fully unrolled: the arrays stay in registers)
-                if (!near[u]) continue;
-                double dd, mm;
-                norms64_smem(pa[u], R, dd, mm);
-                const double k64 = mm / dd;
-                const float sw = lds_f32(pa[u] + kColOff + 12);
-                const float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u], -0.72134752044448170f)));
-                t[u] = k64 <= fc.lam2 ? fminf(uu, kMaxBlendTF) : 0.0f;
-                unc[u] = fabs(k64 - fc.lam2) <= (double)lds_f32(pa[u] + kExtOff);
-                ++rechecks;
+            for (int u = 0; u < G; ++u) {  // (fully unrolled: the arrays stay in registers)
+#pragma unroll
+                for (int x = 0; x < PX; ++x) {
+                    if (!near[u][x]) continue;
+                    double dd, mm;
+                    norms64_smem(pa[u], R[x], dd, mm);
+                    const double k64 = mm / dd;
+                    const float sw = lds_f32(pa[u] + kColOff + 12);
+                    const float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u][x], -0.72134752044448170f)));
+                    t[u][x] = k64 <= fc.lam2 ? fminf(uu, kMaxBlendTF) : 0.0f;
+                    unc[u][x] = fabs(k64 - fc.lam2) <= (double)lds_f32(pa[u] + kExtOff);
+                    ++rechecks;
+                }
             }
         }
 #pragma unroll
-        for (int u = 0; u < kFwdGroup; ++u) {
+        for (int u = 0; u < G; ++u) {
             const float4 col = lds_f4(pa[u] + kColOff);
-            pixel_update(ps, kap[u], t[u], col, unc[u], base + jj[u] + 1);
+#pragma unroll
+            for (int x = 0; x < PX; ++x) pixel_update(ps[x], kap[u][x], t[u][x], col, unc[u][x], base + jj[u] + 1);
         }
     }
     went += k0 < cnt ? k0 : cnt;
@@ -653,14 +678,22 @@ __device__ __forceinline__ float4 ray_mirror_bounds(const FrameConst &fc, const 
     return b;
 }
 
-// Cone around a warp's pixel rays in the camera frame: axis c = normalised sum of the lanes' rays,
-// sin^2(beta) = max over lanes of |c x d|^2 / |d|^2, widened by 2% + 1e-9 for rounding (no
+// Cone around a warp's pixel rays in the camera frame (PX rays per lane): axis c = normalised sum of
+// the rays, sin^2(beta) = max over rays of |c x d|^2 / |d|^2, widened by 2% + 1e-9 for rounding (no
 // transcendental functions: this runs once per CTA on every consumer thread).
-__device__ __forceinline__ float4 warp_cone(const FrameConst &fc, bool valid, const double d[3]) {
-    double c[3];
-    for (int i = 0; i < 3; ++i)
-        c[i] = valid ? fma(fc.R[i * 3 + 2], d[2], fma(fc.R[i * 3 + 1], d[1], fc.R[i * 3 + 0] * d[0])) : 0.0;
-    double sx = c[0], sy = c[1], sz = c[2];
+template <int PX>
+__device__ __forceinline__ float4 warp_cone(const FrameConst &fc, const bool (&valid)[PX], const double (&d)[PX][3]) {
+    double c[PX][3];
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+#pragma unroll
+    for (int x = 0; x < PX; ++x) {
+        for (int i = 0; i < 3; ++i)
+            c[x][i] = valid[x] ? fma(fc.R[i * 3 + 2], d[x][2], fma(fc.R[i * 3 + 1], d[x][1], fc.R[i * 3 + 0] * d[x][0]))
+                               : 0.0;
+        sx += c[x][0];
+        sy += c[x][1];
+        sz += c[x][2];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         sx += __shfl_xor_sync(0xffffffffu, sx, o);
@@ -669,10 +702,13 @@ __device__ __forceinline__ float4 warp_cone(const FrameConst &fc, bool valid, co
     }
     const double nrm2 = sx * sx + sy * sy + sz * sz;
     float sin2 = 0.f;
-    if (valid && nrm2 > 0.0) {
-        const double x0 = sy * c[2] - sz * c[1], x1 = sz * c[0] - sx * c[2], x2 = sx * c[1] - sy * c[0];
-        const double dn2 = c[0] * c[0] + c[1] * c[1] + c[2] * c[2];
-        sin2 = (float)((x0 * x0 + x1 * x1 + x2 * x2) / (nrm2 * dn2));  // |c_hat x d_hat|^2
+#pragma unroll
+    for (int x = 0; x < PX; ++x) {
+        if (valid[x] && nrm2 > 0.0) {
+            const double x0 = sy * c[x][2] - sz * c[x][1], x1 = sz * c[x][0] - sx * c[x][2], x2 = sx * c[x][1] - sy * c[x][0];
+            const double dn2 = c[x][0] * c[x][0] + c[x][1] * c[x][1] + c[x][2] * c[x][2];
+            sin2 = fmaxf(sin2, (float)((x0 * x0 + x1 * x1 + x2 * x2) / (nrm2 * dn2)));  // |c_hat x d_hat|^2
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sin2 = fmaxf(sin2, __shfl_xor_sync(0xffffffffu, sin2, o));
@@ -681,6 +717,15 @@ __device__ __forceinline__ float4 warp_cone(const FrameConst &fc, bool valid, co
     // the bound needs beta <= 45 deg (sin^2 <= 0.5); cos^2 = 0 disables the test otherwise
     return nrm2 > 0.0 && sin2 < 0.5f ? make_float4((float)sx * inv, (float)sy * inv, (float)sz * inv, 1.0f - sin2)
                                      : make_float4(0.f, 0.f, 1.f, 0.f);
+}
+__device__ __forceinline__ float4 warp_cone1(const FrameConst &fc, bool valid, const double (&d)[3]) {
+    const bool v[1] = {valid};
+    const double dd[1][3] = {{d[0], d[1], d[2]}};
+    return warp_cone<1>(fc, v, dd);
+}
+
+__device__ __forceinline__ float4 bounds_union(const float4 &a, const float4 &b) {
+    return make_float4(fminf(a.x, b.x), fmaxf(a.y, b.y), fminf(a.z, b.z), fmaxf(a.w, b.w));
 }
 
 // Warp-wide union of the lanes' mirror bounds (lanes without a pixel contribute nothing); lane 0
@@ -710,8 +755,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
+#ifndef GEER_FWD_PX
+#define GEER_FWD_PX 1
+#endif
+constexpr int kFwdPX = GEER_FWD_PX;                         // pixels per consumer thread
+constexpr int kFwdNW = kConsumerWarps / kFwdPX;             // consumer warps
+constexpr int kFwdThreads = kRasterThreads / kFwdPX + 32;   // + the producer warp
+#ifndef FWD_MIN_BLOCKS2
+#define FWD_MIN_BLOCKS2 (kFwdPX == 1 ? 3 : 4)
+#endif
+using FwdSmem = PipeSmem<false, kFwdNW>;
+
+// K5.  Each consumer thread owns kFwdPX pixels (q = tid + k * 32 * kFwdNW of the work item; the BEAP
+// pixel lists put them in one 8 x 8 patch per warp, k_beap_csr), sharing every payload load and
+// the pipeline overheads between them.
 template <bool kBEAP>
-__global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
+__global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
     k_forward(FrameConst fc, geer_scene sc, const int4 *__restrict__ items, const int32_t *__restrict__ n_items,
               const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
               const double2 *__restrict__ row_sc, const double *__restrict__ dir64, const int32_t *__restrict__ ranges,
@@ -719,8 +778,9 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
               const uint8_t *__restrict__ flags, float *__restrict__ color,
               float *__restrict__ remaining, int32_t *__restrict__ count, int32_t *__restrict__ n_eval,
               unsigned long long *__restrict__ counters, int32_t *__restrict__ fixup_list) {
+    constexpr int PX = kFwdPX, NW = kFwdNW, NT = 32 * kFwdNW;
     extern __shared__ __align__(16) unsigned char dsmem[];  // PipeSmem (dynamic: deep rings exceed 48 KB)
-    PipeSmem<false> &S = *reinterpret_cast<PipeSmem<false> *>(align128(dsmem));
+    FwdSmem &S = *reinterpret_cast<FwdSmem *>(align128(dsmem));
     __shared__ double sray[kRasterThreads][3];  // fp64 pixel rays (mode-1 payloads only)
     // n_items: [0] items with entries (work[0, n0)), [1] empty items (work[max_items - n1, max_items))
     const int n_full = n_items[0];
@@ -728,8 +788,8 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
     const int4 it = items[(int)blockIdx.x < n_full ? blockIdx.x : gridDim.x - 1 - (blockIdx.x - n_full)];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if ((int)blockIdx.x >= n_full) {  // tile without entries: background only (renderer.py:118)
-        if (tid < it.z) {
-            const int p = pix_list[it.y + tid];
+        for (int q = tid; q < it.z; q += blockDim.x) {
+            const int p = pix_list[it.y + q];
             color[(int64_t)p * 3 + 0] = fc.bg[0];
             color[(int64_t)p * 3 + 1] = fc.bg[1];
             color[(int64_t)p * 3 + 2] = fc.bg[2];
@@ -752,26 +812,48 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
 #endif
     // the producer starts streaming right away; the consumers set up their pixels meanwhile
     pipe_init(S);
-    if (warp == kConsumerWarps) {
+    if (warp == NW) {
         pipe_produce<false, false>(S, order, &pay_map, nullptr, e0, e1 - e0, true, &counters[4]);
         return;
     }
-    const bool valid = tid < it.z;
-    const int p = valid ? pix_list[it.y + tid] : 0;
-    double d64[3] = {0.0, 0.0, 1.0};
-    if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
-    const float4 my_patch = warp_patch(valid, ray_mirror_bounds(fc, d64));
-    const float4 my_cone = warp_cone(fc, valid, d64);
+    int q[PX], p[PX];
+    bool valid[PX];
+    double d64[PX][3];
+    float4 bnd = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
+    bool any_valid = false;
+#pragma unroll
+    for (int x = 0; x < PX; ++x) {
+        q[x] = tid + x * NT;
+        valid[x] = q[x] < it.z;
+        p[x] = valid[x] ? pix_list[it.y + q[x]] : 0;
+        d64[x][0] = 0.0;
+        d64[x][1] = 0.0;
+        d64[x][2] = 1.0;
+        if (valid[x]) {
+            pixel_ray<kBEAP>(fc, p[x], col_sc, row_sc, dir64, d64[x]);
+            bnd = bounds_union(bnd, ray_mirror_bounds(fc, d64[x]));
+            any_valid = true;
+        }
+    }
+    const float4 my_patch = warp_patch(any_valid, bnd);
+    const float4 my_cone = warp_cone<PX>(fc, valid, d64);
 #ifdef GEER_CTA_TIMING
     if (tid == 0 && blockIdx.x < (1u << 16)) g_cta_ts[blockIdx.x] = gtimer();
 #endif
-    const Ray64 R = make_ray(d64);
-    sray[tid][0] = d64[0];
-    sray[tid][1] = d64[1];
-    sray[tid][2] = d64[2];
-    PixelState ps{0.f, 0.f, 0.f, valid ? 1.0f : 0.0f, 1.0f, 0.f, -1.0f, 0, 0, 0};
+    Ray64 R[PX];
+    const double *dray[PX];
+    PixelState ps[PX];
+#pragma unroll
+    for (int x = 0; x < PX; ++x) {
+        R[x] = make_ray(d64[x]);
+        sray[q[x]][0] = d64[x][0];
+        sray[q[x]][1] = d64[x][1];
+        sray[q[x]][2] = d64[x][2];
+        dray[x] = sray[q[x]];
+        ps[x] = PixelState{0.f, 0.f, 0.f, valid[x] ? 1.0f : 0.0f, 1.0f, 0.f, -1.0f, 0, 0, 0};
+    }
     int rechecks = 0, went = 0;
-    bool warp_live = __any_sync(0xffffffffu, valid);
+    bool warp_live = __any_sync(0xffffffffu, any_valid);
     if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
     unsigned phase = 0;
     int s = 0, base = 0;
@@ -787,15 +869,18 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
             const int cnt = stage_keep(S, s, warp, lane, n, fc.cull != 0, my_patch, my_cone, m);
             // a mode-1 (cross-product) payload anywhere in the stage selects the generic path
             if (__any_sync(0xffffffffu, lane < n && ring_at(S, s, lane).col.w < 0.0f))
-                consume_stage_generic(S, s, warp, cnt, base, R, sray[tid], fc, ps, rechecks, went);
+                consume_stage_generic<PX>(S, s, warp, cnt, base, R, dray, fc, ps, rechecks, went);
             else if (fc.cutoff)
-                consume_stage_fast<true>(S, s, warp, cnt, base, R, fc, ps, rechecks, went);
+                consume_stage_fast<true, PX, GEER_FWD_GROUP>(S, s, warp, cnt, base, R, fc, ps, rechecks, went);
             else
-                consume_stage_fast<false>(S, s, warp, cnt, base, R, fc, ps, rechecks, went);
-            warp_live = __any_sync(0xffffffffu, ps.r > 0.0f);
+                consume_stage_fast<false, PX, GEER_FWD_GROUP>(S, s, warp, cnt, base, R, fc, ps, rechecks, went);
+            bool live = false;
+#pragma unroll
+            for (int x = 0; x < PX; ++x) live |= ps[x].r > 0.0f;
+            warp_live = __any_sync(0xffffffffu, live);
             if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
         }
-        if (!warp_live) {  // all 32 pixels opaque: leave the pipeline, stop issuing
+        if (!warp_live) {  // every pixel of the warp opaque: leave the pipeline, stop issuing
             pipe_drop_out(S, s, phase);
             break;
         }
@@ -807,19 +892,23 @@ __global__ void __launch_bounds__(kPipeThreads, FWD_MIN_BLOCKS)
             phase ^= 1;
         }
     }
-    if (ps.r > 0.0f) ps.ne = e1 - e0;  // alive through the whole list
-    if (valid) {
-        const float rem = ps.r > 0.0f ? ps.r : ps.rfin;  // live to the end of the list, or stopped
-        // renderer.py:118 background with the final remaining transmittance
-        color[(int64_t)p * 3 + 0] = __fmaf_rn(rem, fc.bg[0], ps.cr);
-        color[(int64_t)p * 3 + 1] = __fmaf_rn(rem, fc.bg[1], ps.cg);
-        color[(int64_t)p * 3 + 2] = __fmaf_rn(rem, fc.bg[2], ps.cb);
-        remaining[p] = rem;
-        count[p] = ps.cnt;
-        n_eval[p] = ps.ne;
-        if (pixel_border(ps)) {
-            unsigned long long slot = atomicAdd(&counters[2], 1ull);
-            fixup_list[slot] = (int32_t)(((int64_t)blockIdx.x << 8) | tid);  // work item, thread
+#pragma unroll
+    for (int x = 0; x < PX; ++x) {
+        PixelState &px = ps[x];
+        if (px.r > 0.0f) px.ne = e1 - e0;  // alive through the whole list
+        if (valid[x]) {
+            const float rem = px.r > 0.0f ? px.r : px.rfin;  // live to the end of the list, or stopped
+            // renderer.py:118 background with the final remaining transmittance
+            color[(int64_t)p[x] * 3 + 0] = __fmaf_rn(rem, fc.bg[0], px.cr);
+            color[(int64_t)p[x] * 3 + 1] = __fmaf_rn(rem, fc.bg[1], px.cg);
+            color[(int64_t)p[x] * 3 + 2] = __fmaf_rn(rem, fc.bg[2], px.cb);
+            remaining[p[x]] = rem;
+            count[p[x]] = px.cnt;
+            n_eval[p[x]] = px.ne;
+            if (pixel_border(px)) {
+                unsigned long long slot = atomicAdd(&counters[2], 1ull);
+                fixup_list[slot] = (int32_t)(((int64_t)blockIdx.x << 8) | q[x]);  // work item, pixel of the item
+            }
         }
     }
     rechecks = __reduce_add_sync(0xffffffffu, rechecks);
@@ -854,44 +943,70 @@ __device__ void fixup_pixel(FrameConst fc, const geer_scene &sc, const int4 *__r
     int cnt = 0, ne = 0;
     bool alive = true;
     const Ray64 R = make_ray(d);
-    for (int base = e0; base < e1 && alive; base += 32) {
-        const int e = base + lane;
-        double t = 0.0;
-        uint32_t g = 0;
-        float4 cl = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (e < e1) {
-            // fp64 kappa (payload quadratic forms / cross product), fp64 exp: renderer.py:96-105 in fp64
-            g = order[e];
-            const Payload &P = payload[g];
-            cl = P.col;
-            double dd, mm;
-            norms64(P, R, d, P.col.w < 0.0f, dd, mm);
-            double kap = mm / dd;
-            if (fc.cutoff && fabs(kap - fc.lam2) <= (double)P.ext.x)
-                kap = kappa_fp64(sc.means, sc.log_scales, sc.quats, fc.origin[0], fc.origin[1], fc.origin[2], g, d[0],
-                                 d[1], d[2]);
-            const double x = (double)sc.opacity_logits[g];
-            const double sig = x >= 0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x));
-            double u = sig * exp(-0.5 * kap);
-            if (fc.cutoff && !(kap <= fc.lam2)) u = 0.0;
-            t = u < kMaxBlendT ? u : kMaxBlendT;
-        }
+    // fp64 t of entry e (renderer.py:96-105 in fp64: payload quadratic forms / cross product, the
+    // reference formulation near the cutoff, fp64 sigmoid and exp)
+    auto eval64 = [&](int e, double &t, float4 &cl) {
+        t = 0.0;
+        cl = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (e >= e1) return;
+        const uint32_t g = order[e];
+        const Payload &P = payload[g];
+        cl = P.col;
+        double dd, mm;
+        norms64(P, R, d, P.col.w < 0.0f, dd, mm);
+        double kap = mm / dd;
+        if (fc.cutoff && fabs(kap - fc.lam2) <= (double)P.ext.x)
+            kap = kappa_fp64(sc.means, sc.log_scales, sc.quats, fc.origin[0], fc.origin[1], fc.origin[2], g, d[0], d[1],
+                             d[2]);
+        const double x = (double)sc.opacity_logits[g];
+        const double sig = x >= 0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x));
+        double u = sig * exp(-0.5 * kap);
+        if (fc.cutoff && !(kap <= fc.lam2)) u = 0.0;
+        t = u < kMaxBlendT ? u : kMaxBlendT;
+    };
+    constexpr int kSub = 4;  // batches of 32 evaluated together: their loads overlap
+    for (int sbase = e0; sbase < e1 && alive; sbase += 32 * kSub) {
+        double tt[kSub];
+        float4 cc[kSub];
+#pragma unroll
+        for (int k = 0; k < kSub; ++k) eval64(sbase + 32 * k + lane, tt[k], cc[k]);
+#pragma unroll
+        for (int k = 0; k < kSub; ++k) {
+        const int base = sbase + 32 * k;
+        if (!(base < e1 && alive)) break;
+        const double t = tt[k];
+        const float4 cl = cc[k];
+        // composite the batch with a warp scan: rem before entry j = rem * prod_{i<j} (1 - t_i); the
+        // alive test (rem >= 1e-4, renderer.py:113) holds on a prefix of the batch since rem only
+        // decreases (same fp64 products as the reference's loop up to the association order)
         const int n = min(32, e1 - base);
-        for (int j = 0; j < n; ++j) {
-            const double tj = __shfl_sync(0xffffffffu, t, j);
-            const float4 col = make_float4(__shfl_sync(0xffffffffu, cl.x, j), __shfl_sync(0xffffffffu, cl.y, j),
-                                           __shfl_sync(0xffffffffu, cl.z, j), 0.f);
-            if (!(rem >= kMinRemaining)) {
-                alive = false;
-                break;
-            }
-            ++ne;
-            const double w = rem * tj;
-            cr += w * col.x;
-            cg += w * col.y;
-            cb += w * col.z;
-            rem = rem * (1.0 - tj);
-            cnt += tj > 0;
+        double P = lane < n ? 1.0 - t : 1.0;  // inclusive prefix product
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, P, o);
+            if (lane >= o) P *= y;
+        }
+        const double up1 = __shfl_up_sync(0xffffffffu, P, 1);  // (every lane takes part in the shuffle)
+        const double pex = lane == 0 ? 1.0 : up1;
+        const double rb = rem * pex;
+        const bool live = lane < n && rb >= kMinRemaining;
+        const int na = __popc(__ballot_sync(0xffffffffu, live));
+        double w = live ? rb * t : 0.0;
+        double wr = w * cl.x, wg = w * cl.y, wb = w * cl.z;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            wr += __shfl_xor_sync(0xffffffffu, wr, o);
+            wg += __shfl_xor_sync(0xffffffffu, wg, o);
+            wb += __shfl_xor_sync(0xffffffffu, wb, o);
+        }
+        cr += wr;
+        cg += wg;
+        cb += wb;
+        cnt += __popc(__ballot_sync(0xffffffffu, live && t > 0.0));
+        ne += na;
+        const double pl = __shfl_sync(0xffffffffu, P, na > 0 ? na - 1 : 0);
+        if (na > 0) rem = rem * pl;
+        if (na < n) alive = false;
         }
     }
     if (lane == 0) {
@@ -998,7 +1113,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
     double d64[3] = {0.0, 0.0, 1.0};
     if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
     const float4 my_patch = warp_patch(valid, ray_mirror_bounds(fc, d64));
-    const float4 my_cone = warp_cone(fc, valid, d64);
+    const float4 my_cone = warp_cone1(fc, valid, d64);
     const Ray64 R = make_ray(d64);
     if (valid) {
         sray[tid][0] = d64[0];
@@ -1136,8 +1251,8 @@ static void raster_smem_optin() {
     static bool done = false;
     if (done) return;
     done = true;
-    cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<false>) + 128);
-    cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<false>) + 128);
+    cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FwdSmem) + 128);
+    cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FwdSmem) + 128);
     cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<true>) + 128);
     cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<true>) + 128);
 }
@@ -1150,13 +1265,13 @@ void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, c
     if (max_items <= 0) return;
     raster_smem_optin();
     if (fc.model == GEER_BEAP) {
-        k_forward<true><<<max_items, kPipeThreads, sizeof(PipeSmem<false>) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
+        k_forward<true><<<max_items, kFwdThreads, sizeof(FwdSmem) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
                                                             ranges, order, pay_map, flags, color, remaining, count,
                                                             n_eval, counters, fixup_list);
         k_fixup<true><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                counters, fixup_list, color, remaining, count, n_eval);
     } else {
-        k_forward<false><<<max_items, kPipeThreads, sizeof(PipeSmem<false>) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
+        k_forward<false><<<max_items, kFwdThreads, sizeof(FwdSmem) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
                                                              ranges, order, pay_map, flags, color, remaining, count,
                                                              n_eval, counters, fixup_list);
         k_fixup<false><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
