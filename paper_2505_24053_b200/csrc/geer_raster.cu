@@ -1072,13 +1072,20 @@ __device__ __forceinline__ float warp_transpose_reduce16(float v[16], int lane) 
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+#ifndef GEER_BWD_SMEM_REDUCE
+#define GEER_BWD_SMEM_REDUCE 0
+#endif
+
 // Reverse-order backward (renderer.py:259-310).  The producer streams the
 // tile's first max_n entries back to front; each lane walks its pixel's alive
 // entries (index < n_eval) from the last to the first, recovering
 // T_i = T_{i+1} / (1 - t_i) from the forward's final remaining, and the warp
 // adds its 16 per-entry partials to the Gaussian's accumulators.
+#ifndef BWD_MIN_BLOCKS
+#define BWD_MIN_BLOCKS 3
+#endif
 template <bool kBEAP>
-__global__ void __launch_bounds__(kPipeThreads, 2)
+__global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
     k_backward(FrameConst fc, geer_scene sc, const int4 *__restrict__ items, const int32_t *__restrict__ n_items,
                const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
                const double2 *__restrict__ row_sc, const double *__restrict__ dir64,
@@ -1090,6 +1097,9 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
     extern __shared__ __align__(16) unsigned char dsmem[];
     PipeSmem<true> &S = *reinterpret_cast<PipeSmem<true> *>(align128(dsmem));
     __shared__ double sray[kRasterThreads][3];
+#if GEER_BWD_SMEM_REDUCE
+    __shared__ float sred[kConsumerWarps][32 * 17];  // per-warp reduction scratch
+#endif
     __shared__ int smax;
     if ((int)blockIdx.x >= n_items[0]) return;  // tiles without entries have no gradient
     const int4 it = items[blockIdx.x];
@@ -1197,9 +1207,25 @@ __global__ void __launch_bounds__(kPipeThreads, 2)
                         v[6] = dd2 * dx; v[7] = dd2 * dy; v[8] = dd2 * dz;
                     }
                 }
+#if GEER_BWD_SMEM_REDUCE
+                // warp sum of the 16 partials through shared memory (stride 17: conflict-free both
+                // ways): lane L sums partial L % 16 over 16 pixels, the two halves meet by one shuffle
+                float *red = sred[warp];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) red[lane * 17 + k] = v[k];
+                __syncwarp();
+                float tot = 0.f;
+                const int h16 = (lane >> 4) * 16, kk = lane & 15;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) tot += red[(h16 + i) * 17 + kk];
+                tot += __shfl_xor_sync(0xffffffffu, tot, 16);
+                __syncwarp();
+                if (lane < 16 && tot != 0.0f) atomicAdd(accum + (int64_t)S.gid[s][jj] * 16 + lane, tot);
+#else
                 const float tot = warp_transpose_reduce16(v, lane);
                 if ((lane & 1) == 0 && tot != 0.0f)
                     atomicAdd(accum + (int64_t)S.gid[s][jj] * 16 + (lane >> 1), tot);
+#endif
             }
         }
         __syncwarp();
