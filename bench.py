@@ -141,9 +141,11 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and not dist.is_initialized():
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # GEER_DIST_BACKEND=gloo runs several ranks on one GPU (host-side test of the multi-rank path)
+        backend = os.environ.get("GEER_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         dist.init_process_group(backend=backend)
     if torch.cuda.is_available():
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
     return rank, world, local
 
@@ -188,6 +190,7 @@ def run_reference(args):
 
     scene = synth.config_scene("C2")
     cam = synth.config_camera("C2")
+    O.set_num_threads(os.cpu_count() or 1)  # every host core (torchrun sets OMP_NUM_THREADS=1)
     cores = O.num_threads()
     for _ in range(args.warmup):
         cpu_frame_seconds(scene, cam)
@@ -425,6 +428,7 @@ def run_ours(args):
         try:
             from oracle import oracle as O
 
+            O.set_num_threads(os.cpu_count() or 1)
             cpu_s = cpu_frame_seconds(scene, base_cam)
             cpu = {"value": 1.0 / cpu_s, "unit": "FPS", "cores": O.num_threads(), "kind": "port",
                    "sample": "one full C2 frame (association + raster) of the fp64 C port oracle/geer_oracle.c",

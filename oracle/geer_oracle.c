@@ -941,6 +941,15 @@ int geo_backward(int64_t n, int n_bands, const double *means, const double *log_
     return 0;
 }
 
+/* Use n OpenMP threads from now on (torchrun exports OMP_NUM_THREADS=1; the CPU baseline wants all). */
+void geo_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int geo_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

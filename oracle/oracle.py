@@ -296,3 +296,10 @@ def render_backward(scene, camera, dl_dimage, config=None, threads=None, graph: 
 
 def num_threads() -> int:
     return int(_load().geo_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the oracle from now on (torchrun exports OMP_NUM_THREADS=1)."""
+    lib = _load()
+    lib.geo_set_num_threads.argtypes = [ctypes.c_int]
+    lib.geo_set_num_threads(int(n))
