@@ -147,7 +147,14 @@ class FlatScene:
 
 
 class MultiViewTrainer:
-    def __init__(self, init_scene, cameras, targets, rank=0, world=1, device=0, config=None, lrs=None):
+    """C4 step: every local view rendered, lossed and back-propagated, ONE allreduce, one Adam.
+
+    ``inflight`` views run concurrently on as many contexts/streams (each with its own gradient
+    buffer; the buffers are summed before the allreduce), so one view's association overlaps
+    another's raster.
+    """
+
+    def __init__(self, init_scene, cameras, targets, rank=0, world=1, device=0, config=None, lrs=None, inflight=2):
         self.rank, self.world = rank, world
         self.device = torch.device(f"cuda:{device}")
         self.config = config or RenderConfig()
@@ -155,7 +162,9 @@ class MultiViewTrainer:
         nb = int(np.asarray(init_scene.sh).shape[1])
         self.params = FlatScene(n, nb, self.device)
         self.params.load(init_scene)
+        self.inflight = max(1, int(inflight))
         self.grads = FlatScene(n, nb, self.device)
+        self.grads_extra = [FlatScene(n, nb, self.device) for _ in range(self.inflight - 1)]
         self.m = torch.zeros_like(self.params.buf)
         self.v = torch.zeros_like(self.params.buf)
         extent = float(init_scene.extent()) if hasattr(init_scene, "extent") else 1.0
@@ -164,17 +173,20 @@ class MultiViewTrainer:
         self.lr = self.params.lr_vector(lrs)
         self.cameras = cameras
         self.targets = targets  # list of (H,W,3) fp32 CUDA tensors, one per local view
-        self.renderer = DeviceRenderer(device)
+        self.renderers = [DeviceRenderer(device) for _ in range(self.inflight)]
+        self.renderer = self.renderers[0]
+        self.streams = [torch.cuda.current_stream(self.device)] + [torch.cuda.Stream(self.device)
+                                                                    for _ in range(self.inflight - 1)]
         self.t = 0
         self.grad_numel = self.params.numel
         self.last_loss = None
         self._bufs = {}
         self.ssim_weight = SSIM_WEIGHT
-        self.loss_ws = LossWorkspace()
+        self.loss_ws = [LossWorkspace() for _ in range(self.inflight)]
         self.lib = _lib.load()
 
     @classmethod
-    def for_config4(cls, target_scene, n_views=64, rank=0, world=1, device=0, width=1920, height=1080):
+    def for_config4(cls, target_scene, n_views=64, rank=0, world=1, device=0, width=1920, height=1080, inflight=2):
         """C4: target = C2 scene, init = perturbed(C2, default_rng(1)), ring of BEAP 180x101.25 views."""
         cams_all = synth.ring_cameras(n_views, 2.0, width, height, fov_deg=180.0, fov_y_deg=180.0 * height / width)
         mine = [cams_all[i] for i in shard(n_views, rank, world)]
@@ -187,12 +199,12 @@ class MultiViewTrainer:
             color, _, _ = r.forward(tscene, cam, cfg)
             targets.append(color.clone())
         del r, tscene
-        return cls(init, mine, targets, rank, world, device, cfg)
+        return cls(init, mine, targets, rank, world, device, cfg, inflight=inflight)
 
-    def _out(self, cam):
-        key = (cam.height, cam.width)
+    def _out(self, cam, j=0):
+        key = (cam.height, cam.width, j)
         if key not in self._bufs:
-            h, w = key
+            h, w, _ = key
             self._bufs[key] = (torch.empty((h, w, 3), dtype=torch.float32, device=self.device),
                                torch.empty((h, w), dtype=torch.float32, device=self.device),
                                torch.empty((h, w), dtype=torch.int32, device=self.device),
@@ -200,22 +212,43 @@ class MultiViewTrainer:
         return self._bufs[key]
 
     def step(self, compute_loss=False):
-        stream = torch.cuda.current_stream(self.device).cuda_stream
-        self.grads.buf.zero_()
-        loss = 0.0
-        for cam, target in zip(self.cameras, self.targets):
-            color, rem, cnt, dl = self._out(cam)
-            self.renderer.forward(self.params.scene, cam, self.config, out=(color, rem, cnt))
-            # trainer.py:269 loss(): (1 - w) L1 + w (1 - SSIM) and its image gradient
-            out, _ = loss_device(color, target, None, self.ssim_weight, grad=dl, workspace=self.loss_ws)
-            self.renderer.backward(dl, grads=self.grads.scene, accumulate=True, opacity_logit=True)
-            if compute_loss:
-                loss += float(out[0].item())
+        loss = self.accumulate(compute_loss)
         allreduce_grads(self.grads.buf, self.world)
         self.t += 1
+        stream = self.streams[0].cuda_stream
         _lib.check(self.lib.geer_adam(self.params.buf.data_ptr(), self.grads.buf.data_ptr(), self.m.data_ptr(),
                                       self.v.data_ptr(), self.lr.data_ptr(), self.params.numel, ctypes.c_float(0.9),
                                       ctypes.c_float(0.999), ctypes.c_float(1e-15), self.t, stream))
         if compute_loss:
             self.last_loss = loss
         return loss
+
+    def accumulate(self, compute_loss=False):
+        """Sum over the local views of the stored-space gradients into ``self.grads`` (no collective)."""
+        main = self.streams[0]
+        gbufs = [self.grads] + self.grads_extra
+        start = torch.cuda.Event()
+        start.record(main)
+        for j, s in enumerate(self.streams):
+            if j:
+                s.wait_event(start)  # the previous step's Adam update is done
+            with torch.cuda.stream(s):
+                gbufs[j].buf.zero_()
+        outs = []
+        for v, (cam, target) in enumerate(zip(self.cameras, self.targets)):
+            j = v % self.inflight
+            with torch.cuda.stream(self.streams[j]):
+                color, rem, cnt, dl = self._out(cam, j)
+                r = self.renderers[j]
+                r.forward(self.params.scene, cam, self.config, out=(color, rem, cnt))
+                # trainer.py:269 loss(): (1 - w) L1 + w (1 - SSIM) and its image gradient
+                out, _ = loss_device(color, target, None, self.ssim_weight, grad=dl, workspace=self.loss_ws[j])
+                r.backward(dl, grads=gbufs[j].scene, accumulate=True, opacity_logit=True)
+                if compute_loss:
+                    outs.append(out[0].clone())
+        for j, s in enumerate(self.streams[1:], start=1):
+            done = torch.cuda.Event()
+            done.record(s)
+            main.wait_event(done)
+            self.grads.buf.add_(gbufs[j].buf)
+        return float(sum(float(o) for o in outs)) if compute_loss else 0.0

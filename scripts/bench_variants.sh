@@ -1,7 +1,7 @@
 cd $GRAFT_REPO_ROOT
 for defs in "$@"; do
   GEER_NVCC_DEFS="$defs" python -m paper_2505_24053_b200.build --force > /dev/null 2>&1 || { echo "build failed: $defs"; continue; }
-  timeout 600 python bench.py --steps 50 --warmup 5 --no-e2e --no-train --no-cpu 2>/dev/null | python -c "
+  timeout 600 python bench.py --steps 50 --warmup 5 --no-e2e --no-train --no-cpu --no-c5 $BENCH_ARGS 2>/dev/null | python -c "
 import json,sys
 for l in sys.stdin:
     if l.startswith('{'):

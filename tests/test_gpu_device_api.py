@@ -123,3 +123,19 @@ def test_camera_setup_cache_follows_the_camera():
     for name, cam in (("a", cam_a), ("b", cam_b), ("a", cam_a), ("a", cam_a), ("b", cam_b)):
         col = r.forward(ds, cam, cfg)[0]
         assert torch.equal(col, fresh[name]), name
+
+
+def test_multiview_inflight_matches_serial():
+    """C4 glue: views on two contexts/streams sum to the same gradients as one context."""
+    from paper_2505_24053_b200 import train
+
+    scene = synth.config_scene("C2", n=20_000)
+    tr1 = train.MultiViewTrainer.for_config4(scene, n_views=4, width=192, height=108, inflight=1)
+    tr2 = train.MultiViewTrainer(synth.to_f32_values(synth.perturbed(scene, np.random.default_rng(1))),
+                                 tr1.cameras, tr1.targets, inflight=2)
+    tr1.accumulate()
+    tr2.accumulate()
+    torch.cuda.synchronize()
+    g1, g2 = tr1.grads.buf, tr2.grads.buf
+    assert torch.isfinite(g1).all() and float(g1.abs().max()) > 0
+    torch.testing.assert_close(g2, g1, rtol=1e-3, atol=1e-4 * float(g1.abs().max()))
