@@ -211,13 +211,20 @@ class Context:
         return s.as_dict()
 
 
-_default: dict[int, Context] = {}
+_default = threading.local()
 
 
 def default_context(device: int = 0) -> Context:
-    """Per-device context used by the reference-compatible host API."""
-    ctx = _default.get(device)
+    """Per-thread, per-device context of the reference-compatible host API.
+
+    A context is not thread-safe (it owns one stream and the state of its last frame), so every host
+    thread gets its own: several threads can render concurrently (ctypes releases the GIL).
+    """
+    ctxs = getattr(_default, "ctxs", None)
+    if ctxs is None:
+        ctxs = _default.ctxs = {}
+    ctx = ctxs.get(device)
     if ctx is None:
         ctx = Context(device)
-        _default[device] = ctx
+        ctxs[device] = ctx
     return ctx
