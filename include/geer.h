@@ -177,6 +177,12 @@ size_t geer_loss_workspace_bytes(int height, int width);
 int geer_loss(const float *color, const float *target, const uint8_t *mask, int height, int width, float ssim_weight,
               void *workspace, double *out, float *dl_dimage, void *stream);
 
+/* Ground-truth resampling onto the equiangular grid (camera.py:302-339): source (H_s,W_s,3) f32 device
+ * image of a pinhole / kb camera -> color (H,W,3) f32 and mask (H,W) u8 on the grid of a beap target
+ * camera sharing its extrinsics (checked by the caller). */
+int geer_resample_to_beap(const float *source, int source_height, int source_width, const geer_camera *source_camera,
+                          const geer_camera *target_camera, float *color, uint8_t *mask, void *stream);
+
 /* ---- diagnostics ------------------------------------------------------------- */
 /* Measured FP32 FMA throughput of the device (scalar FFMA and packed FFMA2 chains), TFLOP/s: the
  * roofline denominator of the FP32-bound raster kernels (bench.py). */

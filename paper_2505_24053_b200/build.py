@@ -34,6 +34,7 @@ UNITS = {
     "geer_api.cu": [],
     "geer_train.cu": [],
     "geer_loss.cu": [],
+    "geer_camera.cu": ["-fmad=false"],
 }
 
 
