@@ -183,6 +183,12 @@ int geer_loss(const float *color, const float *target, const uint8_t *mask, int 
 int geer_resample_to_beap(const float *source, int source_height, int source_width, const geer_camera *source_camera,
                           const geer_camera *target_camera, float *color, uint8_t *mask, void *stream);
 
+/* 3DGS-compatible PLY vertex block (n records of n_props float32, already on the device) into the fp32
+ * SoA of geer_scene, laid out contiguously: means (n,3), log_scales (n,3), quats (n,4), opacity (n),
+ * sh (n, (n_vals - 11) / 3, 3); cols[k] = record column of SoA value k (ply.py:94-137). */
+int geer_ply_to_soa(const float *block, int64_t n, int n_props, const int32_t *cols, int n_vals, float *soa,
+                    void *stream);
+
 /* ---- diagnostics ------------------------------------------------------------- */
 /* Measured FP32 FMA throughput of the device (scalar FFMA and packed FFMA2 chains), TFLOP/s: the
  * roofline denominator of the FP32-bound raster kernels (bench.py). */

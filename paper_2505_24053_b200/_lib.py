@@ -31,7 +31,7 @@ EXPORTED = (
     "geer_abi_version", "geer_last_error", "geer_create", "geer_destroy", "geer_set_timing", "geer_forward",
     "geer_backward", "geer_frame_stats", "geer_graph_info", "geer_graph_export", "geer_build_graph_host",
     "geer_render_host", "geer_render_backward_host", "geer_l1_grad", "geer_adam", "geer_measure_fp32_peak",
-    "geer_loss_workspace_bytes", "geer_loss", "geer_resample_to_beap",
+    "geer_loss_workspace_bytes", "geer_loss", "geer_resample_to_beap", "geer_ply_to_soa",
 )
 
 
@@ -126,6 +126,7 @@ def load():
             "geer_loss_workspace_bytes": ([I, I], ctypes.c_size_t),
             "geer_loss": ([P, P, P, I, I, F, P, P, P, P], I),
             "geer_resample_to_beap": ([P, I, I, P, P, P, P, P], I),
+            "geer_ply_to_soa": ([P, I64, I, P, I, P, P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

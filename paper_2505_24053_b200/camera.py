@@ -50,3 +50,54 @@ def resample_to_beap(source_image, source_camera, target_camera, device: int = 0
                           device=torch.device(f"cuda:{device}"))
     color, mask = resample_to_beap_device(src, source_camera, target_camera)
     return BEAPImage(color=color.double().cpu().numpy(), mask=mask.cpu().numpy())
+
+
+# ---------------------------------------------------------------------------------- camera JSON
+# camera.py:371-422: the same keys (w, h, model, R, t, fovx_deg/fovy_deg, fx/fy/cx/cy, k).
+
+
+def camera_from_dict(cfg: dict) -> Camera:
+    rot = np.asarray(cfg.get("R", np.eye(3).ravel()), dtype=np.float64).reshape(3, 3)
+    return Camera(width=int(cfg["w"]), height=int(cfg["h"]), model=cfg.get("model", "beap"), rotation=rot,
+                  translation=np.asarray(cfg.get("t", (0, 0, 0)), dtype=np.float64),
+                  fov_x=np.deg2rad(cfg["fovx_deg"]) if "fovx_deg" in cfg else None,
+                  fov_y=np.deg2rad(cfg["fovy_deg"]) if "fovy_deg" in cfg else None,
+                  fx=cfg.get("fx"), fy=cfg.get("fy"), cx=cfg.get("cx"), cy=cfg.get("cy"),
+                  k=np.asarray(cfg.get("k", (0, 0, 0, 0)), dtype=np.float64))
+
+
+def camera_to_dict(camera) -> dict:
+    cfg = {"model": camera.model, "w": camera.width, "h": camera.height,
+           "R": [float(v) for v in np.asarray(camera.rotation).ravel()],
+           "t": [float(v) for v in np.asarray(camera.translation)]}
+    if camera.fov_x is not None:
+        cfg["fovx_deg"] = float(np.rad2deg(camera.fov_x))
+    if camera.fov_y is not None:
+        cfg["fovy_deg"] = float(np.rad2deg(camera.fov_y))
+    for name in ("fx", "fy", "cx", "cy"):
+        val = getattr(camera, name)
+        if val is not None:
+            cfg[name] = float(val)
+    k = np.asarray(getattr(camera, "k", np.zeros(4)), dtype=np.float64)
+    if np.any(k != 0):
+        cfg["k"] = [float(v) for v in k]
+    return cfg
+
+
+def load_cameras(path) -> list:
+    """One camera or a list of cameras from a JSON file."""
+    import json
+
+    with open(path) as f:
+        data = json.load(f)
+    if isinstance(data, dict):
+        data = [data]
+    return [camera_from_dict(c) for c in data]
+
+
+def save_cameras(cameras, path):
+    import json
+
+    data = [camera_to_dict(c) for c in cameras]
+    with open(path, "w") as f:
+        json.dump(data[0] if len(data) == 1 else data, f, indent=2)

@@ -97,3 +97,45 @@ extern "C" int geer_resample_to_beap(const float *source, int source_height, int
     k_resample<<<blocks, 256, 0, (cudaStream_t)stream>>>(P, source, color, mask);
     return cudaGetLastError() == cudaSuccess ? GEER_OK : GEER_ERR_CUDA;
 }
+
+// ---------------------------------------------------------------- PLY vertex block -> device SoA
+// (ply.py:94-137 without the float64 detour): record v holds n_props float32; column cols[k] of it
+// goes to SoA value k (means 3, log_scales 3, quats 4, opacity 1, sh band-major).  One thread per value.
+namespace {
+struct ColMap {
+    int c[64];
+};
+__global__ void k_ply_to_soa(const float *__restrict__ block, int64_t n, int n_props, ColMap cm, int n_vals,
+                             float *__restrict__ soa) {
+    const int64_t total = n * n_vals;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / n_vals;
+        const int k = (int)(i - v * n_vals);
+        const float x = block[v * n_props + cm.c[k]];
+        // SoA groups: [0,3) means, [3,6) log_scales, [6,10) quats, [10,11) opacity, [11, n_vals) sh
+        int64_t dst;
+        if (k < 3) dst = v * 3 + k;
+        else if (k < 6) dst = 3 * n + v * 3 + (k - 3);
+        else if (k < 10) dst = 6 * n + v * 4 + (k - 6);
+        else if (k < 11) dst = 10 * n + v;
+        else dst = 11 * n + v * (n_vals - 11) + (k - 11);
+        soa[dst] = x;
+    }
+}
+}  // namespace
+
+extern "C" int geer_ply_to_soa(const float *block, int64_t n, int n_props, const int32_t *cols, int n_vals, float *soa,
+                               void *stream) {
+    if (!block || !cols || !soa || n < 0 || n_vals < 11 || n_vals > 64 || n_props <= 0) return GEER_ERR_INVALID;
+    ColMap cm;
+    for (int k = 0; k < n_vals; ++k) {
+        if (cols[k] < 0 || cols[k] >= n_props) return GEER_ERR_INVALID;
+        cm.c[k] = cols[k];
+    }
+    if (n == 0) return GEER_OK;
+    const int64_t total = n * n_vals;
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    k_ply_to_soa<<<blocks, 256, 0, (cudaStream_t)stream>>>(block, n, n_props, cm, n_vals, soa);
+    return cudaGetLastError() == cudaSuccess ? GEER_OK : GEER_ERR_CUDA;
+}
