@@ -72,6 +72,10 @@ typedef struct geer_config {
 
 /* Disable the per-warp PBF culling of the raster (results are identical; for tests). */
 #define GEER_CFG_NO_CULL 1
+/* Exhaustive forward (an oracle of the association at scale, oracle.py:172-228 exhaustive_render):
+ * every tile composites ALL kept Gaussians in global (depth, gid) order instead of its association
+ * list.  Forward only (a following geer_backward fails with GEER_ERR_STATE). */
+#define GEER_CFG_EXHAUSTIVE 2
 
 /* Device scene: fp32 SoA in the reference's stored spaces (scene.py:35-51). */
 typedef struct geer_scene {

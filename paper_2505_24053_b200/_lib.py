@@ -169,6 +169,7 @@ def camera_struct(camera) -> GeerCamera:
 
 
 GEER_CFG_NO_CULL = 1
+GEER_CFG_EXHAUSTIVE = 2  # every tile composites all kept Gaussians (association oracle, forward only)
 
 
 def config_struct(config, flags: int = 0) -> GeerConfig:

@@ -175,6 +175,7 @@ int make_frame_const(const geer_camera *cam, const geer_config *cfg, int n_bands
     fc->cutoff = cfg->support_cutoff ? 1 : 0;
     // per-warp PBF culling is exact only under the support cutoff (renderer.py:103-105)
     fc->cull = (cfg->support_cutoff && !(cfg->flags & GEER_CFG_NO_CULL)) ? 1 : 0;
+    fc->exhaustive = (cfg->flags & GEER_CFG_EXHAUSTIVE) ? 1 : 0;
     for (int i = 0; i < 9; ++i) fc->R[i] = cam->rotation[i];
     for (int i = 0; i < 3; ++i) fc->t[i] = cam->translation[i];
     // camera.py:71-74: o = -R^T t
@@ -331,6 +332,28 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     if (err == GEER_ERR_NOT_PD) return fail(GEER_ERR_NOT_PD, "view covariance must be positive definite");
     if (err == GEER_ERR_NOT_SYMMETRIC) return fail(GEER_ERR_NOT_SYMMETRIC, "view covariance must be symmetric");
     if (err) return fail(GEER_ERR_INVALID, "preprocess error %d", err);
+    if (fc.exhaustive) {  // every tile composites all kept Gaussians: no emit, no tile sort
+        int32_t *r2 = ENSURE(int32_t, c->tile_ranges, fc.n_tiles + 1);
+        launch_exhaustive_ranges((const uint8_t *)c->flags.p, n, r2, st);
+        int32_t *nwork = ENSURE(int32_t, c->n_work, 2);
+        GEER_CUDA(cudaMemcpyAsync(nwork, c->n_items.p, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        GEER_CUDA(cudaMemsetAsync(nwork + 1, 0, sizeof(int32_t), st));
+        if (c->timing) {
+            GEER_CUDA(cudaEventRecord(c->ev[2], st));
+            GEER_CUDA(cudaEventRecord(c->ev[3], st));
+        }
+        c->n_entries = 0;
+        if (color) {
+            int32_t *ne = ENSURE(int32_t, c->n_eval, npx);
+            int32_t *fix = ENSURE(int32_t, c->fixup, npx);
+            launch_forward(fc, sc, c->max_items, (const int4 *)c->items.p, nwork, (const int32_t *)c->pix_list.p,
+                           (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p, (const double *)c->dir64.p,
+                           r2, (const uint32_t *)gsorted, payload, c->pay_map, flags, color, remaining, count, ne,
+                           c->d_counters, fix, st);
+        }
+        GEER_CUDA(cudaGetLastError());
+        return GEER_OK;  // forward only: have_frame / have_raster stay false
+    }
     total = c->h_hdr[0];
     if (total >= ((int64_t)1 << 31) - 1)
         return fail(GEER_ERR_NOMEM, "render graph has %lld entries (limit 2^31)", (long long)total);

@@ -29,6 +29,7 @@ struct FrameConst {
     int n_x, n_y, n_tiles, n_bands;
     int cutoff;
     int cull;  // per-warp PBF culling of raster entries (support cutoff on and not disabled)
+    int exhaustive;  // GEER_CFG_EXHAUSTIVE: every tile's list = all kept Gaussians in depth order
     double R[9], t[3], origin[3];
     double fov_x, fov_y, fx, fy, cx, cy, k[4];
     double lam, lam2;

@@ -623,7 +623,8 @@ __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, con
     cr.box = bx;  // (the visual-cone part of the record is written by the payload half)
     // association.py:335-340 key bits (depth > 0): f32 bits | 0x80000000; non-emitting last
     const uint32_t kb = __float_as_uint((float)depth) | 0x80000000u;
-    depth_key[g] = n_ent > 0 ? kb : 0xFFFFFFFFu;
+    // (exhaustive mode: every kept Gaussian takes part, whatever its tile set)
+    depth_key[g] = (fc.exhaustive ? (fl & 1) != 0 : n_ent > 0) ? kb : 0xFFFFFFFFu;
     return fl;
 }
 

@@ -799,7 +799,8 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
         }
         return;
     }
-    const int e0 = ranges[it.x], e1 = ranges[it.x + 1];
+    const int tr = fc.exhaustive ? 0 : it.x;  // exhaustive mode: one shared list [0, n_kept)
+    const int e0 = ranges[tr], e1 = ranges[tr + 1];
 #ifdef GEER_CTA_TIMING
     if (tid == 0 && blockIdx.x < (1u << 16)) {
         unsigned smid;
@@ -938,7 +939,8 @@ __device__ void fixup_pixel(FrameConst fc, const geer_scene &sc, const int4 *__r
     const int p = pix_list[it.y + (code & 255)];
     double d[3];
     pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d);
-    const int e0 = ranges[it.x], e1 = ranges[it.x + 1];
+    const int tr = fc.exhaustive ? 0 : it.x;  // exhaustive mode: one shared list [0, n_kept)
+    const int e0 = ranges[tr], e1 = ranges[tr + 1];
     double cr = 0, cg = 0, cb = 0, rem = 1.0;
     int cnt = 0, ne = 0;
     bool alive = true;
@@ -1238,6 +1240,19 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
     }
 }
 
+
+// Exhaustive mode: ranges2 = {0, number of kept Gaussians} (they lead the depth order).
+__global__ void k_exhaustive_ranges(const uint8_t *__restrict__ flags, int64_t n, int32_t *__restrict__ ranges2) {
+    int c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        c += flags[i] & 1;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ranges2[1], c);
+}
+void launch_exhaustive_ranges(const uint8_t *flags, int64_t n, int32_t *ranges2, cudaStream_t st) {
+    cudaMemsetAsync(ranges2, 0, 2 * sizeof(int32_t), st);
+    if (n > 0) k_exhaustive_ranges<<<(int)lmin((n + 255) / 256, 148 * 8), 256, 0, st>>>(flags, n, ranges2);
+}
 
 __global__ void k_sum_i32(const int32_t *v, int64_t n, unsigned long long *out) {
     unsigned long long s = 0;
