@@ -85,6 +85,7 @@ struct geer_ctx {
     geer_scene scene{};
     bool have_frame = false;
     bool have_raster = false;
+    bool have_stats = false;  // a raster ran (also exhaustive forwards, which have no backward)
     bool keys16 = false;  // tile keys stored as uint16
     int64_t n_entries = 0;
     int max_items = 0;
@@ -272,6 +273,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     const int64_t npx = (int64_t)fc.width * fc.height;
     c->have_frame = false;
     c->have_raster = false;
+    c->have_stats = false;
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
     GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 6 * sizeof(unsigned long long), st));
     GEER_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
@@ -350,6 +352,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
                            (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p, (const double *)c->dir64.p,
                            r2, (const uint32_t *)gsorted, payload, c->pay_map, flags, color, remaining, count, ne,
                            c->d_counters, fix, st);
+            c->have_stats = true;
         }
         GEER_CUDA(cudaGetLastError());
         return GEER_OK;  // forward only: have_frame / have_raster stay false
@@ -404,7 +407,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
                        (const double *)c->dir64.p, ranges, order, payload, c->pay_map, flags, color, remaining, count, ne,
                        c->d_counters, fix, st);
         c->fwd_remaining = remaining;
-        c->have_raster = true;
+        c->have_raster = c->have_stats = true;
     }
     if (c->timing) {
         GEER_CUDA(cudaEventRecord(c->ev[4], st));
@@ -582,6 +585,7 @@ int geer_forward(geer_ctx *c, const geer_scene *scene, const geer_camera *camera
         launch_fill_background(c->fc, color, remaining, count, ne, st);
         c->have_frame = false;
         c->have_raster = false;
+        c->have_stats = false;
         c->n_entries = 0;
         GEER_CUDA(cudaGetLastError());
         return GEER_OK;
@@ -606,7 +610,7 @@ int geer_frame_stats(geer_ctx *c, geer_stats *out) {
     out->n_gaussians = c->scene.n;
     out->n_entries = c->n_entries;
     out->n_tiles = c->fc.n_tiles;
-    if (c->have_raster) {
+    if (c->have_stats) {
         cudaStream_t st = c->own_stream;
         GEER_CUDA(cudaDeviceSynchronize());
         GEER_CUDA(cudaMemsetAsync(c->d_counters + 1, 0, sizeof(unsigned long long), st));
@@ -763,7 +767,7 @@ static int host_forward(geer_ctx *c, const geer_host_scene *scene, const geer_ca
         int32_t *ne = ensure<int32_t>(c->n_eval, (size_t)npx, &rc);
         if (rc) return rc;
         launch_fill_background(c->fc, col, rem, cnt, ne, st);
-        c->have_frame = c->have_raster = false;
+        c->have_frame = c->have_raster = c->have_stats = false;
         c->n_entries = 0;
         GEER_CUDA(cudaGetLastError());
         return GEER_OK;
