@@ -157,6 +157,17 @@ int geer_graph_export(geer_ctx *ctx, int64_t *order, int64_t *entry_tile, int64_
                       double *depth, uint8_t *keep, uint8_t *clamped, int64_t *pixel_tile, double *medges_x,
                       double *medges_y);
 
+/* ---- GPU oracle of the association (validation only) --------- */
+/* oracle.association_bruteforce (oracle.py:235-281) on the GPU for the context's last graph (after
+ * geer_forward / geer_build_graph_host): side x side rays per tile (side = max(8, ceil(sqrt(rays_per_tile))),
+ * at most 16), Gaussian g in tile t iff min kappa <= lam^2 over the rays.  out[0] = brute-force
+ * (tile, Gaussian) pairs, out[1] = those missing from the tile lists (0 for a sound association),
+ * out[2] = kept Gaussians, out[3] = graph entries.  missing (host, may be NULL): the first
+ * max_missing missing pairs as (tile, gid).  hit_bits (device, may be NULL): the brute-force sets
+ * as an (n_tiles, ceil(n/32)) u32 bitmap, bit g%32 of word g/32.  Synchronous. */
+int geer_association_check(geer_ctx *ctx, int32_t rays_per_tile, int64_t *out, int32_t *missing,
+                           int32_t max_missing, uint32_t *hit_bits);
+
 /* ---- host level (drop-in replacements of the reference's Python calls) -------- */
 int geer_build_graph_host(geer_ctx *ctx, const geer_host_scene *scene, const geer_camera *camera, double lam,
                           int32_t tile_px);

@@ -303,3 +303,50 @@ def set_num_threads(n: int) -> None:
     lib = _load()
     lib.geo_set_num_threads.argtypes = [ctypes.c_int]
     lib.geo_set_num_threads(int(n))
+
+
+def _rotations(quats: np.ndarray) -> np.ndarray:
+    """scene.py:17-32: unit quaternion (r, i, j, k) -> rotation matrix."""
+    q = quats / np.linalg.norm(quats, axis=1, keepdims=True)
+    r, i, j, k = q[:, 0], q[:, 1], q[:, 2], q[:, 3]
+    return np.stack([1 - 2 * (j * j + k * k), 2 * (i * j - r * k), 2 * (i * k + r * j),
+                     2 * (i * j + r * k), 1 - 2 * (i * i + k * k), 2 * (j * k - r * i),
+                     2 * (i * k - r * j), 2 * (j * k + r * i), 1 - 2 * (i * i + j * j)], axis=1).reshape(-1, 3, 3)
+
+
+def association_bruteforce(scene, camera, lam: float = 3.0, rays_per_tile: int = 64, tile_px: int = 16,
+                           graph: OracleGraph | None = None) -> np.ndarray:
+    """oracle.py:235-281 ``association_bruteforce`` as an (n_tiles, ceil(n/32)) uint32 bitmap.
+
+    Tile t holds kept Gaussian g iff min kappa over side x side rays at the centres of a regular
+    bipolar-angle grid between the tile's mirror edges is <= lam^2 (side = max(8, ceil(sqrt(rays)))).
+    The keep mask and the mirror edges come from this oracle's own build_render_graph.
+    """
+    graph = graph or build_render_graph(scene, camera, lam, tile_px)
+    grid = graph.grid
+    means, log_scales, quats, _, _ = _scene_arrays(scene)
+    n = len(means)
+    words = (n + 31) // 32
+    bits = np.zeros((grid.n_tiles, words), np.uint32)
+    kept = np.nonzero(graph.keep)[0]
+    if len(kept) == 0:
+        return bits
+    whit = _rotations(quats[kept]).transpose(0, 2, 1) / np.exp(log_scales[kept])[:, :, None]  # scene.py:72-75
+    rot = np.asarray(camera.rotation, np.float64)
+    origin = -rot.T @ np.asarray(camera.translation, np.float64)  # camera.py:72-74
+    o_u = np.einsum("nij,nj->ni", whit, origin[None, :] - means[kept])
+    side = max(8, int(np.ceil(np.sqrt(rays_per_tile))))
+    frac = (np.arange(side) + 0.5) / side
+    for tile in range(grid.n_tiles):
+        iy, ix = divmod(tile, grid.n_x)
+        t0, t1 = 2.0 * np.arctan(grid.mirror_edges_x[ix]), 2.0 * np.arctan(grid.mirror_edges_x[ix + 1])
+        p0, p1 = 2.0 * np.arctan(grid.mirror_edges_y[iy]), 2.0 * np.arctan(grid.mirror_edges_y[iy + 1])
+        tt, pp = np.meshgrid(t0 + (t1 - t0) * frac, p0 + (p1 - p0) * frac)
+        st, ct, sp, cp = np.sin(tt), np.cos(tt), np.sin(pp), np.cos(pp)  # camera.py:141-155
+        d = np.stack([st * cp, ct * sp, ct * cp], axis=-1).reshape(-1, 3)
+        d = (d / np.linalg.norm(d, axis=1, keepdims=True)) @ rot
+        d_u = np.einsum("nij,rj->nri", whit, d)
+        m = np.cross(o_u[:, None, :], d_u)
+        hit = kept[(((m * m).sum(-1) / (d_u * d_u).sum(-1)).min(axis=1) <= lam * lam)]
+        np.bitwise_or.at(bits[tile], hit >> 5, (np.uint32(1) << (hit & 31).astype(np.uint32)))
+    return bits

@@ -32,6 +32,7 @@ EXPORTED = (
     "geer_backward", "geer_frame_stats", "geer_graph_info", "geer_graph_export", "geer_build_graph_host",
     "geer_render_host", "geer_render_backward_host", "geer_l1_grad", "geer_adam", "geer_measure_fp32_peak",
     "geer_loss_workspace_bytes", "geer_loss", "geer_resample_to_beap", "geer_ply_to_soa",
+    "geer_association_check",
 )
 
 
@@ -127,6 +128,7 @@ def load():
             "geer_loss": ([P, P, P, I, I, F, P, P, P, P], I),
             "geer_resample_to_beap": ([P, I, I, P, P, P, P, P], I),
             "geer_ply_to_soa": ([P, I64, I, P, I, P, P], I),
+            "geer_association_check": ([P, ctypes.c_int32, P, P, ctypes.c_int32, P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -212,6 +214,22 @@ class Context:
         s = GeerStats()
         check(self._lib.geer_frame_stats(self.ptr, ctypes.byref(s)))
         return s.as_dict()
+
+    def association_check(self, rays_per_tile: int = 64, max_missing: int = 16, hit_bits_ptr: int = 0) -> dict:
+        """GPU ``oracle.association_bruteforce`` (oracle.py:235-281) against this context's last graph.
+
+        Returns brute-force pair, missing pair (0 = sound), kept-Gaussian and entry counts and the
+        first ``max_missing`` missing (tile, gid) pairs.  Validation only.
+        """
+        import numpy as np
+
+        out = np.zeros(4, np.int64)
+        miss = np.zeros((max(max_missing, 1), 2), np.int32)
+        check(self._lib.geer_association_check(self.ptr, int(rays_per_tile), out.ctypes.data, miss.ctypes.data,
+                                                int(max_missing), hit_bits_ptr or None))
+        k = int(min(out[1], max_missing))
+        return {"brute_pairs": int(out[0]), "missing": int(out[1]), "n_kept": int(out[2]),
+                "graph_entries": int(out[3]), "missing_pairs": miss[:k].tolist()}
 
 
 _default = threading.local()

@@ -35,6 +35,7 @@ UNITS = {
     "geer_train.cu": [],
     "geer_loss.cu": [],
     "geer_camera.cu": ["-fmad=false"],
+    "geer_check.cu": ["-fmad=false"],
 }
 
 

@@ -649,6 +649,47 @@ int geer_frame_stats(geer_ctx *c, geer_stats *out) {
     return GEER_OK;
 }
 
+int geer_association_check(geer_ctx *c, int32_t rays_per_tile, int64_t *out, int32_t *missing, int32_t max_missing,
+                           uint32_t *hit_bits) {
+    if (!c || !out) return fail(GEER_ERR_INVALID, "null argument");
+    if (!c->have_frame) return fail(GEER_ERR_STATE, "association check needs a preceding forward or graph build");
+    int side = 8;
+    while (side * side < rays_per_tile) ++side;  // oracle.py:247 max(8, ceil(sqrt(rays_per_tile)))
+    if (side > 16) return fail(GEER_ERR_INVALID, "rays_per_tile must be at most 256");
+    if (max_missing < 0 || (max_missing > 0 && !missing)) return fail(GEER_ERR_INVALID, "bad missing buffer");
+    const FrameConst &fc = c->fc;
+    const int64_t n = c->scene.n, words = (n + 31) / 32;
+    cudaStream_t st = c->own_stream;
+    GEER_CUDA(cudaDeviceSynchronize());
+    int rc = 0;
+    Buf wo, bits, misc;  // transient (the bitmap is n_tiles * n / 8 bytes: 1 GB at 1M Gaussians, 1080p)
+    struct Free {
+        Buf *b[3];
+        ~Free() {
+            for (Buf *x : b) free_buf(*x);
+        }
+    } guard{{&wo, &bits, &misc}};
+    double *w = ENSURE(double, wo, n * 12 + 1);
+    uint32_t *gb = ENSURE(uint32_t, bits, (size_t)fc.n_tiles * words + 1);
+    char *m = ENSURE(char, misc, 64 + 8 * (size_t)max_missing + 8);
+    unsigned long long *cnt = (unsigned long long *)m;
+    double *origin3 = (double *)(m + 24);
+    int32_t *dmiss = max_missing ? (int32_t *)(m + 64) : nullptr;
+    rc = launch_assoc_check(fc, c->scene, (const double *)c->medges_x.p, (const double *)c->medges_y.p,
+                            (const uint8_t *)c->flags.p, (const int32_t *)c->tile_ranges.p, (const uint32_t *)c->order.p,
+                            side, w, origin3, gb, hit_bits, cnt, dmiss, max_missing, st);
+    if (rc) return fail(rc, "association check launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    unsigned long long h[3];
+    GEER_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
+    if (max_missing) GEER_CUDA(cudaMemcpyAsync(missing, dmiss, 8 * (size_t)max_missing, cudaMemcpyDeviceToHost, st));
+    GEER_CUDA(cudaStreamSynchronize(st));
+    out[0] = (int64_t)h[0];
+    out[1] = (int64_t)h[1];
+    out[2] = (int64_t)h[2];
+    out[3] = c->n_entries;
+    return GEER_OK;
+}
+
 int geer_graph_info(geer_ctx *c, int64_t *n_entries, int32_t *n_x, int32_t *n_y) {
     if (!c) return fail(GEER_ERR_INVALID, "null context");
     if (n_entries) *n_entries = c->n_entries;

@@ -74,6 +74,10 @@ void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, 
                      const CUtensorMap &gpay_map, const uint8_t *flags,
                      const float *remaining,
                      const int32_t *n_eval, const float *dl_dimage, float *accum, cudaStream_t st);
+int launch_assoc_check(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
+                       const uint8_t *flags, const int32_t *ranges, const uint32_t *order, int side, double *wo,
+                       double *origin3, uint32_t *graph_bits, uint32_t *hit_bits, unsigned long long *counters,
+                       int32_t *missing, int max_missing, cudaStream_t st);
 void launch_exhaustive_ranges(const uint8_t *flags, int64_t n, int32_t *ranges2, cudaStream_t st);
 void launch_sum_i32(const int32_t *v, int64_t n, unsigned long long *out, cudaStream_t st);
 void launch_convert_f64_f32(const double *in, float *out, int64_t n, cudaStream_t st);

@@ -13,7 +13,7 @@ from paper_2505_24053_b200.scene import Camera, GaussianScene
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 SMALL_CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                     if os.path.basename(p) not in ("C1.npz", "loss_cases.npz", "resample_cases.npz"))
+                     if os.path.basename(p) not in ("C1.npz", "loss_cases.npz", "resample_cases.npz", "assoc_brute.npz"))
 
 
 def load(name: str) -> dict:
