@@ -125,6 +125,13 @@ __device__ __forceinline__ Ray64 make_ray(const double d[3]) {
     return r;
 }
 
+// Mode-0 quadratic form q . (m00, m11, m22, m01, m02, m12) in fp64 as one FMA chain (1 DMUL +
+// 5 DFMA; the payload's error bound ext.x covers any summation order).  The single definition
+// keeps the forward, its fast path and the backward bit-identical.
+__device__ __forceinline__ double qform(const double2 &a0, const double2 &a1, const double2 &a2, const Ray64 &r) {
+    return fma(a2.y, r.m12, fma(a2.x, r.m02, fma(a1.y, r.m01, fma(a1.x, r.m22, fma(a0.y, r.m11, a0.x * r.m00)))));
+}
+
 struct PairT {
     float kap, alpha, u, t, dd;
 };
@@ -141,9 +148,8 @@ __device__ __forceinline__ void norms64(const Payload &P, const Ray64 &R, const 
         const double2 b0 = *reinterpret_cast<const double2 *>(&P.q[6]);
         const double2 b1 = *reinterpret_cast<const double2 *>(&P.q[8]);
         const double2 b2 = *reinterpret_cast<const double2 *>(&P.q[10]);
-        // (q0 m00 + q1 m11) + (q2 m22 + q3 m01) + (q4 m02 + q5 m12): 4-deep instead of 6-deep chains
-        dd = (fma(a0.y, R.m11, a0.x * R.m00) + fma(a1.y, R.m01, a1.x * R.m22)) + fma(a2.y, R.m12, a2.x * R.m02);
-        mm = (fma(b0.y, R.m11, b0.x * R.m00) + fma(b1.y, R.m01, b1.x * R.m22)) + fma(b2.y, R.m12, b2.x * R.m02);
+        dd = qform(a0, a1, a2, R);
+        mm = qform(b0, b1, b2, R);
     } else {
         const double d0 = dray[0], d1 = dray[1], d2 = dray[2];
         const double u0 = fma(P.q[2], d2, fma(P.q[1], d1, P.q[0] * d0));
@@ -237,6 +243,7 @@ struct __align__(128) PipeSmem {
     uint32_t gid[kStages][kStageEntries];
     int count[kStages];  // entries in the stage; 0 = end of stream
     uint8_t idx[kStages][NW][kStageEntries + 4];  // per warp: its kept entries, padded with null slots
+    alignas(16) uint32_t iadr[kStages][NW][kStageEntries + 4];  // the same entries' shared addresses
     unsigned long long full[kStages];
     unsigned long long empty[kStages];
     int done_warps;
@@ -294,6 +301,21 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
+        : "memory");
+}
+// Wait with a suspend-time hint: the waiting warp sleeps in the barrier (woken when the phase
+// completes or after ~ns) instead of spinning; used by the producer, whose spinning would take
+// issue slots from the consumer warps it waits for.
+__device__ __forceinline__ void mbar_wait_suspend(unsigned long long *bar, unsigned parity) {
+#ifndef GEER_PRODUCER_SUSPEND_NS
+#define GEER_PRODUCER_SUSPEND_NS 20000
+#endif
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITS_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(GEER_PRODUCER_SUSPEND_NS)
         : "memory");
 }
 // TMA gather4: rows r[0..3] of a 2D row-major tensor (one row = one payload) into 4 consecutive
@@ -380,7 +402,7 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
         if (stop_when_done && *((volatile int *)&S.done_warps) == Smem::kNW) break;
         const uint32_t g = g_next;
         if (n > 0) g_next = load_gid(b + 1);
-        mbar_wait(&S.empty[s], phase ^ 1);
+        mbar_wait_suspend(&S.empty[s], phase ^ 1);
         if (n <= 0) {
             if (lane == 0) {
                 S.count[s] = 0;
@@ -436,8 +458,16 @@ __device__ __forceinline__ int stage_keep(Smem &S, int s, int warp, int lane, in
     }
     m = __ballot_sync(0xffffffffu, ov);
     const int c = __popc(m);
-    if (ov) S.idx[s][warp][__popc(m & ((1u << lane) - 1u))] = (uint8_t)lane;
-    if (lane < 4) S.idx[s][warp][c + lane] = (uint8_t)kStageEntries;  // pad to a multiple of 4
+    const uint32_t rb = smem_u32(&S.ring[s][0][0]);
+    if (ov) {
+        const int pos = __popc(m & ((1u << lane) - 1u));
+        S.idx[s][warp][pos] = (uint8_t)lane;
+        S.iadr[s][warp][pos] = rb + ring_off(lane);
+    }
+    if (lane < 4) {  // pad to a multiple of 4
+        S.idx[s][warp][c + lane] = (uint8_t)kStageEntries;
+        S.iadr[s][warp][c + lane] = rb + ring_off(kStageEntries);
+    }
     __syncwarp();
     return c;
 }
@@ -527,6 +557,11 @@ __device__ __forceinline__ double2 lds_d2(uint32_t a) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
     return v;
 }
+__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -537,8 +572,8 @@ __device__ __forceinline__ float4 lds_f4(uint32_t a) {
 __device__ __forceinline__ void norms64_smem(uint32_t pa, const Ray64 &R, double &dd, double &mm) {
     const double2 a0 = lds_d2(pa + 0), a1 = lds_d2(pa + 16), a2 = lds_d2(pa + 32);
     const double2 b0 = lds_d2(pa + 48), b1 = lds_d2(pa + 64), b2 = lds_d2(pa + 80);
-    dd = (fma(a0.y, R.m11, a0.x * R.m00) + fma(a1.y, R.m01, a1.x * R.m22)) + fma(a2.y, R.m12, a2.x * R.m02);
-    mm = (fma(b0.y, R.m11, b0.x * R.m00) + fma(b1.y, R.m01, b1.x * R.m22)) + fma(b2.y, R.m12, b2.x * R.m02);
+    dd = qform(a0, a1, a2, R);
+    mm = qform(b0, b1, b2, R);
 }
 
 constexpr uint32_t kColOff = 96;  // offsetof(Payload, col)
@@ -584,35 +619,36 @@ __device__ __forceinline__ void consume_stage_generic(Smem &S, int s, int warp, 
 #define GEER_FWD_GROUP 4
 #endif
 
-// Stage of mode-0 payloads (the common case): G entries' t first (independent work, explicit shared
-// loads), one warp vote for the rare fp64 cutoff re-decisions, then the serial pixel updates.  t is
-// bit-identical to finish_t's (the backward recomputes it with eval_t).
+// Stage of mode-0 payloads (the common case): G = 4 entries' t first (independent work, explicit
+// shared loads from the addresses stage_keep listed), one warp vote for the rare fp64 cutoff
+// re-decisions, then the serial pixel updates (without the undecidable-cutoff handling unless one
+// occurred).  t is bit-identical to finish_t's (the backward recomputes it with eval_t).
 template <bool kCutoff, int PX, int G, class Smem>
 __device__ __forceinline__ void consume_stage_fast(Smem &S, int s, int warp, int cnt, int base, const Ray64 (&R)[PX],
                                                    const FrameConst &fc, PixelState (&ps)[PX], int &rechecks,
                                                    int &went) {
+    static_assert(G == 4, "entries are consumed in groups of 4 (the list padding)");
 #ifdef GEER_EXP_NOCOMPUTE
     went += cnt;
     return;  // tuning experiment: the pipeline alone (results are wrong)
 #endif
-    const uint32_t rb = smem_u32(&S.ring[s][0][0]);
     const uint32_t ib = smem_u32(&S.idx[s][warp][0]);
+    const uint32_t ab = smem_u32(&S.iadr[s][warp][0]);
+    const int jbase = base + 1;
     int k0 = 0;
     for (; k0 < cnt; k0 += G) {
         bool live = false;
 #pragma unroll
         for (int x = 0; x < PX; ++x) live |= ps[x].r > 0.0f;
         if (k0 > 0 && !__any_sync(0xffffffffu, live)) break;  // warp opaque
-        const uint32_t q = G == 4 ? lds_u32(ib + k0) : (lds_u32(ib + (k0 & ~3)) >> (8 * (k0 & 3)));
+        const uint32_t q = lds_u32(ib + k0);
+        const uint4 adr = lds_u4(ab + 4 * k0);
+        const uint32_t pa[G] = {adr.x, adr.y, adr.z, adr.w};
         float kap[G][PX], t[G][PX];
-        uint32_t pa[G];
-        int jj[G];
         bool near[G][PX], unc[G][PX];
         bool any_near = false;
 #pragma unroll
         for (int u = 0; u < G; ++u) {
-            jj[u] = (q >> (8 * u)) & 0xFF;
-            pa[u] = rb + ring_off(jj[u]);
             const double2 a0 = lds_d2(pa[u] + 0), a1 = lds_d2(pa[u] + 16), a2 = lds_d2(pa[u] + 32);
             const double2 b0 = lds_d2(pa[u] + 48), b1 = lds_d2(pa[u] + 64), b2 = lds_d2(pa[u] + 80);
             const float sw = lds_f32(pa[u] + kColOff + 12);
@@ -620,10 +656,8 @@ __device__ __forceinline__ void consume_stage_fast(Smem &S, int s, int warp, int
             for (int x = 0; x < PX; ++x) {
                 const Ray64 &r = R[x];
                 // (same arithmetic as norms64 mode 0)
-                const double dd = (fma(a0.y, r.m11, a0.x * r.m00) + fma(a1.y, r.m01, a1.x * r.m22)) +
-                                  fma(a2.y, r.m12, a2.x * r.m02);
-                const double mm = (fma(b0.y, r.m11, b0.x * r.m00) + fma(b1.y, r.m01, b1.x * r.m22)) +
-                                  fma(b2.y, r.m12, b2.x * r.m02);
+                const double dd = qform(a0, a1, a2, r);
+                const double mm = qform(b0, b1, b2, r);
                 kap[u][x] = __fmul_rn((float)mm, rcp_approx((float)dd));
                 float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u][x], -0.72134752044448170f)));
                 near[u][x] = false;
@@ -636,6 +670,7 @@ __device__ __forceinline__ void consume_stage_fast(Smem &S, int s, int warp, int
                 t[u][x] = fminf(uu, kMaxBlendTF);
             }
         }
+        bool any_unc = false;
         if (kCutoff && __any_sync(0xffffffffu, any_near)) {
 #pragma unroll
             for (int u = 0; u < G; ++u) {  // (fully unrolled: the arrays stay in registers)
@@ -649,15 +684,28 @@ __device__ __forceinline__ void consume_stage_fast(Smem &S, int s, int warp, int
                     const float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u][x], -0.72134752044448170f)));
                     t[u][x] = k64 <= fc.lam2 ? fminf(uu, kMaxBlendTF) : 0.0f;
                     unc[u][x] = fabs(k64 - fc.lam2) <= (double)lds_f32(pa[u] + kExtOff);
+                    any_unc |= unc[u][x];
                     ++rechecks;
                 }
             }
+            any_unc = __any_sync(0xffffffffu, any_unc);
         }
+        if (!any_unc) {
 #pragma unroll
-        for (int u = 0; u < G; ++u) {
-            const float4 col = lds_f4(pa[u] + kColOff);
+            for (int u = 0; u < G; ++u) {
+                const float4 col = lds_f4(pa[u] + kColOff);
+                const int jne = jbase + (int)__byte_perm(q, 0u, 0x4440u + u);
 #pragma unroll
-            for (int x = 0; x < PX; ++x) pixel_update(ps[x], kap[u][x], t[u][x], col, unc[u][x], base + jj[u] + 1);
+                for (int x = 0; x < PX; ++x) pixel_update(ps[x], kap[u][x], t[u][x], col, false, jne);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                const float4 col = lds_f4(pa[u] + kColOff);
+                const int jne = jbase + (int)__byte_perm(q, 0u, 0x4440u + u);
+#pragma unroll
+                for (int x = 0; x < PX; ++x) pixel_update(ps[x], kap[u][x], t[u][x], col, unc[u][x], jne);
+            }
         }
     }
     went += k0 < cnt ? k0 : cnt;
