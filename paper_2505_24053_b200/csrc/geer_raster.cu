@@ -1243,7 +1243,7 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                         const float m0 = o1 * du2 - o2 * du1, m1 = o2 * du0 - o0 * du2, m2 = o0 * du1 - o1 * du0;
                         v[12] = dl_dt * e.alpha;
                         const float dk = -0.5f * dl_dt * e.u;
-                        const float coef = 2.0f * dk / e.dd;  // dl_dm = coef * m
+                        const float coef = 2.0f * dk * rcp_approx(e.dd);  // dl_dm = coef * m
                         const float lm0 = coef * m0, lm1 = coef * m1, lm2 = coef * m2;
                         v[9] = du1 * lm2 - du2 * lm1;  // dl_do = d_u x dl_dm
                         v[10] = du2 * lm0 - du0 * lm2;
