@@ -36,6 +36,7 @@ UNITS = {
     "geer_loss.cu": [],
     "geer_camera.cu": ["-fmad=false"],
     "geer_check.cu": ["-fmad=false"],
+    "geer_bin.cu": [],
 }
 
 

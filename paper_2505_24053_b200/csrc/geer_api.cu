@@ -86,7 +86,6 @@ struct geer_ctx {
     bool have_frame = false;
     bool have_raster = false;
     bool have_stats = false;  // a raster ran (also exhaustive forwards, which have no backward)
-    bool keys16 = false;  // tile keys stored as uint16
     int64_t n_entries = 0;
     int max_items = 0;
     CUtensorMap pay_map, gpay_map;  // gather4 maps over the payload / grad payload arrays
@@ -102,10 +101,11 @@ struct geer_ctx {
     Buf col_sc, row_sc, medges_x, medges_y, edges_x, edges_y, dir64, theta, phi, minmax, pixel_tile, pixel_tile_sorted,
         pix_iota, pix_list, tile_count, tile_off, item_count, item_off, items, n_items, work, n_work;
     // per-Gaussian buffers
-    Buf payload, gpayload, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, cnt_sorted, offs, ranges_ax, flags, mu_c,
+    Buf payload, gpayload, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, ranges_ax, flags, mu_c,
         depth;
     // per-entry buffers
-    Buf tile_keys, tile_keys_sorted, gids, order, tile_ranges, block_rank;
+    Buf order, tile_ranges;
+    Buf bin_m1, bin_p1, bin_rows, bin_rowstart, bin_segoff, bin_m2, bin_p2;
     // per-pixel buffers
     Buf color, remaining, count_px, n_eval, dl32, fixup;
     // backward
@@ -294,8 +294,6 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     int32_t *giota = ENSURE(int32_t, c->gid_iota, n);
     int32_t *gsorted = ENSURE(int32_t, c->gid_sorted, n);
     int64_t *cnt = ENSURE(int64_t, c->count, n);
-    int64_t *cnts = ENSURE(int64_t, c->cnt_sorted, n);
-    int64_t *offs = ENSURE(int64_t, c->offs, n + 1);
     AxisRanges *ar = ENSURE(AxisRanges, c->ranges_ax, n);
     uint8_t *flags = ENSURE(uint8_t, c->flags, n);
     double *mu = nullptr, *dep = nullptr;
@@ -322,12 +320,9 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     GEER_CUDA(cudaEventRecord(c->ev_hdr, st));
     if (n > 0) {
         launch_iota(giota, n, st);
-        size_t b1 = sort_depth_temp_bytes(n), b2 = scan_temp_bytes(n);
-        void *tmp = ENSURE(char, c->temp, b1 > b2 ? b1 : b2);
+        size_t b1 = sort_depth_temp_bytes(n);
+        void *tmp = ENSURE(char, c->temp, b1);
         sort_depth(tmp, b1, dkey, dkey_s, giota, gsorted, n, st);
-        gather_counts(gsorted, cnt, cnts, n, st);
-        GEER_CUDA(cudaMemsetAsync(offs, 0, sizeof(int64_t), st));
-        inclusive_scan_i64(tmp, b2, cnts, offs + 1, n, st);
     }
     GEER_CUDA(cudaEventSynchronize(c->ev_hdr));
     int err = (int)(c->h_hdr[1] & 0xFFFFFFFF);
@@ -361,41 +356,26 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     if (total >= ((int64_t)1 << 31) - 1)
         return fail(GEER_ERR_NOMEM, "render graph has %lld entries (limit 2^31)", (long long)total);
     c->n_entries = total;
-    // tile keys: u16 when every tile id fits (2 B less per entry and pass in the sort)
-    c->keys16 = fc.n_tiles <= 65536;
-    const size_t kbytes = c->keys16 ? 2 : 4;
-    void *tk = ENSURE(char, c->tile_keys, total * kbytes);
-    void *tks = ENSURE(char, c->tile_keys_sorted, total * kbytes);
-    uint32_t *gids = ENSURE(uint32_t, c->gids, total);
-    uint32_t *order = ENSURE(uint32_t, c->order, total);
-    int32_t *brank = ENSURE(int32_t, c->block_rank, emit_blocks(total) + 1);
-    if (c->keys16)
-        emit_entries(offs, gsorted, ar, fc.n_x, total, n, brank, (uint16_t *)tk, gids, st);
-    else
-        emit_entries(offs, gsorted, ar, fc.n_x, total, n, brank, (uint32_t *)tk, gids, st);
-    if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[2], st));
-
-    // ---- sort: stable tile sort + ranges
-    if (total > 0) {
-        int bits = ceil_log2(fc.n_tiles);
-        if (c->keys16) {
-            size_t b = sort_tiles_temp_bytes<uint16_t>(total, bits);
-            void *tmp = ENSURE(char, c->temp, b);
-            sort_tiles(tmp, b, (const uint16_t *)tk, (uint16_t *)tks, gids, order, total, bits, st);
-        } else {
-            size_t b = sort_tiles_temp_bytes<uint32_t>(total, bits);
-            void *tmp = ENSURE(char, c->temp, b);
-            sort_tiles(tmp, b, (const uint32_t *)tk, (uint32_t *)tks, gids, order, total, bits, st);
-        }
+    // ---- sort: per-tile lists (stable in depth order) and their ranges, then the raster work order
+    {
+        const BinPlan bp = bin_plan(n, fc.n_x, fc.n_y, total);
+        uint32_t *m1 = ENSURE(uint32_t, c->bin_m1, bp.m1_len + 1);
+        uint32_t *p1 = ENSURE(uint32_t, c->bin_p1, bp.m1_len + 1);
+        uint2 *rows = ENSURE(uint2, c->bin_rows, bp.rows_cap + 1);
+        int32_t *rst = ENSURE(int32_t, c->bin_rowstart, fc.n_y + 1);
+        int32_t *sof = ENSURE(int32_t, c->bin_segoff, fc.n_y + 1);
+        uint32_t *m2 = ENSURE(uint32_t, c->bin_m2, bp.m2_len + 1);
+        uint32_t *p2 = ENSURE(uint32_t, c->bin_p2, bp.m2_len + 1);
+        void *tmp = ENSURE(char, c->temp, bp.temp_bytes);
+        uint32_t *order = ENSURE(uint32_t, c->order, total + 1);
+        if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[2], st));
+        rc = bin_tiles(bp, gsorted, ar, n, fc.n_x, fc.n_y, total, m1, p1, rows, rst, sof, m2, p2, tmp, order, ranges, st);
+        if (rc) return fail(rc, "tile binning failed: %s", cudaGetErrorString(cudaGetLastError()));
+        int4 *work = ENSURE(int4, c->work, c->max_items);
+        int32_t *nwork = ENSURE(int32_t, c->n_work, 2);
+        order_items((const int4 *)c->items.p, (const int32_t *)c->n_items.p, ranges, c->max_items, work, nwork, st);
+        if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[3], st));
     }
-    if (c->keys16)
-        tile_ranges((const uint16_t *)tks, total, fc.n_tiles, ranges, st);
-    else
-        tile_ranges((const uint32_t *)tks, total, fc.n_tiles, ranges, st);
-    int4 *work = ENSURE(int4, c->work, c->max_items);
-    int32_t *nwork = ENSURE(int32_t, c->n_work, 2);
-    order_items((const int4 *)c->items.p, (const int32_t *)c->n_items.p, ranges, c->max_items, work, nwork, st);
-    if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[3], st));
     c->have_frame = true;
 
     // ---- render
@@ -404,7 +384,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         int32_t *fix = ENSURE(int32_t, c->fixup, npx);
         launch_forward(fc, sc, c->max_items, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
                        (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
-                       (const double *)c->dir64.p, ranges, order, payload, c->pay_map, flags, color, remaining, count, ne,
+                       (const double *)c->dir64.p, ranges, (const uint32_t *)c->order.p, payload, c->pay_map, flags, color, remaining, count, ne,
                        c->d_counters, fix, st);
         c->fwd_remaining = remaining;
         c->have_raster = c->have_stats = true;
@@ -546,9 +526,10 @@ void geer_destroy(geer_ctx *c) {
     Buf *bufs[] = {&c->col_sc, &c->row_sc, &c->medges_x, &c->medges_y, &c->edges_x, &c->edges_y, &c->dir64,
                    &c->theta, &c->phi, &c->minmax, &c->pixel_tile, &c->pixel_tile_sorted, &c->pix_iota, &c->pix_list,
                    &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->work, &c->n_work, &c->payload, &c->gpayload,
-                   &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted, &c->count, &c->cnt_sorted,
-                   &c->offs, &c->ranges_ax, &c->flags, &c->mu_c, &c->depth, &c->tile_keys, &c->tile_keys_sorted,
-                   &c->gids, &c->order, &c->tile_ranges, &c->block_rank, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,
+                   &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted, &c->count,
+                   &c->ranges_ax, &c->flags, &c->mu_c, &c->depth,
+                   &c->order, &c->tile_ranges,
+                   &c->bin_m1, &c->bin_p1, &c->bin_rows, &c->bin_rowstart, &c->bin_segoff, &c->bin_m2, &c->bin_p2, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,
                    &c->accum, &c->temp, &c->h64_means, &c->h64_log, &c->h64_quats, &c->h64_op, &c->h64_sh,
                    &c->s32_means, &c->s32_log, &c->s32_quats, &c->s32_op, &c->s32_sh, &c->out64, &c->g64};
     for (Buf *b : bufs) free_buf(*b);
@@ -721,23 +702,20 @@ int geer_graph_export(geer_ctx *c, int64_t *order, int64_t *entry_tile, int64_t 
     const int64_t n = c->scene.n, E = c->n_entries, npx = (int64_t)fc.width * fc.height;
     int rc = d2h_u32_as_i64(c->order.p, order, E);
     if (rc) return rc;
-    if (c->keys16 && entry_tile && E > 0) {
-        uint16_t *tmp = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)E);
-        if (!tmp) return fail(GEER_ERR_NOMEM, "host allocation failed");
-        cudaError_t e = cudaMemcpy(tmp, c->tile_keys_sorted.p, sizeof(uint16_t) * (size_t)E, cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) {
-            free(tmp);
-            return fail(GEER_ERR_CUDA, "graph export copy failed: %s", cudaGetErrorString(e));
+    if (entry_tile || ranges) {  // entry tiles from the tile ranges (the lists are tile-major)
+        const int nt = fc.n_tiles;
+        int64_t *rg = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nt + 1));
+        if (!rg) return fail(GEER_ERR_NOMEM, "host allocation failed");
+        rc = d2h_u32_as_i64(c->tile_ranges.p, rg, nt + 1);
+        if (rc) {
+            free(rg);
+            return rc;
         }
-        for (int64_t i = 0; i < E; ++i) entry_tile[i] = (int64_t)tmp[i];
-        free(tmp);
-    } else {
-        rc = d2h_u32_as_i64(c->tile_keys_sorted.p, entry_tile, E);
-        if (rc) return rc;
-    }
-    if (ranges) {
-        rc = d2h_u32_as_i64(c->tile_ranges.p, ranges, fc.n_tiles + 1);
-        if (rc) return rc;
+        if (entry_tile)
+            for (int t = 0; t < nt; ++t)
+                for (int64_t e = rg[t]; e < rg[t + 1] && e < E; ++e) entry_tile[e] = t;
+        if (ranges) memcpy(ranges, rg, sizeof(int64_t) * (size_t)(nt + 1));
+        free(rg);
     }
     if (pixel_tile) {
         if (!c->pixel_tile.p) return fail(GEER_ERR_STATE, "pixel tiles were not recorded (use the host graph build)");

@@ -1,0 +1,337 @@
+// geer_bin.cu — per-tile Gaussian lists without a tile sort (association.py:452-466: entries
+// ordered by tile, then by depth rank, i.e. a stable sort of the depth-ordered (tile, gid) pairs).
+//
+// The lists are built by a two-level stable bucketing of the depth-ordered Gaussians, each level a
+// count / exclusive-scan / ordered-scatter triple:
+//   level 1 (rows):  chunk c of kBinChunk consecutive depth ranks counts its Gaussians per tile
+//                    row; one flat exclusive scan of the [row][chunk] count matrix gives every
+//                    (row, chunk) its start in the row bins; a warp per chunk then walks its
+//                    Gaussians in depth order and appends (gid, x-range) to each of their rows.
+//   level 2 (tiles): the row bins are cut into segments of kSegLen entries; the [row][tile][segment]
+//                    count matrix, scanned flat in that order, is exactly the final entry position
+//                    of every (tile, segment) (tile-major order, segments of a row in depth order);
+//                    a warp per segment walks it in order and writes gids to their tiles.
+// In the ordered walks lane (i mod 32) owns counter i, so every counter is read and written by a
+// single thread in program order: no atomics, no warp synchronisation, and the output equals the
+// stable tile sort bit for bit.  Traffic is a few bytes per entry (vs. two radix passes over
+// 6-byte pairs plus the emitted pairs themselves).
+#include <cub/cub.cuh>
+#include <stdint.h>
+
+#include "geer_common.cuh"
+#include "geer_kernels.h"
+
+namespace geer {
+namespace {
+
+constexpr int kBinChunk = 256;  // depth-ordered Gaussians per level-1 chunk (= threads of a count block)
+constexpr int kSegLen = 256;    // row-bin entries per level-2 segment (= threads of a count block)
+constexpr int kWalkWarps = 8;   // ordered-walk warps per block
+constexpr uint32_t kMultiX = 0xFFFFFFFFu;  // row-bin x info: several x ranges, read them from AxisRanges
+
+__device__ __forceinline__ int rlen(uint32_t r) { return (int)(r >> 16) - (int)(r & 0xFFFFu); }
+
+__device__ __forceinline__ uint32_t sm_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t ld_sm(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void st_sm(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v)); }
+__device__ __forceinline__ uint2 ld_sm2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_sm4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+// Append value v of one item to the slot of counter index k = lo + ((lane - lo) & 31) (the one this
+// lane owns in [lo, hi)), if any: slot = counter, counter += 1.
+template <typename T>
+__device__ __forceinline__ void own_put(uint32_t cbase, int lane, uint32_t range, T v, T *__restrict__ out) {
+    const int lo = (int)(range & 0xFFFFu), hi = (int)(range >> 16);
+    const int k = lo + ((lane - lo) & 31);
+    if (k < hi) {
+        const uint32_t a = cbase + 4u * (uint32_t)k;
+        const uint32_t pos = ld_sm(a);
+        st_sm(a, pos + 1u);
+        out[pos] = v;
+    }
+}
+
+// Row-bin x info of a Gaussian: its single packed x range, or kMultiX.
+__device__ __forceinline__ uint32_t x_info(const AxisRanges &a) {
+    return (rlen(a.x[1]) > 0 || rlen(a.x[2]) > 0) ? kMultiX : a.x[0];
+}
+__device__ __forceinline__ bool has_entries(const AxisRanges &a) {
+    return (rlen(a.x[0]) + rlen(a.x[1]) + rlen(a.x[2])) > 0 && (rlen(a.y[0]) + rlen(a.y[1]) + rlen(a.y[2])) > 0;
+}
+
+__global__ void __launch_bounds__(kBinChunk) k_rows_count(const int32_t *__restrict__ gsorted,
+                                                          const AxisRanges *__restrict__ ar, int64_t n, int n_y,
+                                                          int nch, uint32_t *__restrict__ m1) {
+    extern __shared__ uint32_t cnt[];
+    for (int r = threadIdx.x; r < n_y; r += blockDim.x) cnt[r] = 0;
+    __syncthreads();
+    const int64_t p = (int64_t)blockIdx.x * kBinChunk + threadIdx.x;
+    if (p < n) {
+        const AxisRanges a = ar[gsorted[p]];
+        if (has_entries(a)) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                for (int r = (int)(a.y[k] & 0xFFFFu); r < (int)(a.y[k] >> 16); ++r) atomicAdd(&cnt[r], 1u);
+        }
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < n_y; r += blockDim.x) m1[(int64_t)r * nch + blockIdx.x] = cnt[r];
+}
+
+// One warp per chunk: its Gaussians in depth order, 32 at a time staged in shared memory and read
+// back as broadcasts; for each, the lanes owning its rows append (gid, x info).  Gaussians with
+// several y ranges or more than 32 rows take the general loop.
+__global__ void __launch_bounds__(kWalkWarps * 32) k_rows_scatter(const int32_t *__restrict__ gsorted,
+                                                                 const AxisRanges *__restrict__ ar, int64_t n, int n_y,
+                                                                 int nch, const uint32_t *__restrict__ p1,
+                                                                 uint2 *__restrict__ rowbin) {
+    extern __shared__ uint32_t smem[];
+    __shared__ uint4 stage[kWalkWarps][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWalkWarps + wib;
+    if (c >= nch) return;
+    uint32_t *cnt = smem + wib * n_y;
+    for (int r = lane; r < n_y; r += 32) cnt[r] = p1[(int64_t)r * nch + c];  // row r: lane r % 32 only
+    const int64_t p0 = (int64_t)c * kBinChunk;
+    const int m_all = (int)lmin(kBinChunk, n - p0);
+    for (int b = 0; b < m_all; b += 32) {
+        const int64_t p = p0 + b + lane;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);  // (gid, x info, y range or kMultiX, -)
+        if (b + lane < m_all) {
+            const uint32_t g = (uint32_t)gsorted[p];
+            const AxisRanges a = ar[g];
+            if (has_entries(a)) {
+                const bool multi = rlen(a.y[1]) > 0 || rlen(a.y[2]) > 0 || rlen(a.y[0]) > 32;
+                v = make_uint4(g, x_info(a), multi ? kMultiX : a.y[0], 0u);
+            }
+        }
+        stage[wib][lane] = v;
+        const bool any_multi = __any_sync(0xffffffffu, v.z == kMultiX);
+        __syncwarp();
+        const int m = min(32, m_all - b);
+        const uint32_t cbase = sm_addr(cnt), sb = sm_addr(&stage[wib][0]);
+        if (!any_multi) {
+#pragma unroll 4
+            for (int i = 0; i < m; ++i) {
+                const uint4 e = ld_sm4(sb + 16u * i);
+                own_put(cbase, lane, e.z, make_uint2(e.x, e.y), rowbin);
+            }
+        } else for (int i = 0; i < m; ++i) {
+            const uint4 e = stage[wib][i];
+            if (e.z != kMultiX) {
+                own_put(cbase, lane, e.z, make_uint2(e.x, e.y), rowbin);
+            } else {
+                const AxisRanges a = ar[e.x];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const int lo = (int)(a.y[k] & 0xFFFFu), hi = (int)(a.y[k] >> 16);
+                    for (int r = lo + ((lane - lo) & 31); r < hi; r += 32) {
+                        const uint32_t pos = cnt[r];
+                        cnt[r] = pos + 1;
+                        rowbin[pos] = make_uint2(e.x, e.y);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Row starts, segments per row (>= 1, so every tile has a (tile, segment 0) slot) and their
+// exclusive prefix; also the list end ranges[n_tiles] = total.  One block.
+__global__ void k_segments(const uint32_t *__restrict__ m1, const uint32_t *__restrict__ p1, int n_y, int nch,
+                           int32_t *__restrict__ rowstart, int32_t *__restrict__ seg_off, int n_tiles,
+                           int32_t total, int32_t *__restrict__ ranges) {
+    __shared__ int carry;
+    const int64_t last = (int64_t)n_y * nch - 1;
+    const uint32_t R = last >= 0 ? p1[last] + m1[last] : 0u;
+    if (threadIdx.x == 0) {
+        carry = 0;
+        rowstart[n_y] = (int32_t)R;
+        ranges[n_tiles] = total;
+    }
+    __syncthreads();
+    for (int r0 = 0; r0 < n_y; r0 += blockDim.x) {
+        const int r = r0 + threadIdx.x;
+        int ns = 0;
+        if (r < n_y) {
+            const uint32_t a = p1[(int64_t)r * nch], b = r + 1 < n_y ? p1[(int64_t)(r + 1) * nch] : R;
+            rowstart[r] = (int32_t)a;
+            ns = max(1, (int)((b - a + kSegLen - 1) / kSegLen));
+        }
+        int incl;
+        {
+            typedef cub::BlockScan<int, 1024> Scan;
+            __shared__ typename Scan::TempStorage tmp;
+            Scan(tmp).InclusiveSum(ns, incl);
+        }
+        if (r < n_y) seg_off[r] = carry + incl - ns;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) seg_off[n_y] = carry;
+}
+
+__device__ __forceinline__ int seg_row(const int32_t *seg_off, int n_y, int sgl) {
+    int lo = 0, hi = n_y;  // largest r with seg_off[r] <= sgl
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (seg_off[mid] <= sgl) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kSegLen) k_tiles_count(const uint2 *__restrict__ rowbin,
+                                                         const AxisRanges *__restrict__ ar,
+                                                         const int32_t *__restrict__ rowstart,
+                                                         const int32_t *__restrict__ seg_off, int n_y, int n_x,
+                                                         uint32_t *__restrict__ m2) {
+    extern __shared__ uint32_t cnt[];
+    const int sgl = blockIdx.x;
+    if (sgl >= seg_off[n_y]) {  // past the real segments: zero one n_x slice of the matrix tail (it is scanned)
+        for (int t = threadIdx.x; t < n_x; t += blockDim.x) m2[(int64_t)n_x * sgl + t] = 0u;
+        return;
+    }
+    const int r = seg_row(seg_off, n_y, sgl);
+    const int s = sgl - seg_off[r], ns = seg_off[r + 1] - seg_off[r];
+    for (int t = threadIdx.x; t < n_x; t += blockDim.x) cnt[t] = 0;
+    __syncthreads();
+    const int e = rowstart[r] + s * kSegLen + threadIdx.x;
+    if (e < rowstart[r + 1] && threadIdx.x < kSegLen) {
+        const uint2 v = rowbin[e];
+        if (v.y != kMultiX) {
+            for (int t = (int)(v.y & 0xFFFFu); t < (int)(v.y >> 16); ++t) atomicAdd(&cnt[t], 1u);
+        } else {
+            const AxisRanges a = ar[v.x];
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                for (int t = (int)(a.x[k] & 0xFFFFu); t < (int)(a.x[k] >> 16); ++t) atomicAdd(&cnt[t], 1u);
+        }
+    }
+    __syncthreads();
+    const int64_t base = (int64_t)n_x * seg_off[r] + s;
+    for (int t = threadIdx.x; t < n_x; t += blockDim.x) m2[base + (int64_t)t * ns] = cnt[t];
+}
+
+__device__ __forceinline__ void put_tiles(uint32_t *cnt, int lane, uint32_t xr, uint32_t gid, uint32_t *order) {
+    const int lo = (int)(xr & 0xFFFFu), hi = (int)(xr >> 16);
+    for (int t = lo + ((lane - lo) & 31); t < hi; t += 32) {  // tile t: lane t % 32 only
+        const uint32_t pos = cnt[t];
+        cnt[t] = pos + 1;
+        order[pos] = gid;
+    }
+}
+
+// One warp per segment: its row-bin entries in order, read as shared-memory broadcasts; for each,
+// the lane owning each of its tiles writes the gid (one tile per lane when the x range spans <= 32
+// tiles, the general loop otherwise).
+__global__ void __launch_bounds__(kWalkWarps * 32) k_tiles_scatter(const uint2 *__restrict__ rowbin,
+                                                                  const AxisRanges *__restrict__ ar,
+                                                                  const int32_t *__restrict__ rowstart,
+                                                                  const int32_t *__restrict__ seg_off, int n_y, int n_x,
+                                                                  const uint32_t *__restrict__ p2,
+                                                                  uint32_t *__restrict__ order,
+                                                                  int32_t *__restrict__ ranges) {
+    extern __shared__ uint32_t smem[];
+    __shared__ uint2 stage[kWalkWarps][kSegLen];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int sgl = blockIdx.x * kWalkWarps + wib;
+    if (sgl >= seg_off[n_y]) return;
+    const int r = seg_row(seg_off, n_y, sgl);
+    const int s = sgl - seg_off[r], ns = seg_off[r + 1] - seg_off[r];
+    uint32_t *cnt = smem + wib * n_x;
+    const int64_t base = (int64_t)n_x * seg_off[r] + s;
+    for (int t = lane; t < n_x; t += 32) {
+        const uint32_t v = p2[base + (int64_t)t * ns];
+        cnt[t] = v;
+        if (s == 0) ranges[r * n_x + t] = (int32_t)v;  // first entry of tile (r, t)
+    }
+    const int e0 = rowstart[r] + s * kSegLen, m = min(kSegLen, rowstart[r + 1] - e0);
+    bool multi = false;
+    for (int i = lane; i < m; i += 32) {
+        uint2 v = rowbin[e0 + i];
+        if (v.y != kMultiX && rlen(v.y) > 32) v.y = kMultiX;  // general loop below
+        multi |= v.y == kMultiX;
+        stage[wib][i] = v;
+    }
+    const bool any_multi = __any_sync(0xffffffffu, multi);
+    __syncwarp();
+    const uint32_t cbase = sm_addr(cnt), sb = sm_addr(&stage[wib][0]);
+    if (!any_multi) {
+#pragma unroll 8
+        for (int i = 0; i < m; ++i) {
+            const uint2 v = ld_sm2(sb + 8u * i);
+            own_put(cbase, lane, v.y, v.x, order);
+        }
+        return;
+    }
+    for (int i = 0; i < m; ++i) {
+        const uint2 v = stage[wib][i];
+        if (v.y != kMultiX) {
+            own_put(cbase, lane, v.y, v.x, order);
+        } else {
+            const AxisRanges a = ar[v.x];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) put_tiles(cnt, lane, a.x[k], v.x, order);
+        }
+    }
+}
+
+}  // namespace
+
+BinPlan bin_plan(int64_t n, int n_x, int n_y, int64_t n_entries) {
+    BinPlan p;
+    p.nch = (int)((n + kBinChunk - 1) / kBinChunk);
+    p.m1_len = (int64_t)n_y * p.nch;
+    p.rows_cap = n_entries;  // every (Gaussian, row) pair holds >= 1 entry
+    p.seg_cap = (n_entries + kSegLen - 1) / kSegLen + n_y;
+    p.m2_len = (int64_t)n_x * p.seg_cap;
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b1, (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)lmax(p.m1_len, 1));
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)lmax(p.m2_len, 1));
+    p.temp_bytes = b1 > b2 ? b1 : b2;
+    return p;
+}
+
+int bin_tiles(const BinPlan &p, const int32_t *gsorted, const AxisRanges *ar, int64_t n, int n_x, int n_y,
+              int64_t n_entries, uint32_t *m1, uint32_t *p1, uint2 *rowbin, int32_t *rowstart, int32_t *seg_off,
+              uint32_t *m2, uint32_t *p2, void *temp, uint32_t *order, int32_t *ranges, cudaStream_t st) {
+    const int n_tiles = n_x * n_y;
+    if (n <= 0 || n_entries <= 0) {  // every tile empty
+        cudaMemsetAsync(ranges, 0, sizeof(int32_t) * (n_tiles + 1), st);
+        return cudaGetLastError() == cudaSuccess ? GEER_OK : GEER_ERR_CUDA;
+    }
+    if ((size_t)n_y * 4 * kWalkWarps > 200 * 1024 || (size_t)n_x * 4 * kWalkWarps > 200 * 1024) return GEER_ERR_INVALID;
+    k_rows_count<<<p.nch, kBinChunk, n_y * 4, st>>>(gsorted, ar, n, n_y, p.nch, m1);
+    size_t tb = p.temp_bytes;
+    cub::DeviceScan::ExclusiveSum(temp, tb, m1, p1, (int)p.m1_len, st);
+    const int wsm_rows = n_y * 4 * kWalkWarps;
+    if (wsm_rows > 48 * 1024) cudaFuncSetAttribute(k_rows_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm_rows);
+    k_rows_scatter<<<(p.nch + kWalkWarps - 1) / kWalkWarps, kWalkWarps * 32, wsm_rows, st>>>(gsorted, ar, n, n_y,
+                                                                                           p.nch, p1, rowbin);
+    k_segments<<<1, 1024, 0, st>>>(m1, p1, n_y, p.nch, rowstart, seg_off, n_tiles, (int32_t)n_entries, ranges);
+    k_tiles_count<<<(unsigned)p.seg_cap, kSegLen, n_x * 4, st>>>(rowbin, ar, rowstart, seg_off, n_y, n_x, m2);
+    tb = p.temp_bytes;
+    cub::DeviceScan::ExclusiveSum(temp, tb, m2, p2, (int)p.m2_len, st);
+    const int wsm_tiles = n_x * 4 * kWalkWarps;
+    if (wsm_tiles > 48 * 1024)
+        cudaFuncSetAttribute(k_tiles_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm_tiles);
+    k_tiles_scatter<<<(unsigned)((p.seg_cap + kWalkWarps - 1) / kWalkWarps), kWalkWarps * 32, wsm_tiles, st>>>(
+        rowbin, ar, rowstart, seg_off, n_y, n_x, p2, order, ranges);
+    return cudaGetLastError() == cudaSuccess ? GEER_OK : GEER_ERR_CUDA;
+}
+
+}  // namespace geer

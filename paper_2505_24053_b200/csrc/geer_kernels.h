@@ -37,28 +37,24 @@ struct SortTemp {
     size_t bytes = 0;
 };
 size_t sort_depth_temp_bytes(int64_t n);
-size_t scan_temp_bytes(int64_t n);
-template <typename K>
-size_t sort_tiles_temp_bytes(int64_t n_entries, int n_bits);
 size_t scan_i32_temp_bytes(int64_t n);
 void sort_depth(void *temp, size_t temp_bytes, const uint32_t *keys_in, uint32_t *keys_out, const int32_t *vals_in,
                 int32_t *vals_out, int64_t n, cudaStream_t st);
-void gather_counts(const int32_t *sorted_gid, const int64_t *count, int64_t *cnt_sorted, int64_t n, cudaStream_t st);
-void inclusive_scan_i64(void *temp, size_t temp_bytes, const int64_t *in, int64_t *out, int64_t n, cudaStream_t st);
 void exclusive_scan_i32(void *temp, size_t temp_bytes, const int32_t *in, int32_t *out, int64_t n, cudaStream_t st);
-int64_t emit_blocks(int64_t n_entries);
-template <typename K>
-void emit_entries(const int64_t *offs, const int32_t *sorted_gid, const AxisRanges *ranges, int n_x,
-                  int64_t n_entries, int64_t n, int32_t *block_rank, K *tile_keys, uint32_t *gids,
-                  cudaStream_t st);
-template <typename K>
-void sort_tiles(void *temp, size_t temp_bytes, const K *keys_in, K *keys_out, const uint32_t *vals_in,
-                uint32_t *vals_out, int64_t n, int n_bits, cudaStream_t st);
+// Per-tile lists by two-level stable bucketing (geer_bin.cu): order / ranges equal the stable tile
+// sort of the depth-ordered entries.
+struct BinPlan {
+    int nch;                                    // level-1 chunks
+    int64_t m1_len, rows_cap, seg_cap, m2_len;  // [row][chunk] counts, row-bin capacity, segments, [row][tile][seg]
+    size_t temp_bytes;                          // CUB scan workspace
+};
+BinPlan bin_plan(int64_t n, int n_x, int n_y, int64_t n_entries);
+int bin_tiles(const BinPlan &p, const int32_t *gsorted, const AxisRanges *ar, int64_t n, int n_x, int n_y,
+              int64_t n_entries, uint32_t *m1, uint32_t *p1, uint2 *rowbin, int32_t *rowstart, int32_t *seg_off,
+              uint32_t *m2, uint32_t *p2, void *temp, uint32_t *order, int32_t *ranges, cudaStream_t st);
 void sort_pixels(void *temp, size_t temp_bytes, const int32_t *keys_in, int32_t *keys_out, const int32_t *vals_in,
                  int32_t *vals_out, int64_t n, int n_bits, cudaStream_t st);
 size_t sort_pixels_temp_bytes(int64_t n, int n_bits);
-template <typename K>
-void tile_ranges(const K *sorted_tiles, int64_t n_entries, int n_tiles, int32_t *ranges, cudaStream_t st);
 void order_items(const int4 *items, const int32_t *n_items, const int32_t *ranges, int max_items, int4 *work,
                  int32_t *n_work, cudaStream_t st);
 
