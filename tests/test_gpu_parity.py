@@ -124,3 +124,45 @@ def test_full_c3_backward_vs_oracle():
     gr = renderer.render_backward(scene, cam, dl, cfg)
     rep = P.assert_grads_close(gr, vars(ob))
     print("C3 gradient parity", rep)
+
+
+def _mixed_scene(n_small, n_big, seed):
+    """Many small Gaussians plus large ones (x/y tile ranges far beyond 32 tiles) and a few huge,
+    very transparent ones around the camera (clamped, routed to every tile)."""
+    rng = np.random.default_rng(seed)
+    parts = [synth.config_scene("C2", n=n_small),
+             synth.random_scene(n_big, rng, spread=1.5, scale_range=(0.2, 0.9), sh_bands=16, anisotropy=4.0),
+             synth.random_scene(6, rng, spread=0.3, scale_range=(2.5, 4.0), sh_bands=16, opacity_range=(0.3, 0.5))]
+    cat = lambda k: np.concatenate([getattr(p, k) for p in parts])
+    from paper_2505_24053_b200.scene import GaussianScene
+
+    return synth.to_f32_values(GaussianScene(cat("means"), cat("log_scales"), cat("quats"), cat("opacity_logits"),
+                                             cat("sh")))
+
+
+@pytest.mark.parametrize("camera", ["c2_1080p", "beap300_inside", "kb_720p_tile8"])
+def test_binning_edge_cases_vs_oracle(camera):
+    """Tile lists (two-level bucketing) bit-exact against the oracle where ranges are long (> 32 tiles),
+    split in several pieces (300 deg camera inside the cloud) or cover every tile (clamped)."""
+    from paper_2505_24053_b200.scene import Camera
+
+    scene = _mixed_scene(30_000, 300, 5)
+    tile_px = 16
+    if camera == "c2_1080p":
+        cam = synth.config_camera("C2")
+    elif camera == "beap300_inside":
+        rot, t = synth.look_at((0.1, -0.05, 0.2), target=(1.0, 0.2, 0.4))
+        cam = Camera(width=960, height=512, model="beap", rotation=rot, translation=t, fov_x=np.deg2rad(300.0),
+                     fov_y=np.deg2rad(160.0))
+    else:
+        cam = synth.config_camera("C5", width=1280, height=720)
+        tile_px = 8
+    og = O.build_render_graph(scene, cam, tile_px=tile_px)
+    assert og.clamped.any()
+    g = association.build_render_graph(scene, cam, tile_px=tile_px)
+    P.assert_graph_equal(g, og.order, og.entry_tile, og.ranges, og.keep, og.clamped)
+    cfg = renderer.RenderConfig(tile_px=tile_px)
+    of = O.render(scene, cam, cfg, graph=og)
+    fr = renderer.render(scene, cam, cfg)
+    P.assert_image_close(fr.color.color, fr.remaining_transmittance, fr.contributor_count, of.color, of.remaining,
+                         of.count)
