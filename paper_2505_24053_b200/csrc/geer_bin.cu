@@ -24,8 +24,14 @@
 namespace geer {
 namespace {
 
-constexpr int kBinChunk = 256;  // depth-ordered Gaussians per level-1 chunk (= threads of a count block)
-constexpr int kSegLen = 256;    // row-bin entries per level-2 segment (= threads of a count block)
+#ifndef GEER_BIN_CHUNK
+#define GEER_BIN_CHUNK 256
+#endif
+#ifndef GEER_SEG_LEN
+#define GEER_SEG_LEN 256
+#endif
+constexpr int kBinChunk = GEER_BIN_CHUNK;  // depth-ordered Gaussians per level-1 chunk (= threads of a count block)
+constexpr int kSegLen = GEER_SEG_LEN;      // row-bin entries per level-2 segment (= threads of a count block)
 constexpr int kWalkWarps = 8;   // ordered-walk warps per block
 constexpr uint32_t kMultiX = 0xFFFFFFFFu;  // row-bin x info: several x ranges, read them from AxisRanges
 

@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
-for f in 1 2 3 4; do
+for f in ${FRAMES:-1 2 3 4}; do
   timeout 600 python bench.py --steps 60 --warmup 5 --no-e2e --no-train --no-cpu --no-c5 --inflight $f 2>/dev/null | python -c "
 import json,sys
 for l in sys.stdin:
