@@ -16,7 +16,7 @@ from collections import OrderedDict
 
 def short(name: str) -> str:
     if "geer::" in name:
-        m = re.search(r"geer::(\w+)(<[^>(]*>)?", name)
+        m = re.search(r"geer::(?:<unnamed>::)?(k_\w+)(<[^>(]*>)?", name)
         return m.group(1) + (m.group(2) or "") if m else name[:60]
     m = re.search(r"cub::\w+::(\w+)", name)
     if m:
