@@ -615,6 +615,25 @@ __device__ __forceinline__ void consume_stage_generic(Smem &S, int s, int warp, 
     went += k0 < cnt ? k0 : cnt;
 }
 
+// Mode-0 pair evaluation from a payload at shared address pa: norms64 + finish_t with m1 = false,
+// operation for operation (t, kappa, alpha, u, dd bit-identical to eval_t's).
+__device__ __forceinline__ void eval_t0_smem(uint32_t pa, const Ray64 &R, const FrameConst &fc, PairT &e) {
+    double dd, mm;
+    norms64_smem(pa, R, dd, mm);
+    const float sw = lds_f32(pa + kColOff + 12);
+    e.dd = (float)dd;
+    e.kap = __fmul_rn((float)mm, rcp_approx(e.dd));
+    e.alpha = ex2_approx(__fmul_rn(e.kap, -0.72134752044448170f));
+    float u = __fmul_rn(fabsf(sw), e.alpha);
+    if (fc.cutoff) {
+        bool inside = e.kap <= fc.lam2f;
+        if (fabsf(__fsub_rn(e.kap, fc.lam2f)) <= fc.cutoff_tol) inside = mm / dd <= fc.lam2;
+        u = inside ? u : 0.0f;
+    }
+    e.u = u;
+    e.t = fminf(u, kMaxBlendTF);
+}
+
 #ifndef GEER_FWD_GROUP
 #define GEER_FWD_GROUP 4
 #endif
@@ -1131,6 +1150,9 @@ __device__ __forceinline__ float warp_transpose_reduce16(float v[16], int lane) 
 // entries (index < n_eval) from the last to the first, recovering
 // T_i = T_{i+1} / (1 - t_i) from the forward's final remaining, and the warp
 // adds its 16 per-entry partials to the Gaussian's accumulators.
+#ifndef GEER_BWD_GROUP
+#define GEER_BWD_GROUP 1  // entries evaluated together in the backward (mode-0 stages; 2 and 4 measured slower)
+#endif
 #ifndef BWD_MIN_BLOCKS
 #define BWD_MIN_BLOCKS 3
 #endif
@@ -1204,18 +1226,15 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
             uint32_t msk;
             stage_keep(S, s, warp, lane, n, fc.cull != 0, my_patch, my_cone, msk);
             if (wmax - lo < 32) msk &= (1u << (wmax - lo)) - 1u;
-            while (msk) {
-                const int jj = 31 - __clz(msk);
-                msk &= ~(1u << jj);
+            // one entry's gradient: T and suffix update, 16 partials, warp reduction, accumulators
+            auto entry = [&](const int jj, const PairT &e) {
                 const int i = lo + jj;
                 float v[16];
 #pragma unroll
                 for (int k = 0; k < 16; ++k) v[k] = 0.f;
                 const Payload &P = ring_at(S, s, jj);
-                PairT e;
-                eval_t(P, R, sray[tid], fc, e, dummy);  // warp-uniform call (mode vote inside)
                 // t = 0 (or not alive) on every lane: T, the suffix and all 16 partials are unchanged
-                if (!__any_sync(0xffffffffu, i < ne && e.t > 0.0f)) continue;
+                if (!__any_sync(0xffffffffu, i < ne && e.t > 0.0f)) return;
                 if (i < ne) {
                     const float omt = __fsub_rn(1.0f, e.t);
                     const float inv = rcp_approx(omt);  // 1 - t >= 0.001: ~1 ulp
@@ -1276,6 +1295,34 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                 if ((lane & 1) == 0 && tot != 0.0f)
                     atomicAdd(accum + (int64_t)S.gid[s][jj] * 16 + (lane >> 1), tot);
 #endif
+            };
+            // a mode-1 (cross-product) payload anywhere in the stage selects the generic evaluation;
+            // otherwise GEER_BWD_GROUP entries are evaluated together (independent fp64 work), then their
+            // gradients are formed in order (back to front)
+            if (__any_sync(0xffffffffu, lane < n && ring_at(S, s, lane).col.w < 0.0f)) {
+                while (msk) {
+                    const int jj = 31 - __clz(msk);
+                    msk &= ~(1u << jj);
+                    PairT e;
+                    eval_t(ring_at(S, s, jj), R, sray[tid], fc, e, dummy);  // warp-uniform call (mode vote inside)
+                    entry(jj, e);
+                }
+            } else {
+                const uint32_t rb = smem_u32(&S.ring[s][0][0]);
+                while (msk) {
+                    int jv[GEER_BWD_GROUP];
+                    PairT ev[GEER_BWD_GROUP];
+#pragma unroll
+                    for (int u = 0; u < GEER_BWD_GROUP; ++u) {
+                        jv[u] = msk ? 31 - __clz(msk) : -1;
+                        if (msk) msk &= ~(1u << jv[u]);
+                        // (a missing slot evaluates the null entry: t = 0)
+                        eval_t0_smem(rb + ring_off(jv[u] >= 0 ? jv[u] : kStageEntries), R, fc, ev[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < GEER_BWD_GROUP; ++u)
+                        if (jv[u] >= 0) entry(jv[u], ev[u]);
+                }
             }
         }
         __syncwarp();
