@@ -338,8 +338,14 @@ def run_ours(args):
             traffic = json.load(f).get(dominant)
     except Exception:
         pass
+    ncu_util = None
+    try:  # issue-slot and pipe utilisation of the same kernel (ncu --set full, profiles/ncu_utilisation.json)
+        with open(os.path.join(ROOT, "profiles", "ncu_utilisation.json")) as f:
+            ncu_util = json.load(f).get(dominant)
+    except Exception:
+        pass
     roofline = {"bound": dv["bound"], "kernel": dominant, "achieved": dv["achieved"], "peak": dv["peak"],
-                "unit": dv["unit"], "frac": dv["frac"], "traffic": traffic,
+                "unit": dv["unit"], "frac": dv["frac"], "traffic": traffic, "ncu": ncu_util,
                 "peak_source": (f"{peaks['source']} MEASURED_PEAKS.json hbm_gbs" if dv["bound"] == "hbm" else
                                 f"FP32 FMA peak measured live by geer_measure_fp32_peak {fp32} TFLOP/s "
                                 f"(MEASURED_PEAKS.json has no FP32 figure; nominal 148 SM x 128 x 2 x 1.965 GHz "

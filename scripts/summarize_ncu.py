@@ -59,6 +59,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("report")
     ap.add_argument("--traffic")
+    ap.add_argument("--issue", help="write {stage: issue-slot / pipe utilisation} (bench.py roofline.ncu)")
     a = ap.parse_args()
     out = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
@@ -90,6 +91,21 @@ def main():
                 wr = value(kern[c], units, "dram__bytes_write.sum") or 0.0
                 t[STAGE[base]] = rd + wr
         with open(a.traffic, "w") as f:
+            json.dump(t, f, indent=1)
+    if a.issue:
+        t = {}
+        keys = {"issue_active": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                "fp32_pipe": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+                "fp64_pipe": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                "lsu_pipe": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+                "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                "occupancy": "sm__warps_active.avg.pct_of_peak_sustained_active"}
+        for c in cols:
+            base = c.split("<")[0]
+            if base in STAGE:
+                t[STAGE[base]] = {k: round((value(kern[c], units, m) or 0.0) / 100.0, 4) for k, m in keys.items()}
+                t[STAGE[base]]["warp_instructions"] = value(kern[c], units, "smsp__inst_executed.sum")
+        with open(a.issue, "w") as f:
             json.dump(t, f, indent=1)
 
 
