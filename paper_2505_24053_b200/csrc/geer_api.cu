@@ -295,7 +295,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     int32_t *gsorted = ENSURE(int32_t, c->gid_sorted, n);
     int64_t *cnt = ENSURE(int64_t, c->count, n);
     AxisRanges *ar = ENSURE(AxisRanges, c->ranges_ax, n);
-    uint8_t *flags = ENSURE(uint8_t, c->flags, n);
+    uint8_t *flags = ENSURE(uint8_t, c->flags, 2 * n);  // [0, n): association bits, [n, 2n): payload bits
     double *mu = nullptr, *dep = nullptr;
     if (want_export) {
         mu = ENSURE(double, c->mu_c, n * 3);
@@ -417,10 +417,10 @@ int run_backward(geer_ctx *c, const float *dl_dimage, bool f64_out, void *const 
                     c->fwd_remaining, (const int32_t *)c->n_eval.p,
                     dl_dimage, accum, st);
     if (f64_out)
-        launch_finalize<double>(fc, sc, (const float4 *)accum, (const uint8_t *)c->flags.p, (double *)gout[0], (double *)gout[1],
+        launch_finalize<double>(fc, sc, (const float4 *)accum, (const uint8_t *)c->flags.p + sc.n, (double *)gout[0], (double *)gout[1],
                                 (double *)gout[2], (double *)gout[3], (double *)gout[4], accumulate, st);
     else
-        launch_finalize<float>(fc, sc, (const float4 *)accum, (const uint8_t *)c->flags.p, (float *)gout[0], (float *)gout[1],
+        launch_finalize<float>(fc, sc, (const float4 *)accum, (const uint8_t *)c->flags.p + sc.n, (float *)gout[0], (float *)gout[1],
                                (float *)gout[2], (float *)gout[3], (float *)gout[4], accumulate, st);
     if (c->timing) {
         GEER_CUDA(cudaEventRecord(c->ev[1], st));

@@ -784,7 +784,10 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS)
 #endif
     }
     __syncthreads();
-    if (threadIdx.x < cnt_b) flags[g0 + threadIdx.x] = (uint8_t)(sfl[0][threadIdx.x] | sfl[1][threadIdx.x]);
+    if (threadIdx.x < cnt_b) {
+        flags[g0 + threadIdx.x] = sfl[0][threadIdx.x];
+        flags[sc.n + g0 + threadIdx.x] = sfl[1][threadIdx.x];
+    }
     if (threadIdx.x < 32) {  // the block's entries, for the frame total (one atomic per block)
         unsigned long long t = 0;
         for (int i = threadIdx.x; i < cnt_b; i += 32) t += (unsigned long long)count[g0 + i];
