@@ -865,8 +865,8 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
               float *__restrict__ remaining, int32_t *__restrict__ count, int32_t *__restrict__ n_eval,
               unsigned long long *__restrict__ counters, int32_t *__restrict__ fixup_list) {
     constexpr int PX = kFwdPX, NW = kFwdNW, NT = 32 * kFwdNW;
-    extern __shared__ __align__(16) unsigned char dsmem[];  // PipeSmem (dynamic: deep rings exceed 48 KB)
-    FwdSmem &S = *reinterpret_cast<FwdSmem *>(align128(dsmem));
+    extern __shared__ __align__(128) unsigned char dsmem[];  // PipeSmem (dynamic: deep rings exceed 48 KB)
+    FwdSmem &S = *reinterpret_cast<FwdSmem *>(dsmem);  // 128-B aligned base: TMA destinations, fixed offsets
     __shared__ double sray[kRasterThreads][3];  // fp64 pixel rays (mode-1 payloads only)
     // n_items: [0] items with entries (work[0, n0)), [1] empty items (work[max_items - n1, max_items))
     const int n_full = n_items[0];
@@ -1185,8 +1185,8 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                const uint8_t *__restrict__ flags, const float *__restrict__ remaining,
                const int32_t *__restrict__ n_eval,
                const float *__restrict__ dl_dimage, float *__restrict__ accum) {
-    extern __shared__ __align__(16) unsigned char dsmem[];
-    PipeSmem<true> &S = *reinterpret_cast<PipeSmem<true> *>(align128(dsmem));
+    extern __shared__ __align__(128) unsigned char dsmem[];
+    PipeSmem<true> &S = *reinterpret_cast<PipeSmem<true> *>(dsmem);
     __shared__ double sray[kRasterThreads][3];
 #if GEER_BWD_SMEM_REDUCE
     __shared__ float sred[kConsumerWarps][32 * 17];  // per-warp reduction scratch
