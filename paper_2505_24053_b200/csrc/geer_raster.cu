@@ -250,12 +250,9 @@ struct __align__(128) PipeSmem {
     int stop;  // producer will not fill any more stages
 };
 
-// The dynamic shared window starts after the static allocations: align the pipeline state to 128 B
-// (TMA destinations) by hand; launches reserve sizeof + 128 bytes.
-__device__ __forceinline__ unsigned char *align128(unsigned char *p) {
-    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-    return p + ((128u - (a & 127u)) & 127u);
-}
+// The pipeline state lives at the start of the dynamic shared window, declared __align__(128) (TMA
+// destinations; the compiler places the window after the static allocations at that alignment, so
+// every member sits at a fixed offset).  Launches still reserve sizeof + 128 bytes.
 
 __device__ __forceinline__ uint32_t ring_off(int j) { return (uint32_t)((j >> 2) * kRingGroupBytes + (j & 3) * (int)sizeof(Payload)); }
 template <class Smem>
