@@ -287,30 +287,32 @@ __device__ __forceinline__ double sigmoid(double x) {  // core.py:58-67
 }
 
 // core.py:289-313
+// One term of the basis (b a compile-time constant after unrolling), same expressions as sh_basis.
+__device__ __forceinline__ double sh_term(int b, double x, double y, double z) {
+    const double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    switch (b) {
+        case 0: return 0.28209479177387814;
+        case 1: return -0.4886025119029199 * y;
+        case 2: return 0.4886025119029199 * z;
+        case 3: return -0.4886025119029199 * x;
+        case 4: return 1.0925484305920792 * xy;
+        case 5: return -1.0925484305920792 * yz;
+        case 6: return 0.31539156525252005 * (2.0 * zz - xx - yy);
+        case 7: return -1.0925484305920792 * xz;
+        case 8: return 0.5462742152960396 * (xx - yy);
+        case 9: return -0.5900435899266435 * y * (3.0 * xx - yy);
+        case 10: return 2.890611442640554 * xy * z;
+        case 11: return -0.4570457994644658 * y * (4.0 * zz - xx - yy);
+        case 12: return 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+        case 13: return -0.4570457994644658 * x * (4.0 * zz - xx - yy);
+        case 14: return 1.445305721320277 * z * (xx - yy);
+        default: return -0.5900435899266435 * x * (xx - 3.0 * yy);
+    }
+}
+
 __device__ __forceinline__ void sh_basis(double x, double y, double z, double b[16]) {
-    const double C0 = 0.28209479177387814, C1 = 0.4886025119029199;
-    const double C2_0 = 1.0925484305920792, C2_1 = -1.0925484305920792, C2_2 = 0.31539156525252005,
-                 C2_3 = -1.0925484305920792, C2_4 = 0.5462742152960396;
-    const double C3_0 = -0.5900435899266435, C3_1 = 2.890611442640554, C3_2 = -0.4570457994644658,
-                 C3_3 = 0.3731763325901154, C3_4 = -0.4570457994644658, C3_5 = 1.445305721320277,
-                 C3_6 = -0.5900435899266435;
-    double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
-    b[0] = C0;
-    b[1] = -C1 * y;
-    b[2] = C1 * z;
-    b[3] = -C1 * x;
-    b[4] = C2_0 * xy;
-    b[5] = C2_1 * yz;
-    b[6] = C2_2 * (2.0 * zz - xx - yy);
-    b[7] = C2_3 * xz;
-    b[8] = C2_4 * (xx - yy);
-    b[9] = C3_0 * y * (3.0 * xx - yy);
-    b[10] = C3_1 * xy * z;
-    b[11] = C3_2 * y * (4.0 * zz - xx - yy);
-    b[12] = C3_3 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
-    b[13] = C3_4 * x * (4.0 * zz - xx - yy);
-    b[14] = C3_5 * z * (xx - yy);
-    b[15] = C3_6 * x * (xx - 3.0 * yy);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) b[k] = sh_term(k, x, y, z);
 }
 
 // association.py:129-145
@@ -679,19 +681,26 @@ __device__ uint8_t payload_block(const FrameConst &fc, const geer_scene &sc, flo
     const double vd[3] = {-rel[0], -rel[1], -rel[2]};
     double vn = sqrt(vd[0] * vd[0] + vd[1] * vd[1] + vd[2] * vd[2]);
     const double ivn = 1.0 / (vn > 1e-12 ? vn : 1e-12);
-    double basis[16];
-    sh_basis(vd[0] * ivn, vd[1] * ivn, vd[2] * ivn, basis);
+    const double ux = vd[0] * ivn, uy = vd[1] * ivn, uz = vd[2] * ivn;
     const float *shg = ssh + (live ? lt : 0) * NB * 3;
     double rgb[3];
     uint8_t gate = 0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        double pre = 0.0;
+    // (band-outer order: each basis value dies after use; per channel the sum is still sequential in b)
+    double pre[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-        for (int b = 0; b < NB; ++b) pre += basis[b] * (double)shg[b * 3 + c];
-        pre += 0.5;
-        if (pre > 0) gate |= (uint8_t)(1u << c);
-        rgb[c] = pre > 0.0 ? pre : 0.0;
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+    {
+        const double basis_b = sh_term(b, ux, uy, uz);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pre[c] += basis_b * (double)shg[b * 3 + c];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        pre[c] += 0.5;
+        if (pre[c] > 0) gate |= (uint8_t)(1u << c);
+        rgb[c] = pre[c] > 0.0 ? pre[c] : 0.0;
     }
     // raster culling: the visual cone of the lam-ellipsoid (camera frame, full line).  With
     // P = Sigma_c^-1 = (W R_c^T)^T (W R_c^T), nu = P mu_c, a = mu_c^T nu - lam^2 > 0 (camera outside):
