@@ -656,6 +656,7 @@ int geer_association_check(geer_ctx *c, int32_t rays_per_tile, int64_t *out, int
     unsigned long long *cnt = (unsigned long long *)m;
     double *origin3 = (double *)(m + 24);
     int32_t *dmiss = max_missing ? (int32_t *)(m + 64) : nullptr;
+    if (dmiss) GEER_CUDA(cudaMemsetAsync(dmiss, 0, 8 * (size_t)max_missing, st));
     rc = launch_assoc_check(fc, c->scene, (const double *)c->medges_x.p, (const double *)c->medges_y.p,
                             (const uint8_t *)c->flags.p, (const int32_t *)c->tile_ranges.p, (const uint32_t *)c->order.p,
                             side, w, origin3, gb, hit_bits, cnt, dmiss, max_missing, st);

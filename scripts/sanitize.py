@@ -1,0 +1,22 @@
+"""Small forward + backward + loss + binning run for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2505_24053_b200 import renderer, synth  # noqa: E402
+from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene  # noqa: E402
+
+for name, n, w, h in (("C2", 3000, 160, 96), ("C5", 3000, 128, 80), ("C1", 2000, 64, 64)):
+    scene = synth.config_scene(name, n=n)
+    cam = synth.config_camera(name, width=w, height=h)
+    r = DeviceRenderer(0)
+    ds = DeviceScene.from_scene(scene)
+    color, rem, cnt = r.forward(ds, cam, renderer.RenderConfig())
+    g = r.backward(torch.ones_like(color) / color.numel())
+    torch.cuda.synchronize()
+    res = r.ctx.association_check(64)
+    print(name, float(color.sum()), int(cnt.sum()), res["missing"], flush=True)
+print("sanitize run ok")
