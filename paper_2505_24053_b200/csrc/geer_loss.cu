@@ -136,7 +136,11 @@ __global__ void __launch_bounds__(256, 3) k_ssim_fwd(const float *__restrict__ c
             const double vx = bm[2][o] - ux * ux, vy = bm[3][o] - uy * uy, vxy = bm[4][o] - ux * uy;
             const double a1 = 2.0 * ux * uy + kC1, a2 = 2.0 * vxy + kC2;
             const double b1 = ux * ux + uy * uy + kC1, b2 = vx + vy + kC2;
-            const double inv = 1.0 / (b1 * b2);  // one division: 1/b1 = b2 inv, 1/b2 = b1 inv
+            // 1 / (b1 b2) from the fp32 reciprocal and two Newton steps (relative error ~1e-15; b1, b2 > 0)
+            const double den = b1 * b2;
+            double inv = (double)__frcp_rn((float)den);
+            inv = fma(inv, fma(-den, inv, 1.0), inv);
+            inv = fma(inv, fma(-den, inv, 1.0), inv);
             const double s = a1 * a2 * inv;
             const bool reg = in_region(mask, y, x, H, W);
             float d_ux = 0.f, d_uxx = 0.f, d_uxy = 0.f;
@@ -160,7 +164,8 @@ __global__ void __launch_bounds__(256, 3) k_ssim_fwd(const float *__restrict__ c
                 nv += valid;
                 nr += reg;
             }
-            if (valid) l1 += fabs((double)color[p * 3 + ch] - (double)target[p * 3 + ch]);
+            // (staged: x = colour where the mask is set)
+            if (valid) l1 += fabs((double)xs[(r0 + o + kR) * kH + c + kR] - (double)ys[(r0 + o + kR) * kH + c + kR]);
         }
         __syncthreads();
     }
