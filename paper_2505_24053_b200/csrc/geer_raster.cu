@@ -660,6 +660,9 @@ __device__ __forceinline__ void consume_stage_fast(Smem &S, int s, int warp, int
 #pragma unroll
         for (int x = 0; x < PX; ++x) live |= ps[x].r > 0.0f;
         if (k0 > 0 && !__any_sync(0xffffffffu, live)) break;  // warp opaque
+#ifdef GEER_EXP_LANESTATS  // tuning experiment: count live lanes x entries instead of warp-entries
+        went += __popc(__ballot_sync(0xffffffffu, live)) * min(G, cnt - k0) - min(G, cnt - k0);
+#endif
         const uint32_t q = lds_u32(ib + k0);
         const uint4 adr = lds_u4(ab + 4 * k0);
         const uint32_t pa[G] = {adr.x, adr.y, adr.z, adr.w};
