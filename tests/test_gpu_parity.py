@@ -166,3 +166,19 @@ def test_binning_edge_cases_vs_oracle(camera):
     fr = renderer.render(scene, cam, cfg)
     P.assert_image_close(fr.color.color, fr.remaining_transmittance, fr.contributor_count, of.color, of.remaining,
                          of.count)
+
+
+def test_binning_many_rows_vs_oracle():
+    """More than 1024 tile rows (the row-segment scan loops) and a wide 480-tile row (lane-owned
+    counters up to 15 per lane): association bit-exact against the oracle."""
+    from paper_2505_24053_b200.scene import Camera
+
+    scene = synth.config_scene("C2", n=20_000)
+    for w, h in ((48, 8400), (3840, 40)):
+        rot, t = synth.look_at((0.0, 0.0, -2.0))
+        cam = Camera(width=w, height=h, model="beap", rotation=rot, translation=t,
+                     fov_x=np.deg2rad(180.0 * w / max(w, h)), fov_y=np.deg2rad(180.0 * h / max(w, h)))
+        og = O.build_render_graph(scene, cam, tile_px=8)
+        g = association.build_render_graph(scene, cam, tile_px=8)
+        assert og.grid.n_y > 1024 or og.grid.n_x > 400
+        P.assert_graph_equal(g, og.order, og.entry_tile, og.ranges, og.keep, og.clamped)
