@@ -85,7 +85,10 @@ struct geer_ctx {
     geer_scene scene{};
     bool have_frame = false;
     bool have_raster = false;
-    bool have_stats = false;  // a raster ran (also exhaustive forwards, which have no backward)
+    bool have_stats = false;
+    const void *iota_ptr = nullptr;  // gid_iota holds 0..iota_len-1 (buffer pointer / capacity it was written at)
+    size_t iota_cap = 0;
+    int64_t iota_len = 0;  // a raster ran (also exhaustive forwards, which have no backward)
     int64_t n_entries = 0;
     int max_items = 0;
     CUtensorMap pay_map, gpay_map;  // gather4 maps over the payload / grad payload arrays
@@ -319,7 +322,13 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[1], c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     GEER_CUDA(cudaEventRecord(c->ev_hdr, st));
     if (n > 0) {
-        launch_iota(giota, n, st);
+        // gid values 0..n-1 stay valid while the buffer is not reallocated (a growth changes its capacity)
+        if (c->iota_ptr != giota || c->iota_cap != c->gid_iota.cap || c->iota_len < n) {
+            launch_iota(giota, n, st);
+            c->iota_ptr = giota;
+            c->iota_cap = c->gid_iota.cap;
+            c->iota_len = n;
+        }
         size_t b1 = sort_depth_temp_bytes(n);
         void *tmp = ENSURE(char, c->temp, b1);
         sort_depth(tmp, b1, dkey, dkey_s, giota, gsorted, n, st);
