@@ -685,13 +685,10 @@ __device__ uint8_t payload_block(const FrameConst &fc, const geer_scene &sc, flo
     const float *shg = ssh + (live ? lt : 0) * NB * 3;
     double rgb[3];
     uint8_t gate = 0;
-#pragma unroll
     // (band-outer order: each basis value dies after use; per channel the sum is still sequential in b)
     double pre[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-    for (int b = 0; b < NB; ++b)
-#pragma unroll
-    {
+    for (int b = 0; b < NB; ++b) {
         const double basis_b = sh_term(b, ux, uy, uz);
 #pragma unroll
         for (int c = 0; c < 3; ++c) pre[c] += basis_b * (double)shg[b * 3 + c];
