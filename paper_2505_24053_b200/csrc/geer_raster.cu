@@ -638,15 +638,99 @@ __device__ __forceinline__ void eval_t0_smem(uint32_t pa, const Ray64 &R, const 
 #define GEER_FWD_GROUP 4
 #endif
 
-// Stage of mode-0 payloads (the common case): G = 4 entries' t first (independent work, explicit
-// shared loads from the addresses stage_keep listed), one warp vote for the rare fp64 cutoff
-// re-decisions, then the serial pixel updates (without the undecidable-cutoff handling unless one
-// occurred).  t is bit-identical to finish_t's (the backward recomputes it with eval_t).
+// GG mode-0 entries (shared addresses pa, alive counts jne if a pixel stops on them) against the
+// thread's pixels: the entries' t first (independent work, explicit shared loads), one warp vote for
+// the rare fp64 cutoff re-decisions, then the serial pixel updates (without the undecidable-cutoff
+// handling unless one occurred).  t is bit-identical to finish_t's (the backward recomputes it).
+template <bool kCutoff, int PX, int GG>
+__device__ __forceinline__ void fast_group(const uint32_t (&pa)[GG], const int (&jne)[GG], const Ray64 (&R)[PX],
+                                           const FrameConst &fc, PixelState (&ps)[PX], int &rechecks) {
+    float kap[GG][PX], t[GG][PX];
+    bool near[GG][PX], unc[GG][PX];
+#if GEER_COL_EARLY
+    float4 colv[GG];
+#endif
+    bool any_near = false;
+#pragma unroll
+    for (int u = 0; u < GG; ++u) {
+        const double2 a0 = lds_d2(pa[u] + 0), a1 = lds_d2(pa[u] + 16), a2 = lds_d2(pa[u] + 32);
+        const double2 b0 = lds_d2(pa[u] + 48), b1 = lds_d2(pa[u] + 64), b2 = lds_d2(pa[u] + 80);
+#if GEER_COL_EARLY
+        colv[u] = lds_f4(pa[u] + kColOff);
+        const float sw = colv[u].w;
+#else
+        const float sw = lds_f32(pa[u] + kColOff + 12);
+#endif
+#pragma unroll
+        for (int x = 0; x < PX; ++x) {
+            const Ray64 &r = R[x];
+            // (same arithmetic as norms64 mode 0)
+            const double dd = qform(a0, a1, a2, r);
+            const double mm = qform(b0, b1, b2, r);
+            kap[u][x] = __fmul_rn((float)mm, rcp_approx((float)dd));
+            float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u][x], -0.72134752044448170f)));
+            near[u][x] = false;
+            unc[u][x] = false;
+            if (kCutoff) {
+                near[u][x] = fabsf(__fsub_rn(kap[u][x], fc.lam2f)) <= fc.cutoff_tol;
+                any_near |= near[u][x];
+                uu = kap[u][x] <= fc.lam2f ? uu : 0.0f;
+            }
+            t[u][x] = fminf(uu, kMaxBlendTF);
+        }
+    }
+    bool any_unc = false;
+    if (kCutoff && __any_sync(0xffffffffu, any_near)) {
+#pragma unroll
+        for (int u = 0; u < GG; ++u) {  // (fully unrolled: the arrays stay in registers)
+#pragma unroll
+            for (int x = 0; x < PX; ++x) {
+                if (!near[u][x]) continue;
+                double dd, mm;
+                norms64_smem(pa[u], R[x], dd, mm);
+                const double k64 = mm / dd;
+                const float sw = lds_f32(pa[u] + kColOff + 12);
+                const float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u][x], -0.72134752044448170f)));
+                t[u][x] = k64 <= fc.lam2 ? fminf(uu, kMaxBlendTF) : 0.0f;
+                unc[u][x] = fabs(k64 - fc.lam2) <= (double)lds_f32(pa[u] + kExtOff);
+                any_unc |= unc[u][x];
+                ++rechecks;
+            }
+        }
+        any_unc = __any_sync(0xffffffffu, any_unc);
+    }
+    if (!any_unc) {
+#pragma unroll
+        for (int u = 0; u < GG; ++u) {
+#if GEER_COL_EARLY
+            const float4 col = colv[u];
+#else
+            const float4 col = lds_f4(pa[u] + kColOff);
+#endif
+#pragma unroll
+            for (int x = 0; x < PX; ++x) pixel_update(ps[x], kap[u][x], t[u][x], col, false, jne[u]);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < GG; ++u) {
+#if GEER_COL_EARLY
+            const float4 col = colv[u];
+#else
+            const float4 col = lds_f4(pa[u] + kColOff);
+#endif
+#pragma unroll
+            for (int x = 0; x < PX; ++x) pixel_update(ps[x], kap[u][x], t[u][x], col, unc[u][x], jne[u]);
+        }
+    }
+}
+
+// Stage of mode-0 payloads (the common case): the warp's kept entries in groups of G = 4, then the
+// last cnt % 4 one at a time (the null padding of the list is never evaluated).
 template <bool kCutoff, int PX, int G, class Smem>
 __device__ __forceinline__ void consume_stage_fast(Smem &S, int s, int warp, int cnt, int base, const Ray64 (&R)[PX],
                                                    const FrameConst &fc, PixelState (&ps)[PX], int &rechecks,
                                                    int &went) {
-    static_assert(G == 4, "entries are consumed in groups of 4 (the list padding)");
+    static_assert(G == 4, "entries are consumed in groups of 4 (one 16-B load of their addresses)");
 #ifdef GEER_EXP_NOCOMPUTE
     went += cnt;
     return;  // tuning experiment: the pipeline alone (results are wrong)
@@ -654,99 +738,35 @@ __device__ __forceinline__ void consume_stage_fast(Smem &S, int s, int warp, int
     const uint32_t ib = smem_u32(&S.idx[s][warp][0]);
     const uint32_t ab = smem_u32(&S.iadr[s][warp][0]);
     const int jbase = base + 1;
-    int k0 = 0;
-    for (; k0 < cnt; k0 += G) {
+    auto warp_live = [&]() {
         bool live = false;
 #pragma unroll
         for (int x = 0; x < PX; ++x) live |= ps[x].r > 0.0f;
-        if (k0 > 0 && !__any_sync(0xffffffffu, live)) break;  // warp opaque
-#ifdef GEER_EXP_LANESTATS  // tuning experiment: count live lanes x entries instead of warp-entries
-        went += __popc(__ballot_sync(0xffffffffu, live)) * min(G, cnt - k0) - min(G, cnt - k0);
-#endif
+        return __any_sync(0xffffffffu, live);
+    };
+    int k0 = 0;
+    for (; k0 + G <= cnt; k0 += G) {
+        if (k0 > 0 && !warp_live()) {  // warp opaque
+            went += k0;
+            return;
+        }
         const uint32_t q = lds_u32(ib + k0);
         const uint4 adr = lds_u4(ab + 4 * k0);
         const uint32_t pa[G] = {adr.x, adr.y, adr.z, adr.w};
-        float kap[G][PX], t[G][PX];
-        bool near[G][PX], unc[G][PX];
-#if GEER_COL_EARLY
-        float4 colv[G];
-#endif
-        bool any_near = false;
+        int jne[G];
 #pragma unroll
-        for (int u = 0; u < G; ++u) {
-            const double2 a0 = lds_d2(pa[u] + 0), a1 = lds_d2(pa[u] + 16), a2 = lds_d2(pa[u] + 32);
-            const double2 b0 = lds_d2(pa[u] + 48), b1 = lds_d2(pa[u] + 64), b2 = lds_d2(pa[u] + 80);
-#if GEER_COL_EARLY
-            colv[u] = lds_f4(pa[u] + kColOff);
-            const float sw = colv[u].w;
-#else
-            const float sw = lds_f32(pa[u] + kColOff + 12);
-#endif
-#pragma unroll
-            for (int x = 0; x < PX; ++x) {
-                const Ray64 &r = R[x];
-                // (same arithmetic as norms64 mode 0)
-                const double dd = qform(a0, a1, a2, r);
-                const double mm = qform(b0, b1, b2, r);
-                kap[u][x] = __fmul_rn((float)mm, rcp_approx((float)dd));
-                float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u][x], -0.72134752044448170f)));
-                near[u][x] = false;
-                unc[u][x] = false;
-                if (kCutoff) {
-                    near[u][x] = fabsf(__fsub_rn(kap[u][x], fc.lam2f)) <= fc.cutoff_tol;
-                    any_near |= near[u][x];
-                    uu = kap[u][x] <= fc.lam2f ? uu : 0.0f;
-                }
-                t[u][x] = fminf(uu, kMaxBlendTF);
-            }
-        }
-        bool any_unc = false;
-        if (kCutoff && __any_sync(0xffffffffu, any_near)) {
-#pragma unroll
-            for (int u = 0; u < G; ++u) {  // (fully unrolled: the arrays stay in registers)
-#pragma unroll
-                for (int x = 0; x < PX; ++x) {
-                    if (!near[u][x]) continue;
-                    double dd, mm;
-                    norms64_smem(pa[u], R[x], dd, mm);
-                    const double k64 = mm / dd;
-                    const float sw = lds_f32(pa[u] + kColOff + 12);
-                    const float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u][x], -0.72134752044448170f)));
-                    t[u][x] = k64 <= fc.lam2 ? fminf(uu, kMaxBlendTF) : 0.0f;
-                    unc[u][x] = fabs(k64 - fc.lam2) <= (double)lds_f32(pa[u] + kExtOff);
-                    any_unc |= unc[u][x];
-                    ++rechecks;
-                }
-            }
-            any_unc = __any_sync(0xffffffffu, any_unc);
-        }
-        if (!any_unc) {
-#pragma unroll
-            for (int u = 0; u < G; ++u) {
-#if GEER_COL_EARLY
-                const float4 col = colv[u];
-#else
-                const float4 col = lds_f4(pa[u] + kColOff);
-#endif
-                const int jne = jbase + (int)__byte_perm(q, 0u, 0x4440u + u);
-#pragma unroll
-                for (int x = 0; x < PX; ++x) pixel_update(ps[x], kap[u][x], t[u][x], col, false, jne);
-            }
-        } else {
-#pragma unroll
-            for (int u = 0; u < G; ++u) {
-#if GEER_COL_EARLY
-                const float4 col = colv[u];
-#else
-                const float4 col = lds_f4(pa[u] + kColOff);
-#endif
-                const int jne = jbase + (int)__byte_perm(q, 0u, 0x4440u + u);
-#pragma unroll
-                for (int x = 0; x < PX; ++x) pixel_update(ps[x], kap[u][x], t[u][x], col, unc[u][x], jne);
-            }
+        for (int u = 0; u < G; ++u) jne[u] = jbase + (int)__byte_perm(q, 0u, 0x4440u + u);
+        fast_group<kCutoff, PX, G>(pa, jne, R, fc, ps, rechecks);
+    }
+    if (k0 < cnt && (k0 == 0 || warp_live())) {
+        const uint32_t q = lds_u32(ib + k0);  // (k0 is a multiple of 4)
+        for (int u = 0; k0 < cnt; ++k0, ++u) {
+            const uint32_t pa[1] = {lds_u32(ab + 4 * k0)};
+            const int jne[1] = {jbase + (int)__byte_perm(q, 0u, 0x4440u + u)};
+            fast_group<kCutoff, PX, 1>(pa, jne, R, fc, ps, rechecks);
         }
     }
-    went += k0 < cnt ? k0 : cnt;
+    went += k0;
 }
 
 // Camera-frame mirror coordinates of a world ray (the CSF/PBF space of association.py:91-126):
