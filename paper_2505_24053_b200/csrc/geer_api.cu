@@ -107,7 +107,7 @@ struct geer_ctx {
     Buf payload, gpayload, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, ranges_ax, flags, mu_c,
         depth;
     // per-entry buffers
-    Buf order, tile_ranges;
+    Buf order, tile_ranges, wcull;
     Buf bin_m1, bin_p1, bin_rows, bin_rowstart, bin_segoff, bin_m2, bin_p2;
     // per-pixel buffers
     Buf color, remaining, count_px, n_eval, dl32, fixup;
@@ -255,6 +255,9 @@ int camera_setup(geer_ctx *c, bool want_pixel_tile, cudaStream_t st) {
     void *tmp = ENSURE(char, c->temp, sb);
     exclusive_scan_i32(tmp, sb, icnt, ioff, fc.n_tiles, st);
     launch_item_fill(fc.n_tiles, tile_off, ioff, items, nit, st);
+    float4 *wc = ENSURE(float4, c->wcull, (size_t)c->max_items * 16);  // 8 warps x (patch, cone) per item
+    launch_warp_cull(fc, c->max_items, items, nit, (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p,
+                     (const double2 *)c->row_sc.p, (const double *)c->dir64.p, wc, st);
     return GEER_OK;
 }
 
@@ -354,7 +357,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
             int32_t *fix = ENSURE(int32_t, c->fixup, npx);
             launch_forward(fc, sc, c->max_items, (const int4 *)c->items.p, nwork, (const int32_t *)c->pix_list.p,
                            (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p, (const double *)c->dir64.p,
-                           r2, (const uint32_t *)gsorted, payload, c->pay_map, flags, color, remaining, count, ne,
+                           r2, (const uint32_t *)gsorted, payload, c->pay_map, (const float4 *)c->wcull.p, color, remaining, count, ne,
                            c->d_counters, fix, st);
             c->have_stats = true;
         }
@@ -393,7 +396,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         int32_t *fix = ENSURE(int32_t, c->fixup, npx);
         launch_forward(fc, sc, c->max_items, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
                        (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
-                       (const double *)c->dir64.p, ranges, (const uint32_t *)c->order.p, payload, c->pay_map, flags, color, remaining, count, ne,
+                       (const double *)c->dir64.p, ranges, (const uint32_t *)c->order.p, payload, c->pay_map, (const float4 *)c->wcull.p, color, remaining, count, ne,
                        c->d_counters, fix, st);
         c->fwd_remaining = remaining;
         c->have_raster = c->have_stats = true;
@@ -422,7 +425,7 @@ int run_backward(geer_ctx *c, const float *dl_dimage, bool f64_out, void *const 
     launch_backward(fc, sc, c->max_items, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
                     (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
                     (const double *)c->dir64.p, (const int32_t *)c->tile_ranges.p, (const uint32_t *)c->order.p,
-                    c->pay_map, c->gpay_map, (const uint8_t *)c->flags.p,
+                    c->pay_map, c->gpay_map, (const float4 *)c->wcull.p,
                     c->fwd_remaining, (const int32_t *)c->n_eval.p,
                     dl_dimage, accum, st);
     if (f64_out)
@@ -537,7 +540,7 @@ void geer_destroy(geer_ctx *c) {
                    &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->work, &c->n_work, &c->payload, &c->gpayload,
                    &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted, &c->count,
                    &c->ranges_ax, &c->flags, &c->mu_c, &c->depth,
-                   &c->order, &c->tile_ranges,
+                   &c->order, &c->tile_ranges, &c->wcull,
                    &c->bin_m1, &c->bin_p1, &c->bin_rows, &c->bin_rowstart, &c->bin_segoff, &c->bin_m2, &c->bin_p2, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,
                    &c->accum, &c->temp, &c->h64_means, &c->h64_log, &c->h64_quats, &c->h64_op, &c->h64_sh,
                    &c->s32_means, &c->s32_log, &c->s32_quats, &c->s32_op, &c->s32_sh, &c->out64, &c->g64};

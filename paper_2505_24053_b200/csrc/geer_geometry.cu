@@ -258,7 +258,7 @@ __global__ void k_item_fill(int n_tiles, const int32_t *tile_off, const int32_t 
         int c = tile_off[t + 1] - tile_off[t];
         int k0 = item_off[t];
         for (int k = 0; k * kRasterThreads < c; ++k)
-            items[k0 + k] = make_int4(t, tile_off[t] + k * kRasterThreads, min(kRasterThreads, c - k * kRasterThreads), 0);
+            items[k0 + k] = make_int4(t, tile_off[t] + k * kRasterThreads, min(kRasterThreads, c - k * kRasterThreads), k0 + k);
         if (t == n_tiles - 1) *n_items = item_off[t] + (c + kRasterThreads - 1) / kRasterThreads;
     }
 }

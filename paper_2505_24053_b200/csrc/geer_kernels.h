@@ -59,15 +59,19 @@ void order_items(const int4 *items, const int32_t *n_items, const int32_t *range
                  int32_t *n_work, cudaStream_t st);
 
 // geer_raster.cu (fp32 raster forward / backward)
+// per-warp culling regions of every work item, cached with the camera (wcull: 2 float4 per warp)
+void launch_warp_cull(const FrameConst &fc, int max_items, const int4 *items, const int32_t *n_items,
+                      const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc, const double *dir64,
+                      float4 *wcull, cudaStream_t st);
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    const CUtensorMap &pay_map, const uint8_t *flags, float *color, float *remaining, int32_t *count, int32_t *n_eval,
+                    const CUtensorMap &pay_map, const float4 *wcull, float *color, float *remaining, int32_t *count, int32_t *n_eval,
                     unsigned long long *counters, int32_t *fixup_list, cudaStream_t st);
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                      const double *dir64, const int32_t *ranges, const uint32_t *order, const CUtensorMap &pay_map,
-                     const CUtensorMap &gpay_map, const uint8_t *flags,
+                     const CUtensorMap &gpay_map, const float4 *wcull,
                      const float *remaining,
                      const int32_t *n_eval, const float *dl_dimage, float *accum, cudaStream_t st);
 int launch_assoc_check(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,

@@ -848,6 +848,31 @@ __device__ __forceinline__ float4 warp_patch(bool valid, float4 b) {
     return b;
 }
 
+// Per-warp culling regions of every raster work item (PBF patch in mirror space, ray cone), cached
+// with the camera: wcull[(item * kConsumerWarps + warp) * 2 + {0, 1}] = patch, cone — exactly what
+// the raster warps would compute from their pixels (one pixel per lane).
+template <bool kBEAP>
+__global__ void __launch_bounds__(kRasterThreads) k_warp_cull(FrameConst fc, const int4 *__restrict__ items,
+                                                              const int32_t *__restrict__ n_items,
+                                                              const int32_t *__restrict__ pix_list,
+                                                              const double2 *__restrict__ col_sc,
+                                                              const double2 *__restrict__ row_sc,
+                                                              const double *__restrict__ dir64, float4 *__restrict__ wcull) {
+    if ((int)blockIdx.x >= n_items[0]) return;
+    const int4 it = items[blockIdx.x];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool valid = tid < it.z;
+    const int p = valid ? pix_list[it.y + tid] : 0;
+    double d64[3] = {0.0, 0.0, 1.0};
+    if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
+    const float4 patch = warp_patch(valid, ray_mirror_bounds(fc, d64));
+    const float4 cone = warp_cone1(fc, valid, d64);
+    if (lane == 0) {
+        wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 0] = patch;
+        wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 1] = cone;
+    }
+}
+
 #ifdef GEER_CTA_TIMING
 // Tuning instrumentation (build with -DGEER_CTA_TIMING): per raster CTA start / end %globaltimer
 // (ns), SM id and warp-entries, read back by geer_debug_cta_times (scripts/cta_timing.py).
@@ -881,7 +906,7 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
               const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
               const double2 *__restrict__ row_sc, const double *__restrict__ dir64, const int32_t *__restrict__ ranges,
               const uint32_t *__restrict__ order, const __grid_constant__ CUtensorMap pay_map,
-              const uint8_t *__restrict__ flags, float *__restrict__ color,
+              const float4 *__restrict__ wcull, float *__restrict__ color,
               float *__restrict__ remaining, int32_t *__restrict__ count, int32_t *__restrict__ n_eval,
               unsigned long long *__restrict__ counters, int32_t *__restrict__ fixup_list) {
     constexpr int PX = kFwdPX, NW = kFwdNW, NT = 32 * kFwdNW;
@@ -938,12 +963,18 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
         d64[x][2] = 1.0;
         if (valid[x]) {
             pixel_ray<kBEAP>(fc, p[x], col_sc, row_sc, dir64, d64[x]);
-            bnd = bounds_union(bnd, ray_mirror_bounds(fc, d64[x]));
+            if (PX != 1) bnd = bounds_union(bnd, ray_mirror_bounds(fc, d64[x]));
             any_valid = true;
         }
     }
-    const float4 my_patch = warp_patch(any_valid, bnd);
-    const float4 my_cone = warp_cone<PX>(fc, valid, d64);
+    float4 my_patch, my_cone;
+    if (PX == 1) {  // cached with the camera (k_warp_cull: the same computation)
+        my_patch = wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 0];
+        my_cone = wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 1];
+    } else {
+        my_patch = warp_patch(any_valid, bnd);
+        my_cone = warp_cone<PX>(fc, valid, d64);
+    }
 #ifdef GEER_CTA_TIMING
     if (tid == 0 && blockIdx.x < (1u << 16)) g_cta_ts[blockIdx.x] = gtimer();
 #endif
@@ -1202,7 +1233,7 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                const double2 *__restrict__ row_sc, const double *__restrict__ dir64,
                const int32_t *__restrict__ ranges, const uint32_t *__restrict__ order,
                const __grid_constant__ CUtensorMap pay_map, const __grid_constant__ CUtensorMap gpay_map,
-               const uint8_t *__restrict__ flags, const float *__restrict__ remaining,
+               const float4 *__restrict__ wcull, const float *__restrict__ remaining,
                const int32_t *__restrict__ n_eval,
                const float *__restrict__ dl_dimage, float *__restrict__ accum) {
     extern __shared__ __align__(128) unsigned char dsmem[];
@@ -1233,8 +1264,8 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
     // the producer streams while the consumers set up their pixels
     double d64[3] = {0.0, 0.0, 1.0};
     if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
-    const float4 my_patch = warp_patch(valid, ray_mirror_bounds(fc, d64));
-    const float4 my_cone = warp_cone1(fc, valid, d64);
+    const float4 my_patch = wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 0];  // (k_warp_cull, cached)
+    const float4 my_cone = wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 1];
     const Ray64 R = make_ray(d64);
     if (valid) {
         sray[tid][0] = d64[0];
@@ -1435,19 +1466,19 @@ static void raster_smem_optin() {
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    const CUtensorMap &pay_map, const uint8_t *flags, float *color, float *remaining, int32_t *count,
+                    const CUtensorMap &pay_map, const float4 *wcull, float *color, float *remaining, int32_t *count,
                     int32_t *n_eval, unsigned long long *counters, int32_t *fixup_list, cudaStream_t st) {
     if (max_items <= 0) return;
     raster_smem_optin();
     if (fc.model == GEER_BEAP) {
         k_forward<true><<<max_items, kFwdThreads, sizeof(FwdSmem) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                            ranges, order, pay_map, flags, color, remaining, count,
+                                                            ranges, order, pay_map, wcull, color, remaining, count,
                                                             n_eval, counters, fixup_list);
         k_fixup<true><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                counters, fixup_list, color, remaining, count, n_eval);
     } else {
         k_forward<false><<<max_items, kFwdThreads, sizeof(FwdSmem) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                             ranges, order, pay_map, flags, color, remaining, count,
+                                                             ranges, order, pay_map, wcull, color, remaining, count,
                                                              n_eval, counters, fixup_list);
         k_fixup<false><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                 counters, fixup_list, color, remaining, count, n_eval);
@@ -1457,18 +1488,28 @@ void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, c
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                      const double *dir64, const int32_t *ranges, const uint32_t *order, const CUtensorMap &pay_map,
-                     const CUtensorMap &gpay_map, const uint8_t *flags, const float *remaining,
+                     const CUtensorMap &gpay_map, const float4 *wcull, const float *remaining,
                      const int32_t *n_eval, const float *dl_dimage, float *accum, cudaStream_t st) {
     if (max_items <= 0) return;
     raster_smem_optin();
     if (fc.model == GEER_BEAP)
         k_backward<true><<<max_items, kPipeThreads, sizeof(PipeSmem<true>) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                             ranges, order, pay_map, gpay_map, flags, remaining,
+                                                             ranges, order, pay_map, gpay_map, wcull, remaining,
                                                              n_eval, dl_dimage, accum);
     else
         k_backward<false><<<max_items, kPipeThreads, sizeof(PipeSmem<true>) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                              ranges, order, pay_map, gpay_map, flags, remaining,
+                                                              ranges, order, pay_map, gpay_map, wcull, remaining,
                                                               n_eval, dl_dimage, accum);
+}
+
+void launch_warp_cull(const FrameConst &fc, int max_items, const int4 *items, const int32_t *n_items,
+                      const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc, const double *dir64,
+                      float4 *wcull, cudaStream_t st) {
+    if (max_items <= 0) return;
+    if (fc.model == GEER_BEAP)
+        k_warp_cull<true><<<max_items, kRasterThreads, 0, st>>>(fc, items, n_items, pix_list, col_sc, row_sc, dir64, wcull);
+    else
+        k_warp_cull<false><<<max_items, kRasterThreads, 0, st>>>(fc, items, n_items, pix_list, col_sc, row_sc, dir64, wcull);
 }
 
 void launch_sum_i32(const int32_t *v, int64_t n, unsigned long long *out, cudaStream_t st) {
