@@ -1220,9 +1220,6 @@ __device__ __forceinline__ float warp_transpose_reduce16(float v[16], int lane) 
 // entries (index < n_eval) from the last to the first, recovering
 // T_i = T_{i+1} / (1 - t_i) from the forward's final remaining, and the warp
 // adds its 16 per-entry partials to the Gaussian's accumulators.
-#ifndef GEER_BWD_GROUP
-#define GEER_BWD_GROUP 1  // entries evaluated together in the backward (mode-0 stages; 2 and 4 measured slower)
-#endif
 #ifndef BWD_MIN_BLOCKS
 #define BWD_MIN_BLOCKS 3
 #endif
@@ -1296,21 +1293,23 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
             uint32_t msk;
             stage_keep(S, s, warp, lane, n, fc.cull != 0, my_patch, my_cone, msk);
             if (wmax - lo < 32) msk &= (1u << (wmax - lo)) - 1u;
+            const uint32_t rb = smem_u32(&S.ring[s][0][0]), gb = smem_u32(&S.gring[s][0][0]);
             // one entry's gradient: T and suffix update, 16 partials, warp reduction, accumulators
+            // (payload and grad payload read at their shared addresses)
             auto entry = [&](const int jj, const PairT &e) {
                 const int i = lo + jj;
+                // t = 0 (or not alive) on every lane: T, the suffix and all 16 partials are unchanged
+                if (!__any_sync(0xffffffffu, i < ne && e.t > 0.0f)) return;
                 float v[16];
 #pragma unroll
                 for (int k = 0; k < 16; ++k) v[k] = 0.f;
-                const Payload &P = ring_at(S, s, jj);
-                // t = 0 (or not alive) on every lane: T, the suffix and all 16 partials are unchanged
-                if (!__any_sync(0xffffffffu, i < ne && e.t > 0.0f)) return;
                 if (i < ne) {
                     const float omt = __fsub_rn(1.0f, e.t);
                     const float inv = rcp_approx(omt);  // 1 - t >= 0.001: ~1 ulp
                     T = T * inv;                        // T_i = T_{i+1} / (1 - t_i)
                     const float w = T * e.t;
-                    const float c0 = P.col.x, c1 = P.col.y, c2 = P.col.z;
+                    const float4 col = lds_f4(rb + ring_off(jj) + kColOff);
+                    const float c0 = col.x, c1 = col.y, c2 = col.z;
                     // renderer.py:284-287
                     const float dcdt0 = T * c0 - (s0 + bgt0) * inv;
                     const float dcdt1 = T * c1 - (s1 + bgt1) * inv;
@@ -1324,11 +1323,12 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                     v[15] = w * gl2;
                     if (e.t > 0.0f && e.u < kMaxBlendTF) {  // renderer.py:289-290 gate
                         // canonical ray (fp32): d_u = W d, m = o_u x d_u (renderer.py:96-99)
-                        const GradPayload &G = gring_at(S, s, jj);
-                        const float du0 = G.r0.x * dx + G.r0.y * dy + G.r0.z * dz;
-                        const float du1 = G.r1.x * dx + G.r1.y * dy + G.r1.z * dz;
-                        const float du2 = G.r2.x * dx + G.r2.y * dy + G.r2.z * dz;
-                        const float o0 = G.r0.w, o1 = G.r1.w, o2 = G.r2.w;
+                        const uint32_t ga = gb + (uint32_t)((jj >> 2) * kGringGroupBytes + (jj & 3) * (int)sizeof(GradPayload));
+                        const float4 G0 = lds_f4(ga), G1 = lds_f4(ga + 16), G2 = lds_f4(ga + 32);
+                        const float du0 = G0.x * dx + G0.y * dy + G0.z * dz;
+                        const float du1 = G1.x * dx + G1.y * dy + G1.z * dz;
+                        const float du2 = G2.x * dx + G2.y * dy + G2.z * dz;
+                        const float o0 = G0.w, o1 = G1.w, o2 = G2.w;
                         const float m0 = o1 * du2 - o2 * du1, m1 = o2 * du0 - o0 * du2, m2 = o0 * du1 - o1 * du0;
                         v[12] = dl_dt * e.alpha;
                         const float dk = -0.5f * dl_dt * e.u;
@@ -1367,8 +1367,7 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
 #endif
             };
             // a mode-1 (cross-product) payload anywhere in the stage selects the generic evaluation;
-            // otherwise GEER_BWD_GROUP entries are evaluated together (independent fp64 work), then their
-            // gradients are formed in order (back to front)
+            // otherwise the shared-address evaluation (entries back to front)
             if (__any_sync(0xffffffffu, lane < n && ring_at(S, s, lane).col.w < 0.0f)) {
                 while (msk) {
                     const int jj = 31 - __clz(msk);
@@ -1378,20 +1377,12 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                     entry(jj, e);
                 }
             } else {
-                const uint32_t rb = smem_u32(&S.ring[s][0][0]);
                 while (msk) {
-                    int jv[GEER_BWD_GROUP];
-                    PairT ev[GEER_BWD_GROUP];
-#pragma unroll
-                    for (int u = 0; u < GEER_BWD_GROUP; ++u) {
-                        jv[u] = msk ? 31 - __clz(msk) : -1;
-                        if (msk) msk &= ~(1u << jv[u]);
-                        // (a missing slot evaluates the null entry: t = 0)
-                        eval_t0_smem(rb + ring_off(jv[u] >= 0 ? jv[u] : kStageEntries), R, fc, ev[u]);
-                    }
-#pragma unroll
-                    for (int u = 0; u < GEER_BWD_GROUP; ++u)
-                        if (jv[u] >= 0) entry(jv[u], ev[u]);
+                    const int jj = 31 - __clz(msk);
+                    msk &= ~(1u << jj);
+                    PairT e;
+                    eval_t0_smem(rb + ring_off(jj), R, fc, e);
+                    entry(jj, e);
                 }
             }
         }
