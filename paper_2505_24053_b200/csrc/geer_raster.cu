@@ -725,7 +725,7 @@ __device__ __forceinline__ void fast_group(const uint32_t (&pa)[GG], const int (
 }
 
 // Stage of mode-0 payloads (the common case): the warp's kept entries in groups of G = 4, then the
-// last cnt % 4 one at a time (the null padding of the list is never evaluated).
+// last cnt % 4 as a pair and/or a single (the null padding of the list is never evaluated).
 template <bool kCutoff, int PX, int G, class Smem>
 __device__ __forceinline__ void consume_stage_fast(Smem &S, int s, int warp, int cnt, int base, const Ray64 (&R)[PX],
                                                    const FrameConst &fc, PixelState (&ps)[PX], int &rechecks,
@@ -760,10 +760,18 @@ __device__ __forceinline__ void consume_stage_fast(Smem &S, int s, int warp, int
     }
     if (k0 < cnt && (k0 == 0 || warp_live())) {
         const uint32_t q = lds_u32(ib + k0);  // (k0 is a multiple of 4)
-        for (int u = 0; k0 < cnt; ++k0, ++u) {
+        if (cnt - k0 >= 2) {  // a pair, then possibly one more
+            const uint2 adr = make_uint2(lds_u32(ab + 4 * k0), lds_u32(ab + 4 * k0 + 4));
+            const uint32_t pa[2] = {adr.x, adr.y};
+            const int jne[2] = {jbase + (int)__byte_perm(q, 0u, 0x4440u), jbase + (int)__byte_perm(q, 0u, 0x4441u)};
+            fast_group<kCutoff, PX, 2>(pa, jne, R, fc, ps, rechecks);
+            k0 += 2;
+        }
+        if (k0 < cnt) {
             const uint32_t pa[1] = {lds_u32(ab + 4 * k0)};
-            const int jne[1] = {jbase + (int)__byte_perm(q, 0u, 0x4440u + u)};
+            const int jne[1] = {jbase + (int)__byte_perm(q, 0u, 0x4440u + (k0 & 3))};
             fast_group<kCutoff, PX, 1>(pa, jne, R, fc, ps, rechecks);
+            ++k0;
         }
     }
     went += k0;
