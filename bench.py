@@ -436,7 +436,7 @@ def run_ours(args):
 
             trainer = MultiViewTrainer.for_config4(scene, n_views=args.train_views, rank=rank, world=world,
                                                    device=local, inflight=max(1, args.inflight))
-            trainer.step()
+            loss_first = trainer.step(compute_loss=True)  # (untimed warm-up step; loss before any update)
             torch.cuda.synchronize()
             kt = max(2, min(args.steps, 5))
             barrier(world)
@@ -448,9 +448,12 @@ def run_ours(args):
             t1.record()
             torch.cuda.synchronize()
             tms = allreduce_max(t0.elapsed_time(t1), world) / kt
+            loss_after = trainer.step(compute_loss=True)  # (untimed: the loss after 1 + kt Adam steps)
             extra["train_step"] = {"views": args.train_views, "ms_per_step": tms, "views_in_flight": trainer.inflight,
                                    "views_per_s": args.train_views / (tms / 1e3),
-                                   "allreduce_bytes": trainer.grad_numel * 4, "loss": trainer.last_loss}
+                                   "allreduce_bytes": trainer.grad_numel * 4,
+                                   "loss_first_step": loss_first, "loss_after_steps": loss_after,
+                                   "loss_note": "sum over this rank's views of trainer.loss (trainer.py:114-155)"}
         except Exception as exc:
             extra["train_step"] = {"error": repr(exc)}
 
