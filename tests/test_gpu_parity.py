@@ -6,6 +6,8 @@ to the full 1M-Gaussian 1080p config are compared with the fp64 C oracle,
 which is itself pinned to the reference by tests/test_oracle_golden.py.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -111,6 +113,22 @@ def test_full_c2_association_and_forward_vs_oracle():
     rep = P.assert_image_close(fr.color.color, fr.remaining_transmittance, fr.contributor_count, of.color,
                                of.remaining, of.count)
     print("C2 image parity", rep, "entries", len(g.order))
+
+
+def test_full_c5_association_and_forward_vs_oracle():
+    """BASELINE config 5 at full size (6M Gaussians, 3840x2160 equidistant KB fisheye): bit-exact graph
+    (23.7M entries), image within tolerance, exact contributor counts."""
+    O.set_num_threads(os.cpu_count())
+    scene = synth.config_scene("C5")
+    cam = synth.config_camera("C5")
+    og = O.build_render_graph(scene, cam)
+    g = association.build_render_graph(scene, cam)
+    P.assert_graph_equal(g, og.order, og.entry_tile, og.ranges, og.keep, og.clamped)
+    of = O.render(scene, cam, None, graph=og)
+    fr = renderer.render(scene, cam, renderer.RenderConfig())
+    rep = P.assert_image_close(fr.color.color, fr.remaining_transmittance, fr.contributor_count, of.color,
+                               of.remaining, of.count)
+    print("C5 image parity", rep, "entries", len(g.order))
 
 
 def test_full_c3_backward_vs_oracle():
