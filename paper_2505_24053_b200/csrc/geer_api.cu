@@ -1,11 +1,12 @@
 // geer_api.cu — the extern "C" boundary (include/geer.h) and the per-frame driver.
 //
 // Frame pipeline on one stream (stage names follow SPEC.md:575,602):
-//   prep : K0 camera setup + K1 per-Gaussian preprocess
-//   dup  : depth-order sort of Gaussians, count scan, one 12-byte D2H
-//          (entry total + error flag), load-balanced emit
-//   sort : tile radix sort + per-tile ranges
-//   render: K5 raster
+//   prep : K0 camera setup (cached per camera: ray tables, tile CSR, work items, per-warp culling
+//          regions) + K1 per-Gaussian preprocess (exact fp64 association half + raster payload half)
+//   dup  : depth-order sort of the Gaussians (queued before the host reads the 12-byte header:
+//          entry total + error flag)
+//   sort : per-tile lists by two-level stable bucketing (geer_bin.cu) + the raster work order
+//   render: K5 raster + fp64 fix-up of borderline pixels
 // The backward (K6 + K7) reuses the forward's graph, payload and per-pixel
 // (n_eval, remaining) state held in the context.
 #include <cuda.h>

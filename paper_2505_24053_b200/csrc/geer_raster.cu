@@ -1,23 +1,23 @@
 // geer_raster.cu — K5 forward raster and K6 reverse-order backward raster.
 //
-// One CTA of 256 threads per raster work item (a tile, or a <=256-pixel chunk
-// of an oversized non-BEAP tile); one pixel per thread.  The tile's depth-
-// sorted entries are staged into shared memory in batches with cp.async
-// (double-buffered in the forward) and every thread walks them front to back:
+// One CTA per raster work item (a tile, or a <=256-pixel chunk of an oversized non-BEAP tile): a
+// producer warp streams the tile's depth-sorted payload rows into a 4-stage shared-memory ring with
+// TMA gather4 copies completed on mbarriers, and 8 consumer warps (one pixel per lane, an 8x4 patch
+// per warp) cull each stage against their patch, then walk the kept entries front to back:
 //
-//   d_u = W d, m = o_u x d_u, kappa = |m|^2/|d_u|^2          (core.py:184-199)
+//   |d_u|^2, |m|^2 from the payload's fp64 quadratic forms (or d_u = W d, m = o_u x d_u),
+//   kappa = |m|^2/|d_u|^2                                     (core.py:184-199)
 //   u = sigma exp(-kappa/2) [kappa <= lam^2], t = min(u, 0.999) (renderer.py:96-105)
 //   C += rem t c; rem *= 1 - t; count += t > 0; stop when rem < 1e-4 (renderer.py:107-118)
 //
-// The per-pair math is written with explicit __f*_rn intrinsics so the
-// forward and backward kernels evaluate bit-identical t values (the backward
-// recovers T_i = T_{i+1} / (1 - t_i) exactly as the forward multiplied).
-// Pairs whose fp32 kappa lies within the per-Gaussian error band of lam^2 are
-// re-decided in fp64, so the support cutoff matches the fp64
-// reference.  The backward (renderer.py:259-310) walks each pixel's alive
-// entries back to front, forms the 16 per-(pixel, Gaussian) partials,
-// warp-reduces them with a shuffle transpose, CTA-reduces them in shared
-// memory and issues one vector atomic per 4 partials per entry.
+// The per-pair math is written with explicit __f*_rn intrinsics so the forward and backward kernels
+// evaluate bit-identical t values (the backward recovers T_i = T_{i+1} / (1 - t_i) exactly as the
+// forward multiplied).  Pairs whose fp32 kappa lies within the error band of lam^2 are re-decided in
+// fp64, and pixels whose stop test is too close to call are recomposited in fp64 by
+// k_fixup, so cutoff decisions and contributor counts match the fp64 reference.  The backward
+// (renderer.py:259-310) streams each tile's alive prefix back to front, forms the 16
+// per-(pixel, Gaussian) partials, warp-reduces them with a shuffle transpose and issues one fp32
+// atomic per (entry, partial).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
