@@ -1219,9 +1219,6 @@ __device__ __forceinline__ float warp_transpose_reduce16(float v[16], int lane) 
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-#ifndef GEER_BWD_SMEM_REDUCE
-#define GEER_BWD_SMEM_REDUCE 0
-#endif
 
 // Reverse-order backward (renderer.py:259-310).  The producer streams the
 // tile's first max_n entries back to front; each lane walks its pixel's alive
@@ -1244,9 +1241,6 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
     extern __shared__ __align__(128) unsigned char dsmem[];
     PipeSmem<true> &S = *reinterpret_cast<PipeSmem<true> *>(dsmem);
     __shared__ double sray[kRasterThreads][3];
-#if GEER_BWD_SMEM_REDUCE
-    __shared__ float sred[kConsumerWarps][32 * 17];  // per-warp reduction scratch
-#endif
     __shared__ int smax;
     if ((int)blockIdx.x >= n_items[0]) return;  // tiles without entries have no gradient
     const int4 it = items[blockIdx.x];
@@ -1354,25 +1348,9 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                         v[6] = dd2 * dx; v[7] = dd2 * dy; v[8] = dd2 * dz;
                     }
                 }
-#if GEER_BWD_SMEM_REDUCE
-                // warp sum of the 16 partials through shared memory (stride 17: conflict-free both
-                // ways): lane L sums partial L % 16 over 16 pixels, the two halves meet by one shuffle
-                float *red = sred[warp];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) red[lane * 17 + k] = v[k];
-                __syncwarp();
-                float tot = 0.f;
-                const int h16 = (lane >> 4) * 16, kk = lane & 15;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) tot += red[(h16 + i) * 17 + kk];
-                tot += __shfl_xor_sync(0xffffffffu, tot, 16);
-                __syncwarp();
-                if (lane < 16 && tot != 0.0f) atomicAdd(accum + (int64_t)S.gid[s][jj] * 16 + lane, tot);
-#else
                 const float tot = warp_transpose_reduce16(v, lane);
                 if ((lane & 1) == 0 && tot != 0.0f)
                     atomicAdd(accum + (int64_t)S.gid[s][jj] * 16 + (lane >> 1), tot);
-#endif
             };
             // a mode-1 (cross-product) payload anywhere in the stage selects the generic evaluation;
             // otherwise the shared-address evaluation (entries back to front)
