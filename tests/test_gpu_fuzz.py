@@ -79,3 +79,33 @@ def test_random_case_vs_oracle(seed, large):
     ob = O.render_backward(scene, cam, dl, cfg, graph=og)
     gr = renderer.render_backward(scene, cam, dl, cfg)
     P.assert_grads_close(gr, vars(ob))
+
+
+@pytest.mark.parametrize("w,h,model,tile", [(1, 1, "beap", 16), (1, 7, "beap", 8), (7, 1, "kb", 16),
+                                            (3, 2, "pinhole", 32), (33, 1, "beap", 32), (1, 65, "pinhole", 16)])
+def test_degenerate_images_vs_oracle(w, h, model, tile):
+    """1-pixel rows / columns and single-pixel images through the whole path."""
+    rng = np.random.default_rng(w * 100 + h)
+    scene = synth.to_f32_values(synth.random_scene(400, rng, spread=1.0, sh_bands=4))
+    rot, t = synth.look_at((0.3, -0.2, -2.5))
+    if model == "beap":
+        cam = Camera(width=w, height=h, model="beap", rotation=rot, translation=t, fov_x=np.deg2rad(90.0),
+                     fov_y=np.deg2rad(60.0))
+    elif model == "kb":
+        cam = Camera(width=w, height=h, model="kb", rotation=rot, translation=t, fx=4.0, fy=4.0, cx=(w - 1) / 2,
+                     cy=(h - 1) / 2, k=np.zeros(4))
+    else:
+        cam = Camera(width=w, height=h, model="pinhole", rotation=rot, translation=t, fx=30.0, fy=30.0, cx=w / 2,
+                     cy=h / 2)
+    cfg = renderer.RenderConfig(tile_px=tile)
+    og = O.build_render_graph(scene, cam, cfg.lam, cfg.tile_px)
+    g = association.build_render_graph(scene, cam, cfg.lam, cfg.tile_px)
+    P.assert_graph_equal(g, og.order, og.entry_tile, og.ranges, og.keep, og.clamped)
+    of = O.render(scene, cam, cfg, graph=og)
+    fr = renderer.render(scene, cam, cfg)
+    P.assert_image_close(fr.color.color, fr.remaining_transmittance, fr.contributor_count, of.color, of.remaining,
+                         of.count)
+    dl = rng.standard_normal((h, w, 3))
+    ob = O.render_backward(scene, cam, dl, cfg, graph=og)
+    gr = renderer.render_backward(scene, cam, dl, cfg)
+    P.assert_grads_close(gr, vars(ob))
