@@ -388,6 +388,32 @@ def run_ours(args):
     r.set_timing(False)
     extra["fwd_bwd_ms_per_view"] = fb_ms
     extra["backward_ms"] = bst["ms_backward"]
+    # the same fwd+bwd with views in flight (one view per context/stream, as in the training step)
+    fb_grads = [grads] + [dscene.zeros_like_grads() for _ in range(nf - 1)]
+
+    def fb_view(j):
+        with torch.cuda.stream(streams[j]):
+            rs[j].forward(dscene, cam, cfg, out=outs[j])
+            rs[j].backward(dl, grads=fb_grads[j])
+
+    for j in range(nf):
+        fb_view(j)
+    torch.cuda.synchronize()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for s_ in streams[1:]:
+        s_.wait_event(f0)
+    for i in range(kfb):
+        fb_view(i % nf)
+    for s_ in streams[1:]:
+        e_ = torch.cuda.Event()
+        e_.record(s_)
+        stream.wait_event(e_)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    extra["fwd_bwd_ms_per_view_inflight"] = allreduce_max(f0.elapsed_time(f1), world) / kfb
+    extra["views_in_flight"] = nf
     stages["backward"] = {"ms": bst["ms_backward"], "bound": "fp32", "unit": "TFLOP/s",
                           "achieved": pairs * SURVEY_K6_FLOPS_PER_PAIR / (bst["ms_backward"] * 1e-3) / 1e12,
                           "peak": fp32_peak}
