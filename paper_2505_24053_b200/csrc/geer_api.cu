@@ -100,7 +100,7 @@ struct geer_ctx {
     float ms[6] = {};
     unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs, [2] fix-up pixels, [3] warp-entries, [4] streamed entries, [5] graph entries (K1)
     int *d_err = nullptr;
-    int64_t *h_hdr = nullptr;  // pinned: [0] total entries, [1] error code
+    int64_t *h_hdr = nullptr;  // pinned: [0] total entries, [1] error code, [2] (Gaussian, tile row) pairs
     // camera buffers
     Buf col_sc, row_sc, medges_x, medges_y, edges_x, edges_y, dir64, theta, phi, minmax, pixel_tile, pixel_tile_sorted,
         pix_iota, pix_list, tile_count, tile_off, item_count, item_off, items, n_items, work, n_work;
@@ -282,7 +282,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     c->have_raster = false;
     c->have_stats = false;
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
-    GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 6 * sizeof(unsigned long long), st));
+    GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 7 * sizeof(unsigned long long), st));
     GEER_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
     if (!camera_cached(c, want_export)) {
         c->cam_valid = false;
@@ -324,6 +324,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     int64_t total = 0;
     GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[0], c->d_counters + 5, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[1], c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[2], c->d_counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     GEER_CUDA(cudaEventRecord(c->ev_hdr, st));
     if (n > 0) {
         // gid values 0..n-1 stay valid while the buffer is not reallocated (a growth changes its capacity)
@@ -371,7 +372,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     c->n_entries = total;
     // ---- sort: per-tile lists (stable in depth order) and their ranges, then the raster work order
     {
-        const BinPlan bp = bin_plan(n, fc.n_x, fc.n_y, total);
+        const BinPlan bp = bin_plan(n, fc.n_x, fc.n_y, total, c->h_hdr[2]);
         uint32_t *m1 = ENSURE(uint32_t, c->bin_m1, bp.m1_len + 1);
         uint32_t *p1 = ENSURE(uint32_t, c->bin_p1, bp.m1_len + 1);
         uint2 *rows = ENSURE(uint2, c->bin_rows, bp.rows_cap + 1);
@@ -521,9 +522,9 @@ geer_ctx *geer_create(int device) {
     bool ok = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) == cudaSuccess;
     for (int i = 0; i < 6 && ok; ++i) ok = cudaEventCreate(&c->ev[i]) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_hdr, cudaEventDisableTiming) == cudaSuccess;
-    ok = ok && cudaMalloc(&c->d_counters, 6 * sizeof(unsigned long long)) == cudaSuccess;
+    ok = ok && cudaMalloc(&c->d_counters, 7 * sizeof(unsigned long long)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->d_err, sizeof(int)) == cudaSuccess;
-    ok = ok && cudaMallocHost(&c->h_hdr, 2 * sizeof(int64_t)) == cudaSuccess;
+    ok = ok && cudaMallocHost(&c->h_hdr, 3 * sizeof(int64_t)) == cudaSuccess;
     if (!ok) {
         fail(GEER_ERR_CUDA, "context creation failed: %s", cudaGetErrorString(cudaGetLastError()));
         geer_destroy(c);

@@ -298,12 +298,13 @@ __global__ void __launch_bounds__(kWalkWarps * 32) k_tiles_scatter(const uint2 *
 
 }  // namespace
 
-BinPlan bin_plan(int64_t n, int n_x, int n_y, int64_t n_entries) {
+BinPlan bin_plan(int64_t n, int n_x, int n_y, int64_t n_entries, int64_t n_rows) {
     BinPlan p;
     p.nch = (int)((n + kBinChunk - 1) / kBinChunk);
     p.m1_len = (int64_t)n_y * p.nch;
-    p.rows_cap = n_entries;  // every (Gaussian, row) pair holds >= 1 entry
-    p.seg_cap = (n_entries + kSegLen - 1) / kSegLen + n_y;
+    // (Gaussian, tile row) pairs, summed by K1 (each holds >= 1 entry, so n_entries bounds it too)
+    p.rows_cap = n_rows > 0 && n_rows <= n_entries ? n_rows : n_entries;
+    p.seg_cap = (p.rows_cap + kSegLen - 1) / kSegLen + n_y;
     p.m2_len = (int64_t)n_x * p.seg_cap;
     size_t b1 = 0, b2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, b1, (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)lmax(p.m1_len, 1));

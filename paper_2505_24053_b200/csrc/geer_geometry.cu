@@ -794,11 +794,22 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS)
         flags[g0 + threadIdx.x] = sfl[0][threadIdx.x];
         flags[sc.n + g0 + threadIdx.x] = sfl[1][threadIdx.x];
     }
-    if (threadIdx.x < 32) {  // the block's entries, for the frame total (one atomic per block)
-        unsigned long long t = 0;
-        for (int i = threadIdx.x; i < cnt_b; i += 32) t += (unsigned long long)count[g0 + i];
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x < 32) {  // the block's entries and (Gaussian, tile row) pairs, for the frame totals
+        unsigned long long t = 0, rows = 0;
+        for (int i = threadIdx.x; i < cnt_b; i += 32) {
+            const int64_t c = count[g0 + i];
+            t += (unsigned long long)c;
+            if (c > 0) {
+                const AxisRanges &a = ranges[g0 + i];
+                for (int k = 0; k < 3; ++k) rows += (a.y[k] >> 16) - (a.y[k] & 0xFFFFu);
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            t += __shfl_xor_sync(0xffffffffu, t, o);
+            rows += __shfl_xor_sync(0xffffffffu, rows, o);
+        }
         if (threadIdx.x == 0 && t) atomicAdd(total_entries, t);
+        if (threadIdx.x == 0 && rows) atomicAdd(total_entries + 1, rows);  // (the next counter)
     }
     // coalesced write-out of the block's payload rows (head + culling record) and grad payloads
     const float4 *sp = reinterpret_cast<const float4 *>(ssh);

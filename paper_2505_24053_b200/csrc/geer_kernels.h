@@ -48,7 +48,7 @@ struct BinPlan {
     int64_t m1_len, rows_cap, seg_cap, m2_len;  // [row][chunk] counts, row-bin capacity, segments, [row][tile][seg]
     size_t temp_bytes;                          // CUB scan workspace
 };
-BinPlan bin_plan(int64_t n, int n_x, int n_y, int64_t n_entries);
+BinPlan bin_plan(int64_t n, int n_x, int n_y, int64_t n_entries, int64_t n_rows);
 int bin_tiles(const BinPlan &p, const int32_t *gsorted, const AxisRanges *ar, int64_t n, int n_x, int n_y,
               int64_t n_entries, uint32_t *m1, uint32_t *p1, uint2 *rowbin, int32_t *rowstart, int32_t *seg_off,
               uint32_t *m2, uint32_t *p2, void *temp, uint32_t *order, int32_t *ranges, cudaStream_t st);
