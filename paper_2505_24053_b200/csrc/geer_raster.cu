@@ -924,7 +924,7 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
     // n_items: [0] items with entries (work[0, n0)), [1] empty items (work[max_items - n1, max_items))
     const int n_full = n_items[0];
     if ((int)blockIdx.x >= n_full + n_items[1]) return;
-    const int4 it = items[(int)blockIdx.x < n_full ? blockIdx.x : gridDim.x - 1 - (blockIdx.x - n_full)];
+    const int4 it = items[(int)blockIdx.x < n_full ? (int)blockIdx.x : n_full + n_items[1] - 1 - ((int)blockIdx.x - n_full)];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if ((int)blockIdx.x >= n_full) {  // tile without entries: background only (renderer.py:118)
         for (int q = tid; q < it.z; q += blockDim.x) {

@@ -75,7 +75,7 @@ __global__ void k_order_items(const int4 *__restrict__ items, const int32_t *__r
     be = __shfl_sync(0xffffffffu, be, 0);
     const unsigned lt = (1u << lane) - 1u;
     if (in && full) work[bf + __popc(mf & lt)] = it;
-    if (in && !full) work[max_items - 1 - (be + __popc(me & lt))] = it;
+    if (in && !full) work[*n_items - 1 - (be + __popc(me & lt))] = it;  // empty items: the tail of [0, n_items)
 }
 
 void order_items(const int4 *items, const int32_t *n_items, const int32_t *ranges, int max_items, int4 *work,
