@@ -1349,8 +1349,14 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                     }
                 }
                 const float tot = warp_transpose_reduce16(v, lane);
-                if ((lane & 1) == 0 && tot != 0.0f)
-                    atomicAdd(accum + (int64_t)S.gid[s][jj] * 16 + (lane >> 1), tot);
+                // lane 2k adds partial k (predicated fire-and-forget reduction, no branch)
+                float *dst = accum + (int64_t)S.gid[s][jj] * 16 + (lane >> 1);
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "setp.ne.u32 p, %2, 0;\n\t"
+                    "@p red.global.add.f32 [%0], %1;\n\t}" ::"l"(dst),
+                    "f"(tot), "r"((int)((lane & 1) == 0 && tot != 0.0f))
+                    : "memory");
             };
             // a mode-1 (cross-product) payload anywhere in the stage selects the generic evaluation;
             // otherwise the shared-address evaluation (entries back to front)
