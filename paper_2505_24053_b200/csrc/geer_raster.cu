@@ -439,6 +439,38 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
     for (int f = b - 1; f >= 0 && f >= oldest; --f) mbar_wait(&S.full[f % kStages], (f / kStages) & 1);
 }
 
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double2 lds_d2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+
+constexpr uint32_t kColOff = 96;  // offsetof(Payload, col)
+constexpr uint32_t kExtOff = 112; // offsetof(Payload, ext)
+constexpr uint32_t kCullOff = 128;  // offsetof(Payload, cull)
+static_assert(offsetof(Payload, col) == kColOff && offsetof(Payload, ext) == kExtOff &&
+              offsetof(Payload, cull) == kCullOff, "payload layout");
+
 // Per-warp culling of one stage (run by the consumer warp itself, one entry per lane): an entry is
 // kept unless its PBF hull misses the warp's mirror-space patch or its visual cone misses the warp's
 // ray cone (both conservative: a dropped entry has kappa > lam^2, i.e. t = 0, on every pixel of the
@@ -446,16 +478,18 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
 // the kept mask.
 template <class Smem>
 __device__ __forceinline__ int stage_keep(Smem &S, int s, int warp, int lane, int n, bool cull, const float4 &patch,
-                                          const float4 &pcone, uint32_t &m) {
+                                          const float4 &pcone, uint32_t &m, bool &any_m1) {
+    const uint32_t rb = smem_u32(&S.ring[s][0][0]);
+    const uint32_t pa = rb + ring_off(lane);  // this lane's entry of the stage
     bool ov = lane < n;
+    // a mode-1 (cross-product) payload anywhere in the stage selects the generic evaluation
+    any_m1 = __any_sync(0xffffffffu, ov && lds_f32(pa + kColOff + 12) < 0.0f);
     if (cull && ov) {
-        const Cull &C = ring_at(S, s, lane).cull;
-        const float4 bx = C.box;
-        ov = !(bx.y < patch.x || bx.x > patch.y || bx.w < patch.z || bx.z > patch.w) && !cone_misses(C.k0, C.k1, pcone);
+        const float4 bx = lds_f4(pa + kCullOff), k0 = lds_f4(pa + kCullOff + 16), k1 = lds_f4(pa + kCullOff + 32);
+        ov = !(bx.y < patch.x || bx.x > patch.y || bx.w < patch.z || bx.z > patch.w) && !cone_misses(k0, k1, pcone);
     }
     m = __ballot_sync(0xffffffffu, ov);
     const int c = __popc(m);
-    const uint32_t rb = smem_u32(&S.ring[s][0][0]);
     if (ov) {
         const int pos = __popc(m & ((1u << lane) - 1u));
         S.idx[s][warp][pos] = (uint8_t)lane;
@@ -539,32 +573,6 @@ __device__ __forceinline__ bool pixel_border(const PixelState &ps) {
     return ps.border || (ps.r == 0.0f && ps.efin >= 0.0f && __fadd_rn(ps.rfin, ps.efin) >= 0.99999e-4f);
 }
 
-__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ float lds_f32(uint32_t a) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ double2 lds_d2(uint32_t a) {
-    double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ float4 lds_f4(uint32_t a) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
-    return v;
-}
-
 // Mode-0 norms from a payload at shared address pa (same arithmetic as norms64).
 __device__ __forceinline__ void norms64_smem(uint32_t pa, const Ray64 &R, double &dd, double &mm) {
     const double2 a0 = lds_d2(pa + 0), a1 = lds_d2(pa + 16), a2 = lds_d2(pa + 32);
@@ -573,8 +581,6 @@ __device__ __forceinline__ void norms64_smem(uint32_t pa, const Ray64 &R, double
     mm = qform(b0, b1, b2, R);
 }
 
-constexpr uint32_t kColOff = 96;  // offsetof(Payload, col)
-constexpr uint32_t kExtOff = 112; // offsetof(Payload, ext)
 
 // The entries of one stage that this warp's culling keeps, front to back, a few at a time (the list
 // is padded with null entries, which are exact no-ops).  Culled entries change nothing; the alive
@@ -1012,9 +1018,9 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
         if (n == 0) break;
         if (warp_live) {
             uint32_t m;
-            const int cnt = stage_keep(S, s, warp, lane, n, fc.cull != 0, my_patch, my_cone, m);
-            // a mode-1 (cross-product) payload anywhere in the stage selects the generic path
-            if (__any_sync(0xffffffffu, lane < n && ring_at(S, s, lane).col.w < 0.0f))
+            bool any_m1;
+            const int cnt = stage_keep(S, s, warp, lane, n, fc.cull != 0, my_patch, my_cone, m, any_m1);
+            if (any_m1)  // a mode-1 (cross-product) payload in the stage: the generic path
                 consume_stage_generic<PX>(S, s, warp, cnt, base, R, dray, fc, ps, rechecks, went);
             else if (fc.cutoff)
                 consume_stage_fast<true, PX, GEER_FWD_GROUP>(S, s, warp, cnt, base, R, fc, ps, rechecks, went);
@@ -1293,7 +1299,8 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
         if (lo < wmax) {  // some lane of this warp has alive entries in the stage
             // entries the culling keeps (culled ones have t = 0: no gradient, T unchanged), below wmax
             uint32_t msk;
-            stage_keep(S, s, warp, lane, n, fc.cull != 0, my_patch, my_cone, msk);
+            bool any_m1;
+            stage_keep(S, s, warp, lane, n, fc.cull != 0, my_patch, my_cone, msk, any_m1);
             if (wmax - lo < 32) msk &= (1u << (wmax - lo)) - 1u;
             const uint32_t rb = smem_u32(&S.ring[s][0][0]), gb = smem_u32(&S.gring[s][0][0]);
             // one entry's gradient: T and suffix update, 16 partials, warp reduction, accumulators
@@ -1360,7 +1367,7 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
             };
             // a mode-1 (cross-product) payload anywhere in the stage selects the generic evaluation;
             // otherwise the shared-address evaluation (entries back to front)
-            if (__any_sync(0xffffffffu, lane < n && ring_at(S, s, lane).col.w < 0.0f)) {
+            if (any_m1) {
                 while (msk) {
                     const int jj = 31 - __clz(msk);
                     msk &= ~(1u << jj);
