@@ -307,7 +307,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     uint32_t *dkey_s = ENSURE(uint32_t, c->depth_key_sorted, n);
     int32_t *giota = ENSURE(int32_t, c->gid_iota, n);
     int32_t *gsorted = ENSURE(int32_t, c->gid_sorted, n);
-    int64_t *cnt = ENSURE(int64_t, c->count, n);
+    int64_t *cnt = nullptr;  // (entry counts stay in K1's shared memory)
     AxisRanges *ar = ENSURE(AxisRanges, c->ranges_ax, n);
     uint8_t *flags = ENSURE(uint8_t, c->flags, 2 * n);  // [0, n): association bits, [n, 2n): payload bits
     double *mu = nullptr, *dep = nullptr;

@@ -514,7 +514,7 @@ __device__ __forceinline__ void named_barrier(int id, int count) {
 // K1a: exact fp64 association of one Gaussian (association.py:82-88, 148-224, 343-350, 373-451).
 // sex / sey: the mirror tile edges in shared memory.  Returns the keep / clamped flag bits.
 __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, const double *sex, const double *sey,
-                                 int64_t g, uint32_t *__restrict__ depth_key, int64_t *__restrict__ count,
+                                 int64_t g, uint32_t *__restrict__ depth_key, int64_t &count,
                                  AxisRanges *__restrict__ ranges, Cull &cr,
                                  double *__restrict__ mu_out, double *__restrict__ depth_out, int *__restrict__ err) {
 
@@ -620,7 +620,7 @@ __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, con
             }
         }
     }
-    count[g] = n_ent;
+    count = n_ent;
     ranges[g] = ar;
     cr.box = bx;  // (the visual-cone part of the record is written by the payload half)
     // association.py:335-340 key bits (depth > 0): f32 bits | 0x80000000; non-emitting last
@@ -765,6 +765,7 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS)
     __shared__ __align__(16) float ssh[128 * (NB * 3 > kStageFloats ? NB * 3 : kStageFloats)];
     __shared__ Cull scull[128];
     __shared__ uint8_t sfl[2][128];
+    __shared__ int64_t scount[128];  // entries per Gaussian (for the block's totals)
     const int64_t g0 = (int64_t)blockIdx.x * 128;
     const int cnt_b = (int)lmin(128, sc.n - g0);
     const int lt = threadIdx.x & 127;
@@ -775,13 +776,15 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS)
         for (int i = lt; i <= fc.n_y; i += 128) sey[i] = medges_y[i];
         named_barrier(1, 128);
 #ifdef GEER_EXP_NO_ASSOC
-        if (lt < cnt_b) count[g0 + lt] = 0;
+        scount[lt] = 0;
         sfl[0][lt] = 0;
         if (false)
 #endif
-        sfl[0][lt] = lt < cnt_b ? associate_one(fc, sc, sex, sey, g0 + lt, depth_key, count, ranges, scull[lt],
+        int64_t ne = 0;
+        sfl[0][lt] = lt < cnt_b ? associate_one(fc, sc, sex, sey, g0 + lt, depth_key, ne, ranges, scull[lt],
                                                 mu_out, depth_out, err)
                                 : 0;
+        scount[lt] = ne;
     } else {
 #ifndef GEER_EXP_NO_PAYLOAD
         sfl[1][lt] = payload_block<NB>(fc, sc, ssh, scull, g0, cnt_b, lt);
@@ -797,7 +800,7 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS)
     if (threadIdx.x < 32) {  // the block's entries and (Gaussian, tile row) pairs, for the frame totals
         unsigned long long t = 0, rows = 0;
         for (int i = threadIdx.x; i < cnt_b; i += 32) {
-            const int64_t c = count[g0 + i];
+            const int64_t c = scount[i];
             t += (unsigned long long)c;
             if (c > 0) {
                 const AxisRanges &a = ranges[g0 + i];
