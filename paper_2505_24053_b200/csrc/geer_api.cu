@@ -107,7 +107,7 @@ struct geer_ctx {
     Buf col_sc, row_sc, medges_x, medges_y, edges_x, edges_y, dir64, theta, phi, minmax, pixel_tile, pixel_tile_sorted,
         pix_iota, pix_list, tile_count, tile_off, item_count, item_off, items, n_items, work, n_work;
     // per-Gaussian buffers
-    Buf payload, gpayload, depth_key, depth_key_sorted, gid_iota, gid_sorted, count, ranges_ax, flags, mu_c,
+    Buf payload, gpayload, depth_key, depth_key_sorted, gid_iota, gid_sorted, ranges_ax, flags, mu_c,
         depth;
     // per-entry buffers
     Buf order, tile_ranges, wcull;
@@ -307,7 +307,6 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     uint32_t *dkey_s = ENSURE(uint32_t, c->depth_key_sorted, n);
     int32_t *giota = ENSURE(int32_t, c->gid_iota, n);
     int32_t *gsorted = ENSURE(int32_t, c->gid_sorted, n);
-    int64_t *cnt = nullptr;  // (entry counts stay in K1's shared memory)
     AxisRanges *ar = ENSURE(AxisRanges, c->ranges_ax, n);
     uint8_t *flags = ENSURE(uint8_t, c->flags, 2 * n);  // [0, n): association bits, [n, 2n): payload bits
     double *mu = nullptr, *dep = nullptr;
@@ -320,7 +319,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     if (rc) return rc;
     rc = make_row_map(&c->gpay_map, gpayload, n, (int)sizeof(GradPayload));
     if (rc) return rc;
-    launch_preprocess(fc, sc, (const double *)c->medges_x.p, (const double *)c->medges_y.p, payload, gpayload, dkey, cnt, ar,
+    launch_preprocess(fc, sc, (const double *)c->medges_x.p, (const double *)c->medges_y.p, payload, gpayload, dkey, ar,
                       flags, mu, dep, c->d_err, c->d_counters + 5, st);
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[1], st));
 
@@ -547,7 +546,7 @@ void geer_destroy(geer_ctx *c) {
     Buf *bufs[] = {&c->col_sc, &c->row_sc, &c->medges_x, &c->medges_y, &c->edges_x, &c->edges_y, &c->dir64,
                    &c->theta, &c->phi, &c->minmax, &c->pixel_tile, &c->pixel_tile_sorted, &c->pix_iota, &c->pix_list,
                    &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->work, &c->n_work, &c->payload, &c->gpayload,
-                   &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted, &c->count,
+                   &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted,
                    &c->ranges_ax, &c->flags, &c->mu_c, &c->depth,
                    &c->order, &c->tile_ranges, &c->wcull,
                    &c->bin_m1, &c->bin_p1, &c->bin_rows, &c->bin_rowstart, &c->bin_segoff, &c->bin_m2, &c->bin_p2, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,

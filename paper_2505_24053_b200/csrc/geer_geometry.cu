@@ -757,7 +757,7 @@ template <int NB>
 __global__ void __launch_bounds__(256, K1_MIN_BLOCKS)
     k_preprocess(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x, const double *__restrict__ medges_y,
                  Payload *__restrict__ payload, GradPayload *__restrict__ gpayload, uint32_t *__restrict__ depth_key,
-                 int64_t *__restrict__ count, AxisRanges *__restrict__ ranges, uint8_t *__restrict__ flags,
+                 AxisRanges *__restrict__ ranges, uint8_t *__restrict__ flags,
                  double *__restrict__ mu_out, double *__restrict__ depth_out, int *__restrict__ err,
                  unsigned long long *__restrict__ total_entries) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -976,7 +976,7 @@ void launch_item_fill(int n_tiles, const int32_t *tile_off, const int32_t *item_
 size_t preprocess_smem(const FrameConst &fc) { return sizeof(double) * (fc.n_x + fc.n_y + 2); }
 
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
-                       Payload *payload, GradPayload *gpayload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges,
+                       Payload *payload, GradPayload *gpayload, uint32_t *depth_key, AxisRanges *ranges,
                        uint8_t *flags, double *mu_out, double *depth_out, int *err,
                        unsigned long long *total_entries, cudaStream_t st) {
     if (sc.n == 0) return;
@@ -985,7 +985,7 @@ void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double 
 #define GEER_NB_CASE(NB)                                                                                            \
     case NB:                                                                                                        \
         k_preprocess<NB><<<blocks, 256, preprocess_smem(fc), st>>>(fc, sc, medges_x, medges_y, payload, gpayload,   \
-                                                                   depth_key, count, ranges, flags,                \
+                                                                   depth_key, ranges, flags,                       \
                                                                    mu_out, depth_out, err, total_entries);         \
         break;
         GEER_NB_CASE(1) GEER_NB_CASE(2) GEER_NB_CASE(3) GEER_NB_CASE(4) GEER_NB_CASE(5) GEER_NB_CASE(6)

@@ -24,7 +24,7 @@ void launch_item_fill(int n_tiles, const int32_t *tile_off, const int32_t *item_
                       cudaStream_t st);
 size_t preprocess_smem(const FrameConst &fc);
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
-                       Payload *payload, GradPayload *gpayload, uint32_t *depth_key, int64_t *count, AxisRanges *ranges, uint8_t *flags,
+                       Payload *payload, GradPayload *gpayload, uint32_t *depth_key, AxisRanges *ranges, uint8_t *flags,
                        double *mu_out, double *depth_out, int *err, unsigned long long *total_entries,
                        cudaStream_t st);
 template <typename T>
