@@ -528,10 +528,6 @@ __device__ __forceinline__ void pipe_drop_out(Smem &S, int s, unsigned phase) {
 
 // ------------------------------------------------------------------------------ K5
 
-#ifndef GEER_ERR_COMPACT
-#define GEER_ERR_COMPACT 1  // one-expression error bound (also charges r 1.2e-7 for t = 0 entries)
-#endif
-
 // Forward pixel state with a running bound on |rem_fp32 - rem_fp64| (err): the alive test of
 // renderer.py:113 is decided against rem64 in [rem - err, rem + err]; a pixel whose test (or a
 // cutoff decision) is too close to call is stopped and redone in fp64 by k_fixup.
@@ -562,12 +558,7 @@ __device__ __forceinline__ void pixel_update(PixelState &ps, float kap, float t,
     ps.cg = __fmaf_rn(w, col.y, ps.cg);
     ps.cb = __fmaf_rn(w, col.z, ps.cb);
     // |d r'| <= |d r| (1 - t) + r |d t| + rounding (none when t = 0),  |d t| <= t * t_rel_bound
-#if GEER_ERR_COMPACT
-    // r (t b(kappa) + 1.2e-7) = w b + r 1.2e-7: the same bound, also charged (needlessly) when t = 0
-    ps.err = __fmaf_rn(ps.err, omt, __fmul_rn(ps.r, __fmaf_rn(t, t_rel_bound(kap), 1.2e-7f)));
-#else
     ps.err = __fmaf_rn(ps.err, omt, __fmaf_rn(w, t_rel_bound(kap), w > 0.0f ? __fmul_rn(ps.r, 1.2e-7f) : 0.0f));
-#endif
     ps.cnt += w > 0.0f ? 1 : 0;
     ps.r = __fmul_rn(ps.r, omt);
     const bool stop = (ps.r > 0.0f) & (__fsub_rn(ps.r, ps.err) < 1.00001e-4f);
