@@ -27,6 +27,7 @@ CASES = {
     # name: (config, n, width, height, RenderConfig kwargs)
     "c2_100k_beap": ("C2", 100_000, 480, 270, {}),
     "c2_1m_beap": ("C2", 1_000_000, 960, 540, {}),
+    "c2_full_1080p": ("C2", 1_000_000, 1920, 1080, {}),  # BASELINE config 2 itself (~9e11 pairs, ~2.5 s)
     "c2_200k_beap_lam2_tile8": ("C2", 200_000, 640, 360, {"lam": 2.0, "tile_px": 8}),
     "c5_200k_kb": ("C5", 200_000, 960, 540, {}),
     "c1_10k_pinhole": ("C1", 10_000, 256, 256, {"background": np.array([0.1, 0.2, 0.3])}),
