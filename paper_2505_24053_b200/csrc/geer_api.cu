@@ -87,7 +87,6 @@ struct geer_ctx {
     bool have_frame = false;
     bool have_raster = false;
     bool have_stats = false;
-    int n_items_host = 0;  // raster work items of the cached camera
     const void *iota_ptr = nullptr;  // gid_iota holds 0..iota_len-1 (buffer pointer / capacity it was written at)
     size_t iota_cap = 0;
     int64_t iota_len = 0;  // a raster ran (also exhaustive forwards, which have no backward)
@@ -101,8 +100,7 @@ struct geer_ctx {
     float ms[6] = {};
     unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs, [2] fix-up pixels, [3] warp-entries, [4] streamed entries, [5] graph entries (K1)
     int *d_err = nullptr;
-    int64_t *h_hdr = nullptr;  // pinned: [0] total entries, [1] error code, [2] (Gaussian, tile row) pairs,
-                               // [3] work items of the camera (little-endian int32 in the low half)
+    int64_t *h_hdr = nullptr;  // pinned: [0] total entries, [1] error code, [2] (Gaussian, tile row) pairs
     // camera buffers
     Buf col_sc, row_sc, medges_x, medges_y, edges_x, edges_y, dir64, theta, phi, minmax, pixel_tile, pixel_tile_sorted,
         pix_iota, pix_list, tile_count, tile_off, item_count, item_off, items, n_items, work, n_work;
@@ -261,11 +259,6 @@ int camera_setup(geer_ctx *c, bool want_pixel_tile, cudaStream_t st) {
     float4 *wc = ENSURE(float4, c->wcull, (size_t)c->max_items * 16);  // 8 warps x (patch, cone) per item
     launch_warp_cull(fc, c->max_items, items, nit, (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p,
                      (const double2 *)c->row_sc.p, (const double *)c->dir64.p, wc, st);
-    // the raster grids are sized to the exact item count (read once per camera)
-    c->h_hdr[3] = 0;
-    GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[3], nit, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    GEER_CUDA(cudaStreamSynchronize(st));
-    c->n_items_host = (int)c->h_hdr[3];
     return GEER_OK;
 }
 
@@ -363,7 +356,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         if (color) {
             int32_t *ne = ENSURE(int32_t, c->n_eval, npx);
             int32_t *fix = ENSURE(int32_t, c->fixup, npx);
-            launch_forward(fc, sc, c->n_items_host, (const int4 *)c->items.p, nwork, (const int32_t *)c->pix_list.p,
+            launch_forward(fc, sc, c->max_items, (const int4 *)c->items.p, nwork, (const int32_t *)c->pix_list.p,
                            (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p, (const double *)c->dir64.p,
                            r2, (const uint32_t *)gsorted, payload, c->pay_map, (const float4 *)c->wcull.p, color, remaining, count, ne,
                            c->d_counters, fix, st);
@@ -402,7 +395,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     if (color) {
         int32_t *ne = ENSURE(int32_t, c->n_eval, npx);
         int32_t *fix = ENSURE(int32_t, c->fixup, npx);
-        launch_forward(fc, sc, c->n_items_host, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
+        launch_forward(fc, sc, c->max_items, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
                        (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
                        (const double *)c->dir64.p, ranges, (const uint32_t *)c->order.p, payload, c->pay_map, (const float4 *)c->wcull.p, color, remaining, count, ne,
                        c->d_counters, fix, st);
@@ -430,7 +423,7 @@ int run_backward(geer_ctx *c, const float *dl_dimage, bool f64_out, void *const 
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
     float *accum = ENSURE(float, c->accum, sc.n * 16);
     if (sc.n > 0) GEER_CUDA(cudaMemsetAsync(accum, 0, sizeof(float) * 16 * sc.n, st));
-    launch_backward(fc, sc, c->n_items_host, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
+    launch_backward(fc, sc, c->max_items, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
                     (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
                     (const double *)c->dir64.p, (const int32_t *)c->tile_ranges.p, (const uint32_t *)c->order.p,
                     c->pay_map, c->gpay_map, (const float4 *)c->wcull.p,
@@ -530,7 +523,7 @@ geer_ctx *geer_create(int device) {
     ok = ok && cudaEventCreateWithFlags(&c->ev_hdr, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaMalloc(&c->d_counters, 7 * sizeof(unsigned long long)) == cudaSuccess;
     ok = ok && cudaMalloc(&c->d_err, sizeof(int)) == cudaSuccess;
-    ok = ok && cudaMallocHost(&c->h_hdr, 4 * sizeof(int64_t)) == cudaSuccess;
+    ok = ok && cudaMallocHost(&c->h_hdr, 3 * sizeof(int64_t)) == cudaSuccess;
     if (!ok) {
         fail(GEER_ERR_CUDA, "context creation failed: %s", cudaGetErrorString(cudaGetLastError()));
         geer_destroy(c);

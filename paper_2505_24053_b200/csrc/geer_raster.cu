@@ -863,8 +863,10 @@ __device__ __forceinline__ float4 warp_patch(bool valid, float4 b) {
 }
 
 // Per-warp culling regions of every raster work item (PBF patch in mirror space, ray cone), cached
-// with the camera: wcull[(item * kConsumerWarps + warp) * 2 + {0, 1}] = patch, cone — exactly what
-// the raster warps would compute from their pixels (one pixel per lane).
+// with the camera: wcull[(item * kConsumerWarps + warp) * 2 + {0, 1}] = patch, cone.  Computed in
+// fp32 from the camera-frame pixel rays and widened outward far beyond fp32 rounding (1e-5 in
+// mirror units, 2 % of sin^2 of the cone): a larger region only keeps more t = 0 entries, so the
+// culling stays exact.
 template <bool kBEAP>
 __global__ void __launch_bounds__(kRasterThreads) k_warp_cull(FrameConst fc, const int4 *__restrict__ items,
                                                               const int32_t *__restrict__ n_items,
@@ -876,11 +878,54 @@ __global__ void __launch_bounds__(kRasterThreads) k_warp_cull(FrameConst fc, con
     const int4 it = items[blockIdx.x];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool valid = tid < it.z;
-    const int p = valid ? pix_list[it.y + tid] : 0;
-    double d64[3] = {0.0, 0.0, 1.0};
-    if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
-    const float4 patch = warp_patch(valid, ray_mirror_bounds(fc, d64));
-    const float4 cone = warp_cone1(fc, valid, d64);
+    float c[3] = {0.f, 0.f, 1.f};  // camera-frame ray
+    if (valid) {
+        const int p = pix_list[it.y + tid];
+        if (kBEAP) {  // camera.py:141-155 angles_to_dir
+            const double2 cs = col_sc[p % fc.width], rs = row_sc[p / fc.width];
+            const float x = (float)cs.x * (float)rs.y, y = (float)cs.y * (float)rs.x, z = (float)cs.y * (float)rs.y;
+            const float inv = rsqrtf(x * x + y * y + z * z);
+            c[0] = x * inv;
+            c[1] = y * inv;
+            c[2] = z * inv;
+        } else {
+            const double *d = dir64 + (int64_t)p * 3;
+            for (int i = 0; i < 3; ++i)
+                c[i] = (float)(fc.R[i * 3 + 0] * d[0] + fc.R[i * 3 + 1] * d[1] + fc.R[i * 3 + 2] * d[2]);
+        }
+    }
+    // PBF patch: mirror coordinates m = tan(angle / 2) of the (x, z) and (y, z) projections
+    float4 b = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
+    if (c[2] > 1e-3f) {
+        const float mx = c[0] / (sqrtf(c[0] * c[0] + c[2] * c[2]) + c[2]);
+        const float my = c[1] / (sqrtf(c[1] * c[1] + c[2] * c[2]) + c[2]);
+        b = make_float4(mx - 1e-5f, mx + 1e-5f, my - 1e-5f, my + 1e-5f);
+    }
+    const float4 patch = warp_patch(valid, b);
+    // ray cone: axis = normalised sum of the rays, sin^2(beta) = max |axis x ray|^2
+    float sx = valid ? c[0] : 0.f, sy = valid ? c[1] : 0.f, sz = valid ? c[2] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        sz += __shfl_xor_sync(0xffffffffu, sz, o);
+    }
+    const float nrm2 = sx * sx + sy * sy + sz * sz;
+    float sin2 = 0.f;
+    if (valid && nrm2 > 0.f) {
+        const float inv = rsqrtf(nrm2);
+        const float ax = sx * inv, ay = sy * inv, az = sz * inv;
+        const float x0 = ay * c[2] - az * c[1], x1 = az * c[0] - ax * c[2], x2 = ax * c[1] - ay * c[0];
+        sin2 = (x0 * x0 + x1 * x1 + x2 * x2) / (c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sin2 = fmaxf(sin2, __shfl_xor_sync(0xffffffffu, sin2, o));
+    sin2 = fmaf(sin2, 1.02f, 1e-7f);
+    float4 cone = make_float4(0.f, 0.f, 1.f, 0.f);  // cos^2 = 0 disables the test (beta > 45 deg)
+    if (nrm2 > 0.f && sin2 < 0.5f) {
+        const float inv = rsqrtf(nrm2);
+        cone = make_float4(sx * inv, sy * inv, sz * inv, 1.0f - sin2);
+    }
     if (lane == 0) {
         wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 0] = patch;
         wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 1] = cone;
