@@ -19,6 +19,7 @@
 
 #include <cmath>
 #include <string>
+#include <utility>
 
 #include "geer_common.cuh"
 #include "geer_kernels.h"
@@ -75,6 +76,24 @@ int make_row_map(CUtensorMap *map, const void *base, int64_t rows, int row_bytes
 
 }  // namespace
 
+// One cached camera setup (K0 outputs): the context swaps its camera buffers with a slot, so a
+// context rendering a recurring set of views (the multi-view training step) sets each camera up once.
+constexpr int kCamSlots = 16;
+constexpr int64_t kCamSlotMaxPixels = 4 << 20;  // larger cameras are not kept (memory)
+#define GEER_CAM_BUFS(X)                                                                                    \
+    X(col_sc) X(row_sc) X(medges_x) X(medges_y) X(edges_x) X(edges_y) X(dir64) X(theta) X(phi) X(minmax)  \
+    X(pixel_tile) X(pixel_tile_sorted) X(pix_iota) X(pix_list) X(tile_count) X(tile_off) X(item_count)      \
+    X(item_off) X(items) X(n_items) X(wcull)
+struct CamSlot {
+#define GEER_DECL(b) Buf b;
+    GEER_CAM_BUFS(GEER_DECL)
+#undef GEER_DECL
+    bool valid = false, pixel_tile_ok = false;
+    FrameConst fc{};
+    int max_items = 0;
+    uint64_t last_use = 0;
+};
+
 struct geer_ctx {
     int device = 0;
     cudaStream_t own_stream = nullptr;
@@ -96,6 +115,8 @@ struct geer_ctx {
     // K0 cache: the camera setup depends only on the camera and the tile size
     bool cam_valid = false, cam_pixel_tile = false;
     FrameConst cam_fc{};
+    CamSlot cam_slots[kCamSlots];
+    uint64_t cam_clock = 0;
     const float *fwd_remaining = nullptr;  // remaining written by the last forward (backward input)
     float ms[6] = {};
     unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs, [2] fix-up pixels, [3] warp-entries, [4] streamed entries, [5] graph entries (K1)
@@ -264,11 +285,50 @@ int camera_setup(geer_ctx *c, bool want_pixel_tile, cudaStream_t st) {
 
 // Whether the K0 outputs in the context are those of this frame's camera (same model, size, tiling,
 // pose and intrinsics, compared bit for bit).
-bool camera_cached(const geer_ctx *c, bool want_pixel_tile) {
-    if (!c->cam_valid || (want_pixel_tile && !c->cam_pixel_tile)) return false;
-    const FrameConst &a = c->cam_fc, &b = c->fc;
+bool same_camera(const FrameConst &a, const FrameConst &b) {
     return a.width == b.width && a.height == b.height && a.model == b.model && a.tile_px == b.tile_px &&
            memcmp(a.R, b.R, sizeof(a.R)) == 0 && memcmp(&a.fov_x, &b.fov_x, sizeof(double) * 10) == 0;
+}
+bool camera_cached(const geer_ctx *c, bool want_pixel_tile) {
+    if (!c->cam_valid || (want_pixel_tile && !c->cam_pixel_tile)) return false;
+    return same_camera(c->cam_fc, c->fc);
+}
+// Exchange the context's camera setup with slot s (buffers by pointer, no copies).
+void swap_camera(geer_ctx *c, CamSlot &s) {
+#define GEER_SWAP(b) std::swap(c->b, s.b);
+    GEER_CAM_BUFS(GEER_SWAP)
+#undef GEER_SWAP
+    std::swap(c->cam_valid, s.valid);
+    std::swap(c->cam_pixel_tile, s.pixel_tile_ok);
+    std::swap(c->cam_fc, s.fc);
+    std::swap(c->max_items, s.max_items);
+}
+// Make the context's camera setup the one of c->fc: from a slot if it is cached there, else (the
+// current setup moving into the least recently used slot) rebuilt by camera_setup.
+int select_camera(geer_ctx *c, bool want_pixel_tile, cudaStream_t st) {
+    if (camera_cached(c, want_pixel_tile)) return GEER_OK;
+    const FrameConst &fc = c->fc;
+    const bool keep = (int64_t)fc.width * fc.height <= kCamSlotMaxPixels &&
+                      (!c->cam_valid || (int64_t)c->cam_fc.width * c->cam_fc.height <= kCamSlotMaxPixels);
+    if (keep) {
+        int hit = -1, lru = 0;
+        for (int i = 0; i < kCamSlots; ++i) {
+            const CamSlot &sl = c->cam_slots[i];
+            if (sl.valid && (!want_pixel_tile || sl.pixel_tile_ok) && same_camera(sl.fc, fc)) hit = i;
+            if (!sl.valid || (c->cam_slots[lru].valid && sl.last_use < c->cam_slots[lru].last_use)) lru = i;
+        }
+        const int k = hit >= 0 ? hit : lru;
+        swap_camera(c, c->cam_slots[k]);  // the previous camera stays cached in slot k
+        c->cam_slots[k].last_use = ++c->cam_clock;
+        if (hit >= 0) return GEER_OK;
+    }
+    c->cam_valid = false;
+    int rc = camera_setup(c, want_pixel_tile, st);
+    if (rc) return rc;
+    c->cam_valid = true;
+    c->cam_pixel_tile = want_pixel_tile || fc.model != GEER_BEAP;
+    c->cam_fc = fc;
+    return GEER_OK;
 }
 
 // Full association (+ raster when color != null) for the scene in c->scene.
@@ -284,14 +344,8 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
     GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 7 * sizeof(unsigned long long), st));
     GEER_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
-    if (!camera_cached(c, want_export)) {
-        c->cam_valid = false;
-        rc = camera_setup(c, want_export, st);
-        if (rc) return rc;
-        c->cam_valid = true;
-        c->cam_pixel_tile = want_export || fc.model != GEER_BEAP;
-        c->cam_fc = fc;
-    }
+    rc = select_camera(c, want_export, st);
+    if (rc) return rc;
 
     // ---- K1 preprocess
     Payload *payload = ENSURE(Payload, c->payload, n);
@@ -546,6 +600,11 @@ void geer_destroy(geer_ctx *c) {
                    &c->accum, &c->temp, &c->h64_means, &c->h64_log, &c->h64_quats, &c->h64_op, &c->h64_sh,
                    &c->s32_means, &c->s32_log, &c->s32_quats, &c->s32_op, &c->s32_sh, &c->out64, &c->g64};
     for (Buf *b : bufs) free_buf(*b);
+    for (CamSlot &sl : c->cam_slots) {
+#define GEER_FREE(b) free_buf(sl.b);
+        GEER_CAM_BUFS(GEER_FREE)
+#undef GEER_FREE
+    }
     for (int i = 0; i < 6; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     if (c->ev_hdr) cudaEventDestroy(c->ev_hdr);
