@@ -121,7 +121,7 @@ class ClockSampler:
 
 def rank_camera(base, rank, world):
     """C2 camera for rank 0; rank r sees the scene from the C2 pose rotated by 2 pi r / N about y."""
-    from paper_2505_24053_b200 import synth
+    import workloads as synth
     from paper_2505_24053_b200.scene import Camera
 
     if rank == 0:
@@ -186,7 +186,7 @@ def run_reference(args):
         barrier(world)
         return
     from oracle import oracle as O
-    from paper_2505_24053_b200 import synth
+    import workloads as synth
 
     scene = synth.config_scene("C2")
     cam = synth.config_camera("C2")
@@ -235,7 +235,8 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_setup(args)
-    from paper_2505_24053_b200 import renderer, synth
+    from paper_2505_24053_b200 import renderer
+    import workloads as synth
     from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene
 
     t_setup = time.perf_counter()
@@ -458,10 +459,9 @@ def run_ours(args):
     # ---- 64-view training step (config 4)
     if not args.no_train:
         try:
-            from paper_2505_24053_b200.train import MultiViewTrainer
 
-            trainer = MultiViewTrainer.for_config4(scene, n_views=args.train_views, rank=rank, world=world,
-                                                   device=local, inflight=max(1, args.inflight))
+            trainer = synth.c4_trainer(scene, n_views=args.train_views, rank=rank, world=world,
+                                       device=local, inflight=max(1, args.inflight))
             loss_first = trainer.step(compute_loss=True)  # (untimed warm-up step; loss before any update)
             torch.cuda.synchronize()
             kt = max(2, min(args.steps, 5))
@@ -527,7 +527,8 @@ def run_c5(args, rank, world, local):
     """BASELINE config 5 forward: K frames timed with CUDA events (max over ranks), stage times, stats."""
     import torch
 
-    from paper_2505_24053_b200 import renderer, synth
+    from paper_2505_24053_b200 import renderer
+    import workloads as synth
     from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene
 
     scene = synth.config_scene("C5")

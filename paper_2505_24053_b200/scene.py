@@ -17,47 +17,6 @@ import numpy as np
 MAX_FOV_DEG = 350.0  # camera.py:22
 
 
-class DegenerateInputError(ValueError):
-    """core.py:54-55."""
-
-
-def sigmoid(x):
-    """core.py:58-67 (split-branch form)."""
-    x = np.asarray(x, dtype=np.float64)
-    out = np.empty_like(x)
-    pos = x >= 0
-    out[pos] = 1.0 / (1.0 + np.exp(-x[pos]))
-    ex = np.exp(x[~pos])
-    out[~pos] = ex / (1.0 + ex)
-    if out.ndim == 0:
-        return float(out)
-    return out
-
-
-def logit(p):
-    """core.py:70-72."""
-    p = np.asarray(p, dtype=np.float64)
-    return np.log(p) - np.log1p(-p)
-
-
-def quats_to_rotations(quats: np.ndarray) -> np.ndarray:
-    """scene.py:17-32."""
-    q = np.asarray(quats, dtype=np.float64)
-    q = q / np.linalg.norm(q, axis=-1, keepdims=True)
-    r, i, j, k = q[:, 0], q[:, 1], q[:, 2], q[:, 3]
-    rot = np.empty((len(q), 3, 3))
-    rot[:, 0, 0] = 1 - 2 * (j * j + k * k)
-    rot[:, 0, 1] = 2 * (i * j - r * k)
-    rot[:, 0, 2] = 2 * (i * k + r * j)
-    rot[:, 1, 0] = 2 * (i * j + r * k)
-    rot[:, 1, 1] = 1 - 2 * (i * i + k * k)
-    rot[:, 1, 2] = 2 * (j * k - r * i)
-    rot[:, 2, 0] = 2 * (i * k - r * j)
-    rot[:, 2, 1] = 2 * (j * k + r * i)
-    rot[:, 2, 2] = 1 - 2 * (i * i + j * j)
-    return rot
-
-
 @dataclass
 class GaussianScene:
     """SoA particle store (scene.py:35-51): (N,3), (N,3), (N,4), (N,), (N,B,3)."""
@@ -82,31 +41,6 @@ class GaussianScene:
 
     def __len__(self):
         return len(self.means)
-
-    @property
-    def scales(self) -> np.ndarray:
-        return np.exp(self.log_scales)
-
-    @property
-    def opacities(self) -> np.ndarray:
-        return sigmoid(self.opacity_logits)
-
-    @property
-    def rotations(self) -> np.ndarray:
-        return quats_to_rotations(self.quats)
-
-    @property
-    def sh_degree(self) -> int:
-        return int(round(np.sqrt(self.sh.shape[1]))) - 1
-
-    def whitening_matrices(self) -> np.ndarray:
-        rot = self.rotations
-        return rot.transpose(0, 2, 1) / self.scales[:, :, None]
-
-    def covariances(self) -> np.ndarray:
-        rot = self.rotations
-        m = rot * self.scales[:, None, :]
-        return m @ m.transpose(0, 2, 1)
 
     def extent(self) -> float:
         """scene.py:82-87."""

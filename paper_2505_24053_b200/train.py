@@ -24,7 +24,7 @@ import ctypes
 import numpy as np
 import torch
 
-from . import _lib, synth
+from . import _lib
 from .device import DeviceRenderer, DeviceScene
 from .renderer import RenderConfig
 
@@ -184,22 +184,6 @@ class MultiViewTrainer:
         self.ssim_weight = SSIM_WEIGHT
         self.loss_ws = [LossWorkspace() for _ in range(self.inflight)]
         self.lib = _lib.load()
-
-    @classmethod
-    def for_config4(cls, target_scene, n_views=64, rank=0, world=1, device=0, width=1920, height=1080, inflight=2):
-        """C4: target = C2 scene, init = perturbed(C2, default_rng(1)), ring of BEAP 180x101.25 views."""
-        cams_all = synth.ring_cameras(n_views, 2.0, width, height, fov_deg=180.0, fov_y_deg=180.0 * height / width)
-        mine = [cams_all[i] for i in shard(n_views, rank, world)]
-        init = synth.to_f32_values(synth.perturbed(target_scene, np.random.default_rng(1)))
-        r = DeviceRenderer(device)
-        tscene = DeviceScene.from_scene(target_scene, device=f"cuda:{device}")
-        cfg = RenderConfig()
-        targets = []
-        for cam in mine:
-            color, _, _ = r.forward(tscene, cam, cfg)
-            targets.append(color.clone())
-        del r, tscene
-        return cls(init, mine, targets, rank, world, device, cfg, inflight=inflight)
 
     def _out(self, cam, j=0):
         key = (cam.height, cam.width, j)

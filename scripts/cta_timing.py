@@ -11,7 +11,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2505_24053_b200 import _lib, renderer, synth  # noqa: E402
+from paper_2505_24053_b200 import _lib, renderer# noqa: E402
+import workloads as synth# noqa: E402
 from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene  # noqa: E402
 
 scene = synth.config_scene("C2")

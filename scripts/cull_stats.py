@@ -4,7 +4,8 @@ import json
 import numpy as np
 import torch
 
-from paper_2505_24053_b200 import renderer, synth
+from paper_2505_24053_b200 import renderer
+import workloads as synth
 from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene
 
 scene = synth.config_scene("C2")

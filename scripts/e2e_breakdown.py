@@ -7,7 +7,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2505_24053_b200 import renderer, synth  # noqa: E402
+from paper_2505_24053_b200 import renderer# noqa: E402
+import workloads as synth# noqa: E402
 
 
 def bw(label, nbytes, fn, k=5):

@@ -1,7 +1,8 @@
 import sys, os, time
 sys.path.insert(0, os.getcwd())
 import torch
-from paper_2505_24053_b200 import renderer, synth
+from paper_2505_24053_b200 import renderer
+import workloads as synth
 from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene
 scene = synth.config_scene("C2")
 cams = synth.ring_cameras(4, 2.0, 1920, 1080, fov_deg=180.0, fov_y_deg=180.0 * 1080 / 1920)

@@ -10,7 +10,8 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle import oracle as O  # noqa: E402
-from paper_2505_24053_b200 import association, renderer, synth  # noqa: E402
+from paper_2505_24053_b200 import association, renderer# noqa: E402
+import workloads as synth# noqa: E402
 from tests import parity as P  # noqa: E402
 
 O.set_num_threads(os.cpu_count())

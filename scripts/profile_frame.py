@@ -6,7 +6,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2505_24053_b200 import renderer, synth  # noqa: E402
+from paper_2505_24053_b200 import renderer# noqa: E402
+import workloads as synth# noqa: E402
 from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene  # noqa: E402
 
 ap = argparse.ArgumentParser()

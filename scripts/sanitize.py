@@ -6,7 +6,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2505_24053_b200 import renderer, synth  # noqa: E402
+from paper_2505_24053_b200 import renderer# noqa: E402
+import workloads as synth# noqa: E402
 from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene  # noqa: E402
 
 for name, n, w, h in (("C2", 3000, 160, 96), ("C5", 3000, 128, 80), ("C1", 2000, 64, 64)):

@@ -20,14 +20,14 @@ from raygauss.association import build_grid  # noqa: E402
 from raygauss.camera import Camera as RCamera, angles_to_dir  # noqa: E402
 from raygauss.scene import GaussianScene as RScene  # noqa: E402
 
-from paper_2505_24053_b200 import synth  # noqa: E402
+import workloads as synth# noqa: E402
 from tests import golden_cases as G  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def kappa_min(scene, camera, grid, side):
-    whit = scene.whitening_matrices()
+    whit = RScene(scene.means, scene.log_scales, scene.quats, scene.opacity_logits, scene.sh).whitening_matrices()
     o_u = np.einsum("nij,nj->ni", whit, camera.optical_center[None, :] - scene.means)
     frac = (np.arange(side) + 0.5) / side
     out = np.empty((grid.n_tiles, len(scene)))

@@ -10,7 +10,8 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2505_24053_b200 import renderer, synth
+from paper_2505_24053_b200 import renderer
+import workloads as synth
 from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene
 from paper_2505_24053_b200.scene import Camera
 from tests.test_oracle_bruteforce import assert_sets_equal, brute_case, brute_cases

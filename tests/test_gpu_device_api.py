@@ -6,7 +6,8 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2505_24053_b200 import _lib, renderer, synth
+from paper_2505_24053_b200 import _lib, renderer
+import workloads as synth
 from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene
 
 pytestmark = pytest.mark.gpu
@@ -130,7 +131,7 @@ def test_multiview_inflight_matches_serial():
     from paper_2505_24053_b200 import train
 
     scene = synth.config_scene("C2", n=20_000)
-    tr1 = train.MultiViewTrainer.for_config4(scene, n_views=4, width=192, height=108, inflight=1)
+    tr1 = synth.c4_trainer(scene, n_views=4, width=192, height=108, inflight=1)
     tr2 = train.MultiViewTrainer(synth.to_f32_values(synth.perturbed(scene, np.random.default_rng(1))),
                                  tr1.cameras, tr1.targets, inflight=2)
     tr1.accumulate()

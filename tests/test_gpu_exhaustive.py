@@ -16,7 +16,8 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2505_24053_b200 import _lib, renderer, synth
+from paper_2505_24053_b200 import _lib, renderer
+import workloads as synth
 from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene
 
 pytestmark = pytest.mark.gpu

@@ -12,7 +12,8 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from paper_2505_24053_b200 import association, renderer, synth
+from paper_2505_24053_b200 import association, renderer
+import workloads as synth
 from paper_2505_24053_b200.scene import Camera
 from tests import parity as P
 

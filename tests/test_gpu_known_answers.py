@@ -110,7 +110,8 @@ def test_gradient_of_one_contribution():
 
 
 def test_forward_is_deterministic():
-    from paper_2505_24053_b200 import association, synth
+    from paper_2505_24053_b200 import association
+    import workloads as synth
 
     scene = synth.config_scene("C2", n=30_000)
     cam = synth.config_camera("C2", width=320, height=180)

@@ -4,7 +4,8 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2505_24053_b200 import ply, synth
+from paper_2505_24053_b200 import ply
+import workloads as synth
 from paper_2505_24053_b200.device import DeviceScene
 
 pytestmark = pytest.mark.gpu

@@ -12,7 +12,7 @@ import pytest
 
 from oracle import oracle as O
 from paper_2505_24053_b200.scene import GaussianScene
-from paper_2505_24053_b200 import synth
+import workloads as synth
 from tests import golden_cases as G
 
 FIX = os.path.join(G.GOLDEN, "assoc_brute.npz")

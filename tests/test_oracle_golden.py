@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from paper_2505_24053_b200 import synth
+import workloads as synth
 from tests import golden_cases as G
 
 

@@ -6,7 +6,8 @@ import sys
 import numpy as np
 import pytest
 
-from paper_2505_24053_b200 import ply, synth
+from paper_2505_24053_b200 import ply
+import workloads as synth
 
 REF = "/root/reference/pkg/src"
 

@@ -1,17 +1,25 @@
-"""Synthetic scenes and camera rigs (restated from synth.py:12-100).
+"""Benchmark and test workloads: synthetic scenes and camera rigs (restated from synth.py:12-100).
+
+Fixture generators, not part of the product package: bench.py, smoke() and the tests use them.
 
 The BASELINE configurations are defined on these generators, so
 bench.py and the tests rebuild bit-identical inputs from a seed without the
 reference installed.  ``random_scene`` consumes the numpy Generator in the
 same call order as the reference, so ``random_scene(n, default_rng(0), ...)``
-equals the reference's output exactly (checked in tests/test_synth.py).
+equals the reference's output exactly (pinned by tests/test_oracle_golden.py::test_synth_scene_regenerates_c1_fixture).
 """
 
 from __future__ import annotations
 
 import numpy as np
 
-from .scene import Camera, GaussianScene, logit
+from paper_2505_24053_b200.scene import Camera, GaussianScene
+
+
+def logit(p):
+    """core.py:70-72."""
+    p = np.asarray(p, dtype=np.float64)
+    return np.log(p) - np.log1p(-p)
 
 
 def random_scene(n, rng, center=(0.0, 0.0, 0.0), spread=1.2, scale_range=(0.06, 0.25),
@@ -124,3 +132,24 @@ def config_camera(name: str, width: int | None = None, height: int | None = None
         return Camera(width=w, height=h, model="kb", rotation=rot, translation=t, fx=f, fy=f,
                       cx=(w - 1) / 2, cy=(h - 1) / 2, k=np.zeros(4))
     raise KeyError(name)
+
+
+def c4_trainer(target_scene, n_views=64, rank=0, world=1, device=0, width=1920, height=1080, inflight=2):
+    """BASELINE config 4 step: target = C2 scene, init = perturbed(C2, default_rng(1)), a ring of BEAP
+    180 x 101.25 deg views sharded over ranks; the targets are rendered by the GPU renderer."""
+    from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene
+    from paper_2505_24053_b200.renderer import RenderConfig
+    from paper_2505_24053_b200.train import MultiViewTrainer, shard
+
+    cams_all = ring_cameras(n_views, 2.0, width, height, fov_deg=180.0, fov_y_deg=180.0 * height / width)
+    mine = [cams_all[i] for i in shard(n_views, rank, world)]
+    init = to_f32_values(perturbed(target_scene, np.random.default_rng(1)))
+    r = DeviceRenderer(device)
+    tscene = DeviceScene.from_scene(target_scene, device=f"cuda:{device}")
+    cfg = RenderConfig()
+    targets = []
+    for cam in mine:
+        color, _, _ = r.forward(tscene, cam, cfg)
+        targets.append(color.clone())
+    del r, tscene
+    return MultiViewTrainer(init, mine, targets, rank, world, device, cfg, inflight=inflight)
