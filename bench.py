@@ -459,7 +459,6 @@ def run_ours(args):
     # ---- 64-view training step (config 4)
     if not args.no_train:
         try:
-
             trainer = synth.c4_trainer(scene, n_views=args.train_views, rank=rank, world=world,
                                        device=local, inflight=max(1, args.inflight))
             loss_first = trainer.step(compute_loss=True)  # (untimed warm-up step; loss before any update)
