@@ -180,9 +180,12 @@ int geer_render_backward_host(geer_ctx *ctx, const geer_host_scene *scene, const
 /* g = sign(color - target) * scale per element, 0 where mask == 0 (trainer.py:129-132 L1 term). */
 int geer_l1_grad(const float *color, const float *target, const uint8_t *mask, float *dl_dimage, int64_t n_pixels,
                  float scale, void *stream);
-/* Adam step over a flat fp32 buffer (trainer.py:181-197), per-element lr. */
+/* Adam step over a flat fp32 buffer (trainer.py:181-197), per-element lr.  nonfinite (device int32,
+ * nullable): when given, the gradients are scanned first; any NaN/Inf sets *nonfinite = 1 and the
+ * update is skipped on the device (the non-finite guard of trainer.py:200-205,270-282; the caller
+ * zeroes the flag, reads it when it next synchronises and raises NaNLossError). */
 int geer_adam(float *param, const float *grad, float *m, float *v, const float *lr, int64_t n, float beta1,
-              float beta2, float eps, int32_t step, void *stream);
+              float beta2, float eps, int32_t step, int32_t *nonfinite, void *stream);
 
 /* Masked (1 - w) L1 + w (1 - SSIM) loss and its image gradient (trainer.py:114-155, SSIM window
  * trainer.py:26-69) for an (H,W,3) f32 device image against an (H,W,3) f32 target; mask (H,W) u8

@@ -122,7 +122,7 @@ def load():
             "geer_render_host": ([P, P, P, P, P, P, P], I),
             "geer_render_backward_host": ([P, P, P, P, P, P], I),
             "geer_l1_grad": ([P, P, P, P, I64, F, P], I),
-            "geer_adam": ([P, P, P, P, P, I64, F, F, F, ctypes.c_int32, P], I),
+            "geer_adam": ([P, P, P, P, P, I64, F, F, F, ctypes.c_int32, P, P], I),
             "geer_measure_fp32_peak": ([I, P, P], I),
             "geer_loss_workspace_bytes": ([I, I], ctypes.c_size_t),
             "geer_loss": ([P, P, P, I, I, F, P, P, P, P], I),

@@ -6,6 +6,10 @@
 //   geer_adam    : Adam with bias correction over one flat fp32 buffer
 //                  (trainer.py:181-197), per-element learning rate so all five
 //                  parameter groups update in one launch after the allreduce.
+//                  With a non-null ``nonfinite`` flag it is guarded: a scan of the
+//                  (reduced) gradients raises the flag on any NaN/Inf and the update is
+//                  then skipped on the device, so the parameters stay those of the
+//                  failing step for the host's NaNLossError dump (trainer.py:200-205,270-282).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -24,8 +28,23 @@ __global__ void k_l1_grad(const float *__restrict__ color, const float *__restri
     }
 }
 
+// Raise *flag if any of g[0, n) is NaN or Inf (float4 loads; every rank scans the same reduced buffer).
+__global__ void k_nonfinite(const float *__restrict__ g, int64_t n, int32_t *__restrict__ flag) {
+    bool bad = false;
+    const int64_t n4 = n >> 2, stride = (int64_t)gridDim.x * blockDim.x;
+    const float4 *g4 = reinterpret_cast<const float4 *>(g);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const float4 v = __ldg(g4 + i);
+        bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+    }
+    for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) bad |= !isfinite(g[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 __global__ void k_adam(float *__restrict__ p, const float *__restrict__ g, float *__restrict__ m, float *__restrict__ v,
-                       const float *__restrict__ lr, int64_t n, float b1, float b2, float eps, float bc1, float bc2) {
+                       const float *__restrict__ lr, int64_t n, float b1, float b2, float eps, float bc1, float bc2,
+                       const int32_t *__restrict__ skip) {
+    if (skip && *skip) return;  // a non-finite gradient: keep the step's parameters for the dump
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float gi = g[i];
         const float mi = b1 * m[i] + (1.0f - b1) * gi;
@@ -58,12 +77,14 @@ int geer_l1_grad(const float *color, const float *target, const uint8_t *mask, f
 }
 
 int geer_adam(float *param, const float *grad, float *m, float *v, const float *lr, int64_t n, float beta1,
-              float beta2, float eps, int32_t step, void *stream) {
+              float beta2, float eps, int32_t step, int32_t *nonfinite, void *stream) {
     if (!param || !grad || !m || !v || !lr || n < 0 || step < 1) return GEER_ERR_INVALID;
     if (n == 0) return GEER_OK;
     const float bc1 = (float)(1.0 - pow((double)beta1, (double)step));
     const float bc2 = (float)(1.0 - pow((double)beta2, (double)step));
-    k_adam<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(param, grad, m, v, lr, n, beta1, beta2, eps, bc1, bc2);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (nonfinite) k_nonfinite<<<148 * 4, 256, 0, st>>>(grad, n, nonfinite);
+    k_adam<<<grid_for(n), 256, 0, st>>>(param, grad, m, v, lr, n, beta1, beta2, eps, bc1, bc2, nonfinite);
     return cudaGetLastError() == cudaSuccess ? GEER_OK : GEER_ERR_CUDA;
 }
 

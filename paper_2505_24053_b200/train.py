@@ -115,6 +115,16 @@ def allreduce_grads(buf: torch.Tensor, world: int) -> torch.Tensor:
     return buf
 
 
+class NaNLossError(RuntimeError):
+    """trainer.py:200-205 (same message)."""
+
+    def __init__(self, iteration, dump_path=None):
+        msg = f"loss became non-finite at iteration {iteration}"
+        if dump_path:
+            msg += f"; scene state dumped to {dump_path}"
+        super().__init__(msg)
+
+
 class FlatScene:
     """A DeviceScene whose five tensors are views of one contiguous fp32 buffer."""
 
@@ -184,6 +194,10 @@ class MultiViewTrainer:
         self.ssim_weight = SSIM_WEIGHT
         self.loss_ws = [LossWorkspace() for _ in range(self.inflight)]
         self.lib = _lib.load()
+        # device non-finite flag of the guarded Adam (trainer.py:270-282): raised by a NaN/Inf in the
+        # reduced gradients, which also skips that update; read by check_finite()
+        self.nonfinite = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.dump_dir = None
 
     def _out(self, cam, j=0):
         key = (cam.height, cam.width, j)
@@ -198,14 +212,36 @@ class MultiViewTrainer:
     def step(self, compute_loss=False):
         loss = self.accumulate(compute_loss)
         allreduce_grads(self.grads.buf, self.world)
+        self.apply()
+        if compute_loss:
+            self.last_loss = loss
+            self.check_finite(loss)
+        return loss
+
+    def check_finite(self, loss=None):
+        """Raise NaNLossError (trainer.py:270-282) if a step's loss or reduced gradients were non-finite.
+
+        Synchronises with the device; the step loop calls it whenever it reads the loss anyway.  The
+        parameters are those before the failing update (the guarded Adam skipped it); with
+        ``dump_dir`` set they are saved to ``nan_dump_iter{t}.npz`` like the reference's dump."""
+        bad = int(self.nonfinite.item()) != 0 or (loss is not None and not np.isfinite(loss))
+        if not bad:
+            return
+        dump_path = None
+        if self.dump_dir is not None:
+            dump_path = f"{self.dump_dir}/nan_dump_iter{self.t}.npz"
+            sc = self.params.scene
+            np.savez(dump_path, **{name: getattr(sc, name).double().cpu().numpy() for name, _ in FIELDS})
+        raise NaNLossError(self.t, dump_path)
+
+    def apply(self):
+        """One Adam update of the flat parameters from the (reduced) flat gradients (trainer.py:181-197)."""
         self.t += 1
         stream = self.streams[0].cuda_stream
         _lib.check(self.lib.geer_adam(self.params.buf.data_ptr(), self.grads.buf.data_ptr(), self.m.data_ptr(),
                                       self.v.data_ptr(), self.lr.data_ptr(), self.params.numel, ctypes.c_float(0.9),
-                                      ctypes.c_float(0.999), ctypes.c_float(1e-15), self.t, stream))
-        if compute_loss:
-            self.last_loss = loss
-        return loss
+                                      ctypes.c_float(0.999), ctypes.c_float(1e-15), self.t,
+                                      self.nonfinite.data_ptr(), stream))
 
     def accumulate(self, compute_loss=False):
         """Sum over the local views of the stored-space gradients into ``self.grads`` (no collective)."""

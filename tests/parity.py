@@ -45,9 +45,9 @@ def assert_image_close(color, remaining, count, ref_color, ref_remaining, ref_co
     return r
 
 
-def grad_report(grads, ref: dict, idx=None):
+def grad_report(grads, ref: dict, idx=None, keys=GRAD_KEYS):
     out = {}
-    for k in GRAD_KEYS:
+    for k in keys:
         g = np.asarray(getattr(grads, k) if not isinstance(grads, dict) else grads[k], np.float64)
         if idx is not None:
             g = g[idx]
@@ -62,8 +62,8 @@ def grad_report(grads, ref: dict, idx=None):
     return out
 
 
-def assert_grads_close(grads, ref: dict, idx=None):
-    rep = grad_report(grads, ref, idx)
+def assert_grads_close(grads, ref: dict, idx=None, keys=GRAD_KEYS):
+    rep = grad_report(grads, ref, idx, keys)
     for k, v in rep.items():
         assert v["violations"] == 0, (k, v)
     return rep

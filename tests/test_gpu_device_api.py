@@ -79,11 +79,24 @@ def test_l1_grad_and_adam_kernels():
     for step in (1, 2, 3):
         _lib.check(lib.geer_adam(p.data_ptr(), grad.data_ptr(), m.data_ptr(), v.data_ptr(), lr.data_ptr(), 5000,
                                  ctypes.c_float(0.9), ctypes.c_float(0.999), ctypes.c_float(1e-15), step,
-                                 torch.cuda.current_stream().cuda_stream))
+                                 None, torch.cuda.current_stream().cuda_stream))
         m_ref = 0.9 * m_ref + 0.1 * grad
         v_ref = 0.999 * v_ref + 0.001 * grad * grad
         p_ref = p_ref - 1e-3 * (m_ref / (1 - 0.9 ** step)) / (torch.sqrt(v_ref / (1 - 0.999 ** step)) + 1e-15)
     torch.testing.assert_close(p, p_ref, rtol=1e-5, atol=1e-6)
+    # the guarded form: finite gradients update as before, a NaN anywhere skips the update and raises the flag
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    before = p.clone()
+    _lib.check(lib.geer_adam(p.data_ptr(), grad.data_ptr(), m.data_ptr(), v.data_ptr(), lr.data_ptr(), 5000,
+                             ctypes.c_float(0.9), ctypes.c_float(0.999), ctypes.c_float(1e-15), 4, flag.data_ptr(),
+                             torch.cuda.current_stream().cuda_stream))
+    assert int(flag) == 0 and not torch.equal(p, before)
+    grad[4321] = float("nan")
+    before = p.clone()
+    _lib.check(lib.geer_adam(p.data_ptr(), grad.data_ptr(), m.data_ptr(), v.data_ptr(), lr.data_ptr(), 5000,
+                             ctypes.c_float(0.9), ctypes.c_float(0.999), ctypes.c_float(1e-15), 5, flag.data_ptr(),
+                             torch.cuda.current_stream().cuda_stream))
+    assert int(flag) == 1 and torch.equal(p, before)
 
 
 @pytest.mark.parametrize("config_name,n,w,h", [("C2", 50_000, 640, 360), ("C5", 40_000, 480, 270),

@@ -77,3 +77,41 @@ def test_oracle_matches_reference_c1():
     idx = d["grad_sample"]
     for k in ("dmeans", "dlog_scales", "dquats", "dopacities", "dsh"):
         assert _grad_close(getattr(gr, k)[idx], d[k]), k
+
+
+def test_oracle_pd_boundary_decisions():
+    """The PD check across its boundary (s_min 1e-8 .. 3e-10; association.py:154-160): the oracle's
+    LAPACK-potf2 restatement raises on the scenes the reference raised on, except pivot ties (the
+    reference's own pivot within rounding noise of zero); the association of every scene neither side
+    rejects is bit-exact."""
+    cases, cam = G.pd_boundary()
+    bad, ties = [], 0
+    for s_min, seed, raised, tie, scene, order, ranges in cases:
+        try:
+            g = O.build_render_graph(scene, cam)
+            got = 0
+        except ValueError as e:
+            got = 1 if "positive definite" in str(e) else 2
+        if got != raised:
+            ties += 1
+            if not tie:
+                bad.append((s_min, seed, raised, got))
+            continue
+        if not raised:
+            np.testing.assert_array_equal(g.order, order)
+            np.testing.assert_array_equal(g.ranges, ranges)
+    assert not bad, bad
+    print(f"pd boundary: {ties} flips, all pivot ties")
+
+
+def test_oracle_backward_catches_the_mutation_hook():
+    """SURVEY §4 tier 1: on single-ray scenes the oracle's backward equals the reference's and is far from
+    the mutant of gradients._debug_negate_dir_cross_term (gradients.py:20-22,114-115)."""
+    from tests import parity as P
+
+    keys = ("dmeans", "dlog_scales", "dquats", "dopacities")
+    for scene, cam, dl, ref, mut in G.mutation_cases():
+        gr = O.render_backward(scene, cam, dl)
+        P.assert_grads_close(gr, ref, keys=keys)
+        rep = P.grad_report(gr, mut, keys=keys)
+        assert rep["dlog_scales"]["violations"] + rep["dmeans"]["violations"] > 0
