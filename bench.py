@@ -201,7 +201,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "FPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth.random_scene seed 0)",
-        "config": {"workload": WORKLOAD, "gaussians": len(scene), "width": 1920, "height": 1080},
+        "config": {"workload": WORKLOAD, "gaussians": len(scene), "width": cam.width, "height": cam.height},
         "mrays_per_s": fps * 1920 * 1080 / 1e6,
         "cpu_baseline": {"value": fps, "unit": "FPS", "cores": cores, "kind": "port",
                          "sample": "full C2 frame per step (association + raster), fp64 C port of the reference "
@@ -489,6 +489,13 @@ def run_ours(args):
         except Exception as exc:
             extra["c5"] = {"error": repr(exc)}
 
+    # ---- config 1: 10k Gaussians, 256x256 pinhole (the reference's own CPU-runnable case)
+    if not args.no_c1:
+        try:
+            extra["c1"] = run_c1(args, local)
+        except Exception as exc:
+            extra["c1"] = {"error": repr(exc)}
+
     # ---- CPU baseline (rank 0, N=1 only): the fp64 C port of the reference path on this host
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -502,6 +509,8 @@ def run_ours(args):
                    "seconds": cpu_s}
         except Exception as exc:
             cpu = {"value": None, "unit": "FPS", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {exc}"}
+        # the unmodified Python reference (baseline/_ref) on C1, beside the port
+        cpu["python_reference_c1"] = time_python_reference_c1()
 
     if rank == 0:
         line = {
@@ -509,10 +518,11 @@ def run_ours(args):
             "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32 raster / f64 association",
             "data": "synthetic (synth.random_scene seed 0, fp32-rounded)",
-            "config": {"workload": WORKLOAD, "gaussians": len(scene), "width": w, "height": h,
-                       "frames_in_flight": nf,
-                       "views": "one per rank (rank r: C2 pose rotated 2*pi*r/N about y)",
-                       "l2": "inputs exceed L2 (scene SoA 236 MB fp32 > 126 MB L2); no explicit flush"},
+            "config": {"workload": WORKLOAD, "gaussians": len(scene), "width": w, "height": h},
+            "frames_in_flight": nf,
+            "fps_single_stream": 1e3 / extra["latency_ms_per_frame"] if extra.get("latency_ms_per_frame") else None,
+            "views": "one per rank (rank r: C2 pose rotated 2*pi*r/N about y)",
+            "l2": "inputs exceed L2 (scene SoA 236 MB fp32 > 126 MB L2); no explicit flush",
             "mrays_per_s": value * w * h / 1e6,
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": gpu_launches,
             "setup_s": time.perf_counter() - t_setup,
@@ -520,6 +530,92 @@ def run_ours(args):
         line.update(extra)
         print(json.dumps(line), flush=True)
     barrier(world)
+
+
+def run_c1(args, local):
+    """BASELINE config 1 on the GPU: forward FPS (one stream, CUDA events) and fwd+bwd ms per view."""
+    import torch
+
+    from paper_2505_24053_b200 import renderer
+    import workloads as synth
+    from paper_2505_24053_b200.device import DeviceRenderer, DeviceScene
+
+    scene = synth.config_scene("C1")
+    cam = synth.config_camera("C1")
+    ds = DeviceScene.from_scene(scene, device=f"cuda:{local}")
+    cfg = renderer.RenderConfig()
+    r = DeviceRenderer(local)
+    out = (torch.empty((cam.height, cam.width, 3), dtype=torch.float32, device="cuda"),
+           torch.empty((cam.height, cam.width), dtype=torch.float32, device="cuda"),
+           torch.empty((cam.height, cam.width), dtype=torch.int32, device="cuda"))
+    dl = torch.randn((cam.height, cam.width, 3), device="cuda",
+                     generator=torch.Generator(device="cuda").manual_seed(1)) / (cam.height * cam.width)
+    grads = ds.zeros_like_grads()
+    for _ in range(5):
+        r.forward(ds, cam, cfg, out=out)
+        r.backward(dl, grads=grads)
+    torch.cuda.synchronize()
+    k = 50
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record()
+    for _ in range(k):
+        r.forward(ds, cam, cfg, out=out)
+    e[1].record()
+    for _ in range(k):
+        r.forward(ds, cam, cfg, out=out)
+        r.backward(dl, grads=grads)
+    e[2].record()
+    torch.cuda.synchronize()
+    fwd_ms = e[0].elapsed_time(e[1]) / k
+    return {"workload": "C1: 10k Gaussians, 256x256 pinhole, forward (+ fwd+bwd)", "fps": 1e3 / fwd_ms,
+            "ms_per_frame": fwd_ms, "fwd_bwd_ms_per_view": e[1].elapsed_time(e[2]) / k, "steps": k,
+            "frames_in_flight": 1}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def time_python_reference_c1():
+    """The unmodified reference (raygauss from baseline/_ref, or already importable) on C1: render with
+    threads=1 and threads=os.cpu_count(), render_backward with os.cpu_count() (renderer.py:24-54,123,234)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(ref) and ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        from raygauss import camera as rcam
+        from raygauss import renderer as rr
+        from raygauss.scene import GaussianScene as RScene
+    except Exception as exc:
+        return {"unavailable": f"raygauss not importable: {exc}"}
+    import workloads as synth
+
+    sc = synth.config_scene("C1")
+    cm = synth.config_camera("C1")
+    rs = RScene(sc.means, sc.log_scales, sc.quats, sc.opacity_logits, sc.sh)
+    rc = rcam.Camera(width=cm.width, height=cm.height, model=cm.model, rotation=cm.rotation,
+                     translation=cm.translation, fx=cm.fx, fy=cm.fy, cx=cm.cx, cy=cm.cy)
+    ncpu = os.cpu_count() or 1
+    res = {"workload": "C1: 10k Gaussians, 256x256 pinhole", "cpu_model": _cpu_model(), "cpu_count": ncpu,
+           "note": "unmodified raygauss 0.1.0 (pure Python + numpy); its tile pool is GIL-bound"}
+    for th in (1, ncpu):
+        t0 = time.perf_counter()
+        rr.render(rs, rc, rr.RenderConfig(threads=th))
+        res[f"render_s_threads{th}"] = time.perf_counter() - t0
+    rng = np.random.default_rng(1)
+    dl = rng.standard_normal((cm.height, cm.width, 3)) / (cm.height * cm.width)
+    t0 = time.perf_counter()
+    rr.render_backward(rs, rc, dl, rr.RenderConfig(threads=ncpu))
+    res[f"render_backward_s_threads{ncpu}"] = time.perf_counter() - t0
+    res["fps_threads1"] = 1.0 / res["render_s_threads1"]
+    return res
 
 
 def run_c5(args, rank, world, local):
@@ -601,6 +697,7 @@ def main():
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-c1", action="store_true")
     ap.add_argument("--inflight", type=int, default=4, help="frames in flight (contexts/streams) for the FPS value")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -111,7 +111,7 @@ struct geer_ctx {
     int64_t iota_len = 0;  // a raster ran (also exhaustive forwards, which have no backward)
     int64_t n_entries = 0;
     int max_items = 0;
-    CUtensorMap pay_map, gpay_map;  // gather4 maps over the payload / grad payload arrays
+    CUtensorMap pay_map;  // gather4 map over the payload array
     // K0 cache: the camera setup depends only on the camera and the tile size
     bool cam_valid = false, cam_pixel_tile = false;
     FrameConst cam_fc{};
@@ -126,7 +126,7 @@ struct geer_ctx {
     Buf col_sc, row_sc, medges_x, medges_y, edges_x, edges_y, dir64, theta, phi, minmax, pixel_tile, pixel_tile_sorted,
         pix_iota, pix_list, tile_count, tile_off, item_count, item_off, items, n_items, work, n_work;
     // per-Gaussian buffers
-    Buf payload, gpayload, depth_key, depth_key_sorted, gid_iota, gid_sorted, ranges_ax, flags, mu_c,
+    Buf payload, depth_key, depth_key_sorted, gid_iota, gid_sorted, ranges_ax, flags, mu_c,
         depth;
     // per-entry buffers
     Buf order, tile_ranges, wcull;
@@ -220,8 +220,15 @@ int make_frame_const(const geer_camera *cam, const geer_config *cfg, int n_bands
     fc->lam2 = cfg->lam * cfg->lam;
     fc->lam2f = (float)fc->lam2;
     fc->cutoff_tol = (float)(1e-6 * fc->lam2 + 1e-7);
+    fc->thrk = (float)(kHalfLog2e * fc->lam2);
+    fc->thrkc = fc->cutoff ? fc->thrk : INFINITY;
     for (int i = 0; i < 3; ++i) fc->bg[i] = (float)cfg->background[i];
     return GEER_OK;
+}
+
+// The item frames follow the per-warp culling regions in the wcull buffer.
+ItemFrame *item_frames(geer_ctx *c) {
+    return reinterpret_cast<ItemFrame *>(reinterpret_cast<float4 *>(c->wcull.p) + (size_t)c->max_items * 16);
 }
 
 // K0: camera setup into ctx buffers (tile CSR + work items).
@@ -277,9 +284,10 @@ int camera_setup(geer_ctx *c, bool want_pixel_tile, cudaStream_t st) {
     void *tmp = ENSURE(char, c->temp, sb);
     exclusive_scan_i32(tmp, sb, icnt, ioff, fc.n_tiles, st);
     launch_item_fill(fc.n_tiles, tile_off, ioff, items, nit, st);
-    float4 *wc = ENSURE(float4, c->wcull, (size_t)c->max_items * 16);  // 8 warps x (patch, cone) per item
+    // per item: 8 warps x (patch, cone), then the item frames
+    float4 *wc = ENSURE(float4, c->wcull, (size_t)c->max_items * (16 + sizeof(ItemFrame) / 16));
     launch_warp_cull(fc, c->max_items, items, nit, (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p,
-                     (const double2 *)c->row_sc.p, (const double *)c->dir64.p, wc, st);
+                     (const double2 *)c->row_sc.p, (const double *)c->dir64.p, wc, item_frames(c), st);
     return GEER_OK;
 }
 
@@ -349,7 +357,6 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
 
     // ---- K1 preprocess
     Payload *payload = ENSURE(Payload, c->payload, n);
-    GradPayload *gpayload = ENSURE(GradPayload, c->gpayload, n);
     uint32_t *dkey = ENSURE(uint32_t, c->depth_key, n);
     uint32_t *dkey_s = ENSURE(uint32_t, c->depth_key_sorted, n);
     int32_t *giota = ENSURE(int32_t, c->gid_iota, n);
@@ -364,9 +371,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     int32_t *ranges = ENSURE(int32_t, c->tile_ranges, fc.n_tiles + 1);
     rc = make_row_map(&c->pay_map, payload, n, (int)sizeof(Payload));
     if (rc) return rc;
-    rc = make_row_map(&c->gpay_map, gpayload, n, (int)sizeof(GradPayload));
-    if (rc) return rc;
-    launch_preprocess(fc, sc, (const double *)c->medges_x.p, (const double *)c->medges_y.p, payload, gpayload, dkey, ar,
+    launch_preprocess(fc, sc, (const double *)c->medges_x.p, (const double *)c->medges_y.p, payload, dkey, ar,
                       flags, mu, dep, c->d_err, c->d_counters + 5, st);
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[1], st));
 
@@ -412,7 +417,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
             int32_t *fix = ENSURE(int32_t, c->fixup, npx);
             launch_forward(fc, sc, c->max_items, (const int4 *)c->items.p, nwork, (const int32_t *)c->pix_list.p,
                            (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p, (const double *)c->dir64.p,
-                           r2, (const uint32_t *)gsorted, payload, c->pay_map, (const float4 *)c->wcull.p, color, remaining, count, ne,
+                           r2, (const uint32_t *)gsorted, payload, c->pay_map, (const float4 *)c->wcull.p, item_frames(c), color, remaining, count, ne,
                            c->d_counters, fix, st);
             c->have_stats = true;
         }
@@ -451,7 +456,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         int32_t *fix = ENSURE(int32_t, c->fixup, npx);
         launch_forward(fc, sc, c->max_items, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
                        (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
-                       (const double *)c->dir64.p, ranges, (const uint32_t *)c->order.p, payload, c->pay_map, (const float4 *)c->wcull.p, color, remaining, count, ne,
+                       (const double *)c->dir64.p, ranges, (const uint32_t *)c->order.p, payload, c->pay_map, (const float4 *)c->wcull.p, item_frames(c), color, remaining, count, ne,
                        c->d_counters, fix, st);
         c->fwd_remaining = remaining;
         c->have_raster = c->have_stats = true;
@@ -480,7 +485,7 @@ int run_backward(geer_ctx *c, const float *dl_dimage, bool f64_out, void *const 
     launch_backward(fc, sc, c->max_items, (const int4 *)c->work.p, (const int32_t *)c->n_work.p,
                     (const int32_t *)c->pix_list.p, (const double2 *)c->col_sc.p, (const double2 *)c->row_sc.p,
                     (const double *)c->dir64.p, (const int32_t *)c->tile_ranges.p, (const uint32_t *)c->order.p,
-                    c->pay_map, c->gpay_map, (const float4 *)c->wcull.p,
+                    c->pay_map, (const float4 *)c->wcull.p, item_frames(c),
                     c->fwd_remaining, (const int32_t *)c->n_eval.p,
                     dl_dimage, accum, st);
     if (f64_out)
@@ -592,7 +597,7 @@ void geer_destroy(geer_ctx *c) {
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     Buf *bufs[] = {&c->col_sc, &c->row_sc, &c->medges_x, &c->medges_y, &c->edges_x, &c->edges_y, &c->dir64,
                    &c->theta, &c->phi, &c->minmax, &c->pixel_tile, &c->pixel_tile_sorted, &c->pix_iota, &c->pix_list,
-                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->work, &c->n_work, &c->payload, &c->gpayload,
+                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->work, &c->n_work, &c->payload,
                    &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted,
                    &c->ranges_ax, &c->flags, &c->mu_c, &c->depth,
                    &c->order, &c->tile_ranges, &c->wcull,

@@ -35,7 +35,22 @@ struct FrameConst {
     double lam, lam2;
     float bg[3];
     float lam2f;
-    float cutoff_tol;  // |kappa_fp32 - lam^2| below which the cutoff is re-decided in fp64
+    float cutoff_tol;  // |kappa_fp32 - lam^2| below which the cutoff is re-decided in fp64 (generic path)
+    float thrk;        // kHalfLog2e * lam^2: the cutoff in the raster's scaled units k = kHalfLog2e * kappa
+    float thrkc;       // thrk under the support cutoff, +inf without it (renderer.py:103-105)
+};
+
+// exp(-kappa / 2) = 2^(-kHalfLog2e kappa): the raster works with k = kHalfLog2e kappa (ex2 argument).
+constexpr double kHalfLog2e = 0.72134752044448170;
+constexpr double kSqrtHalfLog2e = 0.84932180028801907;  // m is stored scaled by this, so |m|^2 / dd = k
+
+// Per raster work item (cached with the camera): an orthonormal fp64 frame (dc = normalised sum of the
+// item's world rays, e1, e2) in which every pixel ray of the item is d' = dc + x e1 + y e2 (d' = d /
+// (d . dc); kappa is scale-invariant in d).  rx, ry bound |x|, |y| over the item's pixels; rx < 0
+// marks an item too wide for the offset evaluation (cone > 60 deg), which takes the fp64 path.
+struct __align__(16) ItemFrame {
+    double dc[3], e1[3], e2[3];
+    float rx, ry, pad0, pad1;
 };
 
 // Raster culling record of one Gaussian (48 B, written by K1, streamed with the payload):
@@ -46,12 +61,10 @@ struct __align__(16) Cull {
     float4 k0, k1;
 };
 
-// Raster payload, one per Gaussian (176 B, see make_payload in geer_geometry.cu; one bulk copy):
-//   q[12]  mode 0: quadratic forms of |d_u|^2 and |m|^2 in the ray d:
-//                  (A00, A11, A22, 2A01, 2A02, 2A12, B00, B11, B22, 2B01, 2B02, 2B12)
-//          mode 1: W (row-major) and o_u for the fp64 cross-product evaluation
-//   col  = (r, g, b, sigma); sigma < 0 flags mode 1
-//   ext  = (absolute kappa error bound of the fp64 evaluation, 0, 0, 0)
+// Raster payload, one per Gaussian (176 B, see make_payload in geer_geometry.cu; one TMA row):
+//   q[12]  W (row-major, W = S^-1 R^T) and o_u = W (o - mu) in fp64 (renderer.py:78-79)
+//   col  = (r, g, b, sigma)
+//   ext  = (absolute kappa error bound of the fp64 cross-product evaluation, 0, 0, 0)
 //   cull = the culling record (written by the association half of K1)
 struct __align__(16) Payload {
     double q[12];
@@ -60,10 +73,6 @@ struct __align__(16) Payload {
     Cull cull;
 };
 
-// fp32 W rows and o_u (w component) for the backward's gradient vectors.
-struct __align__(16) GradPayload {
-    float4 r0, r1, r2;
-};
 
 // Per-axis tile ranges: up to 3 disjoint [lo, hi) pairs packed lo | hi << 16.
 struct AxisRanges {

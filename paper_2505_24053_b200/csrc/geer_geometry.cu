@@ -464,47 +464,19 @@ __device__ int axis_tiles(double t_aa, double t_a2, double t22, double r0, doubl
     return cnt;
 }
 
-// Raster payload of one Gaussian (renderer.py:78-80 quantities, precomputed per view).
-// kappa = |m|^2 / |d_u|^2 with d_u = W d and m = o_u x d_u = M d, M = [o_u]_x W, so both
-// norms are quadratic forms in the pixel ray d: |d_u|^2 = d^T A d (A = W^T W) and
-// |m|^2 = d^T B d (B = M^T M).  Evaluated in fp64 (12 DFMA per pair) their relative error is
-// ~1e-16 |o_u|^2 cond(W)^2; the absolute kappa error bound is stored in ext.x.  When that bound
-// exceeds 1e-7 (|o_u| cond > ~7e3: tiny, far or very anisotropic Gaussians) the payload
-// instead carries W and o_u (mode 1) and the raster uses the fp64 cross product, the
-// reference's own formulation (core.py:184-199), whose error grows only like |o_u|.
-__device__ bool make_payload(const double W[9], const double ou[3], const double rgb[3], double sigma, double cond,
-                             double lam, Payload &pl, GradPayload &gp) {
+// Raster payload of one Gaussian (renderer.py:78-80 quantities, precomputed per view): W and o_u in
+// fp64 for the raster's per-item offset records and its fp64 re-checks (the cross product
+// m = o_u x W d, the reference's formulation, core.py:184-199), whose kappa error grows only like
+// |o_u| cond(W); the absolute bound goes to ext.x.
+__device__ void make_payload(const double W[9], const double ou[3], const double rgb[3], double sigma, double cond,
+                             double lam, Payload &pl) {
     const double u64 = 1.1102230246251565e-16;
-    const double on2 = ou[0] * ou[0] + ou[1] * ou[1] + ou[2] * ou[2];
-    const double band0 = 32.0 * u64 * (on2 * cond * cond + lam * lam + 1.0);
-    const bool mode1 = !(band0 <= 1e-7);
-    if (!mode1) {
-        double A[9], M[9], B[9];
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) A[i * 3 + j] = W[0 * 3 + i] * W[0 * 3 + j] + W[1 * 3 + i] * W[1 * 3 + j] + W[2 * 3 + i] * W[2 * 3 + j];
-        // M = [o]_x W : row i of M = (o x column) components
-        for (int j = 0; j < 3; ++j) {
-            M[0 * 3 + j] = ou[1] * W[2 * 3 + j] - ou[2] * W[1 * 3 + j];
-            M[1 * 3 + j] = ou[2] * W[0 * 3 + j] - ou[0] * W[2 * 3 + j];
-            M[2 * 3 + j] = ou[0] * W[1 * 3 + j] - ou[1] * W[0 * 3 + j];
-        }
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) B[i * 3 + j] = M[0 * 3 + i] * M[0 * 3 + j] + M[1 * 3 + i] * M[1 * 3 + j] + M[2 * 3 + i] * M[2 * 3 + j];
-        pl.q[0] = A[0]; pl.q[1] = A[4]; pl.q[2] = A[8];
-        pl.q[3] = 2.0 * A[1]; pl.q[4] = 2.0 * A[2]; pl.q[5] = 2.0 * A[5];
-        pl.q[6] = B[0]; pl.q[7] = B[4]; pl.q[8] = B[8];
-        pl.q[9] = 2.0 * B[1]; pl.q[10] = 2.0 * B[2]; pl.q[11] = 2.0 * B[5];
-    } else {
-        for (int i = 0; i < 9; ++i) pl.q[i] = W[i];
-        for (int i = 0; i < 3; ++i) pl.q[9 + i] = ou[i];
-    }
-    const double band1 = 64.0 * u64 * (sqrt(on2) + 1.0) * (cond + 1.0) * (2.0 * lam + 1.0);
-    pl.col = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], mode1 ? -(float)sigma : (float)sigma);
-    pl.ext = make_float4((float)(mode1 ? band1 : band0), 0.f, 0.f, 0.f);
-    gp.r0 = make_float4((float)W[0], (float)W[1], (float)W[2], (float)ou[0]);
-    gp.r1 = make_float4((float)W[3], (float)W[4], (float)W[5], (float)ou[1]);
-    gp.r2 = make_float4((float)W[6], (float)W[7], (float)W[8], (float)ou[2]);
-    return mode1;
+    const double on = sqrt(ou[0] * ou[0] + ou[1] * ou[1] + ou[2] * ou[2]);
+    for (int i = 0; i < 9; ++i) pl.q[i] = W[i];
+    for (int i = 0; i < 3; ++i) pl.q[9 + i] = ou[i];
+    const double band1 = 64.0 * u64 * (on + 1.0) * (cond + 1.0) * (2.0 * lam + 1.0);
+    pl.col = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], (float)sigma);
+    pl.ext = make_float4((float)band1, 0.f, 0.f, 0.f);
 }
 
 __device__ __forceinline__ void named_barrier(int id, int count) {
@@ -634,12 +606,11 @@ __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, con
 // Only the pixel-side arithmetic of the raster depends on these values (not the association), so
 // reciprocals replace divisions here.  NB = SH band count (compile-time: static register arrays).
 // Runs on a group of 128 threads (lt = 0..127) that synchronises with named barrier 2; ssh: SH
-// staging, then payload staging (9 + 3 float4 = 48 floats per Gaussian, padded rows).  Returns the
-// SH clamp gate (bits 3-5) and payload-mode (bit 6) flag bits of Gaussian g0 + lt.
+// staging, then payload staging (9 float4 = 36 floats per Gaussian, padded rows).  Returns the
+// SH clamp gate flag bits (3-5) of Gaussian g0 + lt.
 constexpr int kPayHead = offsetof(Payload, cull) / 16;    // float4s of a payload before its culling record
 constexpr int kPayRow = sizeof(Payload) / 16;             // float4s of a payload
 constexpr int kStageRow = kPayHead + 1;                   // padded staging row
-constexpr int kGradRow = sizeof(GradPayload) / 16;
 
 template <int NB>
 __device__ uint8_t payload_block(const FrameConst &fc, const geer_scene &sc, float *ssh, Cull *scull, int64_t g0,
@@ -728,22 +699,17 @@ __device__ uint8_t payload_block(const FrameConst &fc, const geer_scene &sc, flo
     }
     const double smax = fmax(s[0], fmax(s[1], s[2])), smin = fmin(s[0], fmin(s[1], s[2]));
     Payload pl;
-    GradPayload gp;
-    const bool mode1 = make_payload(W, ou, rgb, sigma, smax / smin, fc.lam, pl, gp);
-    // flags: bit0 keep, bit1 clamped (K1a), bits3-5 SH clamp gate per channel, bit6 payload mode 1
-    const uint8_t bits = (uint8_t)((gate << 3) | (mode1 ? 64 : 0));
+    make_payload(W, ou, rgb, sigma, smax / smin, fc.lam, pl);
+    // flags: bit0 keep, bit1 clamped (K1a), bits3-5 SH clamp gate per channel
+    const uint8_t bits = (uint8_t)(gate << 3);
     // stage the block's payloads (first 8 float4; the culling record comes from the association
-    // half) and grad payloads in shared memory, reusing the SH buffer: k_preprocess writes them out
-    // as contiguous float4 runs.  Rows padded to 9 float4: conflict-free 16-B stores.
+    // half) in shared memory, reusing the SH buffer: k_preprocess writes them out as contiguous
+    // float4 runs.  Rows padded to 9 float4: conflict-free 16-B stores.
     float4 *sp = reinterpret_cast<float4 *>(ssh);
-    float4 *sg = sp + 128 * kStageRow;
     named_barrier(2, 128);  // every thread is done reading its SH coefficients
     const float4 *plv = reinterpret_cast<const float4 *>(&pl);
-    const float4 *gpv = reinterpret_cast<const float4 *>(&gp);
 #pragma unroll
     for (int k = 0; k < kPayHead; ++k) sp[lt * kStageRow + k] = plv[k];
-#pragma unroll
-    for (int k = 0; k < kGradRow; ++k) sg[lt * kGradRow + k] = gpv[k];
     return bits;
 }
 
@@ -756,12 +722,12 @@ __device__ uint8_t payload_block(const FrameConst &fc, const geer_scene &sc, flo
 template <int NB>
 __global__ void __launch_bounds__(256, K1_MIN_BLOCKS)
     k_preprocess(FrameConst fc, geer_scene sc, const double *__restrict__ medges_x, const double *__restrict__ medges_y,
-                 Payload *__restrict__ payload, GradPayload *__restrict__ gpayload, uint32_t *__restrict__ depth_key,
+                 Payload *__restrict__ payload, uint32_t *__restrict__ depth_key,
                  AxisRanges *__restrict__ ranges, uint8_t *__restrict__ flags,
                  double *__restrict__ mu_out, double *__restrict__ depth_out, int *__restrict__ err,
                  unsigned long long *__restrict__ total_entries) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int kStageFloats = (kStageRow + kGradRow) * 4;  // payload-head + grad-payload staging
+    constexpr int kStageFloats = kStageRow * 4;  // payload-head staging
     __shared__ __align__(16) float ssh[128 * (NB * 3 > kStageFloats ? NB * 3 : kStageFloats)];
     __shared__ Cull scull[128];
     __shared__ uint8_t sfl[2][128];
@@ -814,17 +780,14 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS)
         if (threadIdx.x == 0 && t) atomicAdd(total_entries, t);
         if (threadIdx.x == 0 && rows) atomicAdd(total_entries + 1, rows);  // (the next counter)
     }
-    // coalesced write-out of the block's payload rows (head + culling record) and grad payloads
+    // coalesced write-out of the block's payload rows (head + culling record)
     const float4 *sp = reinterpret_cast<const float4 *>(ssh);
-    const float4 *sg = sp + 128 * kStageRow;
     const float4 *scv = reinterpret_cast<const float4 *>(scull);
     float4 *dp = reinterpret_cast<float4 *>(payload + g0);
-    float4 *dg = reinterpret_cast<float4 *>(gpayload + g0);
     for (int i = threadIdx.x; i < cnt_b * kPayRow; i += blockDim.x) {
         const int r = i / kPayRow, k = i - r * kPayRow;
         dp[i] = k < kPayHead ? sp[r * kStageRow + k] : scv[r * (sizeof(Cull) / 16) + (k - kPayHead)];
     }
-    for (int i = threadIdx.x; i < cnt_b * kGradRow; i += blockDim.x) dg[i] = sg[i];
 }
 
 // ---------------------------------------------------------------- K7
@@ -976,7 +939,7 @@ void launch_item_fill(int n_tiles, const int32_t *tile_off, const int32_t *item_
 size_t preprocess_smem(const FrameConst &fc) { return sizeof(double) * (fc.n_x + fc.n_y + 2); }
 
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
-                       Payload *payload, GradPayload *gpayload, uint32_t *depth_key, AxisRanges *ranges,
+                       Payload *payload, uint32_t *depth_key, AxisRanges *ranges,
                        uint8_t *flags, double *mu_out, double *depth_out, int *err,
                        unsigned long long *total_entries, cudaStream_t st) {
     if (sc.n == 0) return;
@@ -984,7 +947,7 @@ void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double 
     switch (sc.n_bands) {
 #define GEER_NB_CASE(NB)                                                                                            \
     case NB:                                                                                                        \
-        k_preprocess<NB><<<blocks, 256, preprocess_smem(fc), st>>>(fc, sc, medges_x, medges_y, payload, gpayload,   \
+        k_preprocess<NB><<<blocks, 256, preprocess_smem(fc), st>>>(fc, sc, medges_x, medges_y, payload,             \
                                                                    depth_key, ranges, flags,                       \
                                                                    mu_out, depth_out, err, total_entries);         \
         break;

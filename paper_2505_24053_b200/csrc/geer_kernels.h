@@ -24,7 +24,7 @@ void launch_item_fill(int n_tiles, const int32_t *tile_off, const int32_t *item_
                       cudaStream_t st);
 size_t preprocess_smem(const FrameConst &fc);
 void launch_preprocess(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
-                       Payload *payload, GradPayload *gpayload, uint32_t *depth_key, AxisRanges *ranges, uint8_t *flags,
+                       Payload *payload, uint32_t *depth_key, AxisRanges *ranges, uint8_t *flags,
                        double *mu_out, double *depth_out, int *err, unsigned long long *total_entries,
                        cudaStream_t st);
 template <typename T>
@@ -59,21 +59,21 @@ void order_items(const int4 *items, const int32_t *n_items, const int32_t *range
                  int32_t *n_work, cudaStream_t st);
 
 // geer_raster.cu (fp32 raster forward / backward)
-// per-warp culling regions of every work item, cached with the camera (wcull: 2 float4 per warp)
+// per-warp culling regions (wcull: 2 float4 per warp) and the frame of every work item, cached with the camera
 void launch_warp_cull(const FrameConst &fc, int max_items, const int4 *items, const int32_t *n_items,
                       const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc, const double *dir64,
-                      float4 *wcull, cudaStream_t st);
+                      float4 *wcull, ItemFrame *iframe, cudaStream_t st);
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    const CUtensorMap &pay_map, const float4 *wcull, float *color, float *remaining, int32_t *count, int32_t *n_eval,
-                    unsigned long long *counters, int32_t *fixup_list, cudaStream_t st);
+                    const CUtensorMap &pay_map, const float4 *wcull, const ItemFrame *iframe, float *color,
+                    float *remaining, int32_t *count, int32_t *n_eval, unsigned long long *counters,
+                    int32_t *fixup_list, cudaStream_t st);
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                      const double *dir64, const int32_t *ranges, const uint32_t *order, const CUtensorMap &pay_map,
-                     const CUtensorMap &gpay_map, const float4 *wcull,
-                     const float *remaining,
-                     const int32_t *n_eval, const float *dl_dimage, float *accum, cudaStream_t st);
+                     const float4 *wcull, const ItemFrame *iframe, const float *remaining, const int32_t *n_eval,
+                     const float *dl_dimage, float *accum, cudaStream_t st);
 int launch_assoc_check(const FrameConst &fc, const geer_scene &sc, const double *medges_x, const double *medges_y,
                        const uint8_t *flags, const int32_t *ranges, const uint32_t *order, int side, double *wo,
                        double *origin3, uint32_t *graph_bits, uint32_t *hit_bits, unsigned long long *counters,

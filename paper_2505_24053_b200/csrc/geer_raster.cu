@@ -5,8 +5,8 @@
 // TMA gather4 copies completed on mbarriers, and 8 consumer warps (one pixel per lane, an 8x4 patch
 // per warp) cull each stage against their patch, then walk the kept entries front to back:
 //
-//   |d_u|^2, |m|^2 from the payload's fp64 quadratic forms (or d_u = W d, m = o_u x d_u),
-//   kappa = |m|^2/|d_u|^2                                     (core.py:184-199)
+//   d_u = W d, m = o_u x d_u from the item's offset records (fp64 products rounded once; see
+//   make_record), kappa = |m|^2/|d_u|^2                       (core.py:184-199)
 //   u = sigma exp(-kappa/2) [kappa <= lam^2], t = min(u, 0.999) (renderer.py:96-105)
 //   C += rem t c; rem *= 1 - t; count += t > 0; stop when rem < 1e-4 (renderer.py:107-118)
 //
@@ -48,7 +48,7 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Pixel ray (world frame): fp64 for the cutoff re-check, fp32 for the raster.
+// Pixel ray (world frame, fp64; camera.py:141-155 + renderer.py:77, or the K0 ray table).
 template <bool kBEAP>
 __device__ __forceinline__ void pixel_ray(const FrameConst &fc, int p, const double2 *col_sc, const double2 *row_sc,
                                           const double *dir64, double d[3]) {
@@ -109,78 +109,40 @@ __device__ __noinline__ double kappa_fp64(const float *__restrict__ means, const
     return __ddiv_rn(mm, dd);
 }
 
-// Quadratic monomials of the pixel ray d (fp64) for the mode-0 payload.
-struct Ray64 {
-    double m00, m11, m22, m01, m02, m12;
-};
-
-__device__ __forceinline__ Ray64 make_ray(const double d[3]) {
-    Ray64 r;
-    r.m00 = d[0] * d[0];
-    r.m11 = d[1] * d[1];
-    r.m22 = d[2] * d[2];
-    r.m01 = d[0] * d[1];
-    r.m02 = d[0] * d[2];
-    r.m12 = d[1] * d[2];
-    return r;
-}
-
-// Mode-0 quadratic form q . (m00, m11, m22, m01, m02, m12) in fp64 as one FMA chain (1 DMUL +
-// 5 DFMA; the payload's error bound ext.x covers any summation order).  The single definition
-// keeps the forward, its fast path and the backward bit-identical.
-__device__ __forceinline__ double qform(const double2 &a0, const double2 &a1, const double2 &a2, const Ray64 &r) {
-    return fma(a2.y, r.m12, fma(a2.x, r.m02, fma(a1.y, r.m01, fma(a1.x, r.m22, fma(a0.y, r.m11, a0.x * r.m00)))));
-}
-
 struct PairT {
     float kap, alpha, u, t, dd;
 };
 
-// |d_u|^2 and |m|^2 of (payload P, ray d) in fp64: mode 0 via the quadratic forms, mode 1 via
-// the fp64 cross product d_u = W d, m = o_u x d_u (core.py:184-199).  dray: the ray itself
-// (only read in mode 1).  m1 must be warp-uniform.
-__device__ __forceinline__ void norms64(const Payload &P, const Ray64 &R, const double *dray, bool m1, double &dd,
-                                        double &mm) {
-    if (!m1) {
-        const double2 a0 = *reinterpret_cast<const double2 *>(&P.q[0]);
-        const double2 a1 = *reinterpret_cast<const double2 *>(&P.q[2]);
-        const double2 a2 = *reinterpret_cast<const double2 *>(&P.q[4]);
-        const double2 b0 = *reinterpret_cast<const double2 *>(&P.q[6]);
-        const double2 b1 = *reinterpret_cast<const double2 *>(&P.q[8]);
-        const double2 b2 = *reinterpret_cast<const double2 *>(&P.q[10]);
-        dd = qform(a0, a1, a2, R);
-        mm = qform(b0, b1, b2, R);
-    } else {
-        const double d0 = dray[0], d1 = dray[1], d2 = dray[2];
-        const double u0 = fma(P.q[2], d2, fma(P.q[1], d1, P.q[0] * d0));
-        const double u1 = fma(P.q[5], d2, fma(P.q[4], d1, P.q[3] * d0));
-        const double u2 = fma(P.q[8], d2, fma(P.q[7], d1, P.q[6] * d0));
-        const double o0 = P.q[9], o1 = P.q[10], o2 = P.q[11];
-        const double x0 = fma(o1, u2, -(o2 * u1)), x1 = fma(o2, u0, -(o0 * u2)), x2 = fma(o0, u1, -(o1 * u0));
-        dd = fma(u2, u2, fma(u1, u1, u0 * u0));
-        mm = fma(x2, x2, fma(x1, x1, x0 * x0));
-    }
+// |d_u|^2 and |m|^2 of (payload P, ray d) in fp64 via the cross product d_u = W d, m = o_u x d_u
+// (core.py:184-199; explicit fma: the same rounding in every kernel that calls it).
+__device__ __forceinline__ void norms64(const Payload &P, const double *dray, double &dd, double &mm) {
+    const double d0 = dray[0], d1 = dray[1], d2 = dray[2];
+    const double u0 = fma(P.q[2], d2, fma(P.q[1], d1, P.q[0] * d0));
+    const double u1 = fma(P.q[5], d2, fma(P.q[4], d1, P.q[3] * d0));
+    const double u2 = fma(P.q[8], d2, fma(P.q[7], d1, P.q[6] * d0));
+    const double o0 = P.q[9], o1 = P.q[10], o2 = P.q[11];
+    const double x0 = fma(o1, u2, -(o2 * u1)), x1 = fma(o2, u0, -(o0 * u2)), x2 = fma(o0, u1, -(o1 * u0));
+    dd = fma(u2, u2, fma(u1, u1, u0 * u0));
+    mm = fma(x2, x2, fma(x1, x1, x0 * x0));
 }
 
-// Blend quantities of a pair from its fp64 norms (fp32 from here on):
-//   u = sigma exp(-kappa/2) [kappa <= lam^2], t = min(u, 0.999)   (renderer.py:96-105)
+// Blend quantities of a pair from its fp64 norms (fp32 from here on; the fp64 path of items without an
+// offset frame):  u = sigma exp(-kappa/2) [kappa <= lam^2], t = min(u, 0.999)   (renderer.py:96-105)
 // Returns true when the cutoff decision lies within the fp64 evaluation's own error bound (the
 // forward then hands the pixel to the fp64 fix-up, which uses the reference formulation).
-__device__ __forceinline__ bool finish_t(double dd, double mm, const Payload &P, bool m1, const FrameConst &fc,
-                                         PairT &e, int &rechecks) {
+__device__ __forceinline__ bool finish_t(double dd, double mm, const Payload &P, const FrameConst &fc, PairT &e,
+                                         int &rechecks) {
     const float sw = P.col.w;
     const float ddf = (float)dd;
     e.dd = ddf;
     e.kap = __fmul_rn((float)mm, rcp_approx(ddf));
     e.alpha = ex2_approx(__fmul_rn(e.kap, -0.72134752044448170f));  // exp(-kappa/2)
-    float u = __fmul_rn(fabsf(sw), e.alpha);
+    float u = __fmul_rn(sw, e.alpha);
     bool uncertain = false;
     if (fc.cutoff) {
         bool inside = e.kap <= fc.lam2f;
-        // kappa_fp32 carries ~3e-7 relative error (mode-0 fp64 error <= 1e-7 absolute by construction):
-        // re-decide the cutoff in fp64 near lam^2
-        const float tol = m1 ? fc.cutoff_tol + P.ext.x : fc.cutoff_tol;
-        if (fabsf(__fsub_rn(e.kap, fc.lam2f)) <= tol) {
+        // kappa_fp32 carries ~3e-7 relative error plus the fp64 evaluation's bound ext.x: re-decide near lam^2
+        if (fabsf(__fsub_rn(e.kap, fc.lam2f)) <= fc.cutoff_tol + P.ext.x) {
             const double k64 = mm / dd;
             inside = k64 <= fc.lam2;
             uncertain = fabs(k64 - fc.lam2) <= (double)P.ext.x;
@@ -193,28 +155,143 @@ __device__ __forceinline__ bool finish_t(double dd, double mm, const Payload &P,
     return uncertain;
 }
 
-// Shared verbatim by the forward and backward kernels (called warp-uniformly), so t is
-// bit-identical in both.
-__device__ __forceinline__ bool eval_t(const Payload &P, const Ray64 &R, const double *dray, const FrameConst &fc,
-                                       PairT &e, int &rechecks) {
-    const bool m1 = __any_sync(0xffffffffu, P.col.w < 0.0f);
+// Shared verbatim by the forward and backward kernels, so t is bit-identical in both.
+__device__ __forceinline__ bool eval_t(const Payload &P, const double *dray, const FrameConst &fc, PairT &e,
+                                       int &rechecks) {
     double dd, mm;
-    norms64(P, R, dray, m1, dd, mm);
-    return finish_t(dd, mm, P, m1, fc, e, rechecks);
+    norms64(P, dray, dd, mm);
+    return finish_t(dd, mm, P, fc, e, rechecks);
 }
 
-// Relative bound on |t_fp32 - t_exact| / t for a pair (fp64 kappa rounded to fp32, rcp/ex2 approximations).
+// Relative bound on |t_fp32 - t_exact| / t for a pair of the fp64 path (fp64 kappa rounded to fp32, rcp/ex2 approximations).
 __device__ __forceinline__ float t_rel_bound(float kap) { return 6e-7f + 3e-7f * kap; }
+
+// ------------------------------------------------------------------------------ offset records
+//
+// Within a work item every pixel ray is d' = dc + x e1 + y e2 (ItemFrame), so per (item, Gaussian)
+//   d_u = W d' = a + x b + y c           (a = W dc, b = W e1, c = W e2)
+//   m   = o_u x d_u = ma + x mb + y mc   (ma = o_u x a, ...)
+// The producer warp turns each streamed payload into a record of these vectors (fp64 products
+// rounded once to fp32, m scaled by sqrt(kHalfLog2e)), the quadratic |d_u|^2 = D0 + D1 x + D2 y +
+// D3 x^2 + D4 x y + D5 y^2 and two error bounds; per pair the consumers then evaluate
+//   dd = |d_u|^2 (5 FFMA),  m (6 FFMA),  k = |m|^2 / dd = kHalfLog2e kappa,  u = sigma 2^-k
+// in fp32.  The offsets x, y stay small (|x|, |y| <= ~0.02 for a 16-px tile), so the cancellation
+// of the reference's cross product (o_u x d_u with |o_u| up to ~1e3) happens in fp64 once per
+// (item, Gaussian), not per pair.  Record layout (float4 units):
+//   [0] D0 D1 D2 D3   [1] D4 D5 sigma tol   [2] ma0 mb0 mc0 trel   [3] ma1 mb1 mc1 -   [4] ma2 mb2 mc2 -
+//   [5] r g b -       backward only: [6] a0 b0 c0 ou0   [7] a1 b1 c1 ou1   [8] a2 b2 c2 ou2
+// tol bounds |k_fp32 - kHalfLog2e kappa_ref| near the cutoff (pairs within tol of it are re-decided
+// from the fp64 payload), trel bounds the relative error of t on the pairs that contribute.
+constexpr int kRecF = 24;  // forward record floats
+constexpr int kRecB = 36;  // backward record floats
+
+// Offset coordinates of a pixel ray d in an item frame (x, y of d / (d . dc)).
+__device__ __forceinline__ float2 pixel_xy(const ItemFrame &F, const double d[3]) {
+    const double den = __fma_rn(d[2], F.dc[2], __fma_rn(d[1], F.dc[1], __dmul_rn(d[0], F.dc[0])));
+    const double nx = __fma_rn(d[2], F.e1[2], __fma_rn(d[1], F.e1[1], __dmul_rn(d[0], F.e1[0])));
+    const double ny = __fma_rn(d[2], F.e2[2], __fma_rn(d[1], F.e2[1], __dmul_rn(d[0], F.e2[0])));
+    return make_float2((float)__ddiv_rn(nx, den), (float)__ddiv_rn(ny, den));
+}
+
+struct PixXY {
+    float x, y, xx, xy, yy;
+};
+__device__ __forceinline__ PixXY make_pxy(float2 v) {
+    return PixXY{v.x, v.y, __fmul_rn(v.x, v.x), __fmul_rn(v.x, v.y), __fmul_rn(v.y, v.y)};
+}
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// The record of payload P in frame F (one producer lane per entry; noinline: the forward and backward
+// kernels run this one compiled body, so their records - and hence t - are bit-identical).  Only the
+// cross product that cancels, ma = o_u x W dc (|o_u| up to ~1e3, |ma| down to ~0 for a Gaussian on
+// the item's centre ray), is formed in fp64; the offset terms (x mb + y mc, |x|, |y| <= rx, ry) and
+// the quadratic's coefficients are fp32, and their rounding is charged to the bounds (which carry
+// a 1.5x margin, covering the approximate sqrt / rcp used to form them).
+__device__ __noinline__ void make_record(const Payload &P, const ItemFrame &F, float thrk, float *rec, int grad) {
+    const double *W = P.q;
+    double a[3], b[3], c[3];
+    float wmin2 = INFINITY;  // sigma_min(W)^2 = min row norm^2 (W = S^-1 R^T)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double w0 = W[i * 3 + 0], w1 = W[i * 3 + 1], w2 = W[i * 3 + 2];
+        a[i] = __fma_rn(w2, F.dc[2], __fma_rn(w1, F.dc[1], __dmul_rn(w0, F.dc[0])));
+        b[i] = __fma_rn(w2, F.e1[2], __fma_rn(w1, F.e1[1], __dmul_rn(w0, F.e1[0])));
+        c[i] = __fma_rn(w2, F.e2[2], __fma_rn(w1, F.e2[1], __dmul_rn(w0, F.e2[0])));
+        const float f0 = (float)w0, f1 = (float)w1, f2 = (float)w2;
+        wmin2 = fminf(wmin2, f0 * f0 + f1 * f1 + f2 * f2);
+    }
+    // m = (o_u sqrt(kHalfLog2e)) x (a + x b + y c): the cancelling cross products in fp64
+    const double o0 = __dmul_rn(P.q[9], kSqrtHalfLog2e), o1 = __dmul_rn(P.q[10], kSqrtHalfLog2e),
+                 o2 = __dmul_rn(P.q[11], kSqrtHalfLog2e);
+    auto cross = [&](const double *v, float *m) {
+        m[0] = (float)__fma_rn(o1, v[2], -__dmul_rn(o2, v[1]));
+        m[1] = (float)__fma_rn(o2, v[0], -__dmul_rn(o0, v[2]));
+        m[2] = (float)__fma_rn(o0, v[1], -__dmul_rn(o1, v[0]));
+    };
+    float ma[3], mb[3], mc[3];
+    cross(a, ma);
+    cross(b, mb);
+    cross(c, mc);
+    const float af[3] = {(float)a[0], (float)a[1], (float)a[2]}, bf[3] = {(float)b[0], (float)b[1], (float)b[2]},
+                cf[3] = {(float)c[0], (float)c[1], (float)c[2]};
+    auto dot = [](const float *x, const float *y) {
+        return __fmaf_rn(x[2], y[2], __fmaf_rn(x[1], y[1], __fmul_rn(x[0], y[0])));
+    };
+    const float D0 = dot(af, af), D1 = 2.0f * dot(af, bf), D2 = 2.0f * dot(af, cf);
+    const float D3 = dot(bf, bf), D4 = 2.0f * dot(bf, cf), D5 = dot(cf, cf);
+    // error bounds (u = 2^-24):
+    //   |d dd| <= 16 u Sd, Sd = (|a| + rx |b| + ry |c|)^2  (coefficients from the rounded vectors,
+    //   offsets, 5 FMA);  |d m| <= 4 u (|ma| + rx |mb| + ry |mc|)  (rounding of the fp64 products,
+    //   offsets, 2 FMA);  dd >= ddlo over the item;  at k = thrk
+    //   |d k| <= (2 sqrt(k dd) |d m| + |d m|^2 + k |d dd|) / dd + 6 u k   (rcp.approx + products),
+    // plus the reference's own fp64 error ext.x.
+    const float rx = F.rx, ry = F.ry, u = 5.9604645e-8f;
+    const float na = sqrt_approx(D0), nb = sqrt_approx(D3), nc = sqrt_approx(D5);
+    const float lin = na - rx * nb - ry * nc;
+    const float ddlo = fmaxf(lin > 0.f ? 0.999f * lin * lin : 0.f, 0.98f * wmin2);  // |d'| >= 1
+    const float idd = rcp_approx(ddlo);
+    const float sd = (na + rx * nb + ry * nc) * (na + rx * nb + ry * nc);
+    const float dm = 4.0f * u * (sqrt_approx(dot(ma, ma)) + rx * sqrt_approx(dot(mb, mb)) + ry * sqrt_approx(dot(mc, mc)));
+    const float tol = 1.5f * (2.0f * sqrt_approx(thrk * idd) * dm + dm * dm * idd + thrk * (6.0f * u + 16.0f * u * sd * idd)) +
+                      (float)kHalfLog2e * P.ext.x + 1e-30f;
+    float4 *r4 = reinterpret_cast<float4 *>(rec);
+    const float sig = P.col.w;
+    if (!(tol < 0.25f * thrk) || !(sd < 1e36f) || !(dm < 1e-3f * 1e18f)) {
+        // fp32 cannot carry this Gaussian here (huge or degenerate W / o_u): every pair goes to the fp64
+        // re-check (k = 0 lies within an infinite tol of the cutoff)
+        r4[0] = make_float4(1.f, 0.f, 0.f, 0.f);
+        r4[1] = make_float4(0.f, 0.f, sig, INFINITY);
+        r4[2] = make_float4(0.f, 0.f, 0.f, 1e-5f);
+        r4[3] = make_float4(0.f, 0.f, 0.f, 0.f);
+        r4[4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+        r4[0] = make_float4(D0, D1, D2, D3);
+        r4[1] = make_float4(D4, D5, sig, tol);
+        r4[2] = make_float4(ma[0], mb[0], mc[0], 0.6931472f * tol + 1e-6f);
+        r4[3] = make_float4(ma[1], mb[1], mc[1], 0.f);
+        r4[4] = make_float4(ma[2], mb[2], mc[2], 0.f);
+    }
+    r4[5] = make_float4(P.col.x, P.col.y, P.col.z, 0.f);
+    if (grad) {
+        r4[6] = make_float4(af[0], bf[0], cf[0], (float)P.q[9]);
+        r4[7] = make_float4(af[1], bf[1], cf[1], (float)P.q[10]);
+        r4[8] = make_float4(af[2], bf[2], cf[2], (float)P.q[11]);
+    }
+}
 
 // ------------------------------------------------------------------------------ pipeline plumbing
 //
-// Each raster CTA = kConsumerWarps consumer warps (one pixel per lane) + 1
-// producer warp.  The producer streams the tile's entries through a ring of
-// kStages shared-memory stages: it gathers each entry's 80-byte payload with one
-// cp.async.bulk (global -> shared, completion counted on the stage's "full"
-// mbarrier) and the consumer warps release a stage through its "empty" mbarrier.
-// Consumer warps never meet at a CTA barrier: each warp retires as soon as its
-// own 32 pixels are opaque, and the producer stops streaming once every
+// Each raster CTA = kConsumerWarps consumer warps (one pixel per lane) + 1 producer warp.  The
+// producer streams the tile's entries through a ring of kStages shared-memory stages: it gathers
+// the payload rows with TMA gather4 (completion counted on the stage's "landed" mbarrier), turns
+// each into an offset record and then arrives on the stage's "full" mbarrier; the consumer warps
+// release a stage through its "empty" mbarrier.  Consumer warps never meet at a CTA barrier: each
+// warp retires as soon as its own 32 pixels are opaque, and the producer stops streaming once every
 // consumer warp is done.
 
 constexpr int kConsumerWarps = kRasterThreads / 32;  // 8
@@ -229,22 +306,25 @@ constexpr int kPipeThreads = kRasterThreads + 32;
 #endif
 
 constexpr int kRingGroupBytes = 768;    // 4 x 176-B payloads (704 B), padded to a multiple of 128
-constexpr int kGringGroupBytes = 256;   // 4 x 48-B grad payloads (192 B), padded
 constexpr int kRingGroups = kStageEntries / 4 + 1;
-static_assert(sizeof(Payload) * 4 <= kRingGroupBytes && sizeof(GradPayload) * 4 <= kGringGroupBytes, "ring layout");
+static_assert(sizeof(Payload) * 4 <= kRingGroupBytes, "ring layout");
 
-template <bool kGrad, int NW = kConsumerWarps>
+template <bool kGrad>
 struct __align__(128) PipeSmem {
-    static constexpr int kNW = NW;  // consumer warps
+    static constexpr int kNW = kConsumerWarps;
+    static constexpr int kRec = kGrad ? kRecB : kRecF;
     // Entries land in groups of 4 (one TMA gather4 per group), each group 128-B aligned; group
-    // kStageEntries / 4 holds the null entry (t = 0 for every ray).  Use ring_at / gring_at.
+    // kStageEntries / 4 holds the null entry (t = 0 for every ray).  Use ring_at.
     alignas(128) unsigned char ring[kStages][kRingGroups][kRingGroupBytes];
-    alignas(128) unsigned char gring[kGrad ? kStages : 1][kStageEntries / 4][kGringGroupBytes];  // backward only
+    alignas(16) float rec[kStages][kStageEntries][kRec];  // offset records (producer -> consumers)
+    ItemFrame frame;                                        // the item's frame (producer copy)
+    float4 wc[kNW][2];                                      // per consumer warp: culling patch, cone
+    alignas(16) float red[kGrad ? kNW : 1][16][36];         // backward: per-warp transpose of the 16 partials
     uint32_t gid[kStages][kStageEntries];
     int count[kStages];  // entries in the stage; 0 = end of stream
-    uint8_t idx[kStages][NW][kStageEntries + 4];  // per warp: its kept entries, padded with null slots
-    alignas(16) uint32_t iadr[kStages][NW][kStageEntries + 4];  // the same entries' shared addresses
-    unsigned long long full[kStages];
+    uint8_t idx[kStages][kNW][kStageEntries + 4];  // per warp: its kept entries, padded with null slots
+    unsigned long long landed[kStages];  // TMA fill complete
+    unsigned long long full[kStages];    // records written (consumers may read the stage)
     unsigned long long empty[kStages];
     int done_warps;
     int stop;  // producer will not fill any more stages
@@ -258,10 +338,6 @@ __device__ __forceinline__ uint32_t ring_off(int j) { return (uint32_t)((j >> 2)
 template <class Smem>
 __device__ __forceinline__ Payload &ring_at(Smem &S, int s, int j) {
     return *reinterpret_cast<Payload *>(&S.ring[s][0][0] + ring_off(j));
-}
-template <class Smem>
-__device__ __forceinline__ const GradPayload &gring_at(Smem &S, int s, int j) {
-    return *reinterpret_cast<const GradPayload *>(&S.gring[s][j >> 2][(j & 3) * sizeof(GradPayload)]);
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -315,6 +391,14 @@ __device__ __forceinline__ void mbar_wait_suspend(unsigned long long *bar, unsig
         "r"(parity), "n"(GEER_PRODUCER_SUSPEND_NS)
         : "memory");
 }
+// One probe with a suspend-time hint (the producer's idle sleep; the result is not needed).
+__device__ __forceinline__ void mbar_try_wait_suspend(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(GEER_PRODUCER_SUSPEND_NS)
+        : "memory");
+}
 // TMA gather4: rows r[0..3] of a 2D row-major tensor (one row = one payload) into 4 consecutive
 // rows at dst (128-B aligned), completion counted on bar (sm_100a UTMALDG.2D.GATHER4).
 __device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *map, const uint32_t r[4],
@@ -326,26 +410,20 @@ __device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *map, c
         : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-
 template <class Smem>
 __device__ __forceinline__ void pipe_init(Smem &S) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
+            mbar_init(&S.landed[s], 1);
             mbar_init(&S.full[s], 1);
             mbar_init(&S.empty[s], Smem::kNW);
         }
         S.done_warps = 0;
         S.stop = 0;
-        // null entry: |d_u|^2 = |d|^2, |m|^2 = 0, sigma = 0  ->  kappa = 0, t = 0 exactly (a no-op)
+        // null entry: W = I, o_u = 0, sigma = 0  ->  kappa = 0, t = 0 exactly (a no-op)
         for (int s = 0; s < kStages; ++s) {
             Payload &z = ring_at(S, s, kStageEntries);
-            for (int i = 0; i < 12; ++i) z.q[i] = i < 3 ? 1.0 : 0.0;
+            for (int i = 0; i < 12; ++i) z.q[i] = (i == 0 || i == 4 || i == 8) ? 1.0 : 0.0;
             z.col = make_float4(0.f, 0.f, 0.f, 0.f);
             z.ext = make_float4(0.f, 0.f, 0.f, 0.f);
         }
@@ -373,70 +451,87 @@ __device__ __forceinline__ bool cone_misses(const float4 &ta, const float4 &tb, 
     return lhs < 0.0f && lhs * lhs > 4.0f * s2 * c2 * p2;                          // sin^2(2b) = 4 s2 c2
 }
 
-// Producer warp: stream entries [first, first + n_total) (forward order) or the
-// same range walked from the back (reverse) in stages of kStageEntries.
-template <bool kReverse, bool kGradMaps, class Smem>
+// Producer warp: stream entries [first, first + n_total) (forward order) or the same range walked
+// from the back (reverse) in stages of kStageEntries, then an end-of-stream sentinel (count 0).  It
+// runs a non-blocking loop over two queues: issue the next fill (TMA gather4, completion on
+// "landed") as soon as its slot is free, and finish the oldest landed fill (records written, "full"
+// arrived), so neither a slow consumer warp nor a pending gather holds up the other queue.
+// with_rec = false (items without a frame): no records, a fill is full once it has landed.
+template <bool kReverse, class Smem>
 __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict__ order, const CUtensorMap *pay_map,
-                                             const CUtensorMap *gpay_map, int first, int n_total, bool stop_when_done,
+                                             float thrk, bool with_rec, int first, int n_total, bool stop_when_done,
                                              unsigned long long *streamed = nullptr) {
-    const unsigned per_group = (unsigned)(4 * (sizeof(Payload) + (kGradMaps ? sizeof(GradPayload) : 0)));
+    constexpr bool kGrad = Smem::kRec == kRecB;
+    const unsigned per_group = (unsigned)(4 * sizeof(Payload));
     const int lane = threadIdx.x & 31;
-    // gid of this lane's entry in stage bb (the order load runs one stage ahead of the copies)
+    const int n_fills = (n_total + kStageEntries - 1) / kStageEntries;
+    // gid of this lane's entry in fill bb (the order load runs one fill ahead of the copies)
     auto load_gid = [&](int bb) -> uint32_t {
         const int done = kStageEntries * bb;
         const int n = min(kStageEntries, n_total - done);
         const int base = kReverse ? first + n_total - done - n : first + done;
         return lane < n ? __ldg(order + base + lane) : 0u;
     };
-    unsigned phase = 0;
-    int s = 0, b = 0;
-    bool sentinel = false;
+    // warp-uniform barrier probes (a completed phase stays complete until we act on the slot again)
+    auto ready = [&](unsigned long long *bar, unsigned parity) {
+        return __shfl_sync(0xffffffffu, (int)mbar_try_wait(bar, parity), 0) != 0;
+    };
+    int next = 0, fin = 0;  // next fill to issue (n_fills: the sentinel), oldest fill not yet full
     uint32_t g_next = load_gid(0);
-    for (;; ++b) {
-        const int done = kStageEntries * b;
-        const int n = min(kStageEntries, n_total - done);
-        // every consumer warp has dropped out: stop streaming (no sentinel needed)
-        if (stop_when_done && *((volatile int *)&S.done_warps) == Smem::kNW) break;
-        const uint32_t g = g_next;
-        if (n > 0) g_next = load_gid(b + 1);
-        mbar_wait_suspend(&S.empty[s], phase ^ 1);
-        if (n <= 0) {
-            if (lane == 0) {
-                S.count[s] = 0;
-                mbar_arrive(&S.full[s]);
-            }
-            sentinel = true;
-            break;
-        }
-        if (lane < n) S.gid[s][lane] = g;
-        __syncwarp();
-        if (lane == 0) {
-            S.count[s] = n;
-            mbar_arrive_expect_tx(&S.full[s], ((n + 3) >> 2) * per_group);
-        }
-        __syncwarp();
-        // lane k < ceil(n / 4) gathers rows of entries 4k..4k+3 (a partial last group repeats its
-        // last entry, so every gather moves 4 whole rows)
-        const int ng = (n + 3) >> 2;
-        uint32_t rows[4];
+    for (;;) {
+        if (stop_when_done && *((volatile int *)&S.done_warps) == Smem::kNW) break;  // every consumer left
+        bool progress = false;
+        if (next <= n_fills && ready(&S.empty[next % kStages], ((next / kStages) & 1) ^ 1)) {
+            const int s = next % kStages;
+            if (next == n_fills) {  // sentinel
+                if (lane == 0) {
+                    S.count[s] = 0;
+                    mbar_arrive(&S.full[s]);
+                }
+            } else {
+                const int n = min(kStageEntries, n_total - kStageEntries * next);
+                const uint32_t g = g_next;
+                if (next + 1 < n_fills) g_next = load_gid(next + 1);
+                if (lane < n) S.gid[s][lane] = g;
+                __syncwarp();
+                if (lane == 0) {
+                    S.count[s] = n;
+                    mbar_arrive_expect_tx(&S.landed[s], ((n + 3) >> 2) * per_group);
+                }
+                __syncwarp();
+                // lane k < ceil(n / 4) gathers rows of entries 4k..4k+3 (a partial last group repeats
+                // its last entry, so every gather moves 4 whole rows)
+                uint32_t rows[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) rows[q] = __shfl_sync(0xffffffffu, g, min(4 * (lane & 7) + q, n - 1));
-        if (lane < ng) {
-            tma_gather4(&S.ring[s][lane][0], pay_map, rows, &S.full[s]);
-            if (kGradMaps) tma_gather4(&S.gring[kGradMaps ? s : 0][lane][0], gpay_map, rows, &S.full[s]);
+                for (int q = 0; q < 4; ++q) rows[q] = __shfl_sync(0xffffffffu, g, min(4 * (lane & 7) + q, n - 1));
+                if (lane < ((n + 3) >> 2)) tma_gather4(&S.ring[s][lane][0], pay_map, rows, &S.landed[s]);
+            }
+            ++next;
+            progress = true;
         }
-        if (++s == kStages) {
-            s = 0;
-            phase ^= 1;
+        const int issued = min(next, n_fills);
+        if (fin < issued && ready(&S.landed[fin % kStages], (fin / kStages) & 1)) {
+            const int sp = fin % kStages;
+            if (with_rec && lane < S.count[sp]) make_record(ring_at(S, sp, lane), S.frame, thrk, &S.rec[sp][lane][0], kGrad);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.full[sp]);
+            ++fin;
+            progress = true;
+        }
+        if (next > n_fills && fin == n_fills) break;
+        if (!progress) {  // sleep on the gather we wait for, else on the slot we wait for
+            if (fin < issued)
+                mbar_try_wait_suspend(&S.landed[fin % kStages], (fin / kStages) & 1);
+            else
+                mbar_try_wait_suspend(&S.empty[next % kStages], ((next / kStages) & 1) ^ 1);
         }
     }
     if (lane == 0) *((volatile int *)&S.stop) = 1;
-    // No bulk copy may still be writing shared memory when the CTA retires: wait for the fills
-    // nobody may have waited for.  (After a sentinel, fill b - kStages is known to be consumed and
-    // its slot's barrier has moved on to the sentinel's phase, so it is excluded.)
-    if (streamed && lane == 0) atomicAdd(streamed, (unsigned long long)min(n_total, kStageEntries * b));
-    const int oldest = sentinel ? b - kStages + 1 : b - kStages;
-    for (int f = b - 1; f >= 0 && f >= oldest; --f) mbar_wait(&S.full[f % kStages], (f / kStages) & 1);
+    const int issued = min(next, n_fills);
+    if (streamed && lane == 0) atomicAdd(streamed, (unsigned long long)min(n_total, kStageEntries * issued));
+    // No bulk copy may still be writing shared memory when the CTA retires: wait for the fills not
+    // yet finished (each is the latest fill of its slot).
+    for (int f = fin; f < issued; ++f) mbar_wait(&S.landed[f % kStages], (f / kStages) & 1);
 }
 
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
@@ -447,16 +542,6 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
 __device__ __forceinline__ float lds_f32(uint32_t a) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ double2 lds_d2(uint32_t a) {
-    double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {
@@ -477,28 +562,18 @@ static_assert(offsetof(Payload, col) == kColOff && offsetof(Payload, ext) == kEx
 // warp).  Writes the warp's compacted, null-padded entry list; returns the kept count and (via m)
 // the kept mask.
 template <class Smem>
-__device__ __forceinline__ int stage_keep(Smem &S, int s, int warp, int lane, int n, bool cull, const float4 &patch,
-                                          const float4 &pcone, uint32_t &m, bool &any_m1) {
-    const uint32_t rb = smem_u32(&S.ring[s][0][0]);
-    const uint32_t pa = rb + ring_off(lane);  // this lane's entry of the stage
+__device__ __forceinline__ int stage_keep(Smem &S, int s, int warp, int lane, int n, bool cull, uint32_t &m) {
+    const uint32_t pa = smem_u32(&S.ring[s][0][0]) + ring_off(lane);  // this lane's entry of the stage
     bool ov = lane < n;
-    // a mode-1 (cross-product) payload anywhere in the stage selects the generic evaluation
-    any_m1 = __any_sync(0xffffffffu, ov && lds_f32(pa + kColOff + 12) < 0.0f);
     if (cull && ov) {
+        const float4 patch = S.wc[warp][0], pcone = S.wc[warp][1];
         const float4 bx = lds_f4(pa + kCullOff), k0 = lds_f4(pa + kCullOff + 16), k1 = lds_f4(pa + kCullOff + 32);
         ov = !(bx.y < patch.x || bx.x > patch.y || bx.w < patch.z || bx.z > patch.w) && !cone_misses(k0, k1, pcone);
     }
     m = __ballot_sync(0xffffffffu, ov);
     const int c = __popc(m);
-    if (ov) {
-        const int pos = __popc(m & ((1u << lane) - 1u));
-        S.idx[s][warp][pos] = (uint8_t)lane;
-        S.iadr[s][warp][pos] = rb + ring_off(lane);
-    }
-    if (lane < 4) {  // pad to a multiple of 4
-        S.idx[s][warp][c + lane] = (uint8_t)kStageEntries;
-        S.iadr[s][warp][c + lane] = rb + ring_off(kStageEntries);
-    }
+    if (ov) S.idx[s][warp][__popc(m & ((1u << lane) - 1u))] = (uint8_t)lane;
+    if (lane < 4) S.idx[s][warp][c + lane] = (uint8_t)kStageEntries;  // pad to a multiple of 4
     __syncwarp();
     return c;
 }
@@ -513,8 +588,10 @@ __device__ __forceinline__ void pipe_drop_out(Smem &S, int s, unsigned phase) {
     for (int k = 0; k < kStages; ++k) {
         if (k > 0) {
             bool ready = false;
-            while (!(ready = mbar_try_wait(&S.full[s], phase)))
+            while (!(ready = mbar_try_wait(&S.full[s], phase))) {
                 if (*((volatile int *)&S.stop)) break;
+                __nanosleep(256);  // (a retired warp: do not take issue slots from the working ones)
+            }
             if (!ready || S.count[s] == 0) return;
         }
         __syncwarp();
@@ -524,6 +601,38 @@ __device__ __forceinline__ void pipe_drop_out(Smem &S, int s, unsigned phase) {
             phase ^= 1;
         }
     }
+}
+
+// ------------------------------------------------------------------------------ pair evaluation from records
+
+// k = kHalfLog2e kappa, dd = |d_u|^2 and the scaled m of the record at shared address ra for pixel X
+// (fp32 with explicit rounding: the forward and backward kernels evaluate bit-identical values).
+// Also returns the record's (D4, D5, sigma, tol) and trel.
+__device__ __forceinline__ void rec_k(uint32_t ra, const PixXY &X, float &k, float &dd, float (&m)[3], float4 &c1,
+                                      float &trel) {
+    const float4 c0 = lds_f4(ra), c2 = lds_f4(ra + 32), c3 = lds_f4(ra + 48), c4 = lds_f4(ra + 64);
+    c1 = lds_f4(ra + 16);
+    dd = __fmaf_rn(c1.y, X.yy, __fmaf_rn(c1.x, X.xy, __fmaf_rn(c0.w, X.xx, __fmaf_rn(c0.z, X.y, __fmaf_rn(c0.y, X.x, c0.x)))));
+    m[0] = __fmaf_rn(c2.z, X.y, __fmaf_rn(c2.y, X.x, c2.x));
+    m[1] = __fmaf_rn(c3.z, X.y, __fmaf_rn(c3.y, X.x, c3.x));
+    m[2] = __fmaf_rn(c4.z, X.y, __fmaf_rn(c4.y, X.x, c4.x));
+    const float mm = __fmaf_rn(m[2], m[2], __fmaf_rn(m[1], m[1], __fmul_rn(m[0], m[0])));
+    k = __fmul_rn(mm, rcp_approx(dd));
+    trel = c2.w;
+}
+
+// fp64 re-decision of a pair whose k lies within tol of the cutoff: kappa from the payload's W and o_u
+// (the reference's cross product) for the fp64 ray.  Returns inside; kout = kHalfLog2e kappa64 (t then
+// follows from it, so a record too coarse for fp32 still yields the right t); unc = even fp64 cannot
+// decide (the pixel goes to the fix-up).
+__device__ __forceinline__ bool recheck(const Payload &P, const double *dray, const FrameConst &fc, bool &unc,
+                                        float &kout) {
+    double dd, mm;
+    norms64(P, dray, dd, mm);
+    const double k64 = mm / dd;
+    unc = fc.cutoff && fabs(k64 - fc.lam2) <= (double)P.ext.x;
+    kout = (float)(kHalfLog2e * k64);
+    return !fc.cutoff || k64 <= fc.lam2;
 }
 
 // ------------------------------------------------------------------------------ K5
@@ -545,9 +654,11 @@ struct PixelState {
 // in [r - err, r + err].  A pixel stops either surely opaque or "borderline" (test, or this entry's
 // cutoff, too close to call: redone in fp64 by k_fixup; see pixel_border).  Stopped pixels carry
 // r = 0, which turns every later update into a no-op without branches, and an entry with t = 0
-// changes nothing, so skipping it (PBF culling, null padding entries) is exact.
-__device__ __forceinline__ void pixel_update(PixelState &ps, float kap, float t, const float4 &col, bool unc, int jne) {
-    if (unc) {  // rare: this entry's cutoff is undecidable in fp64 -> whole pixel to the fp64 fix-up
+// changes nothing, so skipping it (PBF culling, null padding entries) is exact.  trel bounds the
+// relative error of t.
+template <bool kUnc>
+__device__ __forceinline__ void pixel_update(PixelState &ps, float trel, float t, const float4 &col, bool unc, int jne) {
+    if (kUnc && unc) {  // rare: this entry's cutoff is undecidable in fp64 -> whole pixel to the fp64 fix-up
         ps.border |= ps.r > 0.0f ? 1 : 0;
         ps.rfin = ps.r > 0.0f ? ps.r : ps.rfin;
         ps.r = 0.0f;
@@ -557,8 +668,9 @@ __device__ __forceinline__ void pixel_update(PixelState &ps, float kap, float t,
     ps.cr = __fmaf_rn(w, col.x, ps.cr);
     ps.cg = __fmaf_rn(w, col.y, ps.cg);
     ps.cb = __fmaf_rn(w, col.z, ps.cb);
-    // |d r'| <= |d r| (1 - t) + r |d t| + rounding (none when t = 0),  |d t| <= t * t_rel_bound
-    ps.err = __fmaf_rn(ps.err, omt, __fmaf_rn(w, t_rel_bound(kap), w > 0.0f ? __fmul_rn(ps.r, 1.2e-7f) : 0.0f));
+    // |d r'| <= |d r| (1 - t) + r |d t| + rounding (none when t = 0: skipping such an entry - PBF
+    // culling, a shorter list - stays an exact no-op),  |d t| <= t * trel
+    ps.err = __fmaf_rn(ps.err, omt, __fmaf_rn(w, trel, w > 0.0f ? __fmul_rn(ps.r, 1.2e-7f) : 0.0f));
     ps.cnt += w > 0.0f ? 1 : 0;
     ps.r = __fmul_rn(ps.r, omt);
     const bool stop = (ps.r > 0.0f) & (__fsub_rn(ps.r, ps.err) < 1.00001e-4f);
@@ -573,314 +685,132 @@ __device__ __forceinline__ bool pixel_border(const PixelState &ps) {
     return ps.border || (ps.r == 0.0f && ps.efin >= 0.0f && __fadd_rn(ps.rfin, ps.efin) >= 0.99999e-4f);
 }
 
-// Mode-0 norms from a payload at shared address pa (same arithmetic as norms64).
-__device__ __forceinline__ void norms64_smem(uint32_t pa, const Ray64 &R, double &dd, double &mm) {
-    const double2 a0 = lds_d2(pa + 0), a1 = lds_d2(pa + 16), a2 = lds_d2(pa + 32);
-    const double2 b0 = lds_d2(pa + 48), b1 = lds_d2(pa + 64), b2 = lds_d2(pa + 80);
-    dd = qform(a0, a1, a2, R);
-    mm = qform(b0, b1, b2, R);
-}
-
-
-// The entries of one stage that this warp's culling keeps, front to back, a few at a time (the list
-// is padded with null entries, which are exact no-ops).  Culled entries change nothing; the alive
-// count is recorded when a pixel stops (base: entries of the tile before this stage).  Each thread
-// owns PX pixels: one payload load from shared memory serves all of them.
-//
-// Stage of mode-1 payloads (rare: tiny, far or very anisotropic Gaussians): the payload mode is
-// decided per entry and each entry runs the reference formulation via finish_t.
-template <int PX, class Smem>
-__device__ __forceinline__ void consume_stage_generic(Smem &S, int s, int warp, int cnt, int base, const Ray64 (&R)[PX],
-                                                      const double *const (&dray)[PX], const FrameConst &fc,
-                                                      PixelState (&ps)[PX], int &rechecks, int &went) {
+// The entries of one stage that this warp's culling keeps, front to back, four at a time (the list
+// is padded with null entries, which are exact no-ops): the fp64 path of items without a frame.
+template <class Smem>
+__device__ __forceinline__ void consume_stage_generic(Smem &S, int s, int warp, int cnt, int base, const double *dray,
+                                                      const FrameConst &fc, PixelState &ps, int &rechecks, int &went) {
     int k0 = 0;
     for (; k0 < cnt; k0 += 4) {
-        bool live = false;
-#pragma unroll
-        for (int x = 0; x < PX; ++x) live |= ps[x].r > 0.0f;
-        if (k0 > 0 && !__any_sync(0xffffffffu, live)) break;  // warp opaque
+        if (k0 > 0 && !__any_sync(0xffffffffu, ps.r > 0.0f)) break;  // warp opaque
         const uint32_t q = *reinterpret_cast<const uint32_t *>(&S.idx[s][warp][k0]);
 #pragma unroll 1
         for (int u = 0; u < 4; ++u) {
             const int j = (q >> (8 * u)) & 0xFF;
             const Payload &P = ring_at(S, s, j);
-            const bool m1 = __any_sync(0xffffffffu, P.col.w < 0.0f);
-#pragma unroll
-            for (int x = 0; x < PX; ++x) {
-                double dd, mm;
-                norms64(P, R[x], dray[x], m1, dd, mm);
-                PairT e;
-                const bool unc = finish_t(dd, mm, P, m1, fc, e, rechecks);
-                pixel_update(ps[x], e.kap, e.t, P.col, unc, base + j + 1);
-            }
+            PairT e;
+            const bool unc = eval_t(P, dray, fc, e, rechecks);
+            pixel_update<true>(ps, t_rel_bound(e.kap), e.t, P.col, unc, base + j + 1);
         }
     }
     went += k0 < cnt ? k0 : cnt;
 }
 
-// Mode-0 pair evaluation from a payload at shared address pa: norms64 + finish_t with m1 = false,
-// operation for operation (t, kappa, alpha, u, dd bit-identical to eval_t's).
-__device__ __forceinline__ void eval_t0_smem(uint32_t pa, const Ray64 &R, const FrameConst &fc, PairT &e) {
-    double dd, mm;
-    norms64_smem(pa, R, dd, mm);
-    const float sw = lds_f32(pa + kColOff + 12);
-    e.dd = (float)dd;
-    e.kap = __fmul_rn((float)mm, rcp_approx(e.dd));
-    e.alpha = ex2_approx(__fmul_rn(e.kap, -0.72134752044448170f));
-    float u = __fmul_rn(fabsf(sw), e.alpha);
-    if (fc.cutoff) {
-        bool inside = e.kap <= fc.lam2f;
-        if (fabsf(__fsub_rn(e.kap, fc.lam2f)) <= fc.cutoff_tol) inside = mm / dd <= fc.lam2;
-        u = inside ? u : 0.0f;
-    }
-    e.u = u;
-    e.t = fminf(u, kMaxBlendTF);
-}
-
-#ifndef GEER_COL_EARLY
-#define GEER_COL_EARLY 0  // read each entry's colour with its sigma (one shared load less, 12 more registers)
-#endif
-#ifndef GEER_FWD_GROUP
-#define GEER_FWD_GROUP 4
-#endif
-
-// GG mode-0 entries (shared addresses pa, alive counts jne if a pixel stops on them) against the
-// thread's pixels: the entries' t first (independent work, explicit shared loads), one warp vote for
-// the rare fp64 cutoff re-decisions, then the serial pixel updates (without the undecidable-cutoff
-// handling unless one occurred).  t is bit-identical to finish_t's (the backward recomputes it).
-template <bool kCutoff, int PX, int GG>
-__device__ __forceinline__ void fast_group(const uint32_t (&pa)[GG], const int (&jne)[GG], const Ray64 (&R)[PX],
-                                           const FrameConst &fc, PixelState (&ps)[PX], int &rechecks) {
-    float kap[GG][PX], t[GG][PX];
-    bool near[GG][PX], unc[GG][PX];
-#if GEER_COL_EARLY
-    float4 colv[GG];
-#endif
+// GG kept entries (stage indices jj) against the thread's pixel: the entries' t first (independent
+// work), one warp vote for the rare fp64 cutoff re-decisions, then the serial pixel updates
+// (without the undecidable-cutoff handling unless one occurred).  fc.thrkc is the cutoff in k units
+// (+inf without the support cutoff: nothing is outside, nothing is near).
+template <int GG, class Smem>
+__device__ __forceinline__ void rec_group(Smem &S, int s, const int (&jj)[GG], int jbase, const PixXY &X,
+                                          const double *dray, const FrameConst &fc, PixelState &ps, int &rechecks) {
+    const uint32_t rb = smem_u32(&S.rec[s][0][0]);
+    float t[GG], trel[GG];
+    bool near[GG];
     bool any_near = false;
 #pragma unroll
     for (int u = 0; u < GG; ++u) {
-        const double2 a0 = lds_d2(pa[u] + 0), a1 = lds_d2(pa[u] + 16), a2 = lds_d2(pa[u] + 32);
-        const double2 b0 = lds_d2(pa[u] + 48), b1 = lds_d2(pa[u] + 64), b2 = lds_d2(pa[u] + 80);
-#if GEER_COL_EARLY
-        colv[u] = lds_f4(pa[u] + kColOff);
-        const float sw = colv[u].w;
-#else
-        const float sw = lds_f32(pa[u] + kColOff + 12);
-#endif
-#pragma unroll
-        for (int x = 0; x < PX; ++x) {
-            const Ray64 &r = R[x];
-            // (same arithmetic as norms64 mode 0)
-            const double dd = qform(a0, a1, a2, r);
-            const double mm = qform(b0, b1, b2, r);
-            kap[u][x] = __fmul_rn((float)mm, rcp_approx((float)dd));
-            float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u][x], -0.72134752044448170f)));
-            near[u][x] = false;
-            unc[u][x] = false;
-            if (kCutoff) {
-                near[u][x] = fabsf(__fsub_rn(kap[u][x], fc.lam2f)) <= fc.cutoff_tol;
-                any_near |= near[u][x];
-                uu = kap[u][x] <= fc.lam2f ? uu : 0.0f;
-            }
-            t[u][x] = fminf(uu, kMaxBlendTF);
-        }
+        float k, dd, m[3];
+        float4 c1;
+        rec_k(rb + (uint32_t)jj[u] * (kRecF * 4), X, k, dd, m, c1, trel[u]);
+        near[u] = fabsf(__fsub_rn(k, fc.thrkc)) <= c1.w;
+        any_near |= near[u];
+        const float uu = __fmul_rn(c1.z, ex2_approx(-k));
+        t[u] = k <= fc.thrkc ? fminf(uu, kMaxBlendTF) : 0.0f;
     }
+    bool unc[GG];
+#pragma unroll
+    for (int u = 0; u < GG; ++u) unc[u] = false;
     bool any_unc = false;
-    if (kCutoff && __any_sync(0xffffffffu, any_near)) {
+    if (__any_sync(0xffffffffu, any_near)) {
 #pragma unroll
-        for (int u = 0; u < GG; ++u) {  // (fully unrolled: the arrays stay in registers)
-#pragma unroll
-            for (int x = 0; x < PX; ++x) {
-                if (!near[u][x]) continue;
-                double dd, mm;
-                norms64_smem(pa[u], R[x], dd, mm);
-                const double k64 = mm / dd;
-                const float sw = lds_f32(pa[u] + kColOff + 12);
-                const float uu = __fmul_rn(fabsf(sw), ex2_approx(__fmul_rn(kap[u][x], -0.72134752044448170f)));
-                t[u][x] = k64 <= fc.lam2 ? fminf(uu, kMaxBlendTF) : 0.0f;
-                unc[u][x] = fabs(k64 - fc.lam2) <= (double)lds_f32(pa[u] + kExtOff);
-                any_unc |= unc[u][x];
-                ++rechecks;
-            }
+        for (int u = 0; u < GG; ++u) {
+            if (!near[u]) continue;
+            float kr;
+            const bool in64 = recheck(ring_at(S, s, jj[u]), dray, fc, unc[u], kr);
+            const float uu = __fmul_rn(lds_f32(rb + (uint32_t)jj[u] * (kRecF * 4) + 24), ex2_approx(-kr));  // sigma
+            t[u] = in64 ? fminf(uu, kMaxBlendTF) : 0.0f;
+            any_unc |= unc[u];
+            ++rechecks;
         }
         any_unc = __any_sync(0xffffffffu, any_unc);
     }
     if (!any_unc) {
 #pragma unroll
-        for (int u = 0; u < GG; ++u) {
-#if GEER_COL_EARLY
-            const float4 col = colv[u];
-#else
-            const float4 col = lds_f4(pa[u] + kColOff);
-#endif
-#pragma unroll
-            for (int x = 0; x < PX; ++x) pixel_update(ps[x], kap[u][x], t[u][x], col, false, jne[u]);
-        }
+        for (int u = 0; u < GG; ++u)
+            pixel_update<false>(ps, trel[u], t[u], lds_f4(rb + (uint32_t)jj[u] * (kRecF * 4) + 80), false, jbase + jj[u]);
     } else {
 #pragma unroll
-        for (int u = 0; u < GG; ++u) {
-#if GEER_COL_EARLY
-            const float4 col = colv[u];
-#else
-            const float4 col = lds_f4(pa[u] + kColOff);
-#endif
-#pragma unroll
-            for (int x = 0; x < PX; ++x) pixel_update(ps[x], kap[u][x], t[u][x], col, unc[u][x], jne[u]);
-        }
+        for (int u = 0; u < GG; ++u)
+            pixel_update<true>(ps, trel[u], t[u], lds_f4(rb + (uint32_t)jj[u] * (kRecF * 4) + 80), unc[u], jbase + jj[u]);
     }
 }
 
-// Stage of mode-0 payloads (the common case): the warp's kept entries in groups of G = 4, then the
-// last cnt % 4 as a pair and/or a single (the null padding of the list is never evaluated).
-template <bool kCutoff, int PX, int G, class Smem>
-__device__ __forceinline__ void consume_stage_fast(Smem &S, int s, int warp, int cnt, int base, const Ray64 (&R)[PX],
-                                                   const FrameConst &fc, PixelState (&ps)[PX], int &rechecks,
-                                                   int &went) {
-    static_assert(G == 4, "entries are consumed in groups of 4 (one 16-B load of their addresses)");
+// Stage of an item with a frame: the warp's kept entries in groups of 4, then the last cnt % 4 one
+// at a time (the null padding of the list is never evaluated).
+template <class Smem>
+__device__ __forceinline__ void consume_stage_rec(Smem &S, int s, int warp, int cnt, int base, const PixXY &X,
+                                                  const double *dray, const FrameConst &fc, PixelState &ps,
+                                                  int &rechecks, int &went) {
 #ifdef GEER_EXP_NOCOMPUTE
     went += cnt;
     return;  // tuning experiment: the pipeline alone (results are wrong)
 #endif
     const uint32_t ib = smem_u32(&S.idx[s][warp][0]);
-    const uint32_t ab = smem_u32(&S.iadr[s][warp][0]);
     const int jbase = base + 1;
-    auto warp_live = [&]() {
-        bool live = false;
-#pragma unroll
-        for (int x = 0; x < PX; ++x) live |= ps[x].r > 0.0f;
-        return __any_sync(0xffffffffu, live);
-    };
     int k0 = 0;
-    for (; k0 + G <= cnt; k0 += G) {
-        if (k0 > 0 && !warp_live()) {  // warp opaque
+    for (; k0 + 4 <= cnt; k0 += 4) {
+        if (k0 > 0 && !__any_sync(0xffffffffu, ps.r > 0.0f)) {  // warp opaque
             went += k0;
             return;
         }
         const uint32_t q = lds_u32(ib + k0);
-        const uint4 adr = lds_u4(ab + 4 * k0);
-        const uint32_t pa[G] = {adr.x, adr.y, adr.z, adr.w};
-        int jne[G];
-#pragma unroll
-        for (int u = 0; u < G; ++u) jne[u] = jbase + (int)__byte_perm(q, 0u, 0x4440u + u);
-        fast_group<kCutoff, PX, G>(pa, jne, R, fc, ps, rechecks);
+        const int jj[4] = {(int)(q & 0xFF), (int)((q >> 8) & 0xFF), (int)((q >> 16) & 0xFF), (int)(q >> 24)};
+        rec_group<4>(S, s, jj, jbase, X, dray, fc, ps, rechecks);
     }
-    if (k0 < cnt && (k0 == 0 || warp_live())) {
-        const uint32_t q = lds_u32(ib + k0);  // (k0 is a multiple of 4)
-        if (cnt - k0 >= 2) {  // a pair, then possibly one more
-            const uint2 adr = make_uint2(lds_u32(ab + 4 * k0), lds_u32(ab + 4 * k0 + 4));
-            const uint32_t pa[2] = {adr.x, adr.y};
-            const int jne[2] = {jbase + (int)__byte_perm(q, 0u, 0x4440u), jbase + (int)__byte_perm(q, 0u, 0x4441u)};
-            fast_group<kCutoff, PX, 2>(pa, jne, R, fc, ps, rechecks);
-            k0 += 2;
-        }
-        if (k0 < cnt) {
-            const uint32_t pa[1] = {lds_u32(ab + 4 * k0)};
-            const int jne[1] = {jbase + (int)__byte_perm(q, 0u, 0x4440u + (k0 & 3))};
-            fast_group<kCutoff, PX, 1>(pa, jne, R, fc, ps, rechecks);
-            ++k0;
-        }
+#pragma unroll 1
+    for (; k0 < cnt; ++k0) {
+        if (k0 > 0 && !__any_sync(0xffffffffu, ps.r > 0.0f)) break;
+        const int jj[1] = {(int)*(const uint8_t *)&S.idx[s][warp][k0]};
+        rec_group<1>(S, s, jj, jbase, X, dray, fc, ps, rechecks);
     }
     went += k0;
 }
 
-// Camera-frame mirror coordinates of a world ray (the CSF/PBF space of association.py:91-126):
-// m = tan(angle / 2) of its (x, z) and (y, z) projections, outward-rounded to fp32.  Rays with
-// z <= 0 on an axis leave that axis unbounded (no culling there).
-__device__ __forceinline__ float4 ray_mirror_bounds(const FrameConst &fc, const double d[3]) {
-    double c[3];
-    for (int i = 0; i < 3; ++i) c[i] = fma(fc.R[i * 3 + 2], d[2], fma(fc.R[i * 3 + 1], d[1], fc.R[i * 3 + 0] * d[0]));
-    float4 b = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
-    if (c[2] > 0.0) {
-        const double mx = c[0] / (sqrt(c[0] * c[0] + c[2] * c[2]) + c[2]);
-        const double my = c[1] / (sqrt(c[1] * c[1] + c[2] * c[2]) + c[2]);
-        b = make_float4(__double2float_rd(mx), __double2float_ru(mx), __double2float_rd(my), __double2float_ru(my));
-    }
-    return b;
-}
-
-// Cone around a warp's pixel rays in the camera frame (PX rays per lane): axis c = normalised sum of
-// the rays, sin^2(beta) = max over rays of |c x d|^2 / |d|^2, widened by 2% + 1e-9 for rounding (no
-// transcendental functions: this runs once per CTA on every consumer thread).
-template <int PX>
-__device__ __forceinline__ float4 warp_cone(const FrameConst &fc, const bool (&valid)[PX], const double (&d)[PX][3]) {
-    double c[PX][3];
-    double sx = 0.0, sy = 0.0, sz = 0.0;
-#pragma unroll
-    for (int x = 0; x < PX; ++x) {
-        for (int i = 0; i < 3; ++i)
-            c[x][i] = valid[x] ? fma(fc.R[i * 3 + 2], d[x][2], fma(fc.R[i * 3 + 1], d[x][1], fc.R[i * 3 + 0] * d[x][0]))
-                               : 0.0;
-        sx += c[x][0];
-        sy += c[x][1];
-        sz += c[x][2];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        sx += __shfl_xor_sync(0xffffffffu, sx, o);
-        sy += __shfl_xor_sync(0xffffffffu, sy, o);
-        sz += __shfl_xor_sync(0xffffffffu, sz, o);
-    }
-    const double nrm2 = sx * sx + sy * sy + sz * sz;
-    float sin2 = 0.f;
-#pragma unroll
-    for (int x = 0; x < PX; ++x) {
-        if (valid[x] && nrm2 > 0.0) {
-            const double x0 = sy * c[x][2] - sz * c[x][1], x1 = sz * c[x][0] - sx * c[x][2], x2 = sx * c[x][1] - sy * c[x][0];
-            const double dn2 = c[x][0] * c[x][0] + c[x][1] * c[x][1] + c[x][2] * c[x][2];
-            sin2 = fmaxf(sin2, (float)((x0 * x0 + x1 * x1 + x2 * x2) / (nrm2 * dn2)));  // |c_hat x d_hat|^2
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sin2 = fmaxf(sin2, __shfl_xor_sync(0xffffffffu, sin2, o));
-    sin2 = fmaf(sin2, 1.02f, 1e-9f);
-    const float inv = nrm2 > 0.0 ? (float)(1.0 / sqrt(nrm2)) : 0.f;
-    // the bound needs beta <= 45 deg (sin^2 <= 0.5); cos^2 = 0 disables the test otherwise
-    return nrm2 > 0.0 && sin2 < 0.5f ? make_float4((float)sx * inv, (float)sy * inv, (float)sz * inv, 1.0f - sin2)
-                                     : make_float4(0.f, 0.f, 1.f, 0.f);
-}
-__device__ __forceinline__ float4 warp_cone1(const FrameConst &fc, bool valid, const double (&d)[3]) {
-    const bool v[1] = {valid};
-    const double dd[1][3] = {{d[0], d[1], d[2]}};
-    return warp_cone<1>(fc, v, dd);
-}
-
-__device__ __forceinline__ float4 bounds_union(const float4 &a, const float4 &b) {
-    return make_float4(fminf(a.x, b.x), fmaxf(a.y, b.y), fminf(a.z, b.z), fmaxf(a.w, b.w));
-}
-
-// Warp-wide union of the lanes' mirror bounds (lanes without a pixel contribute nothing); lane 0
-// stores it as the warp's patch for the producer's culling masks.
-__device__ __forceinline__ float4 warp_patch(bool valid, float4 b) {
-    if (!valid) b = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        b.x = fminf(b.x, __shfl_xor_sync(0xffffffffu, b.x, o));
-        b.y = fmaxf(b.y, __shfl_xor_sync(0xffffffffu, b.y, o));
-        b.z = fminf(b.z, __shfl_xor_sync(0xffffffffu, b.z, o));
-        b.w = fmaxf(b.w, __shfl_xor_sync(0xffffffffu, b.w, o));
-    }
-    return b;
-}
-
-// Per-warp culling regions of every raster work item (PBF patch in mirror space, ray cone), cached
-// with the camera: wcull[(item * kConsumerWarps + warp) * 2 + {0, 1}] = patch, cone.  Computed in
-// fp32 from the camera-frame pixel rays and widened outward far beyond fp32 rounding (1e-5 in
-// mirror units, 2 % of sin^2 of the cone): a larger region only keeps more t = 0 entries, so the
-// culling stays exact.
+// Per-warp culling regions and the frame of every raster work item, cached with the camera:
+// wcull[(item * kConsumerWarps + warp) * 2 + {0, 1}] = patch, cone; iframe[item].  The culling
+// regions are computed in fp32 from the camera-frame pixel rays and widened outward far beyond fp32
+// rounding (1e-5 in mirror units, 2 % of sin^2 of the cone): a larger region only keeps more t = 0
+// entries, so the culling stays exact.  The frame is fp64: dc = normalised sum of the item's world
+// rays, e1 / e2 completing an orthonormal basis; rx, ry = max |x|, |y| of the item's pixel offsets
+// (pixel_xy, the raster's own function), or rx = -1 when some ray is more than 60 deg from dc.
 template <bool kBEAP>
 __global__ void __launch_bounds__(kRasterThreads) k_warp_cull(FrameConst fc, const int4 *__restrict__ items,
                                                               const int32_t *__restrict__ n_items,
                                                               const int32_t *__restrict__ pix_list,
                                                               const double2 *__restrict__ col_sc,
                                                               const double2 *__restrict__ row_sc,
-                                                              const double *__restrict__ dir64, float4 *__restrict__ wcull) {
+                                                              const double *__restrict__ dir64, float4 *__restrict__ wcull,
+                                                              ItemFrame *__restrict__ iframe) {
+    __shared__ double sred[kConsumerWarps][3];
+    __shared__ float sxy[kConsumerWarps][3];
+    __shared__ ItemFrame sF;
     if ((int)blockIdx.x >= n_items[0]) return;
     const int4 it = items[blockIdx.x];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool valid = tid < it.z;
+    const int p = valid ? pix_list[it.y + tid] : 0;
     float c[3] = {0.f, 0.f, 1.f};  // camera-frame ray
     if (valid) {
-        const int p = pix_list[it.y + tid];
         if (kBEAP) {  // camera.py:141-155 angles_to_dir
             const double2 cs = col_sc[p % fc.width], rs = row_sc[p / fc.width];
             const float x = (float)cs.x * (float)rs.y, y = (float)cs.y * (float)rs.x, z = (float)cs.y * (float)rs.y;
@@ -901,7 +831,15 @@ __global__ void __launch_bounds__(kRasterThreads) k_warp_cull(FrameConst fc, con
         const float my = c[1] / (sqrtf(c[1] * c[1] + c[2] * c[2]) + c[2]);
         b = make_float4(mx - 1e-5f, mx + 1e-5f, my - 1e-5f, my + 1e-5f);
     }
-    const float4 patch = warp_patch(valid, b);
+    if (!valid) b = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        b.x = fminf(b.x, __shfl_xor_sync(0xffffffffu, b.x, o));
+        b.y = fmaxf(b.y, __shfl_xor_sync(0xffffffffu, b.y, o));
+        b.z = fminf(b.z, __shfl_xor_sync(0xffffffffu, b.z, o));
+        b.w = fmaxf(b.w, __shfl_xor_sync(0xffffffffu, b.w, o));
+    }
+    const float4 patch = b;
     // ray cone: axis = normalised sum of the rays, sin^2(beta) = max |axis x ray|^2
     float sx = valid ? c[0] : 0.f, sy = valid ? c[1] : 0.f, sz = valid ? c[2] : 0.f;
 #pragma unroll
@@ -930,6 +868,78 @@ __global__ void __launch_bounds__(kRasterThreads) k_warp_cull(FrameConst fc, con
         wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 0] = patch;
         wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 1] = cone;
     }
+    // ---- the item frame (fp64 world rays, as the raster computes them)
+    double d[3] = {0.0, 0.0, 0.0};
+    if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d);
+    double ws[3] = {d[0], d[1], d[2]};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        for (int i = 0; i < 3; ++i) ws[i] += __shfl_xor_sync(0xffffffffu, ws[i], o);
+    if (lane == 0)
+        for (int i = 0; i < 3; ++i) sred[warp][i] = ws[i];
+    __syncthreads();
+    if (tid == 0) {
+        double sum[3] = {0.0, 0.0, 0.0};
+        for (int w = 0; w < kConsumerWarps; ++w)
+            for (int i = 0; i < 3; ++i) sum[i] += sred[w][i];
+        const double nn = sqrt(sum[0] * sum[0] + sum[1] * sum[1] + sum[2] * sum[2]);
+        ItemFrame F{};
+        if (nn > 0.0) {
+            for (int i = 0; i < 3; ++i) F.dc[i] = sum[i] / nn;
+            int k = 0;  // the axis least aligned with dc
+            for (int i = 1; i < 3; ++i)
+                if (fabs(F.dc[i]) < fabs(F.dc[k])) k = i;
+            double e[3] = {-F.dc[k] * F.dc[0], -F.dc[k] * F.dc[1], -F.dc[k] * F.dc[2]};
+            e[k] += 1.0;
+            const double en = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+            for (int i = 0; i < 3; ++i) F.e1[i] = e[i] / en;
+            F.e2[0] = F.dc[1] * F.e1[2] - F.dc[2] * F.e1[1];
+            F.e2[1] = F.dc[2] * F.e1[0] - F.dc[0] * F.e1[2];
+            F.e2[2] = F.dc[0] * F.e1[1] - F.dc[1] * F.e1[0];
+            const double e2n = sqrt(F.e2[0] * F.e2[0] + F.e2[1] * F.e2[1] + F.e2[2] * F.e2[2]);
+            for (int i = 0; i < 3; ++i) F.e2[i] /= e2n;
+            F.rx = 0.f;
+        } else {
+            F.rx = -1.f;
+        }
+        sF = F;
+    }
+    __syncthreads();
+    float ax = 0.f, ay = 0.f, bad = sF.rx < 0.f ? 1.f : 0.f;
+    if (valid && sF.rx >= 0.f) {
+        const double den = d[0] * sF.dc[0] + d[1] * sF.dc[1] + d[2] * sF.dc[2];
+        if (!(den > 0.5 * sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]))) {
+            bad = 1.f;
+        } else {
+            const float2 xy = pixel_xy(sF, d);
+            ax = fabsf(xy.x);
+            ay = fabsf(xy.y);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ax = fmaxf(ax, __shfl_xor_sync(0xffffffffu, ax, o));
+        ay = fmaxf(ay, __shfl_xor_sync(0xffffffffu, ay, o));
+        bad = fmaxf(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+    }
+    if (lane == 0) {
+        sxy[warp][0] = ax;
+        sxy[warp][1] = ay;
+        sxy[warp][2] = bad;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        ItemFrame F = sF;
+        float mx = 0.f, my = 0.f, mb = 0.f;
+        for (int w = 0; w < kConsumerWarps; ++w) {
+            mx = fmaxf(mx, sxy[w][0]);
+            my = fmaxf(my, sxy[w][1]);
+            mb = fmaxf(mb, sxy[w][2]);
+        }
+        F.rx = mb > 0.f ? -1.f : mx;
+        F.ry = my;
+        iframe[it.w] = F;
+    }
 }
 
 #ifdef GEER_CTA_TIMING
@@ -945,34 +955,35 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
-#ifndef GEER_FWD_PX
-#define GEER_FWD_PX 1
-#endif
-constexpr int kFwdPX = GEER_FWD_PX;                         // pixels per consumer thread
-constexpr int kFwdNW = kConsumerWarps / kFwdPX;             // consumer warps
-constexpr int kFwdThreads = kRasterThreads / kFwdPX + 32;   // + the producer warp
+constexpr int kFwdThreads = kPipeThreads;  // 8 consumer warps + the producer warp
 #ifndef FWD_MIN_BLOCKS2
-#define FWD_MIN_BLOCKS2 (kFwdPX == 1 ? 3 : 4)
+#define FWD_MIN_BLOCKS2 3
 #endif
-using FwdSmem = PipeSmem<false, kFwdNW>;
+using FwdSmem = PipeSmem<false>;
 
-// K5.  Each consumer thread owns kFwdPX pixels (q = tid + k * 32 * kFwdNW of the work item; the BEAP
-// pixel lists put them in one 8 x 8 patch per warp, k_beap_csr), sharing every payload load and
-// the pipeline overheads between them.
+// Copy an item frame into shared memory (the producer warp; 24 words).
+__device__ __forceinline__ void load_frame(ItemFrame &dst, const ItemFrame *src, int lane) {
+    const uint32_t *s = reinterpret_cast<const uint32_t *>(src);
+    uint32_t *d = reinterpret_cast<uint32_t *>(&dst);
+    if (lane < (int)(sizeof(ItemFrame) / 4)) d[lane] = __ldg(s + lane);
+    __syncwarp();
+}
+
+// K5.  One pixel per consumer thread.
 template <bool kBEAP>
 __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
     k_forward(FrameConst fc, geer_scene sc, const int4 *__restrict__ items, const int32_t *__restrict__ n_items,
               const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
               const double2 *__restrict__ row_sc, const double *__restrict__ dir64, const int32_t *__restrict__ ranges,
               const uint32_t *__restrict__ order, const __grid_constant__ CUtensorMap pay_map,
-              const float4 *__restrict__ wcull, float *__restrict__ color,
+              const float4 *__restrict__ wcull, const ItemFrame *__restrict__ iframe, float *__restrict__ color,
               float *__restrict__ remaining, int32_t *__restrict__ count, int32_t *__restrict__ n_eval,
               unsigned long long *__restrict__ counters, int32_t *__restrict__ fixup_list) {
-    constexpr int PX = kFwdPX, NW = kFwdNW, NT = 32 * kFwdNW;
+    constexpr int NW = kConsumerWarps;
     extern __shared__ __align__(128) unsigned char dsmem[];  // PipeSmem (dynamic: deep rings exceed 48 KB)
     FwdSmem &S = *reinterpret_cast<FwdSmem *>(dsmem);  // 128-B aligned base: TMA destinations, fixed offsets
-    __shared__ double sray[kRasterThreads][3];  // fp64 pixel rays (mode-1 payloads only)
-    // n_items: [0] items with entries (work[0, n0)), [1] empty items (work[max_items - n1, max_items))
+    __shared__ double sray[kRasterThreads][3];  // fp64 pixel rays (re-checks, fp64 path)
+    // n_items: [0] items with entries (work[0, n0)), [1] empty items (the tail of [0, n0 + n1))
     const int n_full = n_items[0];
     if ((int)blockIdx.x >= n_full + n_items[1]) return;
     const int4 it = items[(int)blockIdx.x < n_full ? (int)blockIdx.x : n_full + n_items[1] - 1 - ((int)blockIdx.x - n_full)];
@@ -1001,61 +1012,41 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
         g_cta_went[blockIdx.x] = 0;
     }
 #endif
+    const ItemFrame *F = iframe + it.w;
+    const bool framed = F->rx >= 0.f;  // uniform over the CTA
     // the producer starts streaming right away; the consumers set up their pixels meanwhile
     pipe_init(S);
     if (warp == NW) {
-        pipe_produce<false, false>(S, order, &pay_map, nullptr, e0, e1 - e0, true, &counters[4]);
+        load_frame(S.frame, F, lane);
+        pipe_produce<false>(S, order, &pay_map, fc.thrk, framed, e0, e1 - e0, true, &counters[4]);
         return;
     }
-    int q[PX], p[PX];
-    bool valid[PX];
-    double d64[PX][3];
-    float4 bnd = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
-    bool any_valid = false;
-#pragma unroll
-    for (int x = 0; x < PX; ++x) {
-        q[x] = tid + x * NT;
-        valid[x] = q[x] < it.z;
-        p[x] = valid[x] ? pix_list[it.y + q[x]] : 0;
-        d64[x][0] = 0.0;
-        d64[x][1] = 0.0;
-        d64[x][2] = 1.0;
-        if (valid[x]) {
-            pixel_ray<kBEAP>(fc, p[x], col_sc, row_sc, dir64, d64[x]);
-            if (PX != 1) bnd = bounds_union(bnd, ray_mirror_bounds(fc, d64[x]));
-            any_valid = true;
-        }
+    const int q = tid;
+    const bool valid = q < it.z;
+    const int p = valid ? pix_list[it.y + q] : 0;
+    double d64[3] = {0.0, 0.0, 1.0};
+    PixXY X{0.f, 0.f, 0.f, 0.f, 0.f};
+    if (valid) {
+        pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
+        if (framed) X = make_pxy(pixel_xy(*F, d64));
     }
-    float4 my_patch, my_cone;
-    if (PX == 1) {  // cached with the camera (k_warp_cull: the same computation)
-        my_patch = wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 0];
-        my_cone = wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 1];
-    } else {
-        my_patch = warp_patch(any_valid, bnd);
-        my_cone = warp_cone<PX>(fc, valid, d64);
-    }
+    if (lane < 2) S.wc[warp][lane] = wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + lane];  // (k_warp_cull)
+    __syncwarp();
 #ifdef GEER_CTA_TIMING
     if (tid == 0 && blockIdx.x < (1u << 16)) g_cta_ts[blockIdx.x] = gtimer();
 #endif
-    Ray64 R[PX];
-    const double *dray[PX];
-    PixelState ps[PX];
-#pragma unroll
-    for (int x = 0; x < PX; ++x) {
-        R[x] = make_ray(d64[x]);
-        sray[q[x]][0] = d64[x][0];
-        sray[q[x]][1] = d64[x][1];
-        sray[q[x]][2] = d64[x][2];
-        dray[x] = sray[q[x]];
-        ps[x] = PixelState{0.f, 0.f, 0.f, valid[x] ? 1.0f : 0.0f, 1.0f, 0.f, -1.0f, 0, 0, 0};
-    }
+    sray[q][0] = d64[0];
+    sray[q][1] = d64[1];
+    sray[q][2] = d64[2];
+    const double *dray = sray[q];
+    PixelState ps{0.f, 0.f, 0.f, valid ? 1.0f : 0.0f, 1.0f, 0.f, -1.0f, 0, 0, 0};
     int rechecks = 0, went = 0;
-    bool warp_live = __any_sync(0xffffffffu, any_valid);
+    bool warp_live = __any_sync(0xffffffffu, valid);
     if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
     unsigned phase = 0;
     int s = 0, base = 0;
     for (;;) {
-        mbar_wait(&S.full[s], phase);
+        mbar_wait_suspend(&S.full[s], phase);
 #ifdef GEER_CTA_TIMING
         if (tid == 0 && base == 0 && blockIdx.x < (1u << 16)) g_cta_tf[blockIdx.x] = gtimer();
 #endif
@@ -1063,18 +1054,12 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
         if (n == 0) break;
         if (warp_live) {
             uint32_t m;
-            bool any_m1;
-            const int cnt = stage_keep(S, s, warp, lane, n, fc.cull != 0, my_patch, my_cone, m, any_m1);
-            if (any_m1)  // a mode-1 (cross-product) payload in the stage: the generic path
-                consume_stage_generic<PX>(S, s, warp, cnt, base, R, dray, fc, ps, rechecks, went);
-            else if (fc.cutoff)
-                consume_stage_fast<true, PX, GEER_FWD_GROUP>(S, s, warp, cnt, base, R, fc, ps, rechecks, went);
+            const int cnt = stage_keep(S, s, warp, lane, n, fc.cull != 0, m);
+            if (!framed)
+                consume_stage_generic(S, s, warp, cnt, base, dray, fc, ps, rechecks, went);
             else
-                consume_stage_fast<false, PX, GEER_FWD_GROUP>(S, s, warp, cnt, base, R, fc, ps, rechecks, went);
-            bool live = false;
-#pragma unroll
-            for (int x = 0; x < PX; ++x) live |= ps[x].r > 0.0f;
-            warp_live = __any_sync(0xffffffffu, live);
+                consume_stage_rec(S, s, warp, cnt, base, X, dray, fc, ps, rechecks, went);
+            warp_live = __any_sync(0xffffffffu, ps.r > 0.0f);
             if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
         }
         if (!warp_live) {  // every pixel of the warp opaque: leave the pipeline, stop issuing
@@ -1089,23 +1074,19 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
             phase ^= 1;
         }
     }
-#pragma unroll
-    for (int x = 0; x < PX; ++x) {
-        PixelState &px = ps[x];
-        if (px.r > 0.0f) px.ne = e1 - e0;  // alive through the whole list
-        if (valid[x]) {
-            const float rem = px.r > 0.0f ? px.r : px.rfin;  // live to the end of the list, or stopped
-            // renderer.py:118 background with the final remaining transmittance
-            color[(int64_t)p[x] * 3 + 0] = __fmaf_rn(rem, fc.bg[0], px.cr);
-            color[(int64_t)p[x] * 3 + 1] = __fmaf_rn(rem, fc.bg[1], px.cg);
-            color[(int64_t)p[x] * 3 + 2] = __fmaf_rn(rem, fc.bg[2], px.cb);
-            remaining[p[x]] = rem;
-            count[p[x]] = px.cnt;
-            n_eval[p[x]] = px.ne;
-            if (pixel_border(px)) {
-                unsigned long long slot = atomicAdd(&counters[2], 1ull);
-                fixup_list[slot] = (int32_t)(((int64_t)blockIdx.x << 8) | q[x]);  // work item, pixel of the item
-            }
+    if (ps.r > 0.0f) ps.ne = e1 - e0;  // alive through the whole list
+    if (valid) {
+        const float rem = ps.r > 0.0f ? ps.r : ps.rfin;  // live to the end of the list, or stopped
+        // renderer.py:118 background with the final remaining transmittance
+        color[(int64_t)p * 3 + 0] = __fmaf_rn(rem, fc.bg[0], ps.cr);
+        color[(int64_t)p * 3 + 1] = __fmaf_rn(rem, fc.bg[1], ps.cg);
+        color[(int64_t)p * 3 + 2] = __fmaf_rn(rem, fc.bg[2], ps.cb);
+        remaining[p] = rem;
+        count[p] = ps.cnt;
+        n_eval[p] = ps.ne;
+        if (pixel_border(ps)) {
+            unsigned long long slot = atomicAdd(&counters[2], 1ull);
+            fixup_list[slot] = (int32_t)(((int64_t)blockIdx.x << 8) | q);  // work item, pixel of the item
         }
     }
     rechecks = __reduce_add_sync(0xffffffffu, rechecks);
@@ -1140,9 +1121,8 @@ __device__ void fixup_pixel(FrameConst fc, const geer_scene &sc, const int4 *__r
     double cr = 0, cg = 0, cb = 0, rem = 1.0;
     int cnt = 0, ne = 0;
     bool alive = true;
-    const Ray64 R = make_ray(d);
-    // fp64 t of entry e (renderer.py:96-105 in fp64: payload quadratic forms / cross product, the
-    // reference formulation near the cutoff, fp64 sigmoid and exp)
+    // fp64 t of entry e (renderer.py:96-105 in fp64: the payload's cross product, the reference
+    // formulation near the cutoff, fp64 sigmoid and exp)
     auto eval64 = [&](int e, double &t, float4 &cl) {
         t = 0.0;
         cl = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1151,7 +1131,7 @@ __device__ void fixup_pixel(FrameConst fc, const geer_scene &sc, const int4 *__r
         const Payload &P = payload[g];
         cl = P.col;
         double dd, mm;
-        norms64(P, R, d, P.col.w < 0.0f, dd, mm);
+        norms64(P, d, dd, mm);
         double kap = mm / dd;
         if (fc.cutoff && fabs(kap - fc.lam2) <= (double)P.ext.x)
             kap = kappa_fp64(sc.means, sc.log_scales, sc.quats, fc.origin[0], fc.origin[1], fc.origin[2], g, d[0], d[1],
@@ -1270,6 +1250,20 @@ __device__ __forceinline__ float warp_transpose_reduce16(float v[16], int lane) 
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+// The same reduction through shared memory (red: this warp's 16 x 36 scratch): lane l stores its 16
+// values as column l (conflict-free), then lane l sums half a row (partial l >> 1, lanes 16 (l & 1) ..
+// + 15) with four 16-B loads (rows padded to 36 words: conflict-free) and one shuffle.  ~40 instead
+// of ~62 instructions.
+__device__ __forceinline__ float smem_transpose_reduce16(float (*red)[36], const float v[16], int lane) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) red[k][lane] = v[k];
+    __syncwarp();
+    const float4 *row = reinterpret_cast<const float4 *>(&red[lane >> 1][16 * (lane & 1)]);
+    const float4 a = row[0], b = row[1], c = row[2], d = row[3];
+    float sum = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w)) + (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w)));
+    __syncwarp();  // (the next entry overwrites the scratch)
+    return sum + __shfl_xor_sync(0xffffffffu, sum, 1);
+}
 
 // Reverse-order backward (renderer.py:259-310).  The producer streams the
 // tile's first max_n entries back to front; each lane walks its pixel's alive
@@ -1279,18 +1273,19 @@ __device__ __forceinline__ float warp_transpose_reduce16(float v[16], int lane) 
 #ifndef BWD_MIN_BLOCKS
 #define BWD_MIN_BLOCKS 3
 #endif
+using BwdSmem = PipeSmem<true>;
 template <bool kBEAP>
 __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
     k_backward(FrameConst fc, geer_scene sc, const int4 *__restrict__ items, const int32_t *__restrict__ n_items,
                const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
                const double2 *__restrict__ row_sc, const double *__restrict__ dir64,
                const int32_t *__restrict__ ranges, const uint32_t *__restrict__ order,
-               const __grid_constant__ CUtensorMap pay_map, const __grid_constant__ CUtensorMap gpay_map,
-               const float4 *__restrict__ wcull, const float *__restrict__ remaining,
+               const __grid_constant__ CUtensorMap pay_map, const float4 *__restrict__ wcull,
+               const ItemFrame *__restrict__ iframe, const float *__restrict__ remaining,
                const int32_t *__restrict__ n_eval,
                const float *__restrict__ dl_dimage, float *__restrict__ accum) {
     extern __shared__ __align__(128) unsigned char dsmem[];
-    PipeSmem<true> &S = *reinterpret_cast<PipeSmem<true> *>(dsmem);
+    BwdSmem &S = *reinterpret_cast<BwdSmem *>(dsmem);
     __shared__ double sray[kRasterThreads][3];
     __shared__ int smax;
     if ((int)blockIdx.x >= n_items[0]) return;  // tiles without entries have no gradient
@@ -1307,22 +1302,34 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
     pipe_init(S);  // (its __syncthreads also publishes smax)
     const int max_n = smax;
     if (max_n == 0) return;
+    const ItemFrame *F = iframe + it.w;
+    const bool framed = F->rx >= 0.f;
     if (warp == kConsumerWarps) {
-        pipe_produce<true, true>(S, order, &pay_map, &gpay_map, e0, max_n, false);
+        load_frame(S.frame, F, lane);
+        pipe_produce<true>(S, order, &pay_map, fc.thrk, framed, e0, max_n, false);
         return;
     }
     // the producer streams while the consumers set up their pixels
     double d64[3] = {0.0, 0.0, 1.0};
+    PixXY X{0.f, 0.f, 0.f, 0.f, 0.f};
+    float dx, dy, dz;  // the ray the gradient is formed with: d' = dc + x e1 + y e2 (framed) or d
     if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
-    const float4 my_patch = wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 0];  // (k_warp_cull, cached)
-    const float4 my_cone = wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + 1];
-    const Ray64 R = make_ray(d64);
-    if (valid) {
-        sray[tid][0] = d64[0];
-        sray[tid][1] = d64[1];
-        sray[tid][2] = d64[2];
+    if (framed) {
+        const float2 xy = valid ? pixel_xy(*F, d64) : make_float2(0.f, 0.f);
+        X = make_pxy(xy);
+        dx = (float)(F->dc[0] + (double)xy.x * F->e1[0] + (double)xy.y * F->e2[0]);
+        dy = (float)(F->dc[1] + (double)xy.x * F->e1[1] + (double)xy.y * F->e2[1]);
+        dz = (float)(F->dc[2] + (double)xy.x * F->e1[2] + (double)xy.y * F->e2[2]);
+    } else {
+        dx = (float)d64[0];
+        dy = (float)d64[1];
+        dz = (float)d64[2];
     }
-    const float dx = (float)d64[0], dy = (float)d64[1], dz = (float)d64[2];
+    if (lane < 2) S.wc[warp][lane] = wcull[((int64_t)it.w * kConsumerWarps + warp) * 2 + lane];  // (k_warp_cull)
+    __syncwarp();
+    sray[tid][0] = d64[0];
+    sray[tid][1] = d64[1];
+    sray[tid][2] = d64[2];
     const float t_fin = valid ? remaining[p] : 0.f;
     float gl0 = 0.f, gl1 = 0.f, gl2 = 0.f;
     if (valid) {
@@ -1337,20 +1344,20 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
     int s = 0;
     int hi = max_n;  // local index one past the current stage
     for (;;) {
-        mbar_wait(&S.full[s], phase);
+        mbar_wait_suspend(&S.full[s], phase);
         const int n = S.count[s];
         if (n == 0) break;
         const int lo = hi - n;
         if (lo < wmax) {  // some lane of this warp has alive entries in the stage
             // entries the culling keeps (culled ones have t = 0: no gradient, T unchanged), below wmax
             uint32_t msk;
-            bool any_m1;
-            stage_keep(S, s, warp, lane, n, fc.cull != 0, my_patch, my_cone, msk, any_m1);
+            stage_keep(S, s, warp, lane, n, fc.cull != 0, msk);
             if (wmax - lo < 32) msk &= (1u << (wmax - lo)) - 1u;
-            const uint32_t rb = smem_u32(&S.ring[s][0][0]), gb = smem_u32(&S.gring[s][0][0]);
-            // one entry's gradient: T and suffix update, 16 partials, warp reduction, accumulators
-            // (payload and grad payload read at their shared addresses)
-            auto entry = [&](const int jj, const PairT &e) {
+            const uint32_t rb = smem_u32(&S.rec[s][0][0]);
+            // one entry's gradient: T and suffix update, 16 partials, warp reduction, accumulators.
+            // du, m, o: d_u = W d, m = o_u x d_u (m unscaled here) for the gradient ray (dx, dy, dz).
+            auto entry = [&](const int jj, const PairT &e, const float *du, const float *mv, const float *o,
+                             const float4 &col) {
                 const int i = lo + jj;
                 // t = 0 (or not alive) on every lane: T, the suffix and all 16 partials are unchanged
                 if (!__any_sync(0xffffffffu, i < ne && e.t > 0.0f)) return;
@@ -1362,7 +1369,6 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                     const float inv = rcp_approx(omt);  // 1 - t >= 0.001: ~1 ulp
                     T = T * inv;                        // T_i = T_{i+1} / (1 - t_i)
                     const float w = T * e.t;
-                    const float4 col = lds_f4(rb + ring_off(jj) + kColOff);
                     const float c0 = col.x, c1 = col.y, c2 = col.z;
                     // renderer.py:284-287
                     const float dcdt0 = T * c0 - (s0 + bgt0) * inv;
@@ -1376,31 +1382,27 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                     v[14] = w * gl1;
                     v[15] = w * gl2;
                     if (e.t > 0.0f && e.u < kMaxBlendTF) {  // renderer.py:289-290 gate
-                        // canonical ray (fp32): d_u = W d, m = o_u x d_u (renderer.py:96-99)
-                        const uint32_t ga = gb + (uint32_t)((jj >> 2) * kGringGroupBytes + (jj & 3) * (int)sizeof(GradPayload));
-                        const float4 G0 = lds_f4(ga), G1 = lds_f4(ga + 16), G2 = lds_f4(ga + 32);
-                        const float du0 = G0.x * dx + G0.y * dy + G0.z * dz;
-                        const float du1 = G1.x * dx + G1.y * dy + G1.z * dz;
-                        const float du2 = G2.x * dx + G2.y * dy + G2.z * dz;
-                        const float o0 = G0.w, o1 = G1.w, o2 = G2.w;
-                        const float m0 = o1 * du2 - o2 * du1, m1 = o2 * du0 - o0 * du2, m2 = o0 * du1 - o1 * du0;
                         v[12] = dl_dt * e.alpha;
                         const float dk = -0.5f * dl_dt * e.u;
                         const float coef = 2.0f * dk * rcp_approx(e.dd);  // dl_dm = coef * m
-                        const float lm0 = coef * m0, lm1 = coef * m1, lm2 = coef * m2;
-                        v[9] = du1 * lm2 - du2 * lm1;  // dl_do = d_u x dl_dm
-                        v[10] = du2 * lm0 - du0 * lm2;
-                        v[11] = du0 * lm1 - du1 * lm0;
+                        const float lm0 = coef * mv[0], lm1 = coef * mv[1], lm2 = coef * mv[2];
+                        v[9] = du[1] * lm2 - du[2] * lm1;  // dl_do = d_u x dl_dm
+                        v[10] = du[2] * lm0 - du[0] * lm2;
+                        v[11] = du[0] * lm1 - du[1] * lm0;
                         const float sc_ = e.kap * coef;  // dl_dd = -(2 kappa dk / dd) d_u + dl_dm x o_u
-                        const float dd0 = -sc_ * du0 + (lm1 * o2 - lm2 * o1);
-                        const float dd1 = -sc_ * du1 + (lm2 * o0 - lm0 * o2);
-                        const float dd2 = -sc_ * du2 + (lm0 * o1 - lm1 * o0);
+                        const float dd0 = -sc_ * du[0] + (lm1 * o[2] - lm2 * o[1]);
+                        const float dd1 = -sc_ * du[1] + (lm2 * o[0] - lm0 * o[2]);
+                        const float dd2 = -sc_ * du[2] + (lm0 * o[1] - lm1 * o[0]);
                         v[0] = dd0 * dx; v[1] = dd0 * dy; v[2] = dd0 * dz;  // renderer.py:304 dW_rc
                         v[3] = dd1 * dx; v[4] = dd1 * dy; v[5] = dd1 * dz;
                         v[6] = dd2 * dx; v[7] = dd2 * dy; v[8] = dd2 * dz;
                     }
                 }
+#ifdef GEER_BWD_SHFL_REDUCE
                 const float tot = warp_transpose_reduce16(v, lane);
+#else
+                const float tot = smem_transpose_reduce16(S.red[warp], v, lane);
+#endif
                 // lane 2k adds partial k (predicated fire-and-forget reduction, no branch)
                 float *dst = accum + (int64_t)S.gid[s][jj] * 16 + (lane >> 1);
                 asm volatile(
@@ -1410,23 +1412,62 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                     "f"(tot), "r"((int)((lane & 1) == 0 && tot != 0.0f))
                     : "memory");
             };
-            // a mode-1 (cross-product) payload anywhere in the stage selects the generic evaluation;
-            // otherwise the shared-address evaluation (entries back to front)
-            if (any_m1) {
+            if (!framed) {  // fp64 path: t from the payload's fp64 cross product, gradient vectors in fp32
                 while (msk) {
                     const int jj = 31 - __clz(msk);
                     msk &= ~(1u << jj);
+                    const Payload &P = ring_at(S, s, jj);
                     PairT e;
-                    eval_t(ring_at(S, s, jj), R, sray[tid], fc, e, dummy);  // warp-uniform call (mode vote inside)
-                    entry(jj, e);
+                    eval_t(P, sray[tid], fc, e, dummy);
+                    float du[3], mv[3], o[3];
+                    for (int r = 0; r < 3; ++r) {
+                        du[r] = (float)P.q[r * 3 + 0] * dx + (float)P.q[r * 3 + 1] * dy + (float)P.q[r * 3 + 2] * dz;
+                        o[r] = (float)P.q[9 + r];
+                    }
+                    mv[0] = o[1] * du[2] - o[2] * du[1];
+                    mv[1] = o[2] * du[0] - o[0] * du[2];
+                    mv[2] = o[0] * du[1] - o[1] * du[0];
+                    entry(jj, e, du, mv, o, P.col);
                 }
             } else {
                 while (msk) {
                     const int jj = 31 - __clz(msk);
                     msk &= ~(1u << jj);
+                    // t exactly as the forward's rec_group computes it
+                    const uint32_t ra = rb + (uint32_t)jj * (kRecB * 4);
+                    float k, dd, trel, ms[3];
+                    float4 c1;
+                    rec_k(ra, X, k, dd, ms, c1, trel);
+                    bool inside = k <= fc.thrkc;
+                    if (fabsf(__fsub_rn(k, fc.thrkc)) <= c1.w) {  // (exactly the forward's re-check)
+                        bool unc;
+                        inside = recheck(ring_at(S, s, jj), sray[tid], fc, unc, k);
+                    }
                     PairT e;
-                    eval_t0_smem(rb + ring_off(jj), R, fc, e);
-                    entry(jj, e);
+                    e.alpha = ex2_approx(-k);
+                    e.u = inside ? __fmul_rn(c1.z, e.alpha) : 0.0f;
+                    e.t = inside ? fminf(e.u, kMaxBlendTF) : 0.0f;
+                    e.kap = k * (float)(1.0 / kHalfLog2e);
+                    // gradient vectors for d' (kappa is scale-invariant in the ray: dW = dl/dd_u (x) d')
+                    const float4 g0 = lds_f4(ra + 96), g1 = lds_f4(ra + 112), g2 = lds_f4(ra + 128);
+                    const float du[3] = {__fmaf_rn(g0.z, X.y, __fmaf_rn(g0.y, X.x, g0.x)),
+                                         __fmaf_rn(g1.z, X.y, __fmaf_rn(g1.y, X.x, g1.x)),
+                                         __fmaf_rn(g2.z, X.y, __fmaf_rn(g2.y, X.x, g2.x))};
+                    const float o[3] = {g0.w, g1.w, g2.w};
+                    float mv[3];
+                    if (c1.w < INFINITY) {  // the record's m and dd (entry-uniform branch)
+                        constexpr float kInvS = (float)(1.0 / kSqrtHalfLog2e);
+                        mv[0] = ms[0] * kInvS;
+                        mv[1] = ms[1] * kInvS;
+                        mv[2] = ms[2] * kInvS;
+                        e.dd = dd;
+                    } else {  // a record without fp32 vectors (fp64 re-check path): from d_u and o_u
+                        mv[0] = o[1] * du[2] - o[2] * du[1];
+                        mv[1] = o[2] * du[0] - o[0] * du[2];
+                        mv[2] = o[0] * du[1] - o[1] * du[0];
+                        e.dd = du[0] * du[0] + du[1] * du[1] + du[2] * du[2];
+                    }
+                    entry(jj, e, du, mv, o, lds_f4(ra + 80));
                 }
             }
         }
@@ -1494,28 +1535,29 @@ static void raster_smem_optin() {
     done = true;
     cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FwdSmem) + 128);
     cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FwdSmem) + 128);
-    cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<true>) + 128);
-    cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem<true>) + 128);
+    cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BwdSmem) + 128);
+    cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BwdSmem) + 128);
 }
 
 void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                     const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                     const double *dir64, const int32_t *ranges, const uint32_t *order, const Payload *payload,
-                    const CUtensorMap &pay_map, const float4 *wcull, float *color, float *remaining, int32_t *count,
-                    int32_t *n_eval, unsigned long long *counters, int32_t *fixup_list, cudaStream_t st) {
+                    const CUtensorMap &pay_map, const float4 *wcull, const ItemFrame *iframe, float *color,
+                    float *remaining, int32_t *count, int32_t *n_eval, unsigned long long *counters,
+                    int32_t *fixup_list, cudaStream_t st) {
     if (max_items <= 0) return;
     raster_smem_optin();
     if (fc.model == GEER_BEAP) {
-        k_forward<true><<<max_items, kFwdThreads, sizeof(FwdSmem) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                            ranges, order, pay_map, wcull, color, remaining, count,
-                                                            n_eval, counters, fixup_list);
-        k_fixup<true><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
+        k_forward<true><<<max_items, kFwdThreads, sizeof(FwdSmem) + 128, st>>>(
+            fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64, ranges, order, pay_map, wcull, iframe, color,
+            remaining, count, n_eval, counters, fixup_list);
+        k_fixup<true><<<148 * 8, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                counters, fixup_list, color, remaining, count, n_eval);
     } else {
-        k_forward<false><<<max_items, kFwdThreads, sizeof(FwdSmem) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                             ranges, order, pay_map, wcull, color, remaining, count,
-                                                             n_eval, counters, fixup_list);
-        k_fixup<false><<<148 * 2, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
+        k_forward<false><<<max_items, kFwdThreads, sizeof(FwdSmem) + 128, st>>>(
+            fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64, ranges, order, pay_map, wcull, iframe, color,
+            remaining, count, n_eval, counters, fixup_list);
+        k_fixup<false><<<148 * 8, 128, 0, st>>>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload,
                                                 counters, fixup_list, color, remaining, count, n_eval);
     }
 }
@@ -1523,28 +1565,28 @@ void launch_forward(const FrameConst &fc, const geer_scene &sc, int max_items, c
 void launch_backward(const FrameConst &fc, const geer_scene &sc, int max_items, const int4 *items,
                      const int32_t *n_items, const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc,
                      const double *dir64, const int32_t *ranges, const uint32_t *order, const CUtensorMap &pay_map,
-                     const CUtensorMap &gpay_map, const float4 *wcull, const float *remaining,
-                     const int32_t *n_eval, const float *dl_dimage, float *accum, cudaStream_t st) {
+                     const float4 *wcull, const ItemFrame *iframe, const float *remaining, const int32_t *n_eval,
+                     const float *dl_dimage, float *accum, cudaStream_t st) {
     if (max_items <= 0) return;
     raster_smem_optin();
     if (fc.model == GEER_BEAP)
-        k_backward<true><<<max_items, kPipeThreads, sizeof(PipeSmem<true>) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                             ranges, order, pay_map, gpay_map, wcull, remaining,
-                                                             n_eval, dl_dimage, accum);
+        k_backward<true><<<max_items, kPipeThreads, sizeof(BwdSmem) + 128, st>>>(
+            fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64, ranges, order, pay_map, wcull, iframe, remaining,
+            n_eval, dl_dimage, accum);
     else
-        k_backward<false><<<max_items, kPipeThreads, sizeof(PipeSmem<true>) + 128, st>>>(fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64,
-                                                              ranges, order, pay_map, gpay_map, wcull, remaining,
-                                                              n_eval, dl_dimage, accum);
+        k_backward<false><<<max_items, kPipeThreads, sizeof(BwdSmem) + 128, st>>>(
+            fc, sc, items, n_items, pix_list, col_sc, row_sc, dir64, ranges, order, pay_map, wcull, iframe, remaining,
+            n_eval, dl_dimage, accum);
 }
 
 void launch_warp_cull(const FrameConst &fc, int max_items, const int4 *items, const int32_t *n_items,
                       const int32_t *pix_list, const double2 *col_sc, const double2 *row_sc, const double *dir64,
-                      float4 *wcull, cudaStream_t st) {
+                      float4 *wcull, ItemFrame *iframe, cudaStream_t st) {
     if (max_items <= 0) return;
     if (fc.model == GEER_BEAP)
-        k_warp_cull<true><<<max_items, kRasterThreads, 0, st>>>(fc, items, n_items, pix_list, col_sc, row_sc, dir64, wcull);
+        k_warp_cull<true><<<max_items, kRasterThreads, 0, st>>>(fc, items, n_items, pix_list, col_sc, row_sc, dir64, wcull, iframe);
     else
-        k_warp_cull<false><<<max_items, kRasterThreads, 0, st>>>(fc, items, n_items, pix_list, col_sc, row_sc, dir64, wcull);
+        k_warp_cull<false><<<max_items, kRasterThreads, 0, st>>>(fc, items, n_items, pix_list, col_sc, row_sc, dir64, wcull, iframe);
 }
 
 void launch_sum_i32(const int32_t *v, int64_t n, unsigned long long *out, cudaStream_t st) {

@@ -5,6 +5,6 @@ for defs in "$@"; do
 import json,sys
 for l in sys.stdin:
     if l.startswith('{'):
-        d=json.loads(l); print('== $defs', round(d['value'],1), 'FPS', round(d['fwd_bwd_ms_per_view'],3), 'fb_ms', 'C5', round(d['c5'].get('ms_per_frame',0),3), {k:round(v['ms'],3) for k,v in d['stages'].items()})
+        d=json.loads(l); print('== $defs', round(d['value'],1), 'FPS', round(d['fwd_bwd_ms_per_view'],3), 'fb_ms', {k:round(v['ms'],3) for k,v in d['stages'].items()})
 "
 done
