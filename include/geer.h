@@ -45,7 +45,11 @@ typedef enum geer_status {
     GEER_ERR_NOT_PD = 3,         /* "view covariance must be positive definite" */
     GEER_ERR_CUDA = 4,           /* CUDA runtime error */
     GEER_ERR_NOMEM = 5,          /* device allocation failed */
-    GEER_ERR_STATE = 6           /* backward without a matching forward */
+    GEER_ERR_STATE = 6,          /* backward without a matching forward */
+    GEER_ERR_OVERFLOW = 7        /* geer_sync: a frame since the last sync outgrew the context's graph
+                                    capacity; the capacity has grown and the LAST frame has been rendered
+                                    again (its outputs are valid), work that consumed an earlier one
+                                    must be redone */
 } geer_status;
 
 typedef enum geer_model { GEER_PINHOLE = 0, GEER_KB = 1, GEER_BEAP = 2 } geer_model;
@@ -136,9 +140,21 @@ int geer_set_timing(geer_ctx *ctx, int enable);
 
 /* ---- device level (fast path) -------------------------------------------------
  * color (H,W,3) f32, remaining (H,W) f32, count (H,W) i32: device buffers.
- * The scene buffers must stay valid until the matching geer_backward. */
+ * The scene buffers must stay valid until the matching geer_backward.
+ * geer_forward is asynchronous on `stream` once the context knows the graph's size (from its first
+ * frame, which still reads the entry total back): nothing blocks the host, and a frame issues the
+ * same kernels with the same arguments each time (CUDA-graph capturable once the camera is cached).
+ * Conditions the reference raises on (non-PD / non-symmetric view covariance, renderer.py ->
+ * association.py:155-160) and a graph larger than the context's capacity are recorded on the device;
+ * geer_sync synchronises the stream and returns the error (GEER_ERR_NOT_PD / NOT_SYMMETRIC), or
+ * GEER_ERR_OVERFLOW after growing the capacity and re-rendering the last frame, else GEER_OK.  An
+ * overflowing frame renders background only (no out-of-bounds work).  Read the outputs after
+ * geer_sync (or after your own synchronisation, if you accept an unchecked frame). */
 int geer_forward(geer_ctx *ctx, const geer_scene *scene, const geer_camera *camera, const geer_config *config,
                  float *color, float *remaining, int32_t *count, void *stream);
+int geer_sync(geer_ctx *ctx, void *stream);
+/* Frees the context's cached camera setups (K0 outputs of up to 16 other cameras, <= 1 GiB). */
+int geer_clear_camera_cache(geer_ctx *ctx);
 
 /* dl_dimage (H,W,3) f32 device.  flags: GEER_ACCUMULATE adds into grads (multi-view);
  * GEER_OPACITY_LOGIT returns dopacities w.r.t. the stored logit (trainer.py:208-217)

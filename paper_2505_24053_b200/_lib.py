@@ -23,6 +23,7 @@ GEER_ERR_NOT_PD = 3
 GEER_ERR_CUDA = 4
 GEER_ERR_NOMEM = 5
 GEER_ERR_STATE = 6
+GEER_ERR_OVERFLOW = 7
 
 MODEL_IDS = {"pinhole": 0, "kb": 1, "beap": 2}
 
@@ -32,7 +33,7 @@ EXPORTED = (
     "geer_backward", "geer_frame_stats", "geer_graph_info", "geer_graph_export", "geer_build_graph_host",
     "geer_render_host", "geer_render_backward_host", "geer_l1_grad", "geer_adam", "geer_measure_fp32_peak",
     "geer_loss_workspace_bytes", "geer_loss", "geer_resample_to_beap", "geer_ply_to_soa",
-    "geer_association_check",
+    "geer_association_check", "geer_sync", "geer_clear_camera_cache",
 )
 
 
@@ -129,6 +130,8 @@ def load():
             "geer_resample_to_beap": ([P, I, I, P, P, P, P, P], I),
             "geer_ply_to_soa": ([P, I64, I, P, I, P, P], I),
             "geer_association_check": ([P, ctypes.c_int32, P, P, ctypes.c_int32, P], I),
+            "geer_sync": ([P, P], I),
+            "geer_clear_camera_cache": ([P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

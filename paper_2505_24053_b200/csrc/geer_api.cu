@@ -3,8 +3,9 @@
 // Frame pipeline on one stream (stage names follow SPEC.md:575,602):
 //   prep : K0 camera setup (cached per camera: ray tables, tile CSR, work items, per-warp culling
 //          regions) + K1 per-Gaussian preprocess (exact fp64 association half + raster payload half)
-//   dup  : depth-order sort of the Gaussians (queued before the host reads the 12-byte header:
-//          entry total + error flag)
+//   dup  : depth-order sort of the Gaussians (a context's first frame reads the 24-byte header -
+//          entry total, (Gaussian, tile row) pairs, error flag - with the sort queued first; later
+//          frames run without the host, sized by the learned capacity, see run_forward)
 //   sort : per-tile lists by two-level stable bucketing (geer_bin.cu) + the raster work order
 //   render: K5 raster + fp64 fix-up of borderline pixels
 // The backward (K6 + K7) reuses the forward's graph, payload and per-pixel
@@ -78,12 +79,18 @@ int make_row_map(CUtensorMap *map, const void *base, int64_t rows, int row_bytes
 
 // One cached camera setup (K0 outputs): the context swaps its camera buffers with a slot, so a
 // context rendering a recurring set of views (the multi-view training step) sets each camera up once.
+// Only what a frame reads after the setup is cached (ray tables, mirror tile edges, pixel lists,
+// work items, per-warp culling regions + item frames, the pixel->tile map); the setup's scratch
+// (angles, bin counts, sort buffers) stays with the context.  A context holds at most kCamSlots
+// setups besides the current one and at most kCamCacheBytes of slot memory; when the slots are
+// full a new camera is set up in the current camera's buffers (the most recently used setup is the
+// one dropped: a cyclic set of more views than slots keeps kCamSlots of them cached instead of
+// none).  geer_clear_camera_cache frees the slots; a failed allocation frees them and retries.
 constexpr int kCamSlots = 16;
 constexpr int64_t kCamSlotMaxPixels = 4 << 20;  // larger cameras are not kept (memory)
-#define GEER_CAM_BUFS(X)                                                                                    \
-    X(col_sc) X(row_sc) X(medges_x) X(medges_y) X(edges_x) X(edges_y) X(dir64) X(theta) X(phi) X(minmax)  \
-    X(pixel_tile) X(pixel_tile_sorted) X(pix_iota) X(pix_list) X(tile_count) X(tile_off) X(item_count)      \
-    X(item_off) X(items) X(n_items) X(wcull)
+constexpr size_t kCamCacheBytes = (size_t)1 << 30;
+#define GEER_CAM_BUFS(X) \
+    X(col_sc) X(row_sc) X(medges_x) X(medges_y) X(dir64) X(pixel_tile) X(pix_list) X(items) X(n_items) X(wcull)
 struct CamSlot {
 #define GEER_DECL(b) Buf b;
     GEER_CAM_BUFS(GEER_DECL)
@@ -109,7 +116,11 @@ struct geer_ctx {
     const void *iota_ptr = nullptr;  // gid_iota holds 0..iota_len-1 (buffer pointer / capacity it was written at)
     size_t iota_cap = 0;
     int64_t iota_len = 0;  // a raster ran (also exhaustive forwards, which have no backward)
-    int64_t n_entries = 0;
+    int64_t n_entries = 0;  // of the last frame; -1: on the device only (asynchronous frame)
+    int64_t cap_entries = 0, cap_rows = 0;  // graph capacity of the asynchronous path (0: not known yet)
+    // the last device-level forward, for geer_sync's re-run after an overflow
+    float *last_color = nullptr, *last_remaining = nullptr;
+    int32_t *last_count = nullptr;
     int max_items = 0;
     CUtensorMap pay_map;  // gather4 map over the payload array
     // K0 cache: the camera setup depends only on the camera and the tile size
@@ -117,6 +128,7 @@ struct geer_ctx {
     FrameConst cam_fc{};
     CamSlot cam_slots[kCamSlots];
     uint64_t cam_clock = 0;
+    bool have_export = false;  // mu_c / depth were recorded by the last forward (graph export)
     const float *fwd_remaining = nullptr;  // remaining written by the last forward (backward input)
     float ms[6] = {};
     unsigned long long *d_counters = nullptr;  // [0] rechecks, [1] evaluated pairs, [2] fix-up pixels, [3] warp-entries, [4] streamed entries, [5] graph entries (K1)
@@ -226,6 +238,14 @@ int make_frame_const(const geer_camera *cam, const geer_config *cfg, int n_bands
     return GEER_OK;
 }
 
+// The entry total of the last frame on the host (an asynchronous frame left it on the device).
+int resolve_entries(geer_ctx *c) {
+    if (c->n_entries >= 0) return GEER_OK;
+    GEER_CUDA(cudaDeviceSynchronize());
+    GEER_CUDA(cudaMemcpy(&c->n_entries, c->d_counters + 5, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    return GEER_OK;
+}
+
 // The item frames follow the per-warp culling regions in the wcull buffer.
 ItemFrame *item_frames(geer_ctx *c) {
     return reinterpret_cast<ItemFrame *>(reinterpret_cast<float4 *>(c->wcull.p) + (size_t)c->max_items * 16);
@@ -311,27 +331,65 @@ void swap_camera(geer_ctx *c, CamSlot &s) {
     std::swap(c->cam_fc, s.fc);
     std::swap(c->max_items, s.max_items);
 }
-// Make the context's camera setup the one of c->fc: from a slot if it is cached there, else (the
-// current setup moving into the least recently used slot) rebuilt by camera_setup.
+size_t slot_bytes(const CamSlot &sl) {
+    size_t t = 0;
+#define GEER_SUM(b) t += sl.b.cap;
+    GEER_CAM_BUFS(GEER_SUM)
+#undef GEER_SUM
+    return t;
+}
+size_t current_camera_bytes(const geer_ctx *c) {
+    size_t t = 0;
+#define GEER_SUM(b) t += c->b.cap;
+    GEER_CAM_BUFS(GEER_SUM)
+#undef GEER_SUM
+    return t;
+}
+void clear_camera_cache(geer_ctx *c) {
+    for (CamSlot &sl : c->cam_slots) {
+#define GEER_FREE(b) free_buf(sl.b);
+        GEER_CAM_BUFS(GEER_FREE)
+#undef GEER_FREE
+        sl.valid = sl.pixel_tile_ok = false;
+        sl.max_items = 0;
+    }
+}
+
+// Make the context's camera setup the one of c->fc: from a slot if it is cached there (the current
+// setup moves into that slot), else rebuilt by camera_setup - after parking the current setup in a
+// free slot when there is one and the byte budget allows, otherwise over the current setup.
 int select_camera(geer_ctx *c, bool want_pixel_tile, cudaStream_t st) {
     if (camera_cached(c, want_pixel_tile)) return GEER_OK;
     const FrameConst &fc = c->fc;
-    const bool keep = (int64_t)fc.width * fc.height <= kCamSlotMaxPixels &&
-                      (!c->cam_valid || (int64_t)c->cam_fc.width * c->cam_fc.height <= kCamSlotMaxPixels);
-    if (keep) {
-        int hit = -1, lru = 0;
-        for (int i = 0; i < kCamSlots; ++i) {
-            const CamSlot &sl = c->cam_slots[i];
-            if (sl.valid && (!want_pixel_tile || sl.pixel_tile_ok) && same_camera(sl.fc, fc)) hit = i;
-            if (!sl.valid || (c->cam_slots[lru].valid && sl.last_use < c->cam_slots[lru].last_use)) lru = i;
-        }
-        const int k = hit >= 0 ? hit : lru;
-        swap_camera(c, c->cam_slots[k]);  // the previous camera stays cached in slot k
-        c->cam_slots[k].last_use = ++c->cam_clock;
-        if (hit >= 0) return GEER_OK;
+    const bool small = (int64_t)fc.width * fc.height <= kCamSlotMaxPixels;
+    int hit = -1, free_slot = -1;
+    size_t used = 0;
+    for (int i = 0; i < kCamSlots; ++i) {
+        const CamSlot &sl = c->cam_slots[i];
+        if (sl.valid && (!want_pixel_tile || sl.pixel_tile_ok) && same_camera(sl.fc, fc)) hit = i;
+        if (!sl.valid && free_slot < 0) free_slot = i;
+        used += slot_bytes(sl);
+    }
+    if (hit >= 0) {
+        swap_camera(c, c->cam_slots[hit]);  // the previous camera stays cached in that slot
+        c->cam_slots[hit].last_use = ++c->cam_clock;
+        return GEER_OK;
+    }
+    const bool park = small && c->cam_valid && free_slot >= 0 &&
+                      (int64_t)c->cam_fc.width * c->cam_fc.height <= kCamSlotMaxPixels &&
+                      used + current_camera_bytes(c) <= kCamCacheBytes;
+    if (park) {
+        CamSlot &sl = c->cam_slots[free_slot];
+        swap_camera(c, sl);  // sl takes the current setup; the context gets the slot's (empty) buffers
+        sl.last_use = ++c->cam_clock;
     }
     c->cam_valid = false;
     int rc = camera_setup(c, want_pixel_tile, st);
+    if (rc == GEER_ERR_NOMEM) {  // give the cached setups' memory back and try once more
+        cudaGetLastError();
+        clear_camera_cache(c);
+        rc = camera_setup(c, want_pixel_tile, st);
+    }
     if (rc) return rc;
     c->cam_valid = true;
     c->cam_pixel_tile = want_pixel_tile || fc.model != GEER_BEAP;
@@ -340,7 +398,8 @@ int select_camera(geer_ctx *c, bool want_pixel_tile, cudaStream_t st) {
 }
 
 // Full association (+ raster when color != null) for the scene in c->scene.
-int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, bool want_export, cudaStream_t st) {
+int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, bool want_export, cudaStream_t st,
+                bool allow_async = false) {
     int rc = 0;
     FrameConst &fc = c->fc;
     const geer_scene &sc = c->scene;
@@ -349,6 +408,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     c->have_frame = false;
     c->have_raster = false;
     c->have_stats = false;
+    c->have_export = false;
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[0], st));
     GEER_CUDA(cudaMemsetAsync(c->d_counters, 0, 7 * sizeof(unsigned long long), st));
     GEER_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
@@ -375,15 +435,21 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
                       flags, mu, dep, c->d_err, c->d_counters + 5, st);
     if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[1], st));
 
-    // ---- dup: depth order, scan, header D2H, emit
-    // The entry total (summed by K1) and the error flag go to the host right after K1; the depth
-    // sort and count scan, which do not need them, are queued before the host waits, so the GPU
-    // never idles on this round trip.
-    int64_t total = 0;
-    GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[0], c->d_counters + 5, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[1], c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
-    GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[2], c->d_counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    GEER_CUDA(cudaEventRecord(c->ev_hdr, st));
+    // ---- dup: depth order
+    // Asynchronous frame: the graph buffers are sized by the context's capacity (learned from earlier
+    // frames) and the frame runs to the end without the host; a total above capacity is flagged on
+    // the device (k_check_capacity) and turns the rest of the association into no-ops (geer_sync
+    // re-runs such a frame).  First frame / export / exhaustive: the 24-byte header (entry total,
+    // (Gaussian, tile row) pairs, error flag) is read back right after K1, with the depth sort queued
+    // before the host waits, so the GPU never idles on the round trip.
+    const bool async = allow_async && c->cap_entries > 0 && !want_export && !fc.exhaustive;
+    int64_t total = 0, rows = 0;
+    if (!async) {
+        GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[0], c->d_counters + 5, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[1], c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+        GEER_CUDA(cudaMemcpyAsync(&c->h_hdr[2], c->d_counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        GEER_CUDA(cudaEventRecord(c->ev_hdr, st));
+    }
     if (n > 0) {
         // gid values 0..n-1 stay valid while the buffer is not reallocated (a growth changes its capacity)
         if (c->iota_ptr != giota || c->iota_cap != c->gid_iota.cap || c->iota_len < n) {
@@ -396,11 +462,13 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         void *tmp = ENSURE(char, c->temp, b1);
         sort_depth(tmp, b1, dkey, dkey_s, giota, gsorted, n, st);
     }
-    GEER_CUDA(cudaEventSynchronize(c->ev_hdr));
-    int err = (int)(c->h_hdr[1] & 0xFFFFFFFF);
-    if (err == GEER_ERR_NOT_PD) return fail(GEER_ERR_NOT_PD, "view covariance must be positive definite");
-    if (err == GEER_ERR_NOT_SYMMETRIC) return fail(GEER_ERR_NOT_SYMMETRIC, "view covariance must be symmetric");
-    if (err) return fail(GEER_ERR_INVALID, "preprocess error %d", err);
+    if (!async) {
+        GEER_CUDA(cudaEventSynchronize(c->ev_hdr));
+        int err = (int)(c->h_hdr[1] & 0xFFFFFFFF);
+        if (err == GEER_ERR_NOT_PD) return fail(GEER_ERR_NOT_PD, "view covariance must be positive definite");
+        if (err == GEER_ERR_NOT_SYMMETRIC) return fail(GEER_ERR_NOT_SYMMETRIC, "view covariance must be symmetric");
+        if (err) return fail(GEER_ERR_INVALID, "preprocess error %d", err);
+    }
     if (fc.exhaustive) {  // every tile composites all kept Gaussians: no emit, no tile sort
         int32_t *r2 = ENSURE(int32_t, c->tile_ranges, fc.n_tiles + 1);
         launch_exhaustive_ranges((const uint8_t *)c->flags.p, n, r2, st);
@@ -424,16 +492,27 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         GEER_CUDA(cudaGetLastError());
         return GEER_OK;  // forward only: have_frame / have_raster stay false
     }
-    total = c->h_hdr[0];
-    if (total >= ((int64_t)1 << 31) - 1)
-        return fail(GEER_ERR_NOMEM, "render graph has %lld entries (limit 2^31)", (long long)total);
-    c->n_entries = total;
+    if (async) {
+        total = c->cap_entries;
+        rows = c->cap_rows;
+        c->n_entries = -1;
+        launch_check_capacity(c->d_counters + 5, c->cap_entries, c->cap_rows, c->d_err, st);
+    } else {
+        total = c->h_hdr[0];
+        rows = c->h_hdr[2];
+        if (total >= ((int64_t)1 << 31) - 1)
+            return fail(GEER_ERR_NOMEM, "render graph has %lld entries (limit 2^31)", (long long)total);
+        c->n_entries = total;
+        // capacity of the following asynchronous frames (grow-only, 25 % headroom)
+        c->cap_entries = lmax(c->cap_entries, lmin(total + total / 4 + 4096, ((int64_t)1 << 31) - 2));
+        c->cap_rows = lmax(c->cap_rows, rows + rows / 4 + 1024);
+    }
     // ---- sort: per-tile lists (stable in depth order) and their ranges, then the raster work order
     {
-        const BinPlan bp = bin_plan(n, fc.n_x, fc.n_y, total, c->h_hdr[2]);
+        const BinPlan bp = bin_plan(n, fc.n_x, fc.n_y, total, rows);
         uint32_t *m1 = ENSURE(uint32_t, c->bin_m1, bp.m1_len + 1);
         uint32_t *p1 = ENSURE(uint32_t, c->bin_p1, bp.m1_len + 1);
-        uint2 *rows = ENSURE(uint2, c->bin_rows, bp.rows_cap + 1);
+        uint2 *brows = ENSURE(uint2, c->bin_rows, bp.rows_cap + 1);
         int32_t *rst = ENSURE(int32_t, c->bin_rowstart, fc.n_y + 1);
         int32_t *sof = ENSURE(int32_t, c->bin_segoff, fc.n_y + 1);
         uint32_t *m2 = ENSURE(uint32_t, c->bin_m2, bp.m2_len + 1);
@@ -441,7 +520,8 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         void *tmp = ENSURE(char, c->temp, bp.temp_bytes);
         uint32_t *order = ENSURE(uint32_t, c->order, total + 1);
         if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[2], st));
-        rc = bin_tiles(bp, gsorted, ar, n, fc.n_x, fc.n_y, total, m1, p1, rows, rst, sof, m2, p2, tmp, order, ranges, st);
+        rc = bin_tiles(bp, gsorted, ar, n, fc.n_x, fc.n_y, c->d_counters + 5, c->d_err, m1, p1, brows, rst, sof, m2, p2,
+                       tmp, order, ranges, st);
         if (rc) return fail(rc, "tile binning failed: %s", cudaGetErrorString(cudaGetLastError()));
         int4 *work = ENSURE(int4, c->work, c->max_items);
         int32_t *nwork = ENSURE(int32_t, c->n_work, 2);
@@ -449,6 +529,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[3], st));
     }
     c->have_frame = true;
+    c->have_export = want_export;
 
     // ---- render
     if (color) {
@@ -581,7 +662,8 @@ geer_ctx *geer_create(int device) {
     for (int i = 0; i < 6 && ok; ++i) ok = cudaEventCreate(&c->ev[i]) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_hdr, cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaMalloc(&c->d_counters, 7 * sizeof(unsigned long long)) == cudaSuccess;
-    ok = ok && cudaMalloc(&c->d_err, sizeof(int)) == cudaSuccess;
+    ok = ok && cudaMalloc(&c->d_err, 8 * sizeof(int)) == cudaSuccess;  // frame error, sticky overflow, maxima
+    ok = ok && cudaMemset(c->d_err, 0, 8 * sizeof(int)) == cudaSuccess;
     ok = ok && cudaMallocHost(&c->h_hdr, 3 * sizeof(int64_t)) == cudaSuccess;
     if (!ok) {
         fail(GEER_ERR_CUDA, "context creation failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -605,11 +687,7 @@ void geer_destroy(geer_ctx *c) {
                    &c->accum, &c->temp, &c->h64_means, &c->h64_log, &c->h64_quats, &c->h64_op, &c->h64_sh,
                    &c->s32_means, &c->s32_log, &c->s32_quats, &c->s32_op, &c->s32_sh, &c->out64, &c->g64};
     for (Buf *b : bufs) free_buf(*b);
-    for (CamSlot &sl : c->cam_slots) {
-#define GEER_FREE(b) free_buf(sl.b);
-        GEER_CAM_BUFS(GEER_FREE)
-#undef GEER_FREE
-    }
+    clear_camera_cache(c);
     for (int i = 0; i < 6; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     if (c->ev_hdr) cudaEventDestroy(c->ev_hdr);
@@ -618,6 +696,14 @@ void geer_destroy(geer_ctx *c) {
     if (c->h_hdr) cudaFreeHost(c->h_hdr);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
+}
+
+int geer_clear_camera_cache(geer_ctx *c) {
+    if (!c) return fail(GEER_ERR_INVALID, "null context");
+    cudaSetDevice(c->device);
+    GEER_CUDA(cudaDeviceSynchronize());  // (slot buffers may still be read by queued frames)
+    clear_camera_cache(c);
+    return GEER_OK;
 }
 
 int geer_set_timing(geer_ctx *c, int enable) {
@@ -648,7 +734,42 @@ int geer_forward(geer_ctx *c, const geer_scene *scene, const geer_camera *camera
         GEER_CUDA(cudaGetLastError());
         return GEER_OK;
     }
-    return run_forward(c, color, remaining, count, false, st);
+    c->last_color = color;
+    c->last_remaining = remaining;
+    c->last_count = count;
+    return run_forward(c, color, remaining, count, false, st, true);
+}
+
+int geer_sync(geer_ctx *c, void *stream) {
+    if (!c) return fail(GEER_ERR_INVALID, "null context");
+    cudaStream_t st = (cudaStream_t)stream;
+    GEER_CUDA(cudaStreamSynchronize(st));
+    int status[8];
+    GEER_CUDA(cudaMemcpy(status, c->d_err, sizeof(status), cudaMemcpyDeviceToHost));
+    const int err = status[0];
+    if (err == GEER_ERR_NOT_PD) return fail(GEER_ERR_NOT_PD, "view covariance must be positive definite");
+    if (err == GEER_ERR_NOT_SYMMETRIC) return fail(GEER_ERR_NOT_SYMMETRIC, "view covariance must be symmetric");
+    if (err && err != GEER_ERR_OVERFLOW) return fail(GEER_ERR_INVALID, "preprocess error %d", err);
+    if (status[1]) {  // a frame since the last sync outgrew the capacity: grow it (25 % headroom)
+        int64_t mx[2];
+        memcpy(mx, status + 2, sizeof(mx));
+        c->cap_entries = lmax(c->cap_entries, lmin(mx[0] + mx[0] / 4 + 4096, ((int64_t)1 << 31) - 2));
+        c->cap_rows = lmax(c->cap_rows, mx[1] + mx[1] / 4 + 1024);
+        GEER_CUDA(cudaMemset(c->d_err + 1, 0, 7 * sizeof(int)));
+        if (err == GEER_ERR_OVERFLOW) {  // the last frame itself: render it again
+            int rc = run_forward(c, c->last_color, c->last_remaining, c->last_count, false, st);
+            if (rc) return rc;
+            GEER_CUDA(cudaStreamSynchronize(st));
+            GEER_CUDA(cudaMemcpy(status, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+            if (status[0]) return fail(GEER_ERR_INVALID, "frame error %d after the re-run", status[0]);
+        }
+        if (c->n_entries < 0 && c->have_frame)
+            GEER_CUDA(cudaMemcpy(&c->n_entries, c->d_counters + 5, sizeof(int64_t), cudaMemcpyDeviceToHost));
+        return fail(GEER_ERR_OVERFLOW, "a frame outgrew the graph capacity (the last frame has been re-rendered)");
+    }
+    if (c->n_entries < 0 && c->have_frame)
+        GEER_CUDA(cudaMemcpy(&c->n_entries, c->d_counters + 5, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    return GEER_OK;
 }
 
 int geer_backward(geer_ctx *c, const float *dl_dimage, const geer_grads *grads, int accumulate, void *stream) {
@@ -665,6 +786,8 @@ int geer_backward(geer_ctx *c, const float *dl_dimage, const geer_grads *grads, 
 int geer_frame_stats(geer_ctx *c, geer_stats *out) {
     if (!c || !out) return fail(GEER_ERR_INVALID, "null argument");
     memset(out, 0, sizeof(*out));
+    int rc0 = resolve_entries(c);
+    if (rc0) return rc0;
     out->n_gaussians = c->scene.n;
     out->n_entries = c->n_entries;
     out->n_tiles = c->fc.n_tiles;
@@ -719,7 +842,8 @@ int geer_association_check(geer_ctx *c, int32_t rays_per_tile, int64_t *out, int
     const int64_t n = c->scene.n, words = (n + 31) / 32;
     cudaStream_t st = c->own_stream;
     GEER_CUDA(cudaDeviceSynchronize());
-    int rc = 0;
+    int rc = resolve_entries(c);
+    if (rc) return rc;
     Buf wo, bits, misc;  // transient (the bitmap is n_tiles * n / 8 bytes: 1 GB at 1M Gaussians, 1080p)
     struct Free {
         Buf *b[3];
@@ -751,6 +875,8 @@ int geer_association_check(geer_ctx *c, int32_t rays_per_tile, int64_t *out, int
 
 int geer_graph_info(geer_ctx *c, int64_t *n_entries, int32_t *n_x, int32_t *n_y) {
     if (!c) return fail(GEER_ERR_INVALID, "null context");
+    int rc0 = resolve_entries(c);
+    if (rc0) return rc0;
     if (n_entries) *n_entries = c->n_entries;
     if (n_x) *n_x = c->fc.n_x;
     if (n_y) *n_y = c->fc.n_y;
@@ -776,6 +902,8 @@ int geer_graph_export(geer_ctx *c, int64_t *order, int64_t *entry_tile, int64_t 
     if (!c) return fail(GEER_ERR_INVALID, "null context");
     if (!c->have_frame) return fail(GEER_ERR_STATE, "no render graph: run a forward or geer_build_graph_host first");
     GEER_CUDA(cudaDeviceSynchronize());
+    int rc0 = resolve_entries(c);
+    if (rc0) return rc0;
     const FrameConst &fc = c->fc;
     const int64_t n = c->scene.n, E = c->n_entries, npx = (int64_t)fc.width * fc.height;
     int rc = d2h_u32_as_i64(c->order.p, order, E);
@@ -796,16 +924,17 @@ int geer_graph_export(geer_ctx *c, int64_t *order, int64_t *entry_tile, int64_t 
         free(rg);
     }
     if (pixel_tile) {
-        if (!c->pixel_tile.p) return fail(GEER_ERR_STATE, "pixel tiles were not recorded (use the host graph build)");
+        if (!c->cam_valid || !c->cam_pixel_tile)
+            return fail(GEER_ERR_STATE, "pixel tiles were not recorded (use the host graph build)");
         rc = d2h_u32_as_i64(c->pixel_tile.p, pixel_tile, npx);
         if (rc) return rc;
     }
     if (mu_c) {
-        if (!c->mu_c.p) return fail(GEER_ERR_STATE, "camera-frame means were not recorded");
+        if (!c->have_export) return fail(GEER_ERR_STATE, "camera-frame means were not recorded");
         GEER_CUDA(cudaMemcpy(mu_c, c->mu_c.p, sizeof(double) * n * 3, cudaMemcpyDeviceToHost));
     }
     if (depth) {
-        if (!c->depth.p) return fail(GEER_ERR_STATE, "depths were not recorded");
+        if (!c->have_export) return fail(GEER_ERR_STATE, "depths were not recorded");
         GEER_CUDA(cudaMemcpy(depth, c->depth.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
     }
     if ((keep || clamped) && n > 0) {

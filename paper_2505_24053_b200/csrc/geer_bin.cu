@@ -78,8 +78,10 @@ __device__ __forceinline__ bool has_entries(const AxisRanges &a) {
 
 __global__ void __launch_bounds__(kBinChunk) k_rows_count(const int32_t *__restrict__ gsorted,
                                                           const AxisRanges *__restrict__ ar, int64_t n, int n_y,
-                                                          int nch, uint32_t *__restrict__ m1) {
+                                                          int nch, uint32_t *__restrict__ m1,
+                                                          const int *__restrict__ err) {
     extern __shared__ uint32_t cnt[];
+    if (*err == GEER_ERR_OVERFLOW) return;  // (the graph exceeds the capacity: the frame is re-run)
     for (int r = threadIdx.x; r < n_y; r += blockDim.x) cnt[r] = 0;
     __syncthreads();
     const int64_t p = (int64_t)blockIdx.x * kBinChunk + threadIdx.x;
@@ -101,8 +103,10 @@ __global__ void __launch_bounds__(kBinChunk) k_rows_count(const int32_t *__restr
 __global__ void __launch_bounds__(kWalkWarps * 32) k_rows_scatter(const int32_t *__restrict__ gsorted,
                                                                  const AxisRanges *__restrict__ ar, int64_t n, int n_y,
                                                                  int nch, const uint32_t *__restrict__ p1,
-                                                                 uint2 *__restrict__ rowbin) {
+                                                                 uint2 *__restrict__ rowbin,
+                                                                 const int *__restrict__ err) {
     extern __shared__ uint32_t smem[];
+    if (*err == GEER_ERR_OVERFLOW) return;
     __shared__ uint4 stage[kWalkWarps][32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int c = blockIdx.x * kWalkWarps + wib;
@@ -158,8 +162,15 @@ __global__ void __launch_bounds__(kWalkWarps * 32) k_rows_scatter(const int32_t 
 // exclusive prefix; also the list end ranges[n_tiles] = total.  One block.
 __global__ void k_segments(const uint32_t *__restrict__ m1, const uint32_t *__restrict__ p1, int n_y, int nch,
                            int32_t *__restrict__ rowstart, int32_t *__restrict__ seg_off, int n_tiles,
-                           int32_t total, int32_t *__restrict__ ranges) {
+                           const unsigned long long *__restrict__ d_total, int32_t *__restrict__ ranges,
+                           const int *__restrict__ err) {
     __shared__ int carry;
+    if (*err == GEER_ERR_OVERFLOW) {  // every tile empty (the raster renders background; the frame is re-run)
+        for (int t = threadIdx.x; t <= n_tiles; t += blockDim.x) ranges[t] = 0;
+        if (threadIdx.x == 0) seg_off[n_y] = 0;
+        return;
+    }
+    const int32_t total = (int32_t)*d_total;
     const int64_t last = (int64_t)n_y * nch - 1;
     const uint32_t R = last >= 0 ? p1[last] + m1[last] : 0u;
     if (threadIdx.x == 0) {
@@ -206,7 +217,7 @@ __global__ void __launch_bounds__(kSegLen) k_tiles_count(const uint2 *__restrict
                                                          const int32_t *__restrict__ seg_off, int n_y, int n_x,
                                                          uint32_t *__restrict__ m2) {
     extern __shared__ uint32_t cnt[];
-    const int sgl = blockIdx.x;
+    const int sgl = blockIdx.x;  // (after an overflow seg_off[n_y] = 0: every block zeroes its slice)
     if (sgl >= seg_off[n_y]) {  // past the real segments: zero one n_x slice of the matrix tail (it is scanned)
         for (int t = threadIdx.x; t < n_x; t += blockDim.x) m2[(int64_t)n_x * sgl + t] = 0u;
         return;
@@ -296,7 +307,25 @@ __global__ void __launch_bounds__(kWalkWarps * 32) k_tiles_scatter(const uint2 *
     }
 }
 
+// status: [0] the frame's error code, [1] sticky overflow flag (cleared by geer_sync), [2..3] the largest
+// (entries, rows) of an overflowing frame since (u64 at byte 8).
+__global__ void k_check_capacity(const unsigned long long *__restrict__ totals, int64_t cap_entries, int64_t cap_rows,
+                                 int *__restrict__ status) {
+    if ((int64_t)totals[0] > cap_entries || (int64_t)totals[1] > cap_rows) {
+        atomicMax(status, (int)GEER_ERR_OVERFLOW);
+        status[1] = 1;
+        unsigned long long *mx = reinterpret_cast<unsigned long long *>(status + 2);
+        atomicMax(mx + 0, totals[0]);
+        atomicMax(mx + 1, totals[1]);
+    }
+}
+
 }  // namespace
+
+void launch_check_capacity(const unsigned long long *totals, int64_t cap_entries, int64_t cap_rows, int *err,
+                           cudaStream_t st) {
+    k_check_capacity<<<1, 1, 0, st>>>(totals, cap_entries, cap_rows, err);
+}
 
 BinPlan bin_plan(int64_t n, int n_x, int n_y, int64_t n_entries, int64_t n_rows) {
     BinPlan p;
@@ -314,22 +343,23 @@ BinPlan bin_plan(int64_t n, int n_x, int n_y, int64_t n_entries, int64_t n_rows)
 }
 
 int bin_tiles(const BinPlan &p, const int32_t *gsorted, const AxisRanges *ar, int64_t n, int n_x, int n_y,
-              int64_t n_entries, uint32_t *m1, uint32_t *p1, uint2 *rowbin, int32_t *rowstart, int32_t *seg_off,
-              uint32_t *m2, uint32_t *p2, void *temp, uint32_t *order, int32_t *ranges, cudaStream_t st) {
+              const unsigned long long *d_total, const int *err, uint32_t *m1, uint32_t *p1, uint2 *rowbin,
+              int32_t *rowstart, int32_t *seg_off, uint32_t *m2, uint32_t *p2, void *temp, uint32_t *order,
+              int32_t *ranges, cudaStream_t st) {
     const int n_tiles = n_x * n_y;
-    if (n <= 0 || n_entries <= 0) {  // every tile empty
+    if (n <= 0) {  // every tile empty
         cudaMemsetAsync(ranges, 0, sizeof(int32_t) * (n_tiles + 1), st);
         return cudaGetLastError() == cudaSuccess ? GEER_OK : GEER_ERR_CUDA;
     }
     if ((size_t)n_y * 4 * kWalkWarps > 200 * 1024 || (size_t)n_x * 4 * kWalkWarps > 200 * 1024) return GEER_ERR_INVALID;
-    k_rows_count<<<p.nch, kBinChunk, n_y * 4, st>>>(gsorted, ar, n, n_y, p.nch, m1);
+    k_rows_count<<<p.nch, kBinChunk, n_y * 4, st>>>(gsorted, ar, n, n_y, p.nch, m1, err);
     size_t tb = p.temp_bytes;
     cub::DeviceScan::ExclusiveSum(temp, tb, m1, p1, (int)p.m1_len, st);
     const int wsm_rows = n_y * 4 * kWalkWarps;
     if (wsm_rows > 48 * 1024) cudaFuncSetAttribute(k_rows_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm_rows);
     k_rows_scatter<<<(p.nch + kWalkWarps - 1) / kWalkWarps, kWalkWarps * 32, wsm_rows, st>>>(gsorted, ar, n, n_y,
-                                                                                           p.nch, p1, rowbin);
-    k_segments<<<1, 1024, 0, st>>>(m1, p1, n_y, p.nch, rowstart, seg_off, n_tiles, (int32_t)n_entries, ranges);
+                                                                                           p.nch, p1, rowbin, err);
+    k_segments<<<1, 1024, 0, st>>>(m1, p1, n_y, p.nch, rowstart, seg_off, n_tiles, d_total, ranges, err);
     k_tiles_count<<<(unsigned)p.seg_cap, kSegLen, n_x * 4, st>>>(rowbin, ar, rowstart, seg_off, n_y, n_x, m2);
     tb = p.temp_bytes;
     cub::DeviceScan::ExclusiveSum(temp, tb, m2, p2, (int)p.m2_len, st);

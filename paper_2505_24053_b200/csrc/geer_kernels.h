@@ -49,9 +49,15 @@ struct BinPlan {
     size_t temp_bytes;                          // CUB scan workspace
 };
 BinPlan bin_plan(int64_t n, int n_x, int n_y, int64_t n_entries, int64_t n_rows);
+// d_total: the device entry total (K1's counter); err: the frame's device status (an overflow turns
+// the binning into no-ops and leaves every tile empty).
 int bin_tiles(const BinPlan &p, const int32_t *gsorted, const AxisRanges *ar, int64_t n, int n_x, int n_y,
-              int64_t n_entries, uint32_t *m1, uint32_t *p1, uint2 *rowbin, int32_t *rowstart, int32_t *seg_off,
-              uint32_t *m2, uint32_t *p2, void *temp, uint32_t *order, int32_t *ranges, cudaStream_t st);
+              const unsigned long long *d_total, const int *err, uint32_t *m1, uint32_t *p1, uint2 *rowbin,
+              int32_t *rowstart, int32_t *seg_off, uint32_t *m2, uint32_t *p2, void *temp, uint32_t *order,
+              int32_t *ranges, cudaStream_t st);
+// err = GEER_ERR_OVERFLOW when totals[0] (entries) > cap_entries or totals[1] ((Gaussian, row) pairs) > cap_rows
+void launch_check_capacity(const unsigned long long *totals, int64_t cap_entries, int64_t cap_rows, int *err,
+                           cudaStream_t st);
 void sort_pixels(void *temp, size_t temp_bytes, const int32_t *keys_in, int32_t *keys_out, const int32_t *vals_in,
                  int32_t *vals_out, int64_t n, int n_bits, cudaStream_t st);
 size_t sort_pixels_temp_bytes(int64_t n, int n_bits);

@@ -70,15 +70,19 @@ class DeviceRenderer:
         self.device = device
         self.ctx = _lib.Context(device)
         self._keep = None  # tensors the last forward's state points into
+        self._stream = None
 
     def set_timing(self, on: bool):
         self.ctx.set_timing(on)
 
-    def forward(self, scene: DeviceScene, camera, config, out=None, flags: int = 0):
+    def forward(self, scene: DeviceScene, camera, config, out=None, flags: int = 0, sync: bool = True):
         """Returns (color (H,W,3) f32, remaining (H,W) f32, count (H,W) i32) CUDA tensors.
 
         ``flags``: ``_lib.GEER_CFG_*`` debug switches (e.g. ``GEER_CFG_NO_CULL``); results do not
-        depend on them.
+        depend on them.  ``sync=False`` leaves the frame in flight on the current stream (the library
+        never blocks the host once the context has seen the graph's size); ``self.sync()`` then
+        synchronises it and raises what the reference raises (ValueError for a non-PD view
+        covariance), re-rendering a frame whose graph outgrew the context's capacity.
         """
         h, w = int(camera.height), int(camera.width)
         dev = scene.means.device
@@ -94,7 +98,25 @@ class DeviceRenderer:
         _lib.check(self.ctx._lib.geer_forward(self.ctx.ptr, ctypes.byref(s), ctypes.byref(cam), ctypes.byref(cfg),
                                               color.data_ptr(), remaining.data_ptr(), count.data_ptr(), stream))
         self._keep = (scene, remaining)
+        self._stream = stream
+        if sync:
+            self.sync()
         return color, remaining, count
+
+    def sync(self) -> bool:
+        """Wait for the last forward and raise its device-side error, if any (geer_sync).
+
+        Returns True when a frame since the previous sync outgrew the context's graph capacity: the
+        capacity has grown and the last frame was rendered again (its outputs are valid), but work
+        that consumed an earlier frame of this context must be redone."""
+        rc = self.ctx._lib.geer_sync(self.ctx.ptr, self._stream)
+        if rc == _lib.GEER_ERR_OVERFLOW:
+            return True
+        _lib.check(rc)
+        return False
+
+    def clear_camera_cache(self):
+        _lib.check(self.ctx._lib.geer_clear_camera_cache(self.ctx.ptr))
 
     def backward(self, dl_dimage: torch.Tensor, grads: DeviceScene | None = None, accumulate: bool = False,
                  opacity_logit: bool = False):

@@ -260,7 +260,7 @@ class MultiViewTrainer:
             with torch.cuda.stream(self.streams[j]):
                 color, rem, cnt, dl = self._out(cam, j)
                 r = self.renderers[j]
-                r.forward(self.params.scene, cam, self.config, out=(color, rem, cnt))
+                r.forward(self.params.scene, cam, self.config, out=(color, rem, cnt), sync=False)
                 # trainer.py:269 loss(): (1 - w) L1 + w (1 - SSIM) and its image gradient
                 out, _ = loss_device(color, target, None, self.ssim_weight, grad=dl, workspace=self.loss_ws[j])
                 r.backward(dl, grads=gbufs[j].scene, accumulate=True, opacity_logit=True)
@@ -271,4 +271,8 @@ class MultiViewTrainer:
             done.record(s)
             main.wait_event(done)
             self.grads.buf.add_(gbufs[j].buf)
+        # device-side status of every view's forward (one host sync per step): a non-PD covariance raises
+        # like the reference; a graph that outgrew a context's capacity re-runs the accumulation
+        if any([r.sync() for r in self.renderers if r._stream is not None]):
+            return self.accumulate(compute_loss)
         return float(sum(float(o) for o in outs)) if compute_loss else 0.0

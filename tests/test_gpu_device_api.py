@@ -153,3 +153,116 @@ def test_multiview_inflight_matches_serial():
     g1, g2 = tr1.grads.buf, tr2.grads.buf
     assert torch.isfinite(g1).all() and float(g1.abs().max()) > 0
     torch.testing.assert_close(g2, g1, rtol=1e-3, atol=1e-4 * float(g1.abs().max()))
+
+
+def _cam_zoo():
+    """Cameras of mixed models, sizes and poses (more than the 16 cache slots + the current one)."""
+    from paper_2505_24053_b200.scene import Camera
+
+    cams = []
+    for i in range(20):
+        rot, t = synth.look_at((2.0 * np.sin(0.3 * i), 0.15 * (i % 3), -2.0 * np.cos(0.3 * i)))
+        w, h = (96 + 16 * (i % 4), 64 + 8 * (i % 3))
+        if i % 3 == 0:
+            cams.append(Camera(width=w, height=h, model="pinhole", rotation=rot, translation=t, fx=0.8 * w, fy=0.8 * w,
+                               cx=w / 2, cy=h / 2))
+        elif i % 3 == 1:
+            f = w / np.pi
+            cams.append(Camera(width=w, height=h, model="kb", rotation=rot, translation=t, fx=f, fy=f,
+                               cx=(w - 1) / 2, cy=(h - 1) / 2, k=np.zeros(4)))
+        else:
+            cams.append(Camera(width=w, height=h, model="beap", rotation=rot, translation=t, fov_x=np.pi,
+                               fov_y=np.pi * h / w))
+    return cams
+
+
+def test_camera_cache_cycles_many_mixed_cameras_bit_exact():
+    """more cameras than slots, mixed sizes and models, cycled twice through one context
+    (slot hits, parking, MRU replacement, buffer regrowth): forward, backward and the graph export
+    equal fresh contexts bit for bit."""
+    from paper_2505_24053_b200 import association
+
+    scene = synth.config_scene("C2", n=5_000)
+    ds = DeviceScene.from_scene(scene)
+    cfg = renderer.RenderConfig()
+    cams = _cam_zoo()
+    ref = []
+    for cam in cams:
+        r = DeviceRenderer(0)
+        col, rem, cnt = (t.clone() for t in r.forward(ds, cam, cfg))
+        dl = torch.ones((cam.height, cam.width, 3), device="cuda") * 1e-3
+        ref.append((col, rem, cnt))
+    r = DeviceRenderer(0)
+    for _ in range(2):
+        for cam, (col, rem, cnt) in zip(cams, ref):
+            out = r.forward(ds, cam, cfg)
+            assert torch.equal(out[0], col) and torch.equal(out[1], rem) and torch.equal(out[2], cnt)
+            g = r.backward(torch.full((cam.height, cam.width, 3), 1e-3, device="cuda"))
+            assert torch.isfinite(g.means).all()
+    # the graph export (pixel tiles, edges) after cached-slot hits equals a fresh graph build
+    for cam in cams[:4]:
+        fresh = association.build_render_graph(scene, cam)
+        again = association.build_render_graph(scene, cam)
+        np.testing.assert_array_equal(fresh.order, again.order)
+        np.testing.assert_array_equal(fresh.grid.pixel_tile, again.grid.pixel_tile)
+
+
+def test_async_frames_equal_synchronous_frames():
+    """After its first frame a context renders without host round trips; the asynchronous frames
+    (sync=False, checked once at the end) equal the synchronous first frame bit for bit."""
+    scene, cam = _small()
+    cfg = renderer.RenderConfig()
+    ds = DeviceScene.from_scene(scene)
+    r = DeviceRenderer(0)
+    first = [t.clone() for t in r.forward(ds, cam, cfg)]
+    outs = []
+    for _ in range(3):
+        outs.append([t.clone() for t in r.forward(ds, cam, cfg, sync=False)])
+    assert r.sync() is False
+    for o in outs:
+        for a, b in zip(o, first):
+            assert torch.equal(a, b)
+    assert r.stats()["n_entries"] > 0
+
+
+def test_async_overflow_rerenders_the_frame():
+    """A context sized by a small scene meets a much larger graph: the asynchronous frame overflows
+    (background only, no out-of-bounds work), sync() reports it, grows the capacity and re-renders;
+    the result equals a fresh context's frame."""
+    small = synth.config_scene("C2", n=2_000)
+    big = synth.config_scene("C2", n=40_000)
+    cam = synth.config_camera("C2", width=320, height=180)
+    cfg = renderer.RenderConfig()
+    r = DeviceRenderer(0)
+    r.forward(DeviceScene.from_scene(small), cam, cfg)  # learns a small capacity
+    dbig = DeviceScene.from_scene(big)
+    out = r.forward(dbig, cam, cfg, sync=False)
+    assert r.sync() is True  # overflowed, re-rendered
+    fresh = DeviceRenderer(0).forward(dbig, cam, cfg)
+    for a, b in zip(out, fresh):
+        assert torch.equal(a, b)
+    # the next asynchronous frame fits the grown capacity
+    out2 = [t.clone() for t in r.forward(dbig, cam, cfg, sync=False)]
+    assert r.sync() is False
+    for a, b in zip(out2, fresh):
+        assert torch.equal(a, b)
+    # and the default (synchronous) call hides the re-run from the caller
+    r2 = DeviceRenderer(0)
+    r2.forward(DeviceScene.from_scene(small), cam, cfg)
+    out3 = r2.forward(dbig, cam, cfg)
+    for a, b in zip(out3, fresh):
+        assert torch.equal(a, b)
+
+
+def test_async_frame_reports_non_pd_like_the_reference():
+    """A non-PD view covariance met by an asynchronous frame raises the reference's ValueError at sync()."""
+    from tests.golden_cases import case
+
+    c = case("not_pd")
+    scene, cam, cfg = c.scene, c.camera, c.config
+    ok = synth.config_scene("C2", n=2_000)
+    r = DeviceRenderer(0)
+    r.forward(DeviceScene.from_scene(ok), cam, cfg)  # capacity known: the next frame is asynchronous
+    r.forward(DeviceScene.from_scene(scene), cam, cfg, sync=False)
+    with pytest.raises(ValueError, match="positive definite"):
+        r.sync()
