@@ -1104,29 +1104,45 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
 
 // One warp per borderline pixel: the pixel is recomposited in fp64 exactly as
 // renderer.py:96-118 (kappa, u, t, remaining in fp64; the 1e-4 early-stop test
-// on the fp64 remaining), so its early-stop decision is the reference's.
+// on the fp64 remaining), so its early-stop decision is the reference's.  The tile's list is walked
+// in batches of 128 entries: each entry's culling record is tested against the pixel's own ray
+// first (the raster's exact PBF-hull and visual-cone tests, for a cone of one ray), and only the
+// survivors - in list order, compacted into shared memory - get the fp64 evaluation.  A culled entry
+// has t = 0: it changes neither remaining nor the count, and it is alive exactly when the survivors
+// before it leave remaining >= 1e-4, so n_eval = position of the stopping survivor + 1.
 template <bool kBEAP>
 __device__ void fixup_pixel(FrameConst fc, const geer_scene &sc, const int4 *__restrict__ items,
                             const int32_t *__restrict__ pix_list, const double2 *__restrict__ col_sc,
                             const double2 *__restrict__ row_sc, const double *__restrict__ dir64,
                             const int32_t *__restrict__ ranges, const uint32_t *__restrict__ order,
-                            const Payload *__restrict__ payload, int code, int lane, float *__restrict__ color,
-                            float *__restrict__ remaining, int32_t *__restrict__ count, int32_t *__restrict__ n_eval) {
+                            const Payload *__restrict__ payload, int code, int lane, int32_t *surv,
+                            float *__restrict__ color, float *__restrict__ remaining, int32_t *__restrict__ count,
+                            int32_t *__restrict__ n_eval) {
     const int4 it = items[code >> 8];
     const int p = pix_list[it.y + (code & 255)];
     double d[3];
     pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d);
     const int tr = fc.exhaustive ? 0 : it.x;  // exhaustive mode: one shared list [0, n_kept)
     const int e0 = ranges[tr], e1 = ranges[tr + 1];
+    // the pixel's culling region: its mirror coordinates (+-1e-5) and a cone of one ray (k_warp_cull)
+    float4 box = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY), cone = make_float4(0.f, 0.f, 1.f, 0.f);
+    {
+        float c[3];
+        for (int i = 0; i < 3; ++i) c[i] = (float)(fc.R[i * 3 + 0] * d[0] + fc.R[i * 3 + 1] * d[1] + fc.R[i * 3 + 2] * d[2]);
+        if (c[2] > 1e-3f) {
+            const float mx = c[0] / (sqrtf(c[0] * c[0] + c[2] * c[2]) + c[2]);
+            const float my = c[1] / (sqrtf(c[1] * c[1] + c[2] * c[2]) + c[2]);
+            box = make_float4(mx - 1e-5f, mx + 1e-5f, my - 1e-5f, my + 1e-5f);
+        }
+        const float inv = rsqrtf(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+        cone = make_float4(c[0] * inv, c[1] * inv, c[2] * inv, 1.0f - 1e-7f);
+    }
     double cr = 0, cg = 0, cb = 0, rem = 1.0;
-    int cnt = 0, ne = 0;
+    int cnt = 0, last = e0 - 1;  // last: the last alive survivor
     bool alive = true;
     // fp64 t of entry e (renderer.py:96-105 in fp64: the payload's cross product, the reference
     // formulation near the cutoff, fp64 sigmoid and exp)
     auto eval64 = [&](int e, double &t, float4 &cl) {
-        t = 0.0;
-        cl = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (e >= e1) return;
         const uint32_t g = order[e];
         const Payload &P = payload[g];
         cl = P.col;
@@ -1142,51 +1158,65 @@ __device__ void fixup_pixel(FrameConst fc, const geer_scene &sc, const int4 *__r
         if (fc.cutoff && !(kap <= fc.lam2)) u = 0.0;
         t = u < kMaxBlendT ? u : kMaxBlendT;
     };
-    constexpr int kSub = 4;  // batches of 32 evaluated together: their loads overlap
-    for (int sbase = e0; sbase < e1 && alive; sbase += 32 * kSub) {
-        double tt[kSub];
-        float4 cc[kSub];
+    for (int sbase = e0; sbase < e1 && alive; sbase += 128) {
+        // survivors of the batch, in list order
+        int ns = 0;
 #pragma unroll
-        for (int k = 0; k < kSub; ++k) eval64(sbase + 32 * k + lane, tt[k], cc[k]);
-#pragma unroll
-        for (int k = 0; k < kSub; ++k) {
-        const int base = sbase + 32 * k;
-        if (!(base < e1 && alive)) break;
-        const double t = tt[k];
-        const float4 cl = cc[k];
-        // composite the batch with a warp scan: rem before entry j = rem * prod_{i<j} (1 - t_i); the
-        // alive test (rem >= 1e-4, renderer.py:113) holds on a prefix of the batch since rem only
-        // decreases (same fp64 products as the reference's loop up to the association order)
-        const int n = min(32, e1 - base);
-        double P = lane < n ? 1.0 - t : 1.0;  // inclusive prefix product
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, P, o);
-            if (lane >= o) P *= y;
+        for (int k = 0; k < 4; ++k) {
+            const int e = sbase + 32 * k + lane;
+            bool keep = e < e1;
+            if (keep && fc.cull) {
+                const Cull cl = payload[order[e]].cull;
+                keep = !(cl.box.y < box.x || cl.box.x > box.y || cl.box.w < box.z || cl.box.z > box.w) &&
+                       !cone_misses(cl.k0, cl.k1, cone);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) surv[ns + __popc(m & ((1u << lane) - 1u))] = e;
+            ns += __popc(m);
         }
-        const double up1 = __shfl_up_sync(0xffffffffu, P, 1);  // (every lane takes part in the shuffle)
-        const double pex = lane == 0 ? 1.0 : up1;
-        const double rb = rem * pex;
-        const bool live = lane < n && rb >= kMinRemaining;
-        const int na = __popc(__ballot_sync(0xffffffffu, live));
-        double w = live ? rb * t : 0.0;
-        double wr = w * cl.x, wg = w * cl.y, wb = w * cl.z;
+        __syncwarp();
+        for (int i0 = 0; i0 < ns && alive; i0 += 32) {
+            const int n = min(32, ns - i0);
+            double t = 0.0;
+            float4 cl = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int e = lane < n ? surv[i0 + lane] : e1;
+            if (lane < n) eval64(e, t, cl);
+            // composite the survivors with a warp scan: rem before survivor j = rem * prod_{i<j} (1 - t_i);
+            // the alive test (rem >= 1e-4, renderer.py:113) holds on a prefix since rem only decreases
+            double P = lane < n ? 1.0 - t : 1.0;  // inclusive prefix product
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            wr += __shfl_xor_sync(0xffffffffu, wr, o);
-            wg += __shfl_xor_sync(0xffffffffu, wg, o);
-            wb += __shfl_xor_sync(0xffffffffu, wb, o);
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, P, o);
+                if (lane >= o) P *= y;
+            }
+            const double up1 = __shfl_up_sync(0xffffffffu, P, 1);  // (every lane takes part in the shuffle)
+            const double pex = lane == 0 ? 1.0 : up1;
+            const double rb = rem * pex;
+            const bool live = lane < n && rb >= kMinRemaining;
+            const int na = __popc(__ballot_sync(0xffffffffu, live));
+            double w = live ? rb * t : 0.0;
+            double wr = w * cl.x, wg = w * cl.y, wb = w * cl.z;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                wr += __shfl_xor_sync(0xffffffffu, wr, o);
+                wg += __shfl_xor_sync(0xffffffffu, wg, o);
+                wb += __shfl_xor_sync(0xffffffffu, wb, o);
+            }
+            cr += wr;
+            cg += wg;
+            cb += wb;
+            cnt += __popc(__ballot_sync(0xffffffffu, live && t > 0.0));
+            const double pl = __shfl_sync(0xffffffffu, P, na > 0 ? na - 1 : 0);
+            const int el = __shfl_sync(0xffffffffu, e, na > 0 ? na - 1 : 0);
+            if (na > 0) {
+                rem = rem * pl;
+                last = el;
+            }
+            if (!(rem >= kMinRemaining)) alive = false;  // the entries after survivor `last` are not alive
         }
-        cr += wr;
-        cg += wg;
-        cb += wb;
-        cnt += __popc(__ballot_sync(0xffffffffu, live && t > 0.0));
-        ne += na;
-        const double pl = __shfl_sync(0xffffffffu, P, na > 0 ? na - 1 : 0);
-        if (na > 0) rem = rem * pl;
-        if (na < n) alive = false;
-        }
+        __syncwarp();
     }
+    const int ne = alive ? e1 - e0 : last - e0 + 1;
     if (lane == 0) {
         color[(int64_t)p * 3 + 0] = (float)(cr + rem * fc.bg[0]);
         color[(int64_t)p * 3 + 1] = (float)(cg + rem * fc.bg[1]);
@@ -1207,12 +1237,13 @@ __global__ void __launch_bounds__(128) k_fixup(FrameConst fc, geer_scene sc, con
                                                const int32_t *__restrict__ fixup_list, float *__restrict__ color,
                                                float *__restrict__ remaining, int32_t *__restrict__ count,
                                                int32_t *__restrict__ n_eval) {
+    __shared__ int32_t surv[4][128];  // per warp: the batch's surviving entries
     const int lane = threadIdx.x & 31;
     const int n_fix = (int)counters[2];
     const int n_warps = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
     for (int wg = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); wg < n_fix; wg += n_warps)
         fixup_pixel<kBEAP>(fc, sc, items, pix_list, col_sc, row_sc, dir64, ranges, order, payload, fixup_list[wg], lane,
-                           color, remaining, count, n_eval);
+                           surv[threadIdx.x >> 5], color, remaining, count, n_eval);
 }
 
 // ------------------------------------------------------------------------------ K6
