@@ -11,7 +11,7 @@ raises.
 __version__ = "0.1.0"
 
 
-def install(with_graph: bool = False):
+def install(with_graph: bool | None = None):
     """Patch a live ``raygauss`` so its render / render_backward / build_render_graph run here (dropin.py)."""
     from .dropin import install as _install
 

@@ -35,16 +35,23 @@ def _to_ref_graph(g, ra):
                           keep=g.keep, clamped=g.clamped, grid=grid)
 
 
-def make_render(with_graph: bool = False):
-    """``raygauss.renderer.render`` replacement (renderer.py:123-176)."""
+def make_render(with_graph: bool | None = None):
+    """``raygauss.renderer.render`` replacement (renderer.py:123-176): ``FrameOutput.graph`` is the
+    reference's ``RenderGraph`` (lazily exported by default, see ``renderer.lazy_dataclass``)."""
     from . import renderer
 
     def render(scene, camera, config=None):
         rr, rc, ra = _ref("renderer"), _ref("camera"), _ref("association")
-        out = renderer.render(scene, camera, config, return_graph=with_graph)
+        out = renderer.render(scene, camera, config, return_graph=False if with_graph is None else with_graph)
+        if with_graph is None:
+            cfg = config or renderer.RenderConfig()
+            graph = renderer.lazy_dataclass(
+                ra.RenderGraph, lambda: _to_ref_graph(renderer.build_graph_for(scene, camera, cfg.lam, cfg.tile_px), ra))
+        else:
+            graph = _to_ref_graph(out.graph, ra)
         return rr.FrameOutput(color=rc.BEAPImage(color=out.color.color, mask=out.color.mask),
                               remaining_transmittance=out.remaining_transmittance,
-                              contributor_count=out.contributor_count, graph=_to_ref_graph(out.graph, ra))
+                              contributor_count=out.contributor_count, graph=graph)
 
     render.__doc__ = "B200 drop-in for raygauss.renderer.render (libgeer_b200.so)"
     return render
@@ -83,7 +90,7 @@ TARGETS = (("renderer", "render"), ("renderer", "render_backward"), ("associatio
            ("trainer", "render"), ("trainer", "render_backward"), ("trainer", "loss"))
 
 
-def install(with_graph: bool = False) -> list[str]:
+def install(with_graph: bool | None = None) -> list[str]:
     """Rebind the reference's render entry points to the B200 path; returns what was patched.
 
     Modules of ``raygauss`` that are not importable (or do not bind a name) are

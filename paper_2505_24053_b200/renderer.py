@@ -20,6 +20,8 @@ tensor-level fast path (device tensors, no host copies) is
 
 from __future__ import annotations
 
+import dataclasses
+
 import ctypes
 import os
 from dataclasses import dataclass, field
@@ -126,13 +128,41 @@ def _host_empty(shape, dtype) -> np.ndarray:
     return t.numpy()
 
 
-def render(scene, camera, config: RenderConfig | None = None, *, return_graph: bool = False,
+def lazy_dataclass(cls, thunk):
+    """An instance of dataclass ``cls`` whose fields come from ``thunk()`` on first access.
+
+    ``FrameOutput.graph`` uses it: the reference always attaches the render graph
+    (renderer.py:170-175); here it is exported from the device only if the caller reads it (the
+    association is deterministic, so rebuilding it then gives the frame's own graph - as long as
+    the caller has not modified the scene's arrays in place meanwhile)."""
+    lazy = _LAZY_TYPES.get(cls)
+    if lazy is None:
+        def __getattr__(self, name):
+            d = object.__getattribute__(self, "__dict__")
+            if name.startswith("__") or "_thunk" not in d:
+                raise AttributeError(name)
+            obj = d.pop("_thunk")()
+            for f in dataclasses.fields(cls):
+                d[f.name] = getattr(obj, f.name)
+            return object.__getattribute__(self, name)
+
+        lazy = type("Lazy" + cls.__name__, (cls,), {"__getattr__": __getattr__})
+        _LAZY_TYPES[cls] = lazy
+    inst = object.__new__(lazy)
+    inst.__dict__["_thunk"] = thunk
+    return inst
+
+
+_LAZY_TYPES: dict = {}
+
+
+def render(scene, camera, config: RenderConfig | None = None, *, return_graph: bool | None = None,
            device: int = 0) -> FrameOutput:
     """Render ``scene`` through ``camera`` (renderer.py:123-176) on the GPU.
 
-    ``return_graph=True`` also exports the association (``FrameOutput.graph``),
-    which the reference always builds; it costs a device->host copy of the
-    whole graph, so it is opt-in.
+    ``FrameOutput.graph`` is the association, as in the reference: by default (``return_graph=None``)
+    a lazily exported ``RenderGraph`` (nothing is copied unless it is read); ``True`` exports it
+    now, ``False`` leaves ``None``.
     """
     config = config or RenderConfig()
     validate_camera(camera)
@@ -147,7 +177,10 @@ def render(scene, camera, config: RenderConfig | None = None, *, return_graph: b
     _lib.check(ctx._lib.geer_render_host(ctx.ptr, ctypes.byref(hs.struct), ctypes.byref(cam), ctypes.byref(cfg),
                                          color.ctypes.data, remaining.ctypes.data, count.ctypes.data))
     graph = None
-    if return_graph and hs.n > 0:
+    if return_graph is None:
+        lam, tile_px = config.lam, config.tile_px
+        graph = lazy_dataclass(RenderGraph, lambda: build_graph_for(scene, camera, lam, tile_px, device=device))
+    elif return_graph:
         graph = build_graph_for(scene, camera, config.lam, config.tile_px, device=device)
     return FrameOutput(color=BEAPImage(color=color, mask=np.ones((h, w), dtype=bool)),
                        remaining_transmittance=remaining, contributor_count=count, graph=graph)
