@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "geer_common.cuh"
 #include "geer_kernels.h"
@@ -367,7 +368,39 @@ __device__ __forceinline__ bool mbar_try_wait(unsigned long long *bar, unsigned 
         : "memory");
     return ok != 0;
 }
+#ifdef GEER_WATCHDOG
+// Diagnosis build: a barrier wait that lasts over 2 s prints where it is stuck and traps.
+__device__ __forceinline__ unsigned long long wd_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __noinline__ void wd_wait(unsigned long long *bar, unsigned parity, int tag) {
+    const unsigned long long t0 = wd_now();
+    for (;;) {
+        unsigned ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (wd_now() - t0 > 2000000000ull) {
+            printf("WATCHDOG tag %d block %d thread %d bar %p parity %u\n", tag, (int)blockIdx.x, (int)threadIdx.x,
+                   (void *)bar, parity);
+            __trap();
+        }
+    }
+}
+#endif
+
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+#ifdef GEER_WATCHDOG
+    wd_wait(bar, parity, 1);
+    return;
+#endif
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
@@ -382,6 +415,10 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
 __device__ __forceinline__ void mbar_wait_suspend(unsigned long long *bar, unsigned parity) {
 #ifndef GEER_PRODUCER_SUSPEND_NS
 #define GEER_PRODUCER_SUSPEND_NS 20000
+#endif
+#ifdef GEER_WATCHDOG
+    wd_wait(bar, parity, 2);
+    return;
 #endif
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -478,8 +515,12 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
     };
     int next = 0, fin = 0;  // next fill to issue (n_fills: the sentinel), oldest fill not yet full
     uint32_t g_next = load_gid(0);
+#ifdef GEER_WATCHDOG
+    unsigned long long t_prog = wd_now();
+#endif
     for (;;) {
-        if (stop_when_done && *((volatile int *)&S.done_warps) == Smem::kNW) break;  // every consumer left
+        // every consumer left (lane 0's reading, broadcast: the warp must take this branch as one)
+        if (stop_when_done && __shfl_sync(0xffffffffu, *((volatile int *)&S.done_warps), 0) == Smem::kNW) break;
         bool progress = false;
         if (next <= n_fills && ready(&S.empty[next % kStages], ((next / kStages) & 1) ^ 1)) {
             const int s = next % kStages;
@@ -519,6 +560,15 @@ __device__ __forceinline__ void pipe_produce(Smem &S, const uint32_t *__restrict
             progress = true;
         }
         if (next > n_fills && fin == n_fills) break;
+#ifdef GEER_WATCHDOG
+        if (progress) t_prog = wd_now();
+        else if (wd_now() - t_prog > 2000000000ull) {
+            if (lane == 0)
+                printf("WATCHDOG producer block %d next %d fin %d n_fills %d done %d count0 %d\n", (int)blockIdx.x, next,
+                       fin, n_fills, *((volatile int *)&S.done_warps), S.count[0]);
+            __trap();
+        }
+#endif
         if (!progress) {  // sleep on the gather we wait for, else on the slot we wait for
             if (fin < issued)
                 mbar_try_wait_suspend(&S.landed[fin % kStages], (fin / kStages) & 1);
@@ -587,12 +637,16 @@ __device__ __forceinline__ void pipe_drop_out(Smem &S, int s, unsigned phase) {
     const int lane = threadIdx.x & 31;
     for (int k = 0; k < kStages; ++k) {
         if (k > 0) {
+            // Every decision here is made on lane 0's observation and broadcast: lanes that judged
+            // "filled" and "producer stopped" differently would wait at different warp barriers
+            // (this __syncwarp vs the epilogue's warp reductions) forever.
             bool ready = false;
-            while (!(ready = mbar_try_wait(&S.full[s], phase))) {
-                if (*((volatile int *)&S.stop)) break;
+            for (;;) {
+                ready = __shfl_sync(0xffffffffu, (int)mbar_try_wait(&S.full[s], phase), 0) != 0;
+                if (ready || __shfl_sync(0xffffffffu, *((volatile int *)&S.stop), 0)) break;
                 __nanosleep(256);  // (a retired warp: do not take issue slots from the working ones)
             }
-            if (!ready || S.count[s] == 0) return;
+            if (!ready || __shfl_sync(0xffffffffu, S.count[s], 0) == 0) return;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_drop(&S.empty[s]);
@@ -1046,7 +1100,7 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
     unsigned phase = 0;
     int s = 0, base = 0;
     for (;;) {
-        mbar_wait_suspend(&S.full[s], phase);
+        mbar_wait(&S.full[s], phase);
 #ifdef GEER_CTA_TIMING
         if (tid == 0 && base == 0 && blockIdx.x < (1u << 16)) g_cta_tf[blockIdx.x] = gtimer();
 #endif
@@ -1375,7 +1429,7 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
     int s = 0;
     int hi = max_n;  // local index one past the current stage
     for (;;) {
-        mbar_wait_suspend(&S.full[s], phase);
+        mbar_wait(&S.full[s], phase);
         const int n = S.count[s];
         if (n == 0) break;
         const int lo = hi - n;
