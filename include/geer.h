@@ -156,6 +156,20 @@ int geer_sync(geer_ctx *ctx, void *stream);
 /* Frees the context's cached camera setups (K0 outputs of up to 16 other cameras, <= 1 GiB). */
 int geer_clear_camera_cache(geer_ctx *ctx);
 
+/* ---- caller-owned workspace (SURVEY 8b ownership) -------------------------------
+ * geer_workspace_bytes: device bytes the device-level path (geer_forward + geer_backward) needs for
+ * n Gaussians and one camera/config, for a graph of up to max_entries entries (<= 0: the context's
+ * learned capacity, or 24 per Gaussian if it has none; ctx may be NULL).  Returns 0 on bad input.
+ * geer_set_workspace: the context carves every buffer from [ptr, ptr + bytes) (caller-owned, e.g. a
+ * torch tensor) instead of cudaMalloc; synchronises the device and drops the buffers it held.  With a
+ * workspace the camera-setup cache is off (one camera's setup at a time), an undersized workspace
+ * fails with GEER_ERR_NOMEM naming the bytes needed, ptr = NULL returns to library-owned memory.
+ * Host-level calls and geer_association_check still allocate their own staging. */
+size_t geer_workspace_bytes(geer_ctx *ctx, int64_t n, int32_t n_bands, const geer_camera *camera,
+                            const geer_config *config, int64_t max_entries);
+int geer_set_workspace(geer_ctx *ctx, void *ptr, size_t bytes);
+int geer_workspace_used(geer_ctx *ctx, size_t *used);
+
 /* dl_dimage (H,W,3) f32 device.  flags: GEER_ACCUMULATE adds into grads (multi-view);
  * GEER_OPACITY_LOGIT returns dopacities w.r.t. the stored logit (trainer.py:208-217)
  * instead of the reference's linear-opacity convention. */

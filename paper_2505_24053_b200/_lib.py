@@ -33,7 +33,8 @@ EXPORTED = (
     "geer_backward", "geer_frame_stats", "geer_graph_info", "geer_graph_export", "geer_build_graph_host",
     "geer_render_host", "geer_render_backward_host", "geer_l1_grad", "geer_adam", "geer_measure_fp32_peak",
     "geer_loss_workspace_bytes", "geer_loss", "geer_resample_to_beap", "geer_ply_to_soa",
-    "geer_association_check", "geer_sync", "geer_clear_camera_cache",
+    "geer_association_check", "geer_sync", "geer_clear_camera_cache", "geer_workspace_bytes",
+    "geer_set_workspace", "geer_workspace_used",
 )
 
 
@@ -132,6 +133,9 @@ def load():
             "geer_association_check": ([P, ctypes.c_int32, P, P, ctypes.c_int32, P], I),
             "geer_sync": ([P, P], I),
             "geer_clear_camera_cache": ([P], I),
+            "geer_workspace_bytes": ([P, I64, ctypes.c_int32, P, P, I64], ctypes.c_size_t),
+            "geer_set_workspace": ([P, P, ctypes.c_size_t], I),
+            "geer_workspace_used": ([P, P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

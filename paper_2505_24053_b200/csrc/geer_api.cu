@@ -51,7 +51,16 @@ int fail(int code, const char *fmt, ...) {
 struct Buf {
     void *p = nullptr;
     size_t cap = 0;
+    bool owned = true;  // cudaMalloc'ed by the library (else: a slice of the caller's workspace)
 };
+
+// A caller-owned device workspace (geer_set_workspace): buffers are carved from it by a bump
+// pointer instead of cudaMalloc, so the caller's allocator (torch) owns every byte of the path.
+struct Arena {
+    char *base = nullptr;
+    size_t size = 0, used = 0;
+};
+thread_local Arena *t_arena = nullptr;  // the arena of the context of the current API call
 
 // TMA tensor map over an array of fixed-size rows (payloads), for the raster's gather4 copies.
 int make_row_map(CUtensorMap *map, const void *base, int64_t rows, int row_bytes) {
@@ -151,6 +160,7 @@ struct geer_ctx {
     Buf temp;
     // host-path staging
     Buf h64_means, h64_log, h64_quats, h64_op, h64_sh, s32_means, s32_log, s32_quats, s32_op, s32_sh, out64, g64;
+    Arena arena;  // caller-owned workspace (geer_set_workspace), if attached
 };
 
 namespace {
@@ -160,9 +170,23 @@ T *ensure(Buf &b, size_t count, int *rc) {
     size_t bytes = count * sizeof(T);
     if (bytes == 0) bytes = 16;
     if (bytes > b.cap) {
-        if (b.p) cudaFree(b.p);
+        if (b.p && b.owned) cudaFree(b.p);
         b.p = nullptr;
         b.cap = 0;
+        b.owned = true;
+        if (t_arena && t_arena->base) {  // caller-owned workspace: exact size, 256-B aligned slices
+            const size_t off = (t_arena->used + 255) & ~(size_t)255;
+            if (off + bytes > t_arena->size) {
+                *rc = fail(GEER_ERR_NOMEM, "caller workspace too small: %zu of %zu bytes used, %zu more needed "
+                           "(size it with geer_workspace_bytes)", t_arena->used, t_arena->size, bytes);
+                return nullptr;
+            }
+            b.p = t_arena->base + off;
+            b.cap = bytes;
+            b.owned = false;
+            t_arena->used = off + bytes;
+            return reinterpret_cast<T *>(b.p);
+        }
         size_t want = bytes + bytes / 4;
         cudaError_t e = cudaMalloc(&b.p, want);
         if (e == cudaErrorMemoryAllocation) {
@@ -187,10 +211,18 @@ T *ensure(Buf &b, size_t count, int *rc) {
     if (rc) return rc
 
 void free_buf(Buf &b) {
-    if (b.p) cudaFree(b.p);
+    if (b.p && b.owned) cudaFree(b.p);
     b.p = nullptr;
     b.cap = 0;
+    b.owned = true;
 }
+
+// Sets the thread's current arena to the context's for the duration of an API call.
+struct ArenaScope {
+    Arena *prev;
+    explicit ArenaScope(Arena *a) : prev(t_arena) { t_arena = a; }
+    ~ArenaScope() { t_arena = prev; }
+};
 
 int make_frame_const(const geer_camera *cam, const geer_config *cfg, int n_bands, FrameConst *fc) {
     if (!cam || !cfg) return fail(GEER_ERR_INVALID, "camera and config are required");
@@ -355,6 +387,29 @@ void clear_camera_cache(geer_ctx *c) {
     }
 }
 
+// Every workspace buffer of a context (and its cached camera setups) released; state that points
+// into them reset.
+void free_all_buffers(geer_ctx *c) {
+    Buf *bufs[] = {&c->col_sc, &c->row_sc, &c->medges_x, &c->medges_y, &c->edges_x, &c->edges_y, &c->dir64,
+                   &c->theta, &c->phi, &c->minmax, &c->pixel_tile, &c->pixel_tile_sorted, &c->pix_iota, &c->pix_list,
+                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->work, &c->n_work, &c->payload,
+                   &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted,
+                   &c->ranges_ax, &c->flags, &c->mu_c, &c->depth,
+                   &c->order, &c->tile_ranges, &c->wcull,
+                   &c->bin_m1, &c->bin_p1, &c->bin_rows, &c->bin_rowstart, &c->bin_segoff, &c->bin_m2, &c->bin_p2, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,
+                   &c->accum, &c->temp, &c->h64_means, &c->h64_log, &c->h64_quats, &c->h64_op, &c->h64_sh,
+                   &c->s32_means, &c->s32_log, &c->s32_quats, &c->s32_op, &c->s32_sh, &c->out64, &c->g64};
+    for (Buf *b : bufs) free_buf(*b);
+    clear_camera_cache(c);
+    c->cam_valid = c->cam_pixel_tile = false;
+    c->have_frame = c->have_raster = c->have_stats = c->have_export = false;
+    c->iota_ptr = nullptr;
+    c->iota_cap = 0;
+    c->iota_len = 0;
+    c->cap_entries = c->cap_rows = 0;
+    c->fwd_remaining = nullptr;
+}
+
 // Make the context's camera setup the one of c->fc: from a slot if it is cached there (the current
 // setup moves into that slot), else rebuilt by camera_setup - after parking the current setup in a
 // free slot when there is one and the byte budget allows, otherwise over the current setup.
@@ -375,7 +430,7 @@ int select_camera(geer_ctx *c, bool want_pixel_tile, cudaStream_t st) {
         c->cam_slots[hit].last_use = ++c->cam_clock;
         return GEER_OK;
     }
-    const bool park = small && c->cam_valid && free_slot >= 0 &&
+    const bool park = small && c->cam_valid && free_slot >= 0 && !c->arena.base &&
                       (int64_t)c->cam_fc.width * c->cam_fc.height <= kCamSlotMaxPixels &&
                       used + current_camera_bytes(c) <= kCamCacheBytes;
     if (park) {
@@ -395,6 +450,84 @@ int select_camera(geer_ctx *c, bool want_pixel_tile, cudaStream_t st) {
     c->cam_pixel_tile = want_pixel_tile || fc.model != GEER_BEAP;
     c->cam_fc = fc;
     return GEER_OK;
+}
+
+// Largest CUB temporary of a frame (depth sort, the two binning scans, the camera setup's scans and
+// pixel sort).
+size_t frame_temp_bytes(const FrameConst &fc, int64_t n, int64_t cap_e, int64_t cap_r) {
+    const int64_t npx = (int64_t)fc.width * fc.height;
+    size_t t = sort_depth_temp_bytes(lmax(n, 1));
+    const BinPlan bp = bin_plan(lmax(n, 1), fc.n_x, fc.n_y, lmax(cap_e, 1), lmax(cap_r, 1));
+    t = t > bp.temp_bytes ? t : bp.temp_bytes;
+    const size_t sc = scan_i32_temp_bytes(fc.n_tiles + 1);
+    t = t > sc ? t : sc;
+    if (fc.model != GEER_BEAP) {
+        const size_t sp = sort_pixels_temp_bytes(npx, ceil_log2(fc.n_tiles));
+        t = t > sp ? t : sp;
+    }
+    return t;
+}
+
+// Device bytes of the device-level path (geer_forward + geer_backward) for one camera: the same
+// buffers camera_setup / run_forward / run_backward ensure, each a 256-B aligned slice.
+size_t workspace_estimate(const FrameConst &fc, int64_t n, int64_t cap_e, int64_t cap_r) {
+    const int64_t npx = (int64_t)fc.width * fc.height, nt = fc.n_tiles;
+    const int64_t max_items = nt + (npx + kRasterThreads - 1) / kRasterThreads;
+    size_t total = 0;
+    auto add = [&](int64_t bytes) { total += (size_t)((lmax(bytes, 16) + 255) & ~(int64_t)255); };
+    // camera setup
+    add((nt + 1) * 4);                                   // tile_off
+    add(npx * 4);                                        // pix_list
+    add((fc.n_x + 1) * 8);                               // medges_x
+    add((fc.n_y + 1) * 8);                               // medges_y
+    if (fc.model == GEER_BEAP) {
+        add(fc.width * 16);                              // col_sc
+        add(fc.height * 16);                             // row_sc
+    } else {
+        add(npx * 24);                                   // dir64
+        add(npx * 8);                                    // theta
+        add(npx * 8);                                    // phi
+        add(32);                                         // minmax
+        add((fc.n_x + 1) * 8);                           // edges_x
+        add((fc.n_y + 1) * 8);                           // edges_y
+        add(npx * 4);                                    // pixel_tile
+        add(npx * 4);                                    // pixel_tile_sorted
+        add(npx * 4);                                    // pix_iota
+        add((nt + 1) * 4);                               // tile_count
+    }
+    add(nt * 4);                                         // item_count
+    add(nt * 4);                                         // item_off
+    add(max_items * 16);                                 // items
+    add(4);                                              // n_items
+    add(max_items * (16 + (int64_t)sizeof(ItemFrame) / 16) * 16);  // wcull + item frames
+    // per Gaussian
+    add(n * (int64_t)sizeof(Payload));
+    add(n * 4);                                          // depth keys
+    add(n * 4);                                          // sorted depth keys
+    add(n * 4);                                          // gid iota
+    add(n * 4);                                          // sorted gids
+    add(n * (int64_t)sizeof(AxisRanges));
+    add(2 * n);                                          // flags
+    add((nt + 1) * 4);                                   // tile ranges
+    // per entry (the capacity) and the binning matrices
+    const BinPlan bp = bin_plan(lmax(n, 1), fc.n_x, fc.n_y, lmax(cap_e, 1), lmax(cap_r, 1));
+    add((bp.m1_len + 1) * 4);
+    add((bp.m1_len + 1) * 4);
+    add((bp.rows_cap + 1) * 8);
+    add((fc.n_y + 1) * 4);
+    add((fc.n_y + 1) * 4);
+    add((bp.m2_len + 1) * 4);
+    add((bp.m2_len + 1) * 4);
+    add((lmax(cap_e, 1) + 1) * 4);                       // order
+    add(max_items * 16);                                 // work
+    add(8);                                              // n_work
+    // per pixel
+    add(npx * 4);                                        // n_eval
+    add(npx * 4);                                        // fix-up list
+    // backward
+    add(n * 64);                                         // accumulators
+    add((int64_t)frame_temp_bytes(fc, n, cap_e, cap_r)); // CUB temp
+    return total;
 }
 
 // Full association (+ raster when color != null) for the scene in c->scene.
@@ -459,7 +592,8 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
             c->iota_len = n;
         }
         size_t b1 = sort_depth_temp_bytes(n);
-        void *tmp = ENSURE(char, c->temp, b1);
+        // (the temp buffer is sized once for every user of the frame: a caller workspace is not regrown)
+        void *tmp = ENSURE(char, c->temp, lmax((int64_t)b1, (int64_t)frame_temp_bytes(fc, n, c->cap_entries, c->cap_rows)));
         sort_depth(tmp, b1, dkey, dkey_s, giota, gsorted, n, st);
     }
     if (!async) {
@@ -503,9 +637,12 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
         if (total >= ((int64_t)1 << 31) - 1)
             return fail(GEER_ERR_NOMEM, "render graph has %lld entries (limit 2^31)", (long long)total);
         c->n_entries = total;
-        // capacity of the following asynchronous frames (grow-only, 25 % headroom)
+        // capacity of the following asynchronous frames (grow-only, 25 % headroom); the buffers are
+        // sized by it from this frame on, so the asynchronous frames never regrow them
         c->cap_entries = lmax(c->cap_entries, lmin(total + total / 4 + 4096, ((int64_t)1 << 31) - 2));
         c->cap_rows = lmax(c->cap_rows, rows + rows / 4 + 1024);
+        total = c->cap_entries;
+        rows = c->cap_rows;
     }
     // ---- sort: per-tile lists (stable in depth order) and their ranges, then the raster work order
     {
@@ -677,17 +814,7 @@ void geer_destroy(geer_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
-    Buf *bufs[] = {&c->col_sc, &c->row_sc, &c->medges_x, &c->medges_y, &c->edges_x, &c->edges_y, &c->dir64,
-                   &c->theta, &c->phi, &c->minmax, &c->pixel_tile, &c->pixel_tile_sorted, &c->pix_iota, &c->pix_list,
-                   &c->tile_count, &c->tile_off, &c->item_count, &c->item_off, &c->items, &c->n_items, &c->work, &c->n_work, &c->payload,
-                   &c->depth_key, &c->depth_key_sorted, &c->gid_iota, &c->gid_sorted,
-                   &c->ranges_ax, &c->flags, &c->mu_c, &c->depth,
-                   &c->order, &c->tile_ranges, &c->wcull,
-                   &c->bin_m1, &c->bin_p1, &c->bin_rows, &c->bin_rowstart, &c->bin_segoff, &c->bin_m2, &c->bin_p2, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,
-                   &c->accum, &c->temp, &c->h64_means, &c->h64_log, &c->h64_quats, &c->h64_op, &c->h64_sh,
-                   &c->s32_means, &c->s32_log, &c->s32_quats, &c->s32_op, &c->s32_sh, &c->out64, &c->g64};
-    for (Buf *b : bufs) free_buf(*b);
-    clear_camera_cache(c);
+    free_all_buffers(c);
     for (int i = 0; i < 6; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     if (c->ev_hdr) cudaEventDestroy(c->ev_hdr);
@@ -696,6 +823,45 @@ void geer_destroy(geer_ctx *c) {
     if (c->h_hdr) cudaFreeHost(c->h_hdr);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
+}
+
+size_t geer_workspace_bytes(geer_ctx *c, int64_t n, int32_t n_bands, const geer_camera *camera,
+                            const geer_config *config, int64_t max_entries) {
+    FrameConst fc;
+    if (make_frame_const(camera, config, n_bands, &fc)) return 0;
+    if (n < 0) {
+        fail(GEER_ERR_INVALID, "negative Gaussian count");
+        return 0;
+    }
+    int64_t cap_e = max_entries, cap_r = max_entries;
+    if (cap_e <= 0) {  // the context's learned capacity, else a generous default (24 entries per Gaussian)
+        cap_e = c && c->cap_entries > 0 ? c->cap_entries : 24 * n + 4096;
+        cap_r = c && c->cap_rows > 0 ? c->cap_rows : cap_e;
+    } else {
+        cap_e = lmin(cap_e + cap_e / 4 + 4096, ((int64_t)1 << 31) - 2);  // (the capacity the frame will keep)
+        cap_r = cap_e;
+    }
+    return workspace_estimate(fc, n, cap_e, cap_r);
+}
+
+int geer_set_workspace(geer_ctx *c, void *ptr, size_t bytes) {
+    if (!c) return fail(GEER_ERR_INVALID, "null context");
+    cudaSetDevice(c->device);
+    GEER_CUDA(cudaDeviceSynchronize());  // (queued frames may still use the current buffers)
+    free_all_buffers(c);                 // library-owned memory back; slices of a previous workspace dropped
+    c->arena = Arena{};
+    if (ptr) {
+        if (bytes < 4096) return fail(GEER_ERR_INVALID, "workspace of %zu bytes is too small", bytes);
+        c->arena.base = reinterpret_cast<char *>(ptr);
+        c->arena.size = bytes;
+    }
+    return GEER_OK;
+}
+
+int geer_workspace_used(geer_ctx *c, size_t *used) {
+    if (!c || !used) return fail(GEER_ERR_INVALID, "null argument");
+    *used = c->arena.used;
+    return GEER_OK;
 }
 
 int geer_clear_camera_cache(geer_ctx *c) {
@@ -715,6 +881,7 @@ int geer_set_timing(geer_ctx *c, int enable) {
 int geer_forward(geer_ctx *c, const geer_scene *scene, const geer_camera *camera, const geer_config *config,
                  float *color, float *remaining, int32_t *count, void *stream) {
     if (!c) return fail(GEER_ERR_INVALID, "null context");
+    ArenaScope arena_scope(&c->arena);
     int rc = check_scene_dev(scene);
     if (rc) return rc;
     if (!color || !remaining || !count) return fail(GEER_ERR_INVALID, "output buffers must be non-null");
@@ -742,6 +909,7 @@ int geer_forward(geer_ctx *c, const geer_scene *scene, const geer_camera *camera
 
 int geer_sync(geer_ctx *c, void *stream) {
     if (!c) return fail(GEER_ERR_INVALID, "null context");
+    ArenaScope arena_scope(&c->arena);
     cudaStream_t st = (cudaStream_t)stream;
     GEER_CUDA(cudaStreamSynchronize(st));
     int status[8];
@@ -774,6 +942,7 @@ int geer_sync(geer_ctx *c, void *stream) {
 
 int geer_backward(geer_ctx *c, const float *dl_dimage, const geer_grads *grads, int accumulate, void *stream) {
     if (!c) return fail(GEER_ERR_INVALID, "null context");
+    ArenaScope arena_scope(&c->arena);
     if (!grads || !dl_dimage) return fail(GEER_ERR_INVALID, "dl_dimage and grads are required");
     cudaStream_t st = (cudaStream_t)stream;
     if (c->scene.n == 0) return GEER_OK;  // renderer.py:248-249
@@ -844,6 +1013,7 @@ int geer_association_check(geer_ctx *c, int32_t rays_per_tile, int64_t *out, int
     GEER_CUDA(cudaDeviceSynchronize());
     int rc = resolve_entries(c);
     if (rc) return rc;
+    ArenaScope no_arena(nullptr);  // (transient buffers: cudaMalloc, freed below)
     Buf wo, bits, misc;  // transient (the bitmap is n_tiles * n / 8 bytes: 1 GB at 1M Gaussians, 1080p)
     struct Free {
         Buf *b[3];

@@ -71,6 +71,7 @@ class DeviceRenderer:
         self.ctx = _lib.Context(device)
         self._keep = None  # tensors the last forward's state points into
         self._stream = None
+        self._workspace = None
 
     def set_timing(self, on: bool):
         self.ctx.set_timing(on)
@@ -117,6 +118,35 @@ class DeviceRenderer:
 
     def clear_camera_cache(self):
         _lib.check(self.ctx._lib.geer_clear_camera_cache(self.ctx.ptr))
+
+    def workspace_bytes(self, scene: DeviceScene, camera, config, max_entries: int = 0) -> int:
+        """Device bytes the forward + backward of ``scene`` through ``camera`` need (geer_workspace_bytes)."""
+        cam = _lib.camera_struct(camera)
+        cfg = _lib.config_struct(config, 0)
+        nb = int(scene.sh.shape[1])
+        b = self.ctx._lib.geer_workspace_bytes(self.ctx.ptr, int(scene.means.shape[0]), nb, ctypes.byref(cam),
+                                               ctypes.byref(cfg), int(max_entries))
+        if b == 0:
+            raise ValueError(_lib.last_error())
+        return int(b)
+
+    def set_workspace(self, workspace: torch.Tensor | None):
+        """Carve every device buffer of this renderer from ``workspace`` (a CUDA tensor owned by the caller,
+        e.g. torch's caching allocator) instead of library cudaMalloc; ``None`` returns to library memory."""
+        if workspace is None:
+            _lib.check(self.ctx._lib.geer_set_workspace(self.ctx.ptr, None, 0))
+        else:
+            if not workspace.is_cuda or not workspace.is_contiguous():
+                raise ValueError("workspace must be a contiguous CUDA tensor")
+            _lib.check(self.ctx._lib.geer_set_workspace(self.ctx.ptr, workspace.data_ptr(),
+                                                        workspace.numel() * workspace.element_size()))
+        self._workspace = workspace  # (kept alive while attached)
+        self._keep = None
+
+    def workspace_used(self) -> int:
+        u = ctypes.c_size_t(0)
+        _lib.check(self.ctx._lib.geer_workspace_used(self.ctx.ptr, ctypes.byref(u)))
+        return int(u.value)
 
     def backward(self, dl_dimage: torch.Tensor, grads: DeviceScene | None = None, accumulate: bool = False,
                  opacity_logit: bool = False):

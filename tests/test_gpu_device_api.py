@@ -266,3 +266,39 @@ def test_async_frame_reports_non_pd_like_the_reference():
     r.forward(DeviceScene.from_scene(scene), cam, cfg, sync=False)
     with pytest.raises(ValueError, match="positive definite"):
         r.sync()
+
+
+def test_caller_owned_workspace_sized_by_geer_workspace_bytes():
+    """SURVEY 8b ownership: a torch tensor of geer_workspace_bytes holds every buffer of the device
+    path (no library cudaMalloc); forward and backward equal a library-owned context bit for bit, and
+    an undersized workspace fails with the size it needs."""
+    scene = synth.config_scene("C2", n=100_000)
+    cam = synth.config_camera("C2", width=480, height=270)
+    cfg = renderer.RenderConfig()
+    ds = DeviceScene.from_scene(scene)
+    dl = torch.full((cam.height, cam.width, 3), 1e-4, device="cuda")
+    ref = DeviceRenderer(0)
+    out_ref = [t.clone() for t in ref.forward(ds, cam, cfg)]
+    g_ref = ref.backward(dl)
+    n_entries = ref.stats()["n_entries"]
+    r = DeviceRenderer(0)
+    need = r.workspace_bytes(ds, cam, cfg, max_entries=n_entries)
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    r.set_workspace(ws)
+    for _ in range(3):  # first frame synchronous, then asynchronous frames sized by the capacity
+        out = r.forward(ds, cam, cfg)
+        g = r.backward(dl)
+    torch.cuda.synchronize()
+    for a, b in zip(out, out_ref):
+        assert torch.equal(a, b)
+    for name in ("means", "log_scales", "quats", "opacity_logits", "sh"):
+        torch.testing.assert_close(getattr(g, name), getattr(g_ref, name), rtol=1e-4,
+                                   atol=1e-5 * float(getattr(g_ref, name).abs().max()))
+    assert 0 < r.workspace_used() <= need
+    small = DeviceRenderer(0)
+    small.set_workspace(torch.empty(need // 4, dtype=torch.uint8, device="cuda"))
+    with pytest.raises(MemoryError, match="workspace too small"):
+        small.forward(ds, cam, cfg)
+    small.set_workspace(None)  # back to library memory: renders again
+    out2 = small.forward(ds, cam, cfg)
+    assert torch.equal(out2[0], out_ref[0])
