@@ -17,6 +17,10 @@ for name, n, w, h in (("C2", 3000, 160, 96), ("C5", 3000, 128, 80), ("C1", 2000,
     ds = DeviceScene.from_scene(scene)
     color, rem, cnt = r.forward(ds, cam, renderer.RenderConfig())
     g = r.backward(torch.ones_like(color) / color.numel())
+    # a second, asynchronous frame (capacity-sized graph buffers) and its backward
+    color, rem, cnt = r.forward(ds, cam, renderer.RenderConfig(), sync=False)
+    g = r.backward(torch.ones_like(color) / color.numel())
+    assert r.sync() is False
     torch.cuda.synchronize()
     res = r.ctx.association_check(64)
     print(name, float(color.sum()), int(cnt.sum()), res["missing"], flush=True)
