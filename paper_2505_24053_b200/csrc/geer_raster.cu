@@ -297,7 +297,7 @@ __device__ __noinline__ void make_record(const Payload &P, const ItemFrame &F, f
 
 constexpr int kConsumerWarps = kRasterThreads / 32;  // 8
 #ifndef GEER_STAGES
-#define GEER_STAGES 4
+#define GEER_STAGES 3
 #endif
 constexpr int kStages = GEER_STAGES;
 constexpr int kStageEntries = 32;  // one entry per producer lane
