@@ -20,8 +20,6 @@ constexpr float kMinRemainingF = 1.00000005e-04f;
 constexpr float kMaxBlendTF = 0.999f;
 
 constexpr int kRasterThreads = 256;  // pixels per raster work item (one CTA)
-constexpr int kFwdBatch = 128;       // entries staged per forward batch
-constexpr int kBwdBatch = 32;        // entries per backward reduction batch
 
 // Per-frame camera / config constants, passed by value to every kernel.
 struct FrameConst {

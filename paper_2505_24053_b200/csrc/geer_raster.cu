@@ -1,9 +1,10 @@
 // geer_raster.cu — K5 forward raster and K6 reverse-order backward raster.
 //
 // One CTA per raster work item (a tile, or a <=256-pixel chunk of an oversized non-BEAP tile): a
-// producer warp streams the tile's depth-sorted payload rows into a 4-stage shared-memory ring with
-// TMA gather4 copies completed on mbarriers, and 8 consumer warps (one pixel per lane, an 8x4 patch
-// per warp) cull each stage against their patch, then walk the kept entries front to back:
+// producer warp streams the tile's depth-sorted payload rows into a 3-stage shared-memory ring with
+// TMA gather4 copies completed on mbarriers and turns each into an offset record, and 8 consumer warps
+// (one pixel per lane, an 8x4 patch per warp) cull each stage against their patch, then walk the kept
+// entries front to back:
 //
 //   d_u = W d, m = o_u x d_u from the item's offset records (fp64 products rounded once; see
 //   make_record), kappa = |m|^2/|d_u|^2                       (core.py:184-199)
@@ -16,8 +17,8 @@
 // fp64, and pixels whose stop test is too close to call are recomposited in fp64 by
 // k_fixup, so cutoff decisions and contributor counts match the fp64 reference.  The backward
 // (renderer.py:259-310) streams each tile's alive prefix back to front, forms the 16
-// per-(pixel, Gaussian) partials, warp-reduces them with a shuffle transpose and issues one fp32
-// atomic per (entry, partial).
+// per-(pixel, Gaussian) partials, reduces them over the warp through a shared-memory transpose and
+// issues one fp32 atomic per (entry, partial).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -37,16 +38,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
-}
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
 // Pixel ray (world frame, fp64; camera.py:141-155 + renderer.py:77, or the K0 ray table).
@@ -815,10 +806,6 @@ template <class Smem>
 __device__ __forceinline__ void consume_stage_rec(Smem &S, int s, int warp, int cnt, int base, const PixXY &X,
                                                   const double *dray, const FrameConst &fc, PixelState &ps,
                                                   int &rechecks, int &went) {
-#ifdef GEER_EXP_NOCOMPUTE
-    went += cnt;
-    return;  // tuning experiment: the pipeline alone (results are wrong)
-#endif
     const uint32_t ib = smem_u32(&S.idx[s][warp][0]);
     const int jbase = base + 1;
     int k0 = 0;
