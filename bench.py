@@ -357,6 +357,71 @@ def run_ours(args):
                          if dominant == "render" else "algorithmic bytes per SURVEY 8d / DESIGN.md")}
     extra["stages"] = stages
     extra["latency_ms_per_frame"] = st["ms_total"]  # one frame alone on one stream (CUDA events)
+    # the same frame captured once into a CUDA graph and replayed (the device path is capturable:
+    # no host round trip, the same launches every frame), one frame at a time
+    try:
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            r.forward(dscene, cam, cfg, out=out, sync=False)
+        stream.wait_stream(cs)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            r.forward(dscene, cam, cfg, out=out, sync=False)
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        kg = max(10, args.steps)
+        g0.record(stream)
+        for _ in range(kg):
+            graph.replay()
+            g_ = torch.cuda.Event()  # one frame at a time: the next replay waits for this one
+            g_.record(stream)
+            g_.synchronize()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        r.sync()
+        extra["graph_latency_ms_per_frame"] = g0.elapsed_time(g1) / kg
+        del graph
+        # frames in flight as CUDA graphs: one captured frame per context, replayed round robin on
+        # the contexts' streams (every replay runs the whole frame: K1 -> sort -> binning -> raster)
+        graphs = []
+        for j in range(nf):
+            with torch.cuda.stream(streams[j]):
+                rs[j].forward(dscene, cam, cfg, out=outs[j], sync=False)
+        torch.cuda.synchronize()
+        for j in range(nf):
+            gj = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gj, stream=streams[j] if j else None):
+                rs[j].forward(dscene, cam, cfg, out=outs[j], sync=False)
+            graphs.append(gj)
+        for j in range(nf):
+            with torch.cuda.stream(streams[j]):
+                graphs[j].replay()
+        torch.cuda.synchronize()
+        h0 = torch.cuda.Event(enable_timing=True)
+        h1 = torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for s_ in streams[1:]:
+            s_.wait_event(h0)
+        for i in range(args.steps):
+            with torch.cuda.stream(streams[i % nf]):
+                graphs[i % nf].replay()
+        for s_ in streams[1:]:
+            e_ = torch.cuda.Event()
+            e_.record(s_)
+            stream.wait_event(e_)
+        h1.record(stream)
+        torch.cuda.synchronize()
+        for rr_ in rs:
+            rr_.sync()
+        extra["value_cuda_graphs"] = args.steps / (h0.elapsed_time(h1) / 1e3)
+        del graphs
+    except Exception as exc:  # noqa: BLE001
+        extra["graph_latency_ms_per_frame"] = {"error": repr(exc)}
     extra["frame"] = {"entries": int(st["n_entries"]), "tiles": int(st["n_tiles"]),
                       "work_items": int(st["n_work_items"]), "evaluated_pairs": int(pairs),
                       "pairs_per_pixel": pairs / n_px, "kappa_rechecks": int(st["kappa_rechecks"]),
