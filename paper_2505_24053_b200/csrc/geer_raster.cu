@@ -1337,6 +1337,16 @@ __device__ __forceinline__ float smem_transpose_reduce16(float (*red)[36], const
     return sum + __shfl_xor_sync(0xffffffffu, sum, 1);
 }
 
+// The second half of smem_transpose_reduce16, for partials already stored as column `lane`.
+__device__ __forceinline__ float smem_column_reduce16(float (*red)[36], int lane) {
+    __syncwarp();
+    const float4 *row = reinterpret_cast<const float4 *>(&red[lane >> 1][16 * (lane & 1)]);
+    const float4 a = row[0], b = row[1], c = row[2], d = row[3];
+    float sum = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w)) + (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w)));
+    __syncwarp();  // (the next entry overwrites the scratch)
+    return sum + __shfl_xor_sync(0xffffffffu, sum, 1);
+}
+
 // Reverse-order backward (renderer.py:259-310).  The producer streams the
 // tile's first max_n entries back to front; each lane walks its pixel's alive
 // entries (index < n_eval) from the last to the first, recovering
@@ -1433,14 +1443,21 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                 const int i = lo + jj;
                 // t = 0 (or not alive) on every lane: T, the suffix and all 16 partials are unchanged
                 if (!__any_sync(0xffffffffu, i < ne && e.t > 0.0f)) return;
+#ifndef GEER_BWD_SHFL_REDUCE
+                // the 16 partials go straight into this lane's column of the warp's transpose scratch
+                // (each value's register dies at its store)
+                float *colp = &S.red[warp][0][lane];
+                auto put = [&](int k, float val) { colp[k * 36] = val; };
+#else
                 float v[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) v[k] = 0.f;
-                if (i < ne) {
-                    const float omt = __fsub_rn(1.0f, e.t);
-                    const float inv = rcp_approx(omt);  // 1 - t >= 0.001: ~1 ulp
-                    T = T * inv;                        // T_i = T_{i+1} / (1 - t_i)
-                    const float w = T * e.t;
+                auto put = [&](int k, float val) { v[k] = val; };
+#endif
+                const bool alive = i < ne;
+                const float omt = __fsub_rn(1.0f, e.t);
+                const float inv = rcp_approx(omt);  // 1 - t >= 0.001: ~1 ulp
+                if (alive) T = T * inv;             // T_i = T_{i+1} / (1 - t_i)
+                const float w = alive ? T * e.t : 0.0f;
+                {
                     const float c0 = col.x, c1 = col.y, c2 = col.z;
                     // renderer.py:284-287
                     const float dcdt0 = T * c0 - (s0 + bgt0) * inv;
@@ -1450,30 +1467,30 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                     s0 += w * c0;
                     s1 += w * c1;
                     s2 += w * c2;
-                    v[13] = w * gl0;  // renderer.py:309 dcol
-                    v[14] = w * gl1;
-                    v[15] = w * gl2;
-                    if (e.t > 0.0f && e.u < kMaxBlendTF) {  // renderer.py:289-290 gate
-                        v[12] = dl_dt * e.alpha;
-                        const float dk = -0.5f * dl_dt * e.u;
-                        const float coef = 2.0f * dk * rcp_approx(e.dd);  // dl_dm = coef * m
-                        const float lm0 = coef * mv[0], lm1 = coef * mv[1], lm2 = coef * mv[2];
-                        v[9] = du[1] * lm2 - du[2] * lm1;  // dl_do = d_u x dl_dm
-                        v[10] = du[2] * lm0 - du[0] * lm2;
-                        v[11] = du[0] * lm1 - du[1] * lm0;
-                        const float sc_ = e.kap * coef;  // dl_dd = -(2 kappa dk / dd) d_u + dl_dm x o_u
-                        const float dd0 = -sc_ * du[0] + (lm1 * o[2] - lm2 * o[1]);
-                        const float dd1 = -sc_ * du[1] + (lm2 * o[0] - lm0 * o[2]);
-                        const float dd2 = -sc_ * du[2] + (lm0 * o[1] - lm1 * o[0]);
-                        v[0] = dd0 * dx; v[1] = dd0 * dy; v[2] = dd0 * dz;  // renderer.py:304 dW_rc
-                        v[3] = dd1 * dx; v[4] = dd1 * dy; v[5] = dd1 * dz;
-                        v[6] = dd2 * dx; v[7] = dd2 * dy; v[8] = dd2 * dz;
-                    }
+                    put(13, w * gl0);  // renderer.py:309 dcol
+                    put(14, w * gl1);
+                    put(15, w * gl2);
+                    // renderer.py:289-290 gate
+                    const bool gate = alive && e.t > 0.0f && e.u < kMaxBlendTF;
+                    put(12, gate ? dl_dt * e.alpha : 0.0f);
+                    const float dk = -0.5f * dl_dt * e.u;
+                    const float coef = gate ? 2.0f * dk * rcp_approx(e.dd) : 0.0f;  // dl_dm = coef * m
+                    const float lm0 = coef * mv[0], lm1 = coef * mv[1], lm2 = coef * mv[2];
+                    put(9, du[1] * lm2 - du[2] * lm1);  // dl_do = d_u x dl_dm
+                    put(10, du[2] * lm0 - du[0] * lm2);
+                    put(11, du[0] * lm1 - du[1] * lm0);
+                    const float sc_ = e.kap * coef;  // dl_dd = -(2 kappa dk / dd) d_u + dl_dm x o_u
+                    const float dd0 = -sc_ * du[0] + (lm1 * o[2] - lm2 * o[1]);
+                    const float dd1 = -sc_ * du[1] + (lm2 * o[0] - lm0 * o[2]);
+                    const float dd2 = -sc_ * du[2] + (lm0 * o[1] - lm1 * o[0]);
+                    put(0, dd0 * dx); put(1, dd0 * dy); put(2, dd0 * dz);  // renderer.py:304 dW_rc
+                    put(3, dd1 * dx); put(4, dd1 * dy); put(5, dd1 * dz);
+                    put(6, dd2 * dx); put(7, dd2 * dy); put(8, dd2 * dz);
                 }
 #ifdef GEER_BWD_SHFL_REDUCE
                 const float tot = warp_transpose_reduce16(v, lane);
 #else
-                const float tot = smem_transpose_reduce16(S.red[warp], v, lane);
+                const float tot = smem_column_reduce16(S.red[warp], lane);
 #endif
                 // lane 2k adds partial k (predicated fire-and-forget reduction, no branch)
                 float *dst = accum + (int64_t)S.gid[s][jj] * 16 + (lane >> 1);
