@@ -575,8 +575,8 @@ __device__ uint8_t associate_one(const FrameConst &fc, const geer_scene &sc, con
                 const bool okp = quadratic_roots(t22, t12, t11, rp0, rp1);
                 clamped = !okt || !okp;
             }
-            const double sigma = sigmoid((double)sc.opacity_logits[g]);
-            const bool keep = !(clamped && sigma < kMinClampedOpacity);  // association.py:343-350
+            // association.py:343-350 (sigma is only needed for a clamped particle)
+            const bool keep = !(clamped && sigmoid((double)sc.opacity_logits[g]) < kMinClampedOpacity);
             if (clamped) fl |= 2;
             if (keep) {
                 fl |= 1;
