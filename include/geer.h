@@ -238,6 +238,8 @@ int geer_ply_to_soa(const float *block, int64_t n, int n_props, const int32_t *c
                     void *stream);
 
 /* ---- diagnostics ------------------------------------------------------------- */
+/* The last forward's per-pixel alive counts n_eval (H,W) i32 to host memory (renderer.py:113). */
+int geer_debug_n_eval(geer_ctx *ctx, int32_t *host_n_eval);
 /* Measured FP32 FMA throughput of the device (scalar FFMA and packed FFMA2 chains), TFLOP/s: the
  * roofline denominator of the FP32-bound raster kernels (bench.py). */
 int geer_measure_fp32_peak(int device, double *tflops_scalar, double *tflops_packed);

@@ -34,7 +34,7 @@ EXPORTED = (
     "geer_render_host", "geer_render_backward_host", "geer_l1_grad", "geer_adam", "geer_measure_fp32_peak",
     "geer_loss_workspace_bytes", "geer_loss", "geer_resample_to_beap", "geer_ply_to_soa",
     "geer_association_check", "geer_sync", "geer_clear_camera_cache", "geer_workspace_bytes",
-    "geer_set_workspace", "geer_workspace_used",
+    "geer_set_workspace", "geer_workspace_used", "geer_debug_n_eval",
 )
 
 
@@ -136,6 +136,7 @@ def load():
             "geer_workspace_bytes": ([P, I64, ctypes.c_int32, P, P, I64], ctypes.c_size_t),
             "geer_set_workspace": ([P, P, ctypes.c_size_t], I),
             "geer_workspace_used": ([P, P], I),
+            "geer_debug_n_eval": ([P, P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

@@ -1043,6 +1043,15 @@ int geer_association_check(geer_ctx *c, int32_t rays_per_tile, int64_t *out, int
     return GEER_OK;
 }
 
+// Diagnostics: the last forward's per-pixel alive counts (n_eval, renderer.py:113) to the host.
+extern "C" int geer_debug_n_eval(geer_ctx *c, int32_t *host) {
+    if (!c || !host) return fail(GEER_ERR_INVALID, "null argument");
+    if (!c->have_stats) return fail(GEER_ERR_STATE, "no forward raster");
+    GEER_CUDA(cudaDeviceSynchronize());
+    GEER_CUDA(cudaMemcpy(host, c->n_eval.p, sizeof(int32_t) * (size_t)c->fc.width * c->fc.height, cudaMemcpyDeviceToHost));
+    return GEER_OK;
+}
+
 int geer_graph_info(geer_ctx *c, int64_t *n_entries, int32_t *n_x, int32_t *n_y) {
     if (!c) return fail(GEER_ERR_INVALID, "null context");
     int rc0 = resolve_entries(c);
