@@ -238,6 +238,10 @@ int geer_ply_to_soa(const float *block, int64_t n, int n_props, const int32_t *c
                     void *stream);
 
 /* ---- diagnostics ------------------------------------------------------------- */
+/* PCIe bytes the last host-buffer call (geer_render_host / _backward_host / geer_build_graph_host)
+ * sent host->device for its inputs: the float64 scene is narrowed to fp32 on host cores, except a raw
+ * float64 tail narrowed on the device (GEER_HOST_RAW_FRACTION, when the arrays are pinned). */
+int64_t geer_last_h2d_bytes(const geer_ctx *ctx);
 /* The last forward's per-pixel alive counts n_eval (H,W) i32 to host memory (renderer.py:113). */
 int geer_debug_n_eval(geer_ctx *ctx, int32_t *host_n_eval);
 /* Measured FP32 FMA throughput of the device (scalar FFMA and packed FFMA2 chains), TFLOP/s: the

@@ -35,6 +35,7 @@ EXPORTED = (
     "geer_loss_workspace_bytes", "geer_loss", "geer_resample_to_beap", "geer_ply_to_soa",
     "geer_association_check", "geer_sync", "geer_clear_camera_cache", "geer_workspace_bytes",
     "geer_set_workspace", "geer_workspace_used", "geer_debug_n_eval",
+    "geer_last_h2d_bytes",
 )
 
 
@@ -137,6 +138,7 @@ def load():
             "geer_set_workspace": ([P, P, ctypes.c_size_t], I),
             "geer_workspace_used": ([P, P], I),
             "geer_debug_n_eval": ([P, P], I),
+            "geer_last_h2d_bytes": ([P], ctypes.c_int64),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

@@ -37,6 +37,7 @@ UNITS = {
     "geer_camera.cu": ["-fmad=false"],
     "geer_check.cu": ["-fmad=false"],
     "geer_bin.cu": [],
+    "geer_host.cu": [],
 }
 
 

@@ -23,6 +23,7 @@
 #include <utility>
 
 #include "geer_common.cuh"
+#include "geer_host.h"
 #include "geer_kernels.h"
 
 using namespace geer;
@@ -159,7 +160,10 @@ struct geer_ctx {
     // temp
     Buf temp;
     // host-path staging
-    Buf h64_means, h64_log, h64_quats, h64_op, h64_sh, s32_means, s32_log, s32_quats, s32_op, s32_sh, out64, g64;
+    int64_t last_h2d = 0;     // PCIe bytes of the last host-buffer call's inputs
+    void *h_stage = nullptr;  // pinned write-combined host staging of the host-buffer entry points
+    size_t h_stage_cap = 0;
+    Buf h64_raw, s32_means, s32_log, s32_quats, s32_op, s32_sh, out64, g64;
     Arena arena;  // caller-owned workspace (geer_set_workspace), if attached
 };
 
@@ -397,7 +401,7 @@ void free_all_buffers(geer_ctx *c) {
                    &c->ranges_ax, &c->flags, &c->mu_c, &c->depth,
                    &c->order, &c->tile_ranges, &c->wcull,
                    &c->bin_m1, &c->bin_p1, &c->bin_rows, &c->bin_rowstart, &c->bin_segoff, &c->bin_m2, &c->bin_p2, &c->color, &c->remaining, &c->count_px, &c->n_eval, &c->dl32, &c->fixup,
-                   &c->accum, &c->temp, &c->h64_means, &c->h64_log, &c->h64_quats, &c->h64_op, &c->h64_sh,
+                   &c->accum, &c->temp, &c->h64_raw,
                    &c->s32_means, &c->s32_log, &c->s32_quats, &c->s32_op, &c->s32_sh, &c->out64, &c->g64};
     for (Buf *b : bufs) free_buf(*b);
     clear_camera_cache(c);
@@ -739,28 +743,37 @@ int upload_host_scene(geer_ctx *c, const geer_host_scene *hs, cudaStream_t st) {
     if (!hs) return fail(GEER_ERR_INVALID, "scene is required");
     const int64_t n = hs->n;
     if (n < 0 || n >= ((int64_t)1 << 31)) return fail(GEER_ERR_INVALID, "bad Gaussian count");
+    c->last_h2d = 0;
     const int64_t nsh = n * hs->n_bands * 3;
-    double *dm = ENSURE(double, c->h64_means, n * 3);
-    double *dl = ENSURE(double, c->h64_log, n * 3);
-    double *dq = ENSURE(double, c->h64_quats, n * 4);
-    double *dop = ENSURE(double, c->h64_op, n);
-    double *dsh = ENSURE(double, c->h64_sh, nsh);
     float *m = ENSURE(float, c->s32_means, n * 3);
     float *l = ENSURE(float, c->s32_log, n * 3);
     float *q = ENSURE(float, c->s32_quats, n * 4);
     float *op = ENSURE(float, c->s32_op, n);
     float *sh = ENSURE(float, c->s32_sh, nsh);
     if (n > 0) {
-        GEER_CUDA(cudaMemcpyAsync(dm, hs->means, sizeof(double) * n * 3, cudaMemcpyHostToDevice, st));
-        GEER_CUDA(cudaMemcpyAsync(dl, hs->log_scales, sizeof(double) * n * 3, cudaMemcpyHostToDevice, st));
-        GEER_CUDA(cudaMemcpyAsync(dq, hs->quats, sizeof(double) * n * 4, cudaMemcpyHostToDevice, st));
-        GEER_CUDA(cudaMemcpyAsync(dop, hs->opacity_logits, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-        GEER_CUDA(cudaMemcpyAsync(dsh, hs->sh, sizeof(double) * nsh, cudaMemcpyHostToDevice, st));
-        launch_convert_f64_f32(dm, m, n * 3, st);
-        launch_convert_f64_f32(dl, l, n * 3, st);
-        launch_convert_f64_f32(dq, q, n * 4, st);
-        launch_convert_f64_f32(dop, op, n, st);
-        launch_convert_f64_f32(dsh, sh, nsh, st);
+        // fp64 -> fp32 on the host cores, overlapped with the DMA of the finished chunks (geer_host.cu)
+        const HostSeg segs[5] = {{hs->means, n * 3, m},
+                                 {hs->log_scales, n * 3, l},
+                                 {hs->quats, n * 4, q},
+                                 {hs->opacity_logits, n, op},
+                                 {hs->sh, nsh, sh}};
+        const size_t need = sizeof(float) * (size_t)(n * 11 + nsh);
+        if (c->h_stage_cap < need) {
+            GEER_CUDA(cudaStreamSynchronize(st));
+            if (c->h_stage) cudaFreeHost(c->h_stage);
+            c->h_stage = nullptr;
+            c->h_stage_cap = 0;
+            if (cudaHostAlloc(&c->h_stage, need, cudaHostAllocWriteCombined) != cudaSuccess) {
+                c->h_stage = nullptr;
+                cudaGetLastError();
+                return fail(GEER_ERR_NOMEM, "pinned staging allocation of %zu bytes failed", need);
+            }
+            c->h_stage_cap = need;
+        }
+        const int64_t raw = raw_upload_elems(n * 11 + nsh);
+        double *raw_dev = nullptr;
+        if (raw > 0) raw_dev = ENSURE(double, c->h64_raw, raw);
+        GEER_CUDA(upload_narrowed(segs, 5, (float *)c->h_stage, raw_dev, raw, st, &c->last_h2d));
     }
     geer_scene s;
     s.n = n;
@@ -821,6 +834,7 @@ void geer_destroy(geer_ctx *c) {
     if (c->d_counters) cudaFree(c->d_counters);
     if (c->d_err) cudaFree(c->d_err);
     if (c->h_hdr) cudaFreeHost(c->h_hdr);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -1043,6 +1057,8 @@ int geer_association_check(geer_ctx *c, int32_t rays_per_tile, int64_t *out, int
     return GEER_OK;
 }
 
+int64_t geer_last_h2d_bytes(const geer_ctx *c) { return c ? c->last_h2d : 0; }
+
 // Diagnostics: the last forward's per-pixel alive counts (n_eval, renderer.py:113) to the host.
 extern "C" int geer_debug_n_eval(geer_ctx *c, int32_t *host) {
     if (!c || !host) return fail(GEER_ERR_INVALID, "null argument");
@@ -1223,6 +1239,7 @@ int geer_render_backward_host(geer_ctx *c, const geer_host_scene *scene, const g
     float *dl32 = ensure<float>(c->dl32, (size_t)npx * 3, &rc);
     if (rc) return rc;
     GEER_CUDA(cudaMemcpyAsync(dl64, dl_dimage, sizeof(double) * npx * 3, cudaMemcpyHostToDevice, st));
+    c->last_h2d += (int64_t)sizeof(double) * npx * 3;
     launch_convert_f64_f32(dl64, dl32, npx * 3, st);
     int64_t tot = 0;
     for (int i = 0; i < 5; ++i) tot += sizes[i];

@@ -114,6 +114,13 @@ def _ctx(device: int = 0) -> _lib.Context:
     return _lib.default_context(device)
 
 
+def last_h2d_bytes(device: int = 0) -> int:
+    """PCIe bytes the calling thread's last ``render``/``render_backward`` sent host->device for its
+    inputs (the float64 scene goes mostly as fp32 narrowed on the host cores; geer_last_h2d_bytes)."""
+    ctx = _ctx(device)
+    return int(ctx._lib.geer_last_h2d_bytes(ctx.ptr))
+
+
 def _host_empty(shape, dtype) -> np.ndarray:
     """A fresh numpy array in page-locked memory (torch's caching host allocator).
 

@@ -338,3 +338,43 @@ def test_async_frame_is_cuda_graph_capturable():
     eager = DeviceRenderer(0).forward(ds, cam, cfg)
     for a, b in zip(bufs, eager):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_narrowing_equals_device_narrowing(pinned):
+    """geer_render_host narrows the float64 scene on host cores (raw fp64 tail narrowed on the device
+    when the arrays are pinned); the device sees the same fp32 values as torch's narrowing, so the
+    frame equals the device-path frame bitwise.  Values are perturbed off the fp32 grid so rounding
+    matters, and the scene is large enough for many host chunks."""
+    from paper_2505_24053_b200.scene import GaussianScene
+
+    base = synth.config_scene("C2", n=200_000)
+    rng = np.random.default_rng(5)
+
+    def off_grid(a):
+        a = np.asarray(a, dtype=np.float64)
+        a = a * (1.0 + rng.uniform(-1e-9, 1e-9, a.shape))
+        if not pinned:
+            return np.ascontiguousarray(a)
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    scene = GaussianScene(off_grid(base.means), off_grid(base.log_scales), off_grid(base.quats),
+                          off_grid(base.opacity_logits), off_grid(base.sh))
+    assert not np.array_equal(scene.sh.astype(np.float32).astype(np.float64), scene.sh)
+    cam = synth.config_camera("C2", width=480, height=270)
+    cfg = renderer.RenderConfig()
+    host = renderer.render(scene, cam, cfg, return_graph=False)
+    total = sum(a.size for a in (scene.means, scene.log_scales, scene.quats, scene.opacity_logits, scene.sh))
+    sent = renderer.last_h2d_bytes(0)
+    if pinned:
+        assert 4 * total < sent < 8 * total
+    else:
+        assert sent == 4 * total
+    r = DeviceRenderer(0)
+    color, rem, cnt = r.forward(DeviceScene.from_scene(scene), cam, cfg)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(color.cpu().numpy().astype(np.float64), host.color.color)
+    np.testing.assert_array_equal(rem.cpu().numpy().astype(np.float64), host.remaining_transmittance)
+    np.testing.assert_array_equal(cnt.cpu().numpy().astype(np.int64), host.contributor_count)
