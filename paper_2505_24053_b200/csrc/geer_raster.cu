@@ -185,11 +185,14 @@ __device__ __forceinline__ float2 pixel_xy(const ItemFrame &F, const double d[3]
     return make_float2((float)__ddiv_rn(nx, den), (float)__ddiv_rn(ny, den));
 }
 
+// A pixel's offsets: x, y (each duplicated into a pair for the packed fp32 FMAs) and the products.
 struct PixXY {
-    float x, y, xx, xy, yy;
+    float2 x2, y2;
+    float xx, xy, yy;
 };
 __device__ __forceinline__ PixXY make_pxy(float2 v) {
-    return PixXY{v.x, v.y, __fmul_rn(v.x, v.x), __fmul_rn(v.x, v.y), __fmul_rn(v.y, v.y)};
+    return PixXY{make_float2(v.x, v.x), make_float2(v.y, v.y), __fmul_rn(v.x, v.x), __fmul_rn(v.x, v.y),
+                 __fmul_rn(v.y, v.y)};
 }
 
 __device__ __forceinline__ float sqrt_approx(float x) {
@@ -253,26 +256,30 @@ __device__ __noinline__ void make_record(const Payload &P, const ItemFrame &F, f
                       (float)kHalfLog2e * P.ext.x + 1e-30f;
     float4 *r4 = reinterpret_cast<float4 *>(rec);
     const float sig = P.col.w;
+    // layout (rec_k): the coefficients that rec_k's packed FMAs combine sit side by side
+    //   r4[0] = (ma0, ma1, mb0, mb1)   r4[1] = (mc0, mc1, ma2, D0)   r4[2] = (mb2, D1, mc2, D2)
+    //   r4[3] = (D3, D4, D5, trel)     r4[4] = (sigma, tol, 0, 0)    r4[5] = colour
+    //   backward: r4[6] = (a0, a1, b0, b1)   r4[7] = (c0, c1, a2, b2)   r4[8] = (c2, o_u)
     if (!(tol < 0.25f * thrk) || !(sd < 1e36f) || !(dm < 1e-3f * 1e18f)) {
         // fp32 cannot carry this Gaussian here (huge or degenerate W / o_u): every pair goes to the fp64
         // re-check (k = 0 lies within an infinite tol of the cutoff)
-        r4[0] = make_float4(1.f, 0.f, 0.f, 0.f);
-        r4[1] = make_float4(0.f, 0.f, sig, INFINITY);
-        r4[2] = make_float4(0.f, 0.f, 0.f, 1e-5f);
-        r4[3] = make_float4(0.f, 0.f, 0.f, 0.f);
-        r4[4] = make_float4(0.f, 0.f, 0.f, 0.f);
+        r4[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        r4[1] = make_float4(0.f, 0.f, 0.f, 1.f);
+        r4[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+        r4[3] = make_float4(0.f, 0.f, 0.f, 1e-5f);
+        r4[4] = make_float4(sig, INFINITY, 0.f, 0.f);
     } else {
-        r4[0] = make_float4(D0, D1, D2, D3);
-        r4[1] = make_float4(D4, D5, sig, tol);
-        r4[2] = make_float4(ma[0], mb[0], mc[0], 0.6931472f * tol + 1e-6f);
-        r4[3] = make_float4(ma[1], mb[1], mc[1], 0.f);
-        r4[4] = make_float4(ma[2], mb[2], mc[2], 0.f);
+        r4[0] = make_float4(ma[0], ma[1], mb[0], mb[1]);
+        r4[1] = make_float4(mc[0], mc[1], ma[2], D0);
+        r4[2] = make_float4(mb[2], D1, mc[2], D2);
+        r4[3] = make_float4(D3, D4, D5, 0.6931472f * tol + 1e-6f);
+        r4[4] = make_float4(sig, tol, 0.f, 0.f);
     }
     r4[5] = make_float4(P.col.x, P.col.y, P.col.z, 0.f);
     if (grad) {
-        r4[6] = make_float4(af[0], bf[0], cf[0], (float)P.q[9]);
-        r4[7] = make_float4(af[1], bf[1], cf[1], (float)P.q[10]);
-        r4[8] = make_float4(af[2], bf[2], cf[2], (float)P.q[11]);
+        r4[6] = make_float4(af[0], af[1], bf[0], bf[1]);
+        r4[7] = make_float4(cf[0], cf[1], af[2], bf[2]);
+        r4[8] = make_float4(cf[2], (float)P.q[9], (float)P.q[10], (float)P.q[11]);
     }
 }
 
@@ -655,15 +662,21 @@ __device__ __forceinline__ void pipe_drop_out(Smem &S, int s, unsigned phase) {
 // Also returns the record's (D4, D5, sigma, tol) and trel.
 __device__ __forceinline__ void rec_k(uint32_t ra, const PixXY &X, float &k, float &dd, float (&m)[3], float4 &c1,
                                       float &trel) {
-    const float4 c0 = lds_f4(ra), c2 = lds_f4(ra + 32), c3 = lds_f4(ra + 48), c4 = lds_f4(ra + 64);
-    c1 = lds_f4(ra + 16);
-    dd = __fmaf_rn(c1.y, X.yy, __fmaf_rn(c1.x, X.xy, __fmaf_rn(c0.w, X.xx, __fmaf_rn(c0.z, X.y, __fmaf_rn(c0.y, X.x, c0.x)))));
-    m[0] = __fmaf_rn(c2.z, X.y, __fmaf_rn(c2.y, X.x, c2.x));
-    m[1] = __fmaf_rn(c3.z, X.y, __fmaf_rn(c3.y, X.x, c3.x));
-    m[2] = __fmaf_rn(c4.z, X.y, __fmaf_rn(c4.y, X.x, c4.x));
+    const float4 A = lds_f4(ra), B = lds_f4(ra + 16), C = lds_f4(ra + 32), D = lds_f4(ra + 48), E = lds_f4(ra + 64);
+    // (m0, m1) and (m2, the linear part of dd) as packed FMA pairs: per element the same FMA chain
+    // (base + x b + y c) as scalar code, so the values do not depend on the packing
+    const float2 m01 = __ffma2_rn(make_float2(B.x, B.y), X.y2,
+                                  __ffma2_rn(make_float2(A.z, A.w), X.x2, make_float2(A.x, A.y)));
+    const float2 m2d = __ffma2_rn(make_float2(C.z, C.w), X.y2,
+                                  __ffma2_rn(make_float2(C.x, C.y), X.x2, make_float2(B.z, B.w)));
+    dd = __fmaf_rn(D.z, X.yy, __fmaf_rn(D.y, X.xy, __fmaf_rn(D.x, X.xx, m2d.y)));
+    m[0] = m01.x;
+    m[1] = m01.y;
+    m[2] = m2d.x;
     const float mm = __fmaf_rn(m[2], m[2], __fmaf_rn(m[1], m[1], __fmul_rn(m[0], m[0])));
     k = __fmul_rn(mm, rcp_approx(dd));
-    trel = c2.w;
+    c1 = make_float4(0.f, 0.f, E.x, E.y);  // (.z sigma, .w tol)
+    trel = D.w;
 }
 
 // fp64 re-decision of a pair whose k lies within tol of the cutoff: kappa from the payload's W and o_u
@@ -782,7 +795,7 @@ __device__ __forceinline__ void rec_group(Smem &S, int s, const int (&jj)[GG], i
             if (!near[u]) continue;
             float kr;
             const bool in64 = recheck(ring_at(S, s, jj[u]), dray, fc, unc[u], kr);
-            const float uu = __fmul_rn(lds_f32(rb + (uint32_t)jj[u] * (kRecF * 4) + 24), ex2_approx(-kr));  // sigma
+            const float uu = __fmul_rn(lds_f32(rb + (uint32_t)jj[u] * (kRecF * 4) + 64), ex2_approx(-kr));  // sigma
             t[u] = in64 ? fminf(uu, kMaxBlendTF) : 0.0f;
             any_unc |= unc[u];
             ++rechecks;
@@ -1066,7 +1079,7 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
     const bool valid = q < it.z;
     const int p = valid ? pix_list[it.y + q] : 0;
     double d64[3] = {0.0, 0.0, 1.0};
-    PixXY X{0.f, 0.f, 0.f, 0.f, 0.f};
+    PixXY X = make_pxy(make_float2(0.f, 0.f));
     if (valid) {
         pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
         if (framed) X = make_pxy(pixel_xy(*F, d64));
@@ -1393,7 +1406,7 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
     }
     // the producer streams while the consumers set up their pixels
     double d64[3] = {0.0, 0.0, 1.0};
-    PixXY X{0.f, 0.f, 0.f, 0.f, 0.f};
+    PixXY X = make_pxy(make_float2(0.f, 0.f));
     float dx, dy, dz;  // the ray the gradient is formed with: d' = dc + x e1 + y e2 (framed) or d
     if (valid) pixel_ray<kBEAP>(fc, p, col_sc, row_sc, dir64, d64);
     if (framed) {
@@ -1539,10 +1552,10 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                     e.kap = k * (float)(1.0 / kHalfLog2e);
                     // gradient vectors for d' (kappa is scale-invariant in the ray: dW = dl/dd_u (x) d')
                     const float4 g0 = lds_f4(ra + 96), g1 = lds_f4(ra + 112), g2 = lds_f4(ra + 128);
-                    const float du[3] = {__fmaf_rn(g0.z, X.y, __fmaf_rn(g0.y, X.x, g0.x)),
-                                         __fmaf_rn(g1.z, X.y, __fmaf_rn(g1.y, X.x, g1.x)),
-                                         __fmaf_rn(g2.z, X.y, __fmaf_rn(g2.y, X.x, g2.x))};
-                    const float o[3] = {g0.w, g1.w, g2.w};
+                    const float2 du01 = __ffma2_rn(make_float2(g1.x, g1.y), X.y2,
+                                                   __ffma2_rn(make_float2(g0.z, g0.w), X.x2, make_float2(g0.x, g0.y)));
+                    const float du[3] = {du01.x, du01.y, __fmaf_rn(g2.x, X.y2.x, __fmaf_rn(g1.w, X.x2.x, g1.z))};
+                    const float o[3] = {g2.y, g2.z, g2.w};
                     float mv[3];
                     if (c1.w < INFINITY) {  // the record's m and dd (entry-uniform branch)
                         constexpr float kInvS = (float)(1.0 / kSqrtHalfLog2e);
