@@ -699,7 +699,8 @@ __device__ __forceinline__ bool recheck(const Payload &P, const double *dray, co
 // renderer.py:113 is decided against rem64 in [rem - err, rem + err]; a pixel whose test (or a
 // cutoff decision) is too close to call is stopped and redone in fp64 by k_fixup.
 struct PixelState {
-    float cr, cg, cb;
+    float2 crg;  // (red, green): one packed FMA per update
+    float cb;
     float r;     // remaining transmittance while the pixel is live, 0 once it stopped
     float rfin;  // remaining transmittance at the stop
     float err;   // bound on |r_fp32 - r_fp64|
@@ -723,8 +724,7 @@ __device__ __forceinline__ void pixel_update(PixelState &ps, float trel, float t
     }
     const float w = __fmul_rn(ps.r, t);
     const float omt = __fsub_rn(1.0f, t);
-    ps.cr = __fmaf_rn(w, col.x, ps.cr);
-    ps.cg = __fmaf_rn(w, col.y, ps.cg);
+    ps.crg = __ffma2_rn(make_float2(col.x, col.y), make_float2(w, w), ps.crg);
     ps.cb = __fmaf_rn(w, col.z, ps.cb);
     // |d r'| <= |d r| (1 - t) + r |d t| + rounding (none when t = 0: skipping such an entry - PBF
     // culling, a shorter list - stays an exact no-op),  |d t| <= t * trel
@@ -1093,7 +1093,7 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
     sray[q][1] = d64[1];
     sray[q][2] = d64[2];
     const double *dray = sray[q];
-    PixelState ps{0.f, 0.f, 0.f, valid ? 1.0f : 0.0f, 1.0f, 0.f, -1.0f, 0, 0, 0};
+    PixelState ps{make_float2(0.f, 0.f), 0.f, valid ? 1.0f : 0.0f, 1.0f, 0.f, -1.0f, 0, 0, 0};
     int rechecks = 0, went = 0;
     bool warp_live = __any_sync(0xffffffffu, valid);
     if (!warp_live && lane == 0) atomicAdd(&S.done_warps, 1);
@@ -1132,8 +1132,8 @@ __global__ void __launch_bounds__(kFwdThreads, FWD_MIN_BLOCKS2)
     if (valid) {
         const float rem = ps.r > 0.0f ? ps.r : ps.rfin;  // live to the end of the list, or stopped
         // renderer.py:118 background with the final remaining transmittance
-        color[(int64_t)p * 3 + 0] = __fmaf_rn(rem, fc.bg[0], ps.cr);
-        color[(int64_t)p * 3 + 1] = __fmaf_rn(rem, fc.bg[1], ps.cg);
+        color[(int64_t)p * 3 + 0] = __fmaf_rn(rem, fc.bg[0], ps.crg.x);
+        color[(int64_t)p * 3 + 1] = __fmaf_rn(rem, fc.bg[1], ps.crg.y);
         color[(int64_t)p * 3 + 2] = __fmaf_rn(rem, fc.bg[2], ps.cb);
         remaining[p] = rem;
         count[p] = ps.cnt;
@@ -1432,8 +1432,12 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
         gl1 = dl_dimage[(int64_t)p * 3 + 1];
         gl2 = dl_dimage[(int64_t)p * 3 + 2];
     }
-    const float bgt0 = t_fin * fc.bg[0], bgt1 = t_fin * fc.bg[1], bgt2 = t_fin * fc.bg[2];
-    float T = t_fin, s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    // (x, y) components kept as pairs for the packed fp32 instructions
+    const float2 gl01 = make_float2(gl0, gl1), dxy = make_float2(dx, dy);
+    const float2 bgt01 = make_float2(t_fin * fc.bg[0], t_fin * fc.bg[1]);
+    const float bgt2 = t_fin * fc.bg[2];
+    float T = t_fin, s2 = 0.f;
+    float2 s01 = make_float2(0.f, 0.f);
     int dummy = 0;
     unsigned phase = 0;
     int s = 0;
@@ -1471,24 +1475,26 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                 if (alive) T = T * inv;             // T_i = T_{i+1} / (1 - t_i)
                 const float w = alive ? T * e.t : 0.0f;
                 {
-                    const float c0 = col.x, c1 = col.y, c2 = col.z;
+                    const float2 c01 = make_float2(col.x, col.y);
+                    const float c2 = col.z;
                     // renderer.py:284-287
-                    const float dcdt0 = T * c0 - (s0 + bgt0) * inv;
-                    const float dcdt1 = T * c1 - (s1 + bgt1) * inv;
+                    const float2 dcdt01 = __ffma2_rn(c01, make_float2(T, T),
+                                                     __fmul2_rn(__fadd2_rn(s01, bgt01), make_float2(-inv, -inv)));
                     const float dcdt2 = T * c2 - (s2 + bgt2) * inv;
-                    const float dl_dt = dcdt0 * gl0 + dcdt1 * gl1 + dcdt2 * gl2;
-                    s0 += w * c0;
-                    s1 += w * c1;
+                    const float dl_dt = dcdt01.x * gl0 + dcdt01.y * gl1 + dcdt2 * gl2;
+                    s01 = __ffma2_rn(c01, make_float2(w, w), s01);
                     s2 += w * c2;
-                    put(13, w * gl0);  // renderer.py:309 dcol
-                    put(14, w * gl1);
+                    const float2 dc01 = __fmul2_rn(gl01, make_float2(w, w));  // renderer.py:309 dcol
+                    put(13, dc01.x);
+                    put(14, dc01.y);
                     put(15, w * gl2);
                     // renderer.py:289-290 gate
                     const bool gate = alive && e.t > 0.0f && e.u < kMaxBlendTF;
                     put(12, gate ? dl_dt * e.alpha : 0.0f);
                     const float dk = -0.5f * dl_dt * e.u;
                     const float coef = gate ? 2.0f * dk * rcp_approx(e.dd) : 0.0f;  // dl_dm = coef * m
-                    const float lm0 = coef * mv[0], lm1 = coef * mv[1], lm2 = coef * mv[2];
+                    const float2 lm01 = __fmul2_rn(make_float2(mv[0], mv[1]), make_float2(coef, coef));
+                    const float lm0 = lm01.x, lm1 = lm01.y, lm2 = coef * mv[2];
                     put(9, du[1] * lm2 - du[2] * lm1);  // dl_do = d_u x dl_dm
                     put(10, du[2] * lm0 - du[0] * lm2);
                     put(11, du[0] * lm1 - du[1] * lm0);
@@ -1496,9 +1502,12 @@ __global__ void __launch_bounds__(kPipeThreads, BWD_MIN_BLOCKS)
                     const float dd0 = -sc_ * du[0] + (lm1 * o[2] - lm2 * o[1]);
                     const float dd1 = -sc_ * du[1] + (lm2 * o[0] - lm0 * o[2]);
                     const float dd2 = -sc_ * du[2] + (lm0 * o[1] - lm1 * o[0]);
-                    put(0, dd0 * dx); put(1, dd0 * dy); put(2, dd0 * dz);  // renderer.py:304 dW_rc
-                    put(3, dd1 * dx); put(4, dd1 * dy); put(5, dd1 * dz);
-                    put(6, dd2 * dx); put(7, dd2 * dy); put(8, dd2 * dz);
+                    // renderer.py:304 dW_rc
+                    const float2 w0 = __fmul2_rn(dxy, make_float2(dd0, dd0)), w1 = __fmul2_rn(dxy, make_float2(dd1, dd1)),
+                                 w2 = __fmul2_rn(dxy, make_float2(dd2, dd2));
+                    put(0, w0.x); put(1, w0.y); put(2, dd0 * dz);
+                    put(3, w1.x); put(4, w1.y); put(5, dd1 * dz);
+                    put(6, w2.x); put(7, w2.y); put(8, dd2 * dz);
                 }
 #ifdef GEER_BWD_SHFL_REDUCE
                 const float tot = warp_transpose_reduce16(v, lane);
