@@ -730,63 +730,52 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS)
     constexpr int kStageFloats = kStageRow * 4;  // payload-head staging
     __shared__ __align__(16) float ssh[128 * (NB * 3 > kStageFloats ? NB * 3 : kStageFloats)];
     __shared__ Cull scull[128];
-    __shared__ uint8_t sfl[2][128];
-    __shared__ int64_t scount[128];  // entries per Gaussian (for the block's totals)
     const int64_t g0 = (int64_t)blockIdx.x * 128;
     const int cnt_b = (int)lmin(128, sc.n - g0);
     const int lt = threadIdx.x & 127;
+    // The two halves never meet at a block barrier (their run times differ per Gaussian, and the
+    // faster half would idle): each writes its own flag byte and its own part of the payload rows.
     if (threadIdx.x < 128) {
         double *sex = reinterpret_cast<double *>(smem_raw);
         double *sey = sex + (fc.n_x + 1);
         for (int i = lt; i <= fc.n_x; i += 128) sex[i] = medges_x[i];
         for (int i = lt; i <= fc.n_y; i += 128) sey[i] = medges_y[i];
         named_barrier(1, 128);
-#ifdef GEER_EXP_NO_ASSOC
-        scount[lt] = 0;
-        sfl[0][lt] = 0;
-        if (false)
-#endif
         int64_t ne = 0;
-        sfl[0][lt] = lt < cnt_b ? associate_one(fc, sc, sex, sey, g0 + lt, depth_key, ne, ranges, scull[lt],
-                                                mu_out, depth_out, err)
-                                : 0;
-        scount[lt] = ne;
-    } else {
-#ifndef GEER_EXP_NO_PAYLOAD
-        sfl[1][lt] = payload_block<NB>(fc, sc, ssh, scull, g0, cnt_b, lt);
-#else
-        sfl[1][lt] = 0;
-#endif
-    }
-    __syncthreads();
-    if (threadIdx.x < cnt_b) {
-        flags[g0 + threadIdx.x] = sfl[0][threadIdx.x];
-        flags[sc.n + g0 + threadIdx.x] = sfl[1][threadIdx.x];
-    }
-    if (threadIdx.x < 32) {  // the block's entries and (Gaussian, tile row) pairs, for the frame totals
-        unsigned long long t = 0, rows = 0;
-        for (int i = threadIdx.x; i < cnt_b; i += 32) {
-            const int64_t c = scount[i];
-            t += (unsigned long long)c;
-            if (c > 0) {
-                const AxisRanges &a = ranges[g0 + i];
+        unsigned long long rows = 0;
+        if (lt < cnt_b) {
+            const int64_t g = g0 + lt;
+            Cull cl;
+            cl.box = make_float4(0.f, 0.f, 0.f, 0.f);
+            flags[g] = associate_one(fc, sc, sex, sey, g, depth_key, ne, ranges, cl, mu_out, depth_out, err);
+            payload[g].cull.box = cl.box;  // (the visual-cone part is the payload half's)
+            if (ne > 0) {
+                const AxisRanges &a = ranges[g];
                 for (int k = 0; k < 3; ++k) rows += (a.y[k] >> 16) - (a.y[k] & 0xFFFFu);
             }
         }
+        // the warp's entries and (Gaussian, tile row) pairs, for the frame totals
+        unsigned long long t = (unsigned long long)ne;
         for (int o = 16; o > 0; o >>= 1) {
             t += __shfl_xor_sync(0xffffffffu, t, o);
             rows += __shfl_xor_sync(0xffffffffu, rows, o);
         }
-        if (threadIdx.x == 0 && t) atomicAdd(total_entries, t);
-        if (threadIdx.x == 0 && rows) atomicAdd(total_entries + 1, rows);  // (the next counter)
-    }
-    // coalesced write-out of the block's payload rows (head + culling record)
-    const float4 *sp = reinterpret_cast<const float4 *>(ssh);
-    const float4 *scv = reinterpret_cast<const float4 *>(scull);
-    float4 *dp = reinterpret_cast<float4 *>(payload + g0);
-    for (int i = threadIdx.x; i < cnt_b * kPayRow; i += blockDim.x) {
-        const int r = i / kPayRow, k = i - r * kPayRow;
-        dp[i] = k < kPayHead ? sp[r * kStageRow + k] : scv[r * (sizeof(Cull) / 16) + (k - kPayHead)];
+        if ((lt & 31) == 0 && t) atomicAdd(total_entries, t);
+        if ((lt & 31) == 0 && rows) atomicAdd(total_entries + 1, rows);  // (the next counter)
+    } else {
+        const uint8_t bits = payload_block<NB>(fc, sc, ssh, scull, g0, cnt_b, lt);
+        if (lt < cnt_b) flags[sc.n + g0 + lt] = bits;
+        named_barrier(2, 128);  // the half's staged rows are complete
+        // coalesced write-out of the block's payload heads and visual-cone records
+        const float4 *sp = reinterpret_cast<const float4 *>(ssh);
+        const float4 *scv = reinterpret_cast<const float4 *>(scull);
+        float4 *dp = reinterpret_cast<float4 *>(payload + g0);
+        constexpr int kBox = kPayHead + (int)(offsetof(Cull, box) / 16);
+        for (int i = lt; i < cnt_b * kPayRow; i += 128) {
+            const int r = i / kPayRow, k = i - r * kPayRow;
+            if (k == kBox) continue;  // the association half's
+            dp[i] = k < kPayHead ? sp[r * kStageRow + k] : scv[r * (sizeof(Cull) / 16) + (k - kPayHead)];
+        }
     }
 }
 
