@@ -764,7 +764,7 @@ def _lib_host_threads():
 
 
 def _raw_fraction():
-    return float(os.environ.get("GEER_HOST_RAW_FRACTION", "0.2"))
+    return float(os.environ.get("GEER_HOST_RAW_FRACTION", "0.1"))
 
 
 def main():

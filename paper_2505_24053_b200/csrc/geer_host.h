@@ -21,7 +21,7 @@ struct HostSeg {
 cudaError_t upload_narrowed(const HostSeg *segs, int nseg, float *staging, double *raw_dev, int64_t raw_elems,
                             cudaStream_t st, int64_t *pcie_bytes);
 
-// Elements of a scene upload sent raw (float64): GEER_HOST_RAW_FRACTION of them (default 0.2,
+// Elements of a scene upload sent raw (float64): GEER_HOST_RAW_FRACTION of them (default 0.1,
 // the measured optimum on the B200 box: profiles/r02_e2e_host_staging.md),
 // rounded to whole chunks by upload_narrowed; raw_dev must hold raw_upload_elems(all) doubles.
 int64_t raw_upload_elems(int64_t all);
