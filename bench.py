@@ -519,7 +519,28 @@ def run_ours(args):
         t0 = time.perf_counter()
         list(pool.map(job, range(ke)))
         dt = allreduce_max(time.perf_counter() - t0, world)
+        # fwd+bwd end to end: renderer.render_backward (renders, then back-propagates) with a host
+        # float64 dL/dimage in and float64 gradients out, the same frames in flight
+        dl_host = _pinned_copy(np.random.default_rng(0).standard_normal((int(cam.height), int(cam.width), 3)) * 1e-3)
+        sent_b = []
+
+        def job_b(_):
+            torch.cuda.set_device(local)
+            renderer.render_backward(hscene, cam, dl_host, cfg, device=local)
+            sent_b.append(renderer.last_h2d_bytes(local))
+
+        list(pool.map(job_b, range(2 * nt)))
+        kb = max(2, min(args.steps, 6)) * nt
+        barrier(world)
+        t0 = time.perf_counter()
+        list(pool.map(job_b, range(kb)))
+        dtb = allreduce_max(time.perf_counter() - t0, world)
         pool.shutdown()
+        n_grad = len(scene.means) * (3 + 3 + 4 + 1 + scene.sh.shape[1] * 3)
+        e2e_fb = {"ms_per_view": 1e3 * dtb / kb, "views_per_s": world * kb / dtb,
+                  "h2d_bytes_per_step": int(max(sent_b[-kb:])), "d2h_bytes_per_step": int(4 * n_grad),
+                  "api": "paper_2505_24053_b200.renderer.render_backward (geer_render_backward_host)",
+                  "note": "fp32 gradients over PCIe, widened to the float64 outputs on host cores (exact)"}
         given = sum(a.nbytes for a in (hscene.means, hscene.log_scales, hscene.quats, hscene.opacity_logits, hscene.sh))
         h2d = max(sent[-ke:])  # what crossed PCIe (fp32 narrowed on host cores + a raw fp64 tail)
         d2h = n_px * (3 * 8 + 8 + 8)
@@ -528,7 +549,8 @@ def run_ours(args):
                "host_memory": "pinned float64 scene arrays", "frames_in_flight": nt,
                "host_input_bytes_per_step": int(given),
                "host_staging": "float64 -> fp32 on the host worker pool (%d threads), last %.0f%% of the elements sent "
-                               "raw and narrowed on the device" % (_lib_host_threads(), 100 * _raw_fraction())}
+                               "raw and narrowed on the device" % (_lib_host_threads(), 100 * _raw_fraction()),
+               "fwd_bwd": e2e_fb}
 
     # ---- 64-view training step (config 4)
     if not args.no_train:

@@ -161,8 +161,11 @@ struct geer_ctx {
     Buf temp;
     // host-path staging
     int64_t last_h2d = 0;     // PCIe bytes of the last host-buffer call's inputs
-    void *h_stage = nullptr;  // pinned write-combined host staging of the host-buffer entry points
+    void *h_stage = nullptr;  // pinned write-combined host staging of the host-buffer entry points' inputs
     size_t h_stage_cap = 0;
+    void *h_down = nullptr;   // pinned (cached) host staging of their fp32 outputs
+    size_t h_down_cap = 0;
+    std::vector<cudaEvent_t> down_evs;
     Buf h64_raw, s32_means, s32_log, s32_quats, s32_op, s32_sh, out64, g64;
     Arena arena;  // caller-owned workspace (geer_set_workspace), if attached
 };
@@ -738,6 +741,23 @@ int check_scene_dev(const geer_scene *s) {
 }
 
 // Copy a host f64 scene into device fp32 buffers held by the context.
+// A grow-only pinned host buffer (write-combined: written by the host, read only by DMA).
+int ensure_pinned(void *&p, size_t &cap, size_t need, bool write_combined, cudaStream_t st) {
+    if (cap >= need) return GEER_OK;
+    GEER_CUDA(cudaStreamSynchronize(st));  // (copies from the old buffer may be in flight)
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    const size_t bytes = need + need / 8;
+    if (cudaHostAlloc(&p, bytes, write_combined ? cudaHostAllocWriteCombined : cudaHostAllocDefault) != cudaSuccess) {
+        p = nullptr;
+        cudaGetLastError();
+        return fail(GEER_ERR_NOMEM, "pinned staging allocation of %zu bytes failed", bytes);
+    }
+    cap = bytes;
+    return GEER_OK;
+}
+
 int upload_host_scene(geer_ctx *c, const geer_host_scene *hs, cudaStream_t st) {
     int rc = 0;
     if (!hs) return fail(GEER_ERR_INVALID, "scene is required");
@@ -757,19 +777,8 @@ int upload_host_scene(geer_ctx *c, const geer_host_scene *hs, cudaStream_t st) {
                                  {hs->quats, n * 4, q},
                                  {hs->opacity_logits, n, op},
                                  {hs->sh, nsh, sh}};
-        const size_t need = sizeof(float) * (size_t)(n * 11 + nsh);
-        if (c->h_stage_cap < need) {
-            GEER_CUDA(cudaStreamSynchronize(st));
-            if (c->h_stage) cudaFreeHost(c->h_stage);
-            c->h_stage = nullptr;
-            c->h_stage_cap = 0;
-            if (cudaHostAlloc(&c->h_stage, need, cudaHostAllocWriteCombined) != cudaSuccess) {
-                c->h_stage = nullptr;
-                cudaGetLastError();
-                return fail(GEER_ERR_NOMEM, "pinned staging allocation of %zu bytes failed", need);
-            }
-            c->h_stage_cap = need;
-        }
+        rc = ensure_pinned(c->h_stage, c->h_stage_cap, sizeof(float) * (size_t)(n * 11 + nsh), true, st);
+        if (rc) return rc;
         const int64_t raw = raw_upload_elems(n * 11 + nsh);
         double *raw_dev = nullptr;
         if (raw > 0) raw_dev = ENSURE(double, c->h64_raw, raw);
@@ -835,6 +844,8 @@ void geer_destroy(geer_ctx *c) {
     if (c->d_err) cudaFree(c->d_err);
     if (c->h_hdr) cudaFreeHost(c->h_hdr);
     if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->h_down) cudaFreeHost(c->h_down);
+    for (cudaEvent_t e : c->down_evs) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -1233,28 +1244,42 @@ int geer_render_backward_host(geer_ctx *c, const geer_host_scene *scene, const g
     if (n == 0) return GEER_OK;
     for (int i = 0; i < 5; ++i)
         if (!hout[i]) return fail(GEER_ERR_INVALID, "gradient pointers must be non-null");
-    // dl_dimage f64 host -> f32 device
-    double *dl64 = ensure<double>(c->out64, (size_t)npx * 3, &rc);
-    if (rc) return rc;
+    // dl_dimage f64 host -> f32 device: narrowed on the host like the scene, into the staging region
+    // after the scene's (whose copies may still be in flight)
     float *dl32 = ensure<float>(c->dl32, (size_t)npx * 3, &rc);
     if (rc) return rc;
-    GEER_CUDA(cudaMemcpyAsync(dl64, dl_dimage, sizeof(double) * npx * 3, cudaMemcpyHostToDevice, st));
-    c->last_h2d += (int64_t)sizeof(double) * npx * 3;
-    launch_convert_f64_f32(dl64, dl32, npx * 3, st);
+    const int64_t scene_floats = n * 11 + n * nb * 3;
+    rc = ensure_pinned(c->h_stage, c->h_stage_cap, sizeof(float) * (size_t)(scene_floats + npx * 3), true, st);
+    if (rc) return rc;
+    {
+        const HostSeg seg = {dl_dimage, npx * 3, dl32};
+        const int64_t raw = raw_upload_elems(npx * 3);
+        double *raw_dev = nullptr;
+        if (raw > 0) raw_dev = ensure<double>(c->out64, (size_t)raw, &rc);
+        if (rc) return rc;
+        int64_t sent = 0;
+        GEER_CUDA(upload_narrowed(&seg, 1, (float *)c->h_stage + scene_floats, raw_dev, raw, st, &sent));
+        c->last_h2d += sent;
+    }
+    // fp32 gradients (k_finalize's arithmetic is fp32; its f64 output would be the exact widening),
+    // downloaded chunk by chunk and widened on the host pool
     int64_t tot = 0;
     for (int i = 0; i < 5; ++i) tot += sizes[i];
-    double *g = ensure<double>(c->g64, (size_t)tot, &rc);
+    float *g = ensure<float>(c->g64, (size_t)tot, &rc);
     if (rc) return rc;
     void *gp[5];
+    HostOut outs[5];
     int64_t off = 0;
     for (int i = 0; i < 5; ++i) {
         gp[i] = g + off;
+        outs[i] = HostOut{g + off, sizes[i], hout[i]};
         off += sizes[i];
     }
-    rc = run_backward(c, dl32, true, gp, 0, st);
+    rc = run_backward(c, dl32, false, gp, 0, st);
     if (rc) return rc;
-    for (int i = 0; i < 5; ++i)
-        GEER_CUDA(cudaMemcpyAsync(hout[i], gp[i], sizeof(double) * sizes[i], cudaMemcpyDeviceToHost, st));
+    rc = ensure_pinned(c->h_down, c->h_down_cap, sizeof(float) * (size_t)tot, false, st);
+    if (rc) return rc;
+    GEER_CUDA(download_widened(outs, 5, (float *)c->h_down, c->down_evs, st));
     GEER_CUDA(cudaStreamSynchronize(st));
     return GEER_OK;
 }

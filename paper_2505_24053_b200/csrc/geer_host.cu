@@ -90,6 +90,27 @@ __attribute__((target("avx2"))) void narrow_avx2(const double *src, float *dst, 
     _mm_sfence();  // the streamed stores are visible before the chunk's done flag
 }
 
+// (float64 results streamed past the cache: no read-for-ownership of the caller's output lines)
+__attribute__((target("avx2"))) void widen_avx2(const float *src, double *dst, int64_t n) {
+    int64_t i = 0;
+    for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 31); ++i) dst[i] = (double)src[i];
+    for (; i + 8 <= n; i += 8) {
+        _mm256_stream_pd(dst + i, _mm256_cvtps_pd(_mm_loadu_ps(src + i)));
+        _mm256_stream_pd(dst + i + 4, _mm256_cvtps_pd(_mm_loadu_ps(src + i + 4)));
+    }
+    for (; i < n; ++i) dst[i] = (double)src[i];
+    _mm_sfence();
+}
+
+void widen_run(const float *src, double *dst, int64_t n) {
+    static const bool avx2 = __builtin_cpu_supports("avx2") && !getenv("GEER_HOST_SCALAR");
+    if (avx2) {
+        widen_avx2(src, dst, n);
+    } else {
+        for (int64_t i = 0; i < n; ++i) dst[i] = (double)src[i];
+    }
+}
+
 void narrow_scalar(const double *src, float *dst, int64_t n) {
     for (int64_t i = 0; i < n; ++i) dst[i] = (float)src[i];
 }
@@ -223,6 +244,79 @@ cudaError_t upload_narrowed(const HostSeg *segs, int nseg, float *staging, doubl
             std::this_thread::yield();
     }
     return first_err;
+}
+
+constexpr int64_t kDownChunk = 1 << 21;  // elements per download chunk (8 MB of fp32)
+
+// One device->host download: chunk c is copied into the staging buffer and recorded on event c;
+// whoever takes chunk c (a worker or the caller) waits for that event and widens it.
+struct DownJob {
+    std::vector<HostOut> outs;
+    std::vector<int64_t> off;
+    const float *staging = nullptr;
+    const cudaEvent_t *evs = nullptr;
+    int64_t total = 0;
+    int nch = 0;
+    std::atomic<int> next{0}, done{0};
+    std::atomic<int> err{0};
+
+    void widen(int c) {
+        cudaError_t e;
+        while ((e = cudaEventQuery(evs[c])) == cudaErrorNotReady) std::this_thread::yield();
+        if (e != cudaSuccess) err.store((int)e);
+        const int64_t a = (int64_t)c * kDownChunk, b = std::min(total, a + kDownChunk);
+        for (size_t s = 0; s < outs.size(); ++s) {
+            const int64_t lo = std::max(a, off[s]), hi = std::min(b, off[s + 1]);
+            if (lo < hi && e == cudaSuccess) widen_run(staging + lo, outs[s].dst + (lo - off[s]), hi - lo);
+        }
+        done.fetch_add(1, std::memory_order_release);
+    }
+    void drain() {
+        for (;;) {
+            const int c = next.fetch_add(1, std::memory_order_relaxed);
+            if (c >= nch) return;
+            widen(c);
+        }
+    }
+};
+
+cudaError_t download_widened(const HostOut *outs, int nout, float *staging, std::vector<cudaEvent_t> &evs,
+                             cudaStream_t st) {
+    auto job = std::make_shared<DownJob>();
+    job->outs.assign(outs, outs + nout);
+    job->off.resize(nout + 1);
+    job->off[0] = 0;
+    for (int s = 0; s < nout; ++s) job->off[s + 1] = job->off[s] + outs[s].n;
+    job->total = job->off[nout];
+    job->staging = staging;
+    job->nch = (int)((job->total + kDownChunk - 1) / kDownChunk);
+    if (job->nch == 0) return cudaSuccess;
+    while ((int)evs.size() < job->nch) {
+        cudaEvent_t e;
+        cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        if (r != cudaSuccess) return r;
+        evs.push_back(e);
+    }
+    job->evs = evs.data();
+    // every chunk's copies, each followed by its event (enqueued before any widening starts)
+    for (int c = 0; c < job->nch; ++c) {
+        const int64_t a = (int64_t)c * kDownChunk, b = std::min(job->total, a + kDownChunk);
+        for (int s = 0; s < nout; ++s) {
+            const int64_t lo = std::max(a, job->off[s]), hi = std::min(b, job->off[s + 1]);
+            if (lo >= hi) continue;
+            cudaError_t r = cudaMemcpyAsync(staging + lo, outs[s].dev + (lo - job->off[s]), sizeof(float) * (size_t)(hi - lo),
+                                            cudaMemcpyDeviceToHost, st);
+            if (r != cudaSuccess) return r;  // (nothing handed to the workers yet)
+        }
+        cudaError_t r = cudaEventRecord(evs[c], st);
+        if (r != cudaSuccess) return r;
+    }
+    Pool &pool = Pool::get();
+    const int helpers = std::min(pool.size(), job->nch - 1);
+    for (int i = 0; i < helpers; ++i) pool.submit([job] { job->drain(); });
+    job->drain();
+    while (job->done.load(std::memory_order_acquire) < job->nch) std::this_thread::yield();
+    return (cudaError_t)job->err.load();
 }
 
 }  // namespace geer

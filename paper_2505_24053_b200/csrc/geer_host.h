@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace geer {
 
 constexpr int64_t kHostChunk = 1 << 19;  // elements per narrowing chunk (2 MB of fp32)
@@ -27,5 +29,17 @@ cudaError_t upload_narrowed(const HostSeg *segs, int nseg, float *staging, doubl
 int64_t raw_upload_elems(int64_t all);
 
 int host_threads();
+
+struct HostOut {
+    const float *dev;  // fp32 device array
+    int64_t n;         // elements
+    double *dst;       // its host float64 destination
+};
+
+// Copy the device arrays into `staging` (pinned, cached, >= sum of n floats) chunk by chunk on `st`
+// and widen each chunk into its float64 destination (exact) on the host pool as soon as it lands.
+// Returns when every destination is written.  `evs` grows to one event per chunk (owned by the caller).
+cudaError_t download_widened(const HostOut *outs, int nout, float *staging, std::vector<cudaEvent_t> &evs,
+                             cudaStream_t st);
 
 }  // namespace geer
