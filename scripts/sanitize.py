@@ -24,4 +24,11 @@ for name, n, w, h in (("C2", 3000, 160, 96), ("C5", 3000, 128, 80), ("C1", 2000,
     torch.cuda.synchronize()
     res = r.ctx.association_check(64)
     print(name, float(color.sum()), int(cnt.sum()), res["missing"], flush=True)
+# the host-buffer entry points (float64 in/out): host narrowing with a raw device-narrowed tail,
+# chunked fp32 gradient download widened on the host pool (12k Gaussians: > one 512k-element chunk)
+scene = synth.config_scene("C2", n=12_000)
+cam = synth.config_camera("C2", width=96, height=64)
+out = renderer.render(scene, cam, renderer.RenderConfig(), return_graph=False)
+grads = renderer.render_backward(scene, cam, np.full((64, 96, 3), 1e-3), renderer.RenderConfig())
+print("host", float(out.color.color.sum()), float(np.abs(grads.dsh).sum()), renderer.last_h2d_bytes(0), flush=True)
 print("sanitize run ok")
