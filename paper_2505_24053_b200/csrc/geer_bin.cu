@@ -307,6 +307,71 @@ __global__ void __launch_bounds__(kWalkWarps * 32) k_tiles_scatter(const uint2 *
     }
 }
 
+// The same level-2 scatter with one thread per row-bin entry (a block per segment) instead of a
+// warp walking the segment entry by entry: every (entry, tile) pair sets entry e's bit in its tile's
+// 256-bit membership mask (kW words, shared memory), then its slot is the (tile, segment) start
+// plus the number of earlier entries of the segment in that tile, popc of the mask below e.  Same
+// output bit for bit (the order within a tile is the entries' order in the segment).
+constexpr int kW = kSegLen / 32;  // mask words per tile
+static_assert(kW % 4 == 0, "the mask is zeroed in 16-byte stores");
+__global__ void __launch_bounds__(kSegLen) k_tiles_scatter_mask(const uint2 *__restrict__ rowbin,
+                                                                const AxisRanges *__restrict__ ar,
+                                                                const int32_t *__restrict__ rowstart,
+                                                                const int32_t *__restrict__ seg_off, int n_y, int n_x,
+                                                                const uint32_t *__restrict__ p2,
+                                                                uint32_t *__restrict__ order,
+                                                                int32_t *__restrict__ ranges) {
+    extern __shared__ uint32_t smem[];
+    uint32_t *mask = smem;             // [kW][n_x] (word-major: the prefix pass reads it conflict-free)
+    uint32_t *pre = smem + n_x * kW;   // [kW][n_x]: slot of the first entry of word w in tile t
+    const int sgl = blockIdx.x;
+    if (sgl >= seg_off[n_y]) return;
+    const int tid = threadIdx.x;
+    const int r = seg_row(seg_off, n_y, sgl);
+    const int s = sgl - seg_off[r], ns = seg_off[r + 1] - seg_off[r];
+    const int64_t base = (int64_t)n_x * seg_off[r] + s;
+    const int e0 = rowstart[r] + s * kSegLen, m = min(kSegLen, rowstart[r + 1] - e0);
+    for (int i = tid; i < n_x * kW / 4; i += kSegLen) reinterpret_cast<uint4 *>(mask)[i] = make_uint4(0u, 0u, 0u, 0u);
+    // (tile, segment) starts, loaded up front so their latency overlaps the mask phase
+    uint32_t start0 = 0;
+    if (tid < n_x) start0 = p2[base + (int64_t)tid * ns];
+    uint32_t gid = 0, xr[3] = {0u, 0u, 0u};  // this entry's x ranges (lo | hi << 16)
+    if (tid < m) {
+        const uint2 v = rowbin[e0 + tid];
+        gid = v.x;
+        if (v.y != kMultiX) {
+            xr[0] = v.y;
+        } else {
+            const AxisRanges a = ar[v.x];
+            xr[0] = a.x[0];
+            xr[1] = a.x[1];
+            xr[2] = a.x[2];
+        }
+    }
+    __syncthreads();
+    const int w = tid >> 5;
+    const uint32_t bit = 1u << (tid & 31);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        for (int t = (int)(xr[k] & 0xFFFFu); t < (int)(xr[k] >> 16); ++t) atomicOr(&mask[w * n_x + t], bit);
+    __syncthreads();
+    for (int t = tid; t < n_x; t += kSegLen) {
+        uint32_t run = t == tid ? start0 : p2[base + (int64_t)t * ns];
+        if (s == 0) ranges[r * n_x + t] = (int32_t)run;  // first entry of tile (r, t)
+#pragma unroll
+        for (int j = 0; j < kW; ++j) {
+            pre[j * n_x + t] = run;
+            run += __popc(mask[j * n_x + t]);
+        }
+    }
+    __syncthreads();
+    const uint32_t below = bit - 1u;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        for (int t = (int)(xr[k] & 0xFFFFu); t < (int)(xr[k] >> 16); ++t)
+            order[pre[w * n_x + t] + __popc(mask[w * n_x + t] & below)] = gid;
+}
+
 // status: [0] the frame's error code, [1] sticky overflow flag (cleared by geer_sync), [2..3] the largest
 // (entries, rows) of an overflowing frame since (u64 at byte 8).
 __global__ void k_check_capacity(const unsigned long long *__restrict__ totals, int64_t cap_entries, int64_t cap_rows,
@@ -363,11 +428,19 @@ int bin_tiles(const BinPlan &p, const int32_t *gsorted, const AxisRanges *ar, in
     k_tiles_count<<<(unsigned)p.seg_cap, kSegLen, n_x * 4, st>>>(rowbin, ar, rowstart, seg_off, n_y, n_x, m2);
     tb = p.temp_bytes;
     cub::DeviceScan::ExclusiveSum(temp, tb, m2, p2, (int)p.m2_len, st);
+#ifndef GEER_TILES_WALK
+    const int wsm_tiles = n_x * kW * 2 * 4;
+    if (wsm_tiles > 48 * 1024)
+        cudaFuncSetAttribute(k_tiles_scatter_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm_tiles);
+    k_tiles_scatter_mask<<<(unsigned)p.seg_cap, kSegLen, wsm_tiles, st>>>(rowbin, ar, rowstart, seg_off, n_y, n_x, p2,
+                                                                         order, ranges);
+#else
     const int wsm_tiles = n_x * 4 * kWalkWarps;
     if (wsm_tiles > 48 * 1024)
         cudaFuncSetAttribute(k_tiles_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm_tiles);
     k_tiles_scatter<<<(unsigned)((p.seg_cap + kWalkWarps - 1) / kWalkWarps), kWalkWarps * 32, wsm_tiles, st>>>(
         rowbin, ar, rowstart, seg_off, n_y, n_x, p2, order, ranges);
+#endif
     return cudaGetLastError() == cudaSuccess ? GEER_OK : GEER_ERR_CUDA;
 }
 
