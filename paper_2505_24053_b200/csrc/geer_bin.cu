@@ -158,6 +158,60 @@ __global__ void __launch_bounds__(kWalkWarps * 32) k_rows_scatter(const int32_t 
     }
 }
 
+// The level-1 scatter with one thread per Gaussian of the chunk (a block per chunk): each (Gaussian,
+// row) pair sets the Gaussian's bit in the row's 256-bit membership mask (shared memory, word-major),
+// and its slot is the (row, chunk) start plus popc of the mask below it: the rows' entries stay in
+// depth order, bit for bit the walk's output.
+constexpr int kRW = kBinChunk / 32;  // mask words per row
+static_assert(kRW % 4 == 0, "the mask is zeroed in 16-byte stores");
+__global__ void __launch_bounds__(kBinChunk) k_rows_scatter_mask(const int32_t *__restrict__ gsorted,
+                                                                 const AxisRanges *__restrict__ ar, int64_t n,
+                                                                 int n_y, int nch, const uint32_t *__restrict__ p1,
+                                                                 uint2 *__restrict__ rowbin,
+                                                                 const int *__restrict__ err) {
+    extern __shared__ uint32_t smem[];
+    if (*err == GEER_ERR_OVERFLOW) return;
+    uint32_t *mask = smem;            // [kRW][n_y]
+    uint32_t *pre = smem + n_y * kRW; // [kRW][n_y]
+    const int c = blockIdx.x, tid = threadIdx.x;
+    for (int i = tid; i < n_y * kRW / 4; i += kBinChunk) reinterpret_cast<uint4 *>(mask)[i] = make_uint4(0u, 0u, 0u, 0u);
+    uint32_t start0 = 0;
+    if (tid < n_y) start0 = p1[(int64_t)tid * nch + c];
+    const int64_t p = (int64_t)c * kBinChunk + tid;
+    uint32_t g = 0, xi = 0, yr[3] = {0u, 0u, 0u};
+    if (p < n) {
+        g = (uint32_t)gsorted[p];
+        const AxisRanges a = ar[g];
+        if (has_entries(a)) {
+            xi = x_info(a);
+            yr[0] = a.y[0];
+            yr[1] = a.y[1];
+            yr[2] = a.y[2];
+        }
+    }
+    __syncthreads();
+    const int w = tid >> 5;
+    const uint32_t bit = 1u << (tid & 31);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        for (int r = (int)(yr[k] & 0xFFFFu); r < (int)(yr[k] >> 16); ++r) atomicOr(&mask[w * n_y + r], bit);
+    __syncthreads();
+    for (int r = tid; r < n_y; r += kBinChunk) {
+        uint32_t run = r == tid ? start0 : p1[(int64_t)r * nch + c];
+#pragma unroll
+        for (int j = 0; j < kRW; ++j) {
+            pre[j * n_y + r] = run;
+            run += __popc(mask[j * n_y + r]);
+        }
+    }
+    __syncthreads();
+    const uint32_t below = bit - 1u;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        for (int r = (int)(yr[k] & 0xFFFFu); r < (int)(yr[k] >> 16); ++r)
+            rowbin[pre[w * n_y + r] + __popc(mask[w * n_y + r] & below)] = make_uint2(g, xi);
+}
+
 // Row starts, segments per row (>= 1, so every tile has a (tile, segment 0) slot) and their
 // exclusive prefix; also the list end ranges[n_tiles] = total.  One block.
 __global__ void k_segments(const uint32_t *__restrict__ m1, const uint32_t *__restrict__ p1, int n_y, int nch,
@@ -420,10 +474,17 @@ int bin_tiles(const BinPlan &p, const int32_t *gsorted, const AxisRanges *ar, in
     k_rows_count<<<p.nch, kBinChunk, n_y * 4, st>>>(gsorted, ar, n, n_y, p.nch, m1, err);
     size_t tb = p.temp_bytes;
     cub::DeviceScan::ExclusiveSum(temp, tb, m1, p1, (int)p.m1_len, st);
+#ifndef GEER_ROWS_WALK
+    const int wsm_rows = n_y * kRW * 2 * 4;
+    if (wsm_rows > 48 * 1024)
+        cudaFuncSetAttribute(k_rows_scatter_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm_rows);
+    k_rows_scatter_mask<<<p.nch, kBinChunk, wsm_rows, st>>>(gsorted, ar, n, n_y, p.nch, p1, rowbin, err);
+#else
     const int wsm_rows = n_y * 4 * kWalkWarps;
     if (wsm_rows > 48 * 1024) cudaFuncSetAttribute(k_rows_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm_rows);
     k_rows_scatter<<<(p.nch + kWalkWarps - 1) / kWalkWarps, kWalkWarps * 32, wsm_rows, st>>>(gsorted, ar, n, n_y,
                                                                                            p.nch, p1, rowbin, err);
+#endif
     k_segments<<<1, 1024, 0, st>>>(m1, p1, n_y, p.nch, rowstart, seg_off, n_tiles, d_total, ranges, err);
     k_tiles_count<<<(unsigned)p.seg_cap, kSegLen, n_x * 4, st>>>(rowbin, ar, rowstart, seg_off, n_y, n_x, m2);
     tb = p.temp_bytes;
