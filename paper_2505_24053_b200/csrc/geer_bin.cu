@@ -5,16 +5,17 @@
 // count / exclusive-scan / ordered-scatter triple:
 //   level 1 (rows):  chunk c of kBinChunk consecutive depth ranks counts its Gaussians per tile
 //                    row; one flat exclusive scan of the [row][chunk] count matrix gives every
-//                    (row, chunk) its start in the row bins; a warp per chunk then walks its
-//                    Gaussians in depth order and appends (gid, x-range) to each of their rows.
+//                    (row, chunk) its start in the row bins; a block per chunk then places each
+//                    (Gaussian, row) pair, (gid, x-range), in depth order.
 //   level 2 (tiles): the row bins are cut into segments of kSegLen entries; the [row][tile][segment]
 //                    count matrix, scanned flat in that order, is exactly the final entry position
 //                    of every (tile, segment) (tile-major order, segments of a row in depth order);
-//                    a warp per segment walks it in order and writes gids to their tiles.
-// In the ordered walks lane (i mod 32) owns counter i, so every counter is read and written by a
-// single thread in program order: no atomics, no warp synchronisation, and the output equals the
-// stable tile sort bit for bit.  Traffic is a few bytes per entry (vs. two radix passes over
-// 6-byte pairs plus the emitted pairs themselves).
+//                    a block per segment places each (entry, tile) pair.
+// The scatters are order-exact without atomics on positions: each pair sets its item's bit in a
+// per-bucket membership mask (one bit per item of the chunk / segment, shared memory), and its slot is
+// the bucket's start plus the number of earlier items in the bucket, popc of the mask below its bit.
+// The output equals the stable tile sort bit for bit.  Traffic is a few bytes per entry (vs. two
+// radix passes over 6-byte pairs plus the emitted pairs themselves).
 #include <cub/cub.cuh>
 #include <stdint.h>
 
@@ -28,45 +29,13 @@ namespace {
 #define GEER_BIN_CHUNK 256
 #endif
 #ifndef GEER_SEG_LEN
-#define GEER_SEG_LEN 256
+#define GEER_SEG_LEN 512
 #endif
 constexpr int kBinChunk = GEER_BIN_CHUNK;  // depth-ordered Gaussians per level-1 chunk (= threads of a count block)
 constexpr int kSegLen = GEER_SEG_LEN;      // row-bin entries per level-2 segment (= threads of a count block)
-constexpr int kWalkWarps = 8;   // ordered-walk warps per block
 constexpr uint32_t kMultiX = 0xFFFFFFFFu;  // row-bin x info: several x ranges, read them from AxisRanges
 
 __device__ __forceinline__ int rlen(uint32_t r) { return (int)(r >> 16) - (int)(r & 0xFFFFu); }
-
-__device__ __forceinline__ uint32_t sm_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ uint32_t ld_sm(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void st_sm(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v)); }
-__device__ __forceinline__ uint2 ld_sm2(uint32_t a) {
-    uint2 v;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint4 ld_sm4(uint32_t a) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-// Append value v of one item to the slot of counter index k = lo + ((lane - lo) & 31) (the one this
-// lane owns in [lo, hi)), if any: slot = counter, counter += 1.
-template <typename T>
-__device__ __forceinline__ void own_put(uint32_t cbase, int lane, uint32_t range, T v, T *__restrict__ out) {
-    const int lo = (int)(range & 0xFFFFu), hi = (int)(range >> 16);
-    const int k = lo + ((lane - lo) & 31);
-    if (k < hi) {
-        const uint32_t a = cbase + 4u * (uint32_t)k;
-        const uint32_t pos = ld_sm(a);
-        st_sm(a, pos + 1u);
-        out[pos] = v;
-    }
-}
 
 // Row-bin x info of a Gaussian: its single packed x range, or kMultiX.
 __device__ __forceinline__ uint32_t x_info(const AxisRanges &a) {
@@ -97,71 +66,10 @@ __global__ void __launch_bounds__(kBinChunk) k_rows_count(const int32_t *__restr
     for (int r = threadIdx.x; r < n_y; r += blockDim.x) m1[(int64_t)r * nch + blockIdx.x] = cnt[r];
 }
 
-// One warp per chunk: its Gaussians in depth order, 32 at a time staged in shared memory and read
-// back as broadcasts; for each, the lanes owning its rows append (gid, x info).  Gaussians with
-// several y ranges or more than 32 rows take the general loop.
-__global__ void __launch_bounds__(kWalkWarps * 32) k_rows_scatter(const int32_t *__restrict__ gsorted,
-                                                                 const AxisRanges *__restrict__ ar, int64_t n, int n_y,
-                                                                 int nch, const uint32_t *__restrict__ p1,
-                                                                 uint2 *__restrict__ rowbin,
-                                                                 const int *__restrict__ err) {
-    extern __shared__ uint32_t smem[];
-    if (*err == GEER_ERR_OVERFLOW) return;
-    __shared__ uint4 stage[kWalkWarps][32];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int c = blockIdx.x * kWalkWarps + wib;
-    if (c >= nch) return;
-    uint32_t *cnt = smem + wib * n_y;
-    for (int r = lane; r < n_y; r += 32) cnt[r] = p1[(int64_t)r * nch + c];  // row r: lane r % 32 only
-    const int64_t p0 = (int64_t)c * kBinChunk;
-    const int m_all = (int)lmin(kBinChunk, n - p0);
-    for (int b = 0; b < m_all; b += 32) {
-        const int64_t p = p0 + b + lane;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);  // (gid, x info, y range or kMultiX, -)
-        if (b + lane < m_all) {
-            const uint32_t g = (uint32_t)gsorted[p];
-            const AxisRanges a = ar[g];
-            if (has_entries(a)) {
-                const bool multi = rlen(a.y[1]) > 0 || rlen(a.y[2]) > 0 || rlen(a.y[0]) > 32;
-                v = make_uint4(g, x_info(a), multi ? kMultiX : a.y[0], 0u);
-            }
-        }
-        stage[wib][lane] = v;
-        const bool any_multi = __any_sync(0xffffffffu, v.z == kMultiX);
-        __syncwarp();
-        const int m = min(32, m_all - b);
-        const uint32_t cbase = sm_addr(cnt), sb = sm_addr(&stage[wib][0]);
-        if (!any_multi) {
-#pragma unroll 4
-            for (int i = 0; i < m; ++i) {
-                const uint4 e = ld_sm4(sb + 16u * i);
-                own_put(cbase, lane, e.z, make_uint2(e.x, e.y), rowbin);
-            }
-        } else for (int i = 0; i < m; ++i) {
-            const uint4 e = stage[wib][i];
-            if (e.z != kMultiX) {
-                own_put(cbase, lane, e.z, make_uint2(e.x, e.y), rowbin);
-            } else {
-                const AxisRanges a = ar[e.x];
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    const int lo = (int)(a.y[k] & 0xFFFFu), hi = (int)(a.y[k] >> 16);
-                    for (int r = lo + ((lane - lo) & 31); r < hi; r += 32) {
-                        const uint32_t pos = cnt[r];
-                        cnt[r] = pos + 1;
-                        rowbin[pos] = make_uint2(e.x, e.y);
-                    }
-                }
-            }
-        }
-        __syncwarp();
-    }
-}
-
-// The level-1 scatter with one thread per Gaussian of the chunk (a block per chunk): each (Gaussian,
-// row) pair sets the Gaussian's bit in the row's 256-bit membership mask (shared memory, word-major),
-// and its slot is the (row, chunk) start plus popc of the mask below it: the rows' entries stay in
-// depth order, bit for bit the walk's output.
+// Level-1 scatter, one thread per Gaussian of the chunk (a block per chunk): each (Gaussian, row)
+// pair sets the Gaussian's bit in the row's kBinChunk-bit membership mask (shared memory,
+// word-major), and its slot is the (row, chunk) start plus popc of the mask below it: the rows'
+// entries stay in depth order.
 constexpr int kRW = kBinChunk / 32;  // mask words per row
 static_assert(kRW % 4 == 0, "the mask is zeroed in 16-byte stores");
 __global__ void __launch_bounds__(kBinChunk) k_rows_scatter_mask(const int32_t *__restrict__ gsorted,
@@ -297,75 +205,10 @@ __global__ void __launch_bounds__(kSegLen) k_tiles_count(const uint2 *__restrict
     for (int t = threadIdx.x; t < n_x; t += blockDim.x) m2[base + (int64_t)t * ns] = cnt[t];
 }
 
-__device__ __forceinline__ void put_tiles(uint32_t *cnt, int lane, uint32_t xr, uint32_t gid, uint32_t *order) {
-    const int lo = (int)(xr & 0xFFFFu), hi = (int)(xr >> 16);
-    for (int t = lo + ((lane - lo) & 31); t < hi; t += 32) {  // tile t: lane t % 32 only
-        const uint32_t pos = cnt[t];
-        cnt[t] = pos + 1;
-        order[pos] = gid;
-    }
-}
-
-// One warp per segment: its row-bin entries in order, read as shared-memory broadcasts; for each,
-// the lane owning each of its tiles writes the gid (one tile per lane when the x range spans <= 32
-// tiles, the general loop otherwise).
-__global__ void __launch_bounds__(kWalkWarps * 32) k_tiles_scatter(const uint2 *__restrict__ rowbin,
-                                                                  const AxisRanges *__restrict__ ar,
-                                                                  const int32_t *__restrict__ rowstart,
-                                                                  const int32_t *__restrict__ seg_off, int n_y, int n_x,
-                                                                  const uint32_t *__restrict__ p2,
-                                                                  uint32_t *__restrict__ order,
-                                                                  int32_t *__restrict__ ranges) {
-    extern __shared__ uint32_t smem[];
-    __shared__ uint2 stage[kWalkWarps][kSegLen];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int sgl = blockIdx.x * kWalkWarps + wib;
-    if (sgl >= seg_off[n_y]) return;
-    const int r = seg_row(seg_off, n_y, sgl);
-    const int s = sgl - seg_off[r], ns = seg_off[r + 1] - seg_off[r];
-    uint32_t *cnt = smem + wib * n_x;
-    const int64_t base = (int64_t)n_x * seg_off[r] + s;
-    for (int t = lane; t < n_x; t += 32) {
-        const uint32_t v = p2[base + (int64_t)t * ns];
-        cnt[t] = v;
-        if (s == 0) ranges[r * n_x + t] = (int32_t)v;  // first entry of tile (r, t)
-    }
-    const int e0 = rowstart[r] + s * kSegLen, m = min(kSegLen, rowstart[r + 1] - e0);
-    bool multi = false;
-    for (int i = lane; i < m; i += 32) {
-        uint2 v = rowbin[e0 + i];
-        if (v.y != kMultiX && rlen(v.y) > 32) v.y = kMultiX;  // general loop below
-        multi |= v.y == kMultiX;
-        stage[wib][i] = v;
-    }
-    const bool any_multi = __any_sync(0xffffffffu, multi);
-    __syncwarp();
-    const uint32_t cbase = sm_addr(cnt), sb = sm_addr(&stage[wib][0]);
-    if (!any_multi) {
-#pragma unroll 8
-        for (int i = 0; i < m; ++i) {
-            const uint2 v = ld_sm2(sb + 8u * i);
-            own_put(cbase, lane, v.y, v.x, order);
-        }
-        return;
-    }
-    for (int i = 0; i < m; ++i) {
-        const uint2 v = stage[wib][i];
-        if (v.y != kMultiX) {
-            own_put(cbase, lane, v.y, v.x, order);
-        } else {
-            const AxisRanges a = ar[v.x];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) put_tiles(cnt, lane, a.x[k], v.x, order);
-        }
-    }
-}
-
-// The same level-2 scatter with one thread per row-bin entry (a block per segment) instead of a
-// warp walking the segment entry by entry: every (entry, tile) pair sets entry e's bit in its tile's
-// 256-bit membership mask (kW words, shared memory), then its slot is the (tile, segment) start
-// plus the number of earlier entries of the segment in that tile, popc of the mask below e.  Same
-// output bit for bit (the order within a tile is the entries' order in the segment).
+// Level-2 scatter, one thread per row-bin entry (a block per segment): every (entry, tile) pair sets entry e's bit in its tile's
+// kSegLen-bit membership mask (kW words, shared memory), then its slot is the (tile, segment) start
+// plus the number of earlier entries of the segment in that tile, popc of the mask below e (the
+// order within a tile is the entries' order in the segment).
 constexpr int kW = kSegLen / 32;  // mask words per tile
 static_assert(kW % 4 == 0, "the mask is zeroed in 16-byte stores");
 __global__ void __launch_bounds__(kSegLen) k_tiles_scatter_mask(const uint2 *__restrict__ rowbin,
@@ -470,38 +313,23 @@ int bin_tiles(const BinPlan &p, const int32_t *gsorted, const AxisRanges *ar, in
         cudaMemsetAsync(ranges, 0, sizeof(int32_t) * (n_tiles + 1), st);
         return cudaGetLastError() == cudaSuccess ? GEER_OK : GEER_ERR_CUDA;
     }
-    if ((size_t)n_y * 4 * kWalkWarps > 200 * 1024 || (size_t)n_x * 4 * kWalkWarps > 200 * 1024) return GEER_ERR_INVALID;
+    if ((size_t)n_y * kRW * 8 > 200 * 1024 || (size_t)n_x * kW * 8 > 200 * 1024) return GEER_ERR_INVALID;
     k_rows_count<<<p.nch, kBinChunk, n_y * 4, st>>>(gsorted, ar, n, n_y, p.nch, m1, err);
     size_t tb = p.temp_bytes;
     cub::DeviceScan::ExclusiveSum(temp, tb, m1, p1, (int)p.m1_len, st);
-#ifndef GEER_ROWS_WALK
     const int wsm_rows = n_y * kRW * 2 * 4;
     if (wsm_rows > 48 * 1024)
         cudaFuncSetAttribute(k_rows_scatter_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm_rows);
     k_rows_scatter_mask<<<p.nch, kBinChunk, wsm_rows, st>>>(gsorted, ar, n, n_y, p.nch, p1, rowbin, err);
-#else
-    const int wsm_rows = n_y * 4 * kWalkWarps;
-    if (wsm_rows > 48 * 1024) cudaFuncSetAttribute(k_rows_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm_rows);
-    k_rows_scatter<<<(p.nch + kWalkWarps - 1) / kWalkWarps, kWalkWarps * 32, wsm_rows, st>>>(gsorted, ar, n, n_y,
-                                                                                           p.nch, p1, rowbin, err);
-#endif
     k_segments<<<1, 1024, 0, st>>>(m1, p1, n_y, p.nch, rowstart, seg_off, n_tiles, d_total, ranges, err);
     k_tiles_count<<<(unsigned)p.seg_cap, kSegLen, n_x * 4, st>>>(rowbin, ar, rowstart, seg_off, n_y, n_x, m2);
     tb = p.temp_bytes;
     cub::DeviceScan::ExclusiveSum(temp, tb, m2, p2, (int)p.m2_len, st);
-#ifndef GEER_TILES_WALK
     const int wsm_tiles = n_x * kW * 2 * 4;
     if (wsm_tiles > 48 * 1024)
         cudaFuncSetAttribute(k_tiles_scatter_mask, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm_tiles);
     k_tiles_scatter_mask<<<(unsigned)p.seg_cap, kSegLen, wsm_tiles, st>>>(rowbin, ar, rowstart, seg_off, n_y, n_x, p2,
                                                                          order, ranges);
-#else
-    const int wsm_tiles = n_x * 4 * kWalkWarps;
-    if (wsm_tiles > 48 * 1024)
-        cudaFuncSetAttribute(k_tiles_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, wsm_tiles);
-    k_tiles_scatter<<<(unsigned)((p.seg_cap + kWalkWarps - 1) / kWalkWarps), kWalkWarps * 32, wsm_tiles, st>>>(
-        rowbin, ar, rowstart, seg_off, n_y, n_x, p2, order, ranges);
-#endif
     return cudaGetLastError() == cudaSuccess ? GEER_OK : GEER_ERR_CUDA;
 }
 

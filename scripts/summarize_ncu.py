@@ -32,7 +32,7 @@ METRICS = [
     ("launch__registers_per_thread", "registers", "", 1),
     ("lts__t_sector_hit_rate.pct", "L2 hit", "%", 1),
 ]
-STAGE = {"k_forward": "render", "k_backward": "backward", "k_preprocess": "prep", "k_tiles_scatter": "sort",
+STAGE = {"k_forward": "render", "k_backward": "backward", "k_preprocess": "prep", "k_tiles_scatter_mask": "sort",
          "k_finalize": "finalize"}
 
 
