@@ -802,7 +802,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-c1", action="store_true")
-    ap.add_argument("--inflight", type=int, default=4, help="frames in flight (contexts/streams) for the FPS value")
+    ap.add_argument("--inflight", type=int, default=6, help="frames in flight (contexts/streams) for the FPS value")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -62,7 +62,8 @@ struct __align__(16) Cull {
 // Raster payload, one per Gaussian (176 B, see make_payload in geer_geometry.cu; one TMA row):
 //   q[12]  W (row-major, W = S^-1 R^T) and o_u = W (o - mu) in fp64 (renderer.py:78-79)
 //   col  = (r, g, b, sigma)
-//   ext  = (absolute kappa error bound of the fp64 cross-product evaluation, 0, 0, 0)
+//   ext  = (absolute kappa error bound of the fp64 cross-product evaluation, the fp64 opacity as two
+//           32-bit halves (lo, hi), 0)
 //   cull = the culling record (written by the association half of K1)
 struct __align__(16) Payload {
     double q[12];

@@ -476,7 +476,8 @@ __device__ void make_payload(const double W[9], const double ou[3], const double
     for (int i = 0; i < 3; ++i) pl.q[9 + i] = ou[i];
     const double band1 = 64.0 * u64 * (on + 1.0) * (cond + 1.0) * (2.0 * lam + 1.0);
     pl.col = make_float4((float)rgb[0], (float)rgb[1], (float)rgb[2], (float)sigma);
-    pl.ext = make_float4((float)band1, 0.f, 0.f, 0.f);
+    // ext.y / ext.z: the bits of the fp64 opacity (core.py:58-67), for the fix-up's fp64 t
+    pl.ext = make_float4((float)band1, __int_as_float(__double2loint(sigma)), __int_as_float(__double2hiint(sigma)), 0.f);
 }
 
 __device__ __forceinline__ void named_barrier(int id, int count) {

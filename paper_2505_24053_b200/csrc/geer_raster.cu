@@ -1195,7 +1195,7 @@ __device__ void fixup_pixel(FrameConst fc, const geer_scene &sc, const int4 *__r
     int cnt = 0, last = e0 - 1;  // last: the last alive survivor
     bool alive = true;
     // fp64 t of entry e (renderer.py:96-105 in fp64: the payload's cross product, the reference
-    // formulation near the cutoff, fp64 sigmoid and exp)
+    // formulation near the cutoff, K1's fp64 sigmoid from the payload, fp64 exp)
     auto eval64 = [&](int e, double &t, float4 &cl) {
         const uint32_t g = order[e];
         const Payload &P = payload[g];
@@ -1206,8 +1206,7 @@ __device__ void fixup_pixel(FrameConst fc, const geer_scene &sc, const int4 *__r
         if (fc.cutoff && fabs(kap - fc.lam2) <= (double)P.ext.x)
             kap = kappa_fp64(sc.means, sc.log_scales, sc.quats, fc.origin[0], fc.origin[1], fc.origin[2], g, d[0], d[1],
                              d[2]);
-        const double x = (double)sc.opacity_logits[g];
-        const double sig = x >= 0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x));
+        const double sig = __hiloint2double(__float_as_int(P.ext.z), __float_as_int(P.ext.y));  // K1's fp64 sigmoid
         double u = sig * exp(-0.5 * kap);
         if (fc.cutoff && !(kap <= fc.lam2)) u = 0.0;
         t = u < kMaxBlendT ? u : kMaxBlendT;
