@@ -527,7 +527,7 @@ size_t workspace_estimate(const FrameConst &fc, int64_t n, int64_t cap_e, int64_
     add((bp.m2_len + 1) * 4);
     add((lmax(cap_e, 1) + 1) * 4);                       // order
     add(max_items * 16);                                 // work
-    add(8);                                              // n_work
+    add(4 * order_items_ints());                         // n_work (+ work-order scratch)
     // per pixel
     add(npx * 4);                                        // n_eval
     add(npx * 4);                                        // fix-up list
@@ -613,7 +613,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
     if (fc.exhaustive) {  // every tile composites all kept Gaussians: no emit, no tile sort
         int32_t *r2 = ENSURE(int32_t, c->tile_ranges, fc.n_tiles + 1);
         launch_exhaustive_ranges((const uint8_t *)c->flags.p, n, r2, st);
-        int32_t *nwork = ENSURE(int32_t, c->n_work, 2);
+        int32_t *nwork = ENSURE(int32_t, c->n_work, order_items_ints());
         GEER_CUDA(cudaMemcpyAsync(nwork, c->n_items.p, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
         GEER_CUDA(cudaMemsetAsync(nwork + 1, 0, sizeof(int32_t), st));
         if (c->timing) {
@@ -668,7 +668,7 @@ int run_forward(geer_ctx *c, float *color, float *remaining, int32_t *count, boo
                        tmp, order, ranges, st);
         if (rc) return fail(rc, "tile binning failed: %s", cudaGetErrorString(cudaGetLastError()));
         int4 *work = ENSURE(int4, c->work, c->max_items);
-        int32_t *nwork = ENSURE(int32_t, c->n_work, 2);
+        int32_t *nwork = ENSURE(int32_t, c->n_work, order_items_ints());
         order_items((const int4 *)c->items.p, (const int32_t *)c->n_items.p, ranges, c->max_items, work, nwork, st);
         if (c->timing) GEER_CUDA(cudaEventRecord(c->ev[3], st));
     }

@@ -63,6 +63,7 @@ void sort_pixels(void *temp, size_t temp_bytes, const int32_t *keys_in, int32_t 
 size_t sort_pixels_temp_bytes(int64_t n, int n_bits);
 void order_items(const int4 *items, const int32_t *n_items, const int32_t *ranges, int max_items, int4 *work,
                  int32_t *n_work, cudaStream_t st);
+int order_items_ints();  // ints order_items needs at n_work (counts + its scratch)
 
 // geer_raster.cu (fp32 raster forward / backward)
 // per-warp culling regions (wcull: 2 float4 per warp) and the frame of every work item, cached with the camera

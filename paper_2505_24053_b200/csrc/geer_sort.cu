@@ -78,10 +78,66 @@ __global__ void k_order_items(const int4 *__restrict__ items, const int32_t *__r
     if (in && !full) work[*n_items - 1 - (be + __popc(me & lt))] = it;  // empty items: the tail of [0, n_items)
 }
 
+// Longest-first work order (the raster's CTAs start in grid order, so the longest tile lists go
+// first and the short ones fill the tail): items bucketed by floor(log2(list length)) + 1, buckets
+// in descending order, empty items (bucket 0) last.  hist[0..33): bucket counts, then cursors.
+constexpr int kLenBuckets = 33;
+__device__ __forceinline__ int len_bucket(int len) { return len > 0 ? 32 - __clz(len) : 0; }
+
+__global__ void k_item_hist(const int4 *__restrict__ items, const int32_t *__restrict__ n_items,
+                            const int32_t *__restrict__ ranges, int32_t *__restrict__ hist) {
+    __shared__ int h[kLenBuckets];
+    if (threadIdx.x < kLenBuckets) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int n = *n_items;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int t = items[i].x;
+        atomicAdd(&h[len_bucket(ranges[t + 1] - ranges[t])], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < kLenBuckets && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void k_item_place(const int4 *__restrict__ items, const int32_t *__restrict__ n_items,
+                             const int32_t *__restrict__ ranges, const int32_t *__restrict__ hist,
+                             int32_t *__restrict__ cursor, int4 *__restrict__ work, int32_t *__restrict__ n_work) {
+    __shared__ int start[kLenBuckets];
+    if (threadIdx.x == 0) {  // bucket starts: 32, 31, ..., 1, then 0 (empty)
+        int run = 0;
+        for (int b = kLenBuckets - 1; b >= 1; --b) {
+            start[b] = run;
+            run += hist[b];
+        }
+        start[0] = run;
+        if (blockIdx.x == 0) {
+            n_work[0] = run;      // items with entries
+            n_work[1] = hist[0];  // empty items
+        }
+    }
+    __syncthreads();
+    const int n = *n_items;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int4 it = items[i];
+        const int b = len_bucket(ranges[it.x + 1] - ranges[it.x]);
+        work[start[b] + atomicAdd(&cursor[b], 1)] = it;
+    }
+}
+
 void order_items(const int4 *items, const int32_t *n_items, const int32_t *ranges, int max_items, int4 *work,
                  int32_t *n_work, cudaStream_t st) {
+#ifdef GEER_ORDER_ARBITRARY
     cudaMemsetAsync(n_work, 0, 2 * sizeof(int32_t), st);
     k_order_items<<<(max_items + 255) / 256, 256, 0, st>>>(items, n_items, ranges, max_items, work, n_work);
+#else
+    // n_work holds 2 + 2 * kLenBuckets ints: the counts, then the histogram and the cursors
+    int32_t *hist = n_work + 2, *cursor = hist + kLenBuckets;
+    cudaMemsetAsync(hist, 0, 2 * kLenBuckets * sizeof(int32_t), st);
+    const int blocks = (max_items + 255) / 256 < 148 ? (max_items + 255) / 256 : 148;
+    k_item_hist<<<blocks, 256, 0, st>>>(items, n_items, ranges, hist);
+    k_item_place<<<blocks, 256, 0, st>>>(items, n_items, ranges, hist, cursor, work, n_work);
+#endif
 }
+
+int order_items_ints() { return 2 + 2 * kLenBuckets; }
 
 }  // namespace geer
